@@ -1,0 +1,124 @@
+/*
+ * mfgpu.h -- C ABI of the B200 decimation / cluster-pooling library (libmfgpu.so).
+ *
+ * Drop-in boundary for the reference package `meshforge` (pure Python/numpy,
+ * /root/reference/pkg/src/meshforge).  The reference has no native FFI, so
+ * each entry point below replaces one Python function of its public API:
+ *
+ *   mf_decimate        <- decimate.decimate_parallel(mesh, config)   decimate.py:344-382
+ *                         (TriMesh and BatchedMesh; round chain decimate.py:294-316;
+ *                          batch merge decimate.py:319-341)
+ *   mf_decimation_*    <- DecimationResult fields mesh / replace / mapping   decimate.py:74-92
+ *   mf_pool            <- pooling.pool(features, result, mode, weights)      pooling.py:49-71
+ *   mf_unpool          <- pooling.unpool(coarse, result)                     pooling.py:74-77
+ *   mf_round_targets   <- decimate._round_targets                            decimate.py:294-316
+ *
+ * Plain pointers and sizes only.  Array pointers may be host or device memory
+ * (detected per pointer); offsets are always host arrays.  Integer outputs are
+ * int64 like the reference.  Every call is stream-ordered on `stream`
+ * (a cudaStream_t, NULL = legacy default stream) and returns once its outputs
+ * are complete.  Error codes map to the reference exception types:
+ *
+ *   MF_OK                0
+ *   MF_ERR_VALUE         1  -> ValueError            (decimate.py:365-370, pooling.py:19-32)
+ *   MF_ERR_STRUCTURAL    2  -> StructuralError       (validation.py:59-65)
+ *   MF_ERR_INFEASIBLE    3  -> InfeasibleTargetError (decimate.py:239-244, 268-273);
+ *                              mf_status.achievable_vertices / .mesh_index filled
+ *   MF_ERR_CUDA          4  -> CUDA runtime failure
+ *   MF_ERR_RUNTIME       5  -> RuntimeError          (pooling.py:27-28 coverage check)
+ *   MF_ERR_LIMIT         6  -> input exceeds a documented device limit
+ */
+#ifndef MFGPU_H
+#define MFGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MF_OK 0
+#define MF_ERR_VALUE 1
+#define MF_ERR_STRUCTURAL 2
+#define MF_ERR_INFEASIBLE 3
+#define MF_ERR_CUDA 4
+#define MF_ERR_RUNTIME 5
+#define MF_ERR_LIMIT 6
+
+#define MF_DTYPE_F64 0
+#define MF_DTYPE_F32 1
+
+#define MF_POOL_AVERAGE 0  /* pooling.py:15 POOL_MODES order */
+#define MF_POOL_MAX 1
+#define MF_POOL_WEIGHTED 2
+#define MF_POOL_SUM 3
+
+typedef struct mf_context mf_context;
+typedef struct mf_decimation mf_decimation;
+
+typedef struct mf_status {
+    int32_t code;
+    int32_t mesh_index;           /* batch entry the error refers to (-1 = none) */
+    int64_t achievable_vertices;  /* MF_ERR_INFEASIBLE */
+    int64_t target_vertices;      /* target of the failing round */
+    int32_t no_edges;             /* infeasible because the round had no edges */
+    int32_t reserved;
+    char message[256];
+} mf_status;
+
+/* TriMesh (mesh.py:13-52) or BatchedMesh (mesh.py:137-205) view. */
+typedef struct mf_mesh_view {
+    const double *positions;        /* [n,3] float64 */
+    const int64_t *facets;          /* [m,3] int64 */
+    const void *features;           /* [n,c] float64/float32, or NULL = copy of positions (mesh.py:28-29) */
+    int32_t features_dtype;         /* MF_DTYPE_* */
+    int32_t reserved;
+    int64_t n, m, c;
+    const int64_t *vertex_offsets;  /* host [n_meshes+1], or NULL for one mesh */
+    const int64_t *facet_offsets;   /* host [n_meshes+1], or NULL */
+    int64_t n_meshes;
+} mf_mesh_view;
+
+/* DecimationConfig (decimate.py:45-71). */
+typedef struct mf_decimate_config {
+    int64_t target_vertices;
+    int32_t rounds;        /* -1 = 'auto' */
+    int32_t placement;     /* 0 = 'average' (1 = 'inverse' not yet supported -> MF_ERR_VALUE) */
+    int32_t seeded;        /* shuffle_seed is not None */
+    int32_t einsum_order;  /* 0 = numpy AVX-512 lane-split dot3, 1 = sequential dot3 */
+    uint64_t pcg_state[4]; /* default_rng(seed).bit_generator.state: state_hi, state_lo, inc_hi, inc_lo */
+} mf_decimate_config;
+
+int mf_context_create(int device, mf_context **out);
+void mf_context_destroy(mf_context *ctx);
+
+int mf_decimate(mf_context *ctx, const mf_mesh_view *mesh, const mf_decimate_config *cfg, void *stream,
+                mf_decimation **out, mf_status *status);
+
+int mf_decimation_sizes(const mf_decimation *res, int64_t *n_in, int64_t *n_out, int64_t *m_out, int64_t *c,
+                        int64_t *n_meshes);
+/* Copy results into caller buffers (host or device; NULL skips an array).
+ * facets / replace / mapping / offsets are written as int64. */
+int mf_decimation_copy(const mf_decimation *res, double *positions, int64_t *facets, void *features,
+                       int32_t features_dtype, int64_t *replace, int64_t *mapping, int64_t *vertex_offsets,
+                       int64_t *facet_offsets, void *stream, mf_status *status);
+void mf_decimation_free(mf_decimation *res);
+
+/* pool over a replace tensor (host/device int64[n]) or over a decimation's
+ * own replace (res != NULL, replace ignored: reuses its device cluster CSR). */
+int mf_pool(mf_context *ctx, const mf_decimation *res, const int64_t *replace, int64_t n, int64_t n_out,
+            const void *features, int32_t dtype, int64_t c, int32_t mode, const void *weights, void *out,
+            void *stream, mf_status *status);
+int mf_unpool(mf_context *ctx, const mf_decimation *res, const int64_t *replace, int64_t n, int64_t n_out,
+              const void *coarse, int32_t dtype, int64_t c, void *out, void *stream, mf_status *status);
+
+int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t *chain, int64_t cap);
+
+/* Number of kernels this library launched on the calling thread since the last reset. */
+int64_t mf_kernel_launch_count(int32_t reset);
+const char *mf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,41 @@
+"""B200-native cluster-parallel mesh decimation and cluster pooling.
+
+Drop-in for the reference package's hot path (meshforge decimate.py /
+pooling.py): decimate_parallel, pool and unpool run as hand-written sm_100a
+CUDA kernels in libmfgpu.so behind a C ABI (include/mfgpu.h).
+"""
+
+from .decimate import (
+    DecimationConfig,
+    DecimationResult,
+    VertexCluster,
+    clusters,
+    decimate_parallel,
+    representative_vertices,
+    round_targets,
+)
+from .errors import InfeasibleTargetError, MeshError, NativeError, StructuralError
+from .mesh import BatchedMesh, TriMesh, concat_batch
+from .pooling import POOL_MODES, pool, unpool
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BatchedMesh",
+    "DecimationConfig",
+    "DecimationResult",
+    "InfeasibleTargetError",
+    "MeshError",
+    "NativeError",
+    "POOL_MODES",
+    "StructuralError",
+    "TriMesh",
+    "VertexCluster",
+    "clusters",
+    "concat_batch",
+    "decimate_parallel",
+    "pool",
+    "representative_vertices",
+    "round_targets",
+    "unpool",
+]

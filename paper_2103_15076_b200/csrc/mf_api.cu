@@ -1,0 +1,281 @@
+// mf_api.cu -- extern "C" entry points of libmfgpu.so (declared in include/mfgpu.h).
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "mf_internal.h"
+#include "mf_kernels.cuh"
+
+struct mf_context {
+    mf::Context c;
+};
+struct mf_decimation {
+    mf::Result r;
+};
+
+namespace mf {
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int grid_n(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    return (int)(g < 1 ? 1 : g);
+}
+
+// int32 device array -> int64 destination (host or device), adding `add`.
+static int copy_i32_as_i64(const int* src, int64_t n, int64_t* dst, cudaStream_t s, mf_status* st) {
+    if (!dst || n <= 0) return MF_OK;
+    if (is_device_ptr(dst)) {
+        k_i32_to_i64<<<grid_n(n), 256, 0, s>>>(n, src, dst, 0);
+        g_launches++;
+        MF_CUDA_TRY(cudaGetLastError());
+        return MF_OK;
+    }
+    int64_t* tmp = nullptr;
+    MF_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * 8, s));
+    k_i32_to_i64<<<grid_n(n), 256, 0, s>>>(n, src, tmp, 0);
+    g_launches++;
+    MF_CUDA_TRY(cudaMemcpyAsync(dst, tmp, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    MF_CUDA_TRY(cudaFreeAsync(tmp, s));
+    return MF_OK;
+}
+
+static int copy_f64_as(const double* src, int64_t n, void* dst, int dtype, cudaStream_t s, mf_status* st) {
+    if (!dst || n <= 0) return MF_OK;
+    if (dtype == MF_DTYPE_F64) {
+        MF_CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)n * 8, cudaMemcpyDefault, s));
+        return MF_OK;
+    }
+    if (is_device_ptr(dst)) {
+        k_f64_to_f32<<<grid_n(n), 256, 0, s>>>(n, src, (float*)dst);
+        g_launches++;
+        return MF_OK;
+    }
+    float* tmp = nullptr;
+    MF_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * 4, s));
+    k_f64_to_f32<<<grid_n(n), 256, 0, s>>>(n, src, tmp);
+    g_launches++;
+    MF_CUDA_TRY(cudaMemcpyAsync(dst, tmp, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    MF_CUDA_TRY(cudaFreeAsync(tmp, s));
+    return MF_OK;
+}
+
+}  // namespace mf
+
+using namespace mf;
+
+static void clear_status(mf_status* st) {
+    if (!st) return;
+    memset(st, 0, sizeof(*st));
+    st->mesh_index = -1;
+}
+
+extern "C" {
+
+int mf_context_create(int device, mf_context** out) {
+    mf_context* c = new mf_context();
+    c->c.device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete c;
+        return MF_ERR_CUDA;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+        delete c;
+        return MF_ERR_CUDA;
+    }
+    c->c.sm_count = prop.multiProcessorCount;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_match, 256, 0);
+    c->c.coop_blocks_match = std::max(1, occ) * prop.multiProcessorCount;
+    occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_select, 256, 0);
+    c->c.coop_blocks_select = std::max(1, occ) * prop.multiProcessorCount;
+    // keep freed stream-ordered allocations cached in the device pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    *out = c;
+    return MF_OK;
+}
+
+void mf_context_destroy(mf_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    if (ctx->c.arena) cudaFree(ctx->c.arena);
+    if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+    delete ctx;
+}
+
+int mf_decimate(mf_context* ctx, const mf_mesh_view* mesh, const mf_decimate_config* cfg, void* stream,
+                mf_decimation** out, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || !mesh || !cfg || !out) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "null argument");
+        return st->code;
+    }
+    *out = nullptr;
+    Result* r = nullptr;
+    int rc = decimate_run(&ctx->c, mesh, cfg, (cudaStream_t)stream, &r, st);
+    if (rc != MF_OK) return rc;
+    mf_decimation* d = new mf_decimation();
+    d->r = *r;
+    delete r;
+    *out = d;
+    return MF_OK;
+}
+
+int mf_decimation_sizes(const mf_decimation* res, int64_t* n_in, int64_t* n_out, int64_t* m_out, int64_t* c,
+                        int64_t* n_meshes) {
+    if (!res) return MF_ERR_VALUE;
+    if (n_in) *n_in = res->r.n_in;
+    if (n_out) *n_out = res->r.n_out;
+    if (m_out) *m_out = res->r.m_out;
+    if (c) *c = res->r.c;
+    if (n_meshes) *n_meshes = res->r.n_meshes;
+    return MF_OK;
+}
+
+int mf_decimation_copy(const mf_decimation* res, double* positions, int64_t* facets, void* features,
+                       int32_t features_dtype, int64_t* replace, int64_t* mapping, int64_t* vertex_offsets,
+                       int64_t* facet_offsets, void* stream, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!res) return MF_ERR_VALUE;
+    const Result& r = res->r;
+    cudaStream_t s = (cudaStream_t)stream;
+    MF_CUDA_TRY(cudaSetDevice(r.device));
+    if (positions && r.n_out)
+        MF_CUDA_TRY(cudaMemcpyAsync(positions, r.positions, (size_t)r.n_out * 24, cudaMemcpyDefault, s));
+    int rc;
+    if ((rc = copy_i32_as_i64(r.facets, r.m_out * 3, facets, s, st))) return rc;
+    if (features) {
+        const double* src = r.features_alias ? r.positions : r.features;
+        if ((rc = copy_f64_as(src, r.n_out * r.c, features, features_dtype, s, st))) return rc;
+    }
+    if ((rc = copy_i32_as_i64(r.replace, r.n_in, replace, s, st))) return rc;
+    if ((rc = copy_i32_as_i64(r.mapping, r.n_in, mapping, s, st))) return rc;
+    for (int which = 0; which < 2; which++) {
+        int64_t* dst = which ? facet_offsets : vertex_offsets;
+        const std::vector<int64_t>& src = which ? r.facet_offsets : r.vertex_offsets;
+        if (!dst) continue;
+        MF_CUDA_TRY(cudaMemcpyAsync(dst, src.data(), src.size() * 8, cudaMemcpyDefault, s));
+    }
+    MF_CUDA_TRY(cudaStreamSynchronize(s));
+    MF_CUDA_TRY(cudaGetLastError());
+    return MF_OK;
+}
+
+void mf_decimation_free(mf_decimation* res) {
+    if (!res) return;
+    cudaSetDevice(res->r.device);
+    if (res->r.block) cudaFree(res->r.block);
+    if (res->r.csr_block) cudaFree(res->r.csr_block);
+    delete res;
+}
+
+int mf_pool(mf_context* ctx, const mf_decimation* res, const int64_t* replace, int64_t n, int64_t n_out,
+            const void* features, int32_t dtype, int64_t c, int32_t mode, const void* weights, void* out,
+            void* stream, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || mode < 0 || mode > 3) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "mode must be one of ('average', 'max', 'weighted', 'sum')");
+        return st->code;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    const int* d_off = nullptr;
+    const int* d_mem = nullptr;
+    void* blk_r = nullptr;
+    void* blk_csr = nullptr;
+    int rc = MF_OK;
+    if (res) {
+        Result& r = const_cast<mf_decimation*>(res)->r;
+        n = r.n_in;
+        n_out = r.n_out;
+        if (!r.csr_block) {
+            int *o, *mm;
+            if ((rc = build_cluster_csr(&ctx->c, r.replace, r.n_in, r.n_out, &o, &mm, &r.csr_block, s, st)))
+                return rc;
+            r.csr_off = o;
+            r.csr_members = mm;
+        }
+        d_off = r.csr_off;
+        d_mem = r.csr_members;
+    } else {
+        int *r32, *cnt;
+        if ((rc = upload_replace(&ctx->c, replace, n, n_out, 1, &r32, &cnt, &blk_r, s, st))) goto done;
+        int *o, *mm;
+        if ((rc = build_cluster_csr(&ctx->c, r32, n, n_out, &o, &mm, &blk_csr, s, st))) goto done;
+        d_off = o;
+        d_mem = mm;
+    }
+    if (mode == MF_POOL_WEIGHTED && !weights) {
+        st->code = rc = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "weighted pooling requires per-input-vertex weights");
+        goto done;
+    }
+    rc = pool_run(&ctx->c, features, dtype, n, c, nullptr, d_off, d_mem, n_out, mode, weights, out, s, st);
+done:
+    if (blk_r) cudaFreeAsync(blk_r, s);
+    if (blk_csr) cudaFreeAsync(blk_csr, s);
+    return rc;
+}
+
+int mf_unpool(mf_context* ctx, const mf_decimation* res, const int64_t* replace, int64_t n, int64_t n_out,
+              const void* coarse, int32_t dtype, int64_t c, void* out, void* stream, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx) return MF_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    int rc;
+    if (res) {
+        const Result& r = res->r;
+        return unpool_run(&ctx->c, coarse, dtype, r.n_out, c, r.replace, r.n_in, out, s, st);
+    }
+    int *r32, *cnt;
+    void* blk = nullptr;
+    rc = upload_replace(&ctx->c, replace, n, n_out, 0, &r32, &cnt, &blk, s, st);
+    if (rc == MF_OK) rc = unpool_run(&ctx->c, coarse, dtype, n_out, c, r32, n, out, s, st);
+    if (blk) cudaFreeAsync(blk, s);
+    return rc;
+}
+
+int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t* chain, int64_t cap) {
+    std::vector<int64_t> v;
+    round_targets(n_in, target, rounds, v);
+    for (int64_t i = 0; i < (int64_t)v.size() && i < cap; i++) chain[i] = v[i];
+    return (int64_t)v.size();
+}
+
+int64_t mf_kernel_launch_count(int32_t reset) {
+    int64_t v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+
+const char* mf_version(void) { return "mfgpu 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,203 @@
+// mf_common.cuh -- device helpers shared by the decimation / pooling kernels.
+//
+// Everything here is integer/byte plumbing sized for B200 (148 SMs, 32-wide
+// warps, 126 MB L2): order-preserving keys, warp-aggregated list appends,
+// a single-pass decoupled look-back scan, and a software grid barrier for
+// the persistent (cooperatively launched) kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MF_DEV __device__ __forceinline__
+
+namespace mf {
+
+constexpr int kWarp = 32;
+
+// ------------------------------------------------------------------------
+// float64 -> order-preserving uint64.  -0.0 is canonicalised to +0.0 and any
+// NaN to the largest key, mirroring numpy's comparison semantics inside
+// lexsort (equal zeros tie; NaN sorts last) -- decimate.py:183, 217-220.
+MF_DEV uint64_t f64_key(double c) {
+    uint64_t u = (uint64_t)__double_as_longlong(c);
+    if (c == 0.0) u = 0ull;
+    if (c != c) u = 0x7FF8000000000000ull;
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+MF_DEV double f64_unkey(uint64_t k) {
+    uint64_t u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double((long long)u);
+}
+
+MF_DEV bool key_lt(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl) {
+    return ah < bh || (ah == bh && al < bl);
+}
+
+// Lane-aggregated append: one atomic per warp-converged group.
+MF_DEV int append_slot(int* counter) {
+    unsigned mask = __activemask();
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(counter, __popc(mask));
+    base = __shfl_sync(mask, base, leader);
+    return base + __popc(mask & ((1u << lane) - 1u));
+}
+
+MF_DEV int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+MF_DEV int warp_incl_scan(int v) {
+    int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+MF_DEV int ld_volatile(const int* p) { return *(const volatile int*)p; }
+MF_DEV unsigned long long ld_volatile(const unsigned long long* p) {
+    return *(const volatile unsigned long long*)p;
+}
+
+// ------------------------------------------------------------------------
+// Software grid barrier for persistent kernels.  The launch must guarantee
+// co-residency (cudaLaunchCooperativeKernel with an occupancy-bounded grid).
+// `bar` = {arrive counter, generation}; zeroed once per launch.
+MF_DEV void grid_sync(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        unsigned g = *gen;
+        __threadfence();
+        unsigned arrived = atomicAdd(bar, 1u) + 1u;
+        if (arrived == gridDim.x) {
+            bar[0] = 0u;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) { __nanosleep(32); }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------------
+// Single-pass exclusive scan of int32 with decoupled look-back.
+// out[i] = sum(in[0..i)), out[n] = total.  `status` must hold ceil(n/TILE)
+// zeroed words and `ticket` one zeroed int (both reset with one memset).
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+constexpr unsigned long long kFlagAgg = 1ull << 32;
+constexpr unsigned long long kFlagPre = 2ull << 32;
+
+template <typename LoadOp>
+__global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, int* __restrict__ out,
+                                                          unsigned long long* status, int* ticket) {
+    __shared__ int s_tile;
+    __shared__ int s_warp[kScanBlock / 32];
+    __shared__ int s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const long long base = (long long)tile * kScanTile + (long long)threadIdx.x * kScanItems;
+    int v[kScanItems];
+    int tsum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) {
+        long long idx = base + i;
+        v[i] = (idx < n) ? load((int)idx) : 0;
+        tsum += v[i];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = warp_incl_scan(tsum);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = (lane < kScanBlock / 32) ? s_warp[lane] : 0;
+        int wi = warp_incl_scan(w);
+        if (lane < kScanBlock / 32) s_warp[lane] = wi - w;  // exclusive per warp
+        int agg = __shfl_sync(0xffffffffu, wi, kScanBlock / 32 - 1);
+        // publish + look back
+        if (lane == 0) {
+            unsigned long long word = (tile == 0 ? kFlagPre : kFlagAgg) | (unsigned)agg;
+            __threadfence();
+            atomicExch(status + tile, word);
+        }
+        int excl = 0;
+        if (tile > 0) {
+            int pred = tile - 1;
+            while (true) {
+                int idx = pred - lane;
+                unsigned long long s = (idx >= 0) ? ld_volatile(status + idx) : (kFlagPre);
+                while (__any_sync(0xffffffffu, (s >> 32) == 0ull)) {
+                    if ((s >> 32) == 0ull) s = ld_volatile(status + idx);
+                }
+                unsigned pmask = __ballot_sync(0xffffffffu, (s >> 32) == 2ull);
+                int first = pmask ? (__ffs(pmask) - 1) : 32;
+                int val = (lane <= first) ? (int)(unsigned)(s & 0xffffffffull) : 0;
+                excl += warp_sum(val);
+                if (pmask) break;
+                pred -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(status + tile, kFlagPre | (unsigned)(excl + agg));
+            }
+        }
+        if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    int run = s_prefix + s_warp[warp] + (incl - tsum);
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) {
+        long long idx = base + i;
+        if (idx < n) out[idx] = run;
+        run += v[i];
+        if (idx == n - 1) out[n] = run;
+    }
+    if (n == 0 && tile == 0 && threadIdx.x == 0) out[0] = 0;
+}
+
+struct LoadArr {
+    const int* p;
+    MF_DEV int operator()(int i) const { return p[i]; }
+};
+
+// In-register insertion sort of a short int array (segment tiers use this
+// for lengths <= the small-tier bound).
+template <int CAP>
+MF_DEV void isort(int* a, int n) {
+    for (int i = 1; i < n; i++) {
+        int x = a[i], j = i - 1;
+        while (j >= 0 && a[j] > x) { a[j + 1] = a[j]; j--; }
+        a[j + 1] = x;
+    }
+}
+
+// Block-wide bitonic sort of `n` ints in shared memory (padded to pow2 with INT_MAX).
+MF_DEV void block_bitonic(int* s, int n_pow2) {
+    for (int k = 2; k <= n_pow2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    int a = s[i], b = s[ixj];
+                    bool up = ((i & k) == 0);
+                    if ((a > b) == up) { s[i] = b; s[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace mf

@@ -1,0 +1,104 @@
+// mf_internal.h -- host-side declarations shared by the library's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mfgpu.h"
+
+namespace mf {
+
+// Status words the device writes and the host reads back once per call.
+struct DevStatus {
+    int abort;            // a round failed (infeasible) -> later kernels exit early
+    int fail_round;       // first failing round
+    int limit_exceeded;   // a per-vertex / per-cluster size exceeded the heavy-tier capacity
+    int pad;
+};
+
+struct Context {
+    int device = 0;
+    int sm_count = 148;
+    int coop_blocks_match = 0;   // co-resident blocks of the matching kernel
+    int coop_blocks_select = 0;  // co-resident blocks of the selection kernel
+    // workspace arena (grown on demand, kept across calls)
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    // pinned host staging for params / status
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    cudaEvent_t done_event = nullptr;
+    std::string last_error;
+};
+
+// Bump allocator over the context arena (256-byte aligned carving).
+struct Arena {
+    char* base = nullptr;
+    size_t cap = 0, off = 0;
+    bool measuring = false;
+    template <typename T>
+    T* take(size_t count) {
+        size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+        if (bytes == 0) bytes = 256;
+        size_t at = off;
+        off += bytes;
+        if (measuring || base == nullptr) return nullptr;
+        return reinterpret_cast<T*>(base + at);
+    }
+};
+
+// Device-resident decimation result (owned by mf_decimation).
+struct Result {
+    int device = 0;
+    int64_t n_in = 0, n_out = 0, m_out = 0, c = 0, n_meshes = 1;
+    int features_alias = 0;  // features == positions bitwise (features omitted on input)
+    double* positions = nullptr;  // n_out*3
+    int* facets = nullptr;        // m_out*3 (int32 on device)
+    double* features = nullptr;   // n_out*c (nullptr when aliasing positions)
+    int* replace = nullptr;       // n_in
+    int* mapping = nullptr;       // n_in
+    std::vector<int64_t> vertex_offsets, facet_offsets;
+    void* block = nullptr;        // single allocation backing all arrays
+    // cluster CSR of `replace` for pooling (built lazily)
+    int* csr_off = nullptr;
+    int* csr_members = nullptr;
+    void* csr_block = nullptr;
+};
+
+int decimate_run(Context* ctx, const mf_mesh_view* mesh, const mf_decimate_config* cfg, cudaStream_t stream,
+                 Result** out, mf_status* st);
+int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c, const int* d_replace,
+             const int* d_off, const int* d_members, int64_t n_out, int mode, const void* weights, void* out,
+             cudaStream_t stream, mf_status* st);
+int build_cluster_csr(Context* ctx, const int* d_replace, int64_t n, int64_t n_out, int** d_off, int** d_members,
+                      void** block, cudaStream_t stream, mf_status* st);
+
+// memory-space helper: true when p is device (or managed) memory on any device
+bool is_device_ptr(const void* p);
+
+#define MF_CUDA_TRY(expr)                                                              \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            if (st) {                                                                  \
+                st->code = MF_ERR_CUDA;                                                \
+                snprintf(st->message, sizeof(st->message), "%s: %s (%s:%d)", #expr,   \
+                         cudaGetErrorString(_e), __FILE__, __LINE__);                  \
+            }                                                                          \
+            return MF_ERR_CUDA;                                                        \
+        }                                                                              \
+    } while (0)
+
+}  // namespace mf
+
+namespace mf {
+int upload_replace(Context* ctx, const int64_t* replace, int64_t n, int64_t n_out, int check_cover, int** d_r32,
+                   int** d_count, void** block, cudaStream_t stream, mf_status* st);
+int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64_t c, const int* d_replace, int64_t n,
+               void* out, cudaStream_t stream, mf_status* st);
+int64_t round_targets(int64_t n_in, int64_t target, int rounds, std::vector<int64_t>& chain);
+extern thread_local int64_t g_launches;
+}  // namespace mf

@@ -1,0 +1,1054 @@
+// mf_kernels.cuh -- device kernels of one decimation round and of cluster pooling.
+//
+// Kernel map (reference call site -> kernel), SURVEY.md §8(a):
+//   mesh.py:72-88 + quadrics.py:36-45    k_facet_plane        facet plane (n, d), incidence degrees
+//   quadrics.py:69-77 (np.add.at order)  k_inc_scatter + k_vertex{,_heavy}: corner-major incidence CSR,
+//                                         sequential per-vertex quadric fold, unique neighbour lists
+//   mesh.py:125-134 + quadrics.py:117-132 k_edges             lexicographic edge ids, pair cost, rank keys
+//   decimate.py:181-191 (seeded)         k_cost_minmax + k_seed_keys  PCG64 jump-ahead keys, buckets
+//   decimate.py:248-263 (greedy)         k_match (persistent)  locally-dominant matching rounds
+//   decimate.py:256-263 (budget stop)    k_select (persistent) MSD radix select of the budget lowest ranks
+//   decimate.py:194-226 (absorb)         k_absorb_cand + k_select + k_absorb_apply
+//   decimate.py:130-137, 275-278         k_relabel{1,2,3}      min-member flags + exclusive scan
+//   decimate.py:142-145, 280-283         k_contract{,_heavy}   ascending-member fold from +0.0, / count
+//   decimate.py:147-167                  k_facet_remap / keep / write   remap, degenerate drop, hash dedupe
+//   decimate.py:380-381                  k_compose             replace / mapping chaining (-1 sticky)
+//   pooling.py:36-77                     k_pool / k_unpool
+//
+// All float64 arithmetic is compiled with --fmad=false: numpy never fuses
+// multiply-add, and bit-exact positions are required for multi-round
+// topology parity.
+#pragma once
+
+#include "mf_common.cuh"
+
+namespace mf {
+
+struct __align__(32) Plane {
+    double n0, n1, n2, d;
+};
+
+constexpr int kSmallDeg = 32;       // thread-tier bound for per-vertex incidence lists / clusters
+constexpr int kChunk = 2048;        // smem chunk of the heavy-tier block sort
+
+// ------------------------------------------------------------------------
+// Block-cooperative sort of vals[0..n) (ascending) for the heavy tier:
+// chunks of kChunk sorted in shared memory (bitonic), then bottom-up
+// merge-path merges ping-ponging through tmp[0..n).  Any n.
+MF_DEV int merge_path_split(const int* a, int na, const int* b, int nb, int diag) {
+    int lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= b[diag - 1 - mid]) lo = mid + 1;  // stable: a before equal b
+        else hi = mid;
+    }
+    return lo;
+}
+
+MF_DEV void block_sort_ints(int* vals, int* tmp, int n, int* smem /* kChunk ints */) {
+    for (int c0 = 0; c0 < n; c0 += kChunk) {
+        int len = min(kChunk, n - c0);
+        int p2 = 1;
+        while (p2 < len) p2 <<= 1;
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) smem[i] = (i < len) ? vals[c0 + i] : 0x7fffffff;
+        __syncthreads();
+        block_bitonic(smem, p2);
+        for (int i = threadIdx.x; i < len; i += blockDim.x) vals[c0 + i] = smem[i];
+        __syncthreads();
+    }
+    int* src = vals;
+    int* dst = tmp;
+    for (int w = kChunk; w < n; w <<= 1) {
+        for (int a0 = 0; a0 < n; a0 += 2 * w) {
+            int na = min(w, n - a0);
+            int nb = max(0, min(w, n - a0 - na));
+            const int* A = src + a0;
+            const int* Bp = src + a0 + na;
+            int tot = na + nb;
+            int per = (tot + blockDim.x - 1) / blockDim.x;
+            int d0 = min(tot, (int)threadIdx.x * per), d1 = min(tot, d0 + per);
+            if (d0 < d1) {
+                int i = merge_path_split(A, na, Bp, nb, d0);
+                int j = d0 - i;
+                for (int d = d0; d < d1; d++) {
+                    bool takeA = (j >= nb) || (i < na && A[i] <= Bp[j]);
+                    dst[a0 + d] = takeA ? A[i++] : Bp[j++];
+                }
+            }
+        }
+        __syncthreads();
+        int* t = src; src = dst; dst = t;
+    }
+    if (src != vals)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) vals[i] = src[i];
+    __syncthreads();
+}
+
+// Block-wide exclusive scan helper (blockDim.x <= 1024), returns total.
+MF_DEV int block_excl_scan(int v, int* s_tmp /* 33 ints */, int* total) {
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = warp_incl_scan(v);
+    if (lane == 31) s_tmp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int nw = (blockDim.x + 31) >> 5;
+        int w = lane < nw ? s_tmp[lane] : 0;
+        int wi = warp_incl_scan(w);
+        if (lane < nw) s_tmp[lane] = wi - w;
+        if (lane == 31) s_tmp[32] = wi;
+    }
+    __syncthreads();
+    int r = s_tmp[warp] + incl - v;
+    *total = s_tmp[32];
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------------------------------
+// small helpers
+MF_DEV double dot3(double u0, double u1, double u2, double v0, double v1, double v2, int order) {
+    // numpy einsum('ij,ij->i') on AVX-512: (u0v0 + u2v2) + u1v1; else sequential.
+    if (order == 0) return (u0 * v0 + u2 * v2) + u1 * v1;
+    return (u0 * v0 + u1 * v1) + u2 * v2;
+}
+
+MF_DEV int mesh_of(const int* __restrict__ vmesh, int v) { return vmesh ? vmesh[v] : 0; }
+
+// ------------------------------------------------------------------------
+// K0: batch bookkeeping -- owning mesh of every vertex of this round.
+__global__ void k_vmesh(int N, const int* __restrict__ voff, int B, int* __restrict__ vmesh) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        int lo = 0, hi = B;  // find b with voff[b] <= v < voff[b+1]
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (voff[mid] <= v) lo = mid; else hi = mid;
+        }
+        vmesh[v] = lo;
+    }
+}
+
+// K1: facet plane (mesh.py:77-87) + incidence degrees.
+__global__ void k_facet_plane(const int* __restrict__ F, const double* __restrict__ P, const int* __restrict__ dM,
+                              const int* __restrict__ vmesh, const int* __restrict__ act, Plane* __restrict__ plane,
+                              int* __restrict__ deg, int order) {
+    const int M = *dM;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
+        int ia = F[3 * f], ib = F[3 * f + 1], ic = F[3 * f + 2];
+        if (!act[mesh_of(vmesh, ia)]) continue;
+        double x0 = P[3 * ia], y0 = P[3 * ia + 1], z0 = P[3 * ia + 2];
+        double ax = P[3 * ib] - x0, ay = P[3 * ib + 1] - y0, az = P[3 * ib + 2] - z0;
+        double bx = P[3 * ic] - x0, by = P[3 * ic + 1] - y0, bz = P[3 * ic + 2] - z0;
+        double cx = ay * bz - az * by;
+        double cy = az * bx - ax * bz;
+        double cz = ax * by - ay * bx;
+        double nrm = sqrt((cx * cx + cy * cy) + cz * cz);
+        Plane p;
+        if (nrm == 0.0) {
+            p.n0 = 0.0; p.n1 = 0.0; p.n2 = 0.0;
+        } else {
+            p.n0 = cx / nrm; p.n1 = cy / nrm; p.n2 = cz / nrm;
+        }
+        p.d = -dot3(p.n0, p.n1, p.n2, x0, y0, z0, order);
+        plane[f] = p;
+        atomicAdd(deg + ia, 1);
+        atomicAdd(deg + ib, 1);
+        atomicAdd(deg + ic, 1);
+    }
+}
+
+// K2: corner-major incidence scatter; key k = corner*Mcap + f keeps the
+// np.add.at order (corner 0 facets ascending, then corner 1, then 2).
+__global__ void k_inc_scatter(const int* __restrict__ F, const int* __restrict__ dM, int Mcap,
+                              const int* __restrict__ vmesh, const int* __restrict__ act,
+                              const int* __restrict__ inc_off, int* __restrict__ cursor, int* __restrict__ inc) {
+    const int M = *dM;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
+        int t[3] = {F[3 * f], F[3 * f + 1], F[3 * f + 2]};
+        if (!act[mesh_of(vmesh, t[0])]) continue;
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            int v = t[c];
+            int pos = inc_off[v] + atomicAdd(cursor + v, 1);
+            inc[pos] = c * Mcap + f;
+        }
+    }
+}
+
+// Quadric accumulation of one facet plane (quadrics.py:42-44 products, 74-76 sums).
+struct Q10 {
+    double a00, a01, a02, a11, a12, a22, b0, b1, b2, c;
+};
+MF_DEV void q_zero(Q10& q) { q.a00 = q.a01 = q.a02 = q.a11 = q.a12 = q.a22 = q.b0 = q.b1 = q.b2 = q.c = 0.0; }
+MF_DEV void q_add_plane(Q10& q, const Plane& p) {
+    q.a00 = q.a00 + p.n0 * p.n0; q.a01 = q.a01 + p.n0 * p.n1; q.a02 = q.a02 + p.n0 * p.n2;
+    q.a11 = q.a11 + p.n1 * p.n1; q.a12 = q.a12 + p.n1 * p.n2; q.a22 = q.a22 + p.n2 * p.n2;
+    q.b0 = q.b0 + p.d * p.n0; q.b1 = q.b1 + p.d * p.n1; q.b2 = q.b2 + p.d * p.n2;
+    q.c = q.c + p.d * p.d;  // degenerate facets: n = 0, d = -0*.. -> d*d == +0 == forced 0 (quadrics.py:65)
+}
+MF_DEV void q_store(double* __restrict__ vq, int v, const Q10& q) {
+    double* o = vq + 10 * (size_t)v;
+    o[0] = q.a00; o[1] = q.a01; o[2] = q.a02; o[3] = q.a11; o[4] = q.a12;
+    o[5] = q.a22; o[6] = q.b0; o[7] = q.b1; o[8] = q.b2; o[9] = q.c;
+}
+MF_DEV void q_load(const double* __restrict__ vq, int v, Q10& q) {
+    const double2* o = reinterpret_cast<const double2*>(vq + 10 * (size_t)v);
+    double2 t0 = o[0], t1 = o[1], t2 = o[2], t3 = o[3], t4 = o[4];
+    q.a00 = t0.x; q.a01 = t0.y; q.a02 = t1.x; q.a11 = t1.y; q.a12 = t2.x;
+    q.a22 = t2.y; q.b0 = t3.x; q.b1 = t3.y; q.b2 = t4.x; q.c = t4.y;
+}
+
+MF_DEV void decode_inc(int k, int Mcap, int& corner, int& f) {
+    corner = (k >= 2 * Mcap) ? 2 : (k >= Mcap ? 1 : 0);
+    f = k - corner * Mcap;
+}
+
+MF_DEV void other_two(const int* __restrict__ F, int f, int corner, int& a, int& b) {
+    int x = F[3 * f], y = F[3 * f + 1], z = F[3 * f + 2];
+    a = corner == 0 ? y : (corner == 1 ? z : x);
+    b = corner == 0 ? z : (corner == 1 ? x : y);
+}
+
+// K3: per-vertex quadric fold + unique neighbour list (thread tier, deg <= kSmallDeg).
+// Neighbours are written sorted & unique to nbr[2*inc_off[v] ...]; ucnt = count,
+// upcnt = count of neighbours > v (the vertex's lexicographic edges).
+__global__ void __launch_bounds__(128) k_vertex(int N, const int* __restrict__ inc_off, const int* __restrict__ inc,
+                                                const int* __restrict__ F, const Plane* __restrict__ plane, int Mcap,
+                                                double* __restrict__ vq, int* __restrict__ nbr, int* __restrict__ ucnt,
+                                                int* __restrict__ upcnt, int* __restrict__ heavy,
+                                                int* __restrict__ heavy_count) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        int s = inc_off[v], d = inc_off[v + 1] - s;
+        if (d > kSmallDeg) {
+            heavy[append_slot(heavy_count)] = v;
+            continue;
+        }
+        int k[kSmallDeg];
+        for (int i = 0; i < d; i++) k[i] = inc[s + i];
+        isort<kSmallDeg>(k, d);
+        Q10 q;
+        q_zero(q);
+        int cand[2 * kSmallDeg];
+        int nc = 0;
+        for (int i = 0; i < d; i++) {
+            int corner, f;
+            decode_inc(k[i], Mcap, corner, f);
+            Plane p = plane[f];
+            q_add_plane(q, p);
+            int a, b;
+            other_two(F, f, corner, a, b);
+            cand[nc++] = a;
+            cand[nc++] = b;
+        }
+        q_store(vq, v, q);
+        isort<2 * kSmallDeg>(cand, nc);
+        int nu = 0, nup = 0;
+        int* out = nbr + 2 * (size_t)s;
+        for (int i = 0; i < nc; i++) {
+            if (i > 0 && cand[i] == cand[i - 1]) continue;
+            out[nu++] = cand[i];
+            nup += cand[i] > v;
+        }
+        ucnt[v] = nu;
+        upcnt[v] = nup;
+    }
+}
+
+// K3h: heavy tier -- one block per high-degree vertex (any degree).
+__global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ heavy, const int* __restrict__ heavy_count,
+                                                      const int* __restrict__ inc_off, int* __restrict__ inc,
+                                                      int* __restrict__ inc_tmp, const int* __restrict__ F,
+                                                      const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
+                                                      int* __restrict__ nbr, int* __restrict__ nbr_tmp,
+                                                      int* __restrict__ ucnt, int* __restrict__ upcnt) {
+    __shared__ int smem[kChunk];
+    __shared__ Plane s_pl[256];
+    __shared__ int s_scan[33];
+    const int H = *heavy_count;
+    for (int h = blockIdx.x; h < H; h += gridDim.x) {
+        int v = heavy[h];
+        int s = inc_off[v], d = inc_off[v + 1] - s;
+        block_sort_ints(inc + s, inc_tmp + s, d, smem);
+        // sequential fold (thread 0) over planes staged 256 at a time
+        Q10 q;
+        q_zero(q);
+        for (int c0 = 0; c0 < d; c0 += 256) {
+            int len = min(256, d - c0);
+            if ((int)threadIdx.x < len) {
+                int corner, f;
+                decode_inc(inc[s + c0 + threadIdx.x], Mcap, corner, f);
+                s_pl[threadIdx.x] = plane[f];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int i = 0; i < len; i++) q_add_plane(q, s_pl[i]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) q_store(vq, v, q);
+        // candidates -> nbr[2s .. 2s+2d)
+        int* cand = nbr + 2 * (size_t)s;
+        for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            int corner, f, a, b;
+            decode_inc(inc[s + i], Mcap, corner, f);
+            other_two(F, f, corner, a, b);
+            cand[2 * i] = a;
+            cand[2 * i + 1] = b;
+        }
+        __syncthreads();
+        block_sort_ints(cand, nbr_tmp + 2 * (size_t)s, 2 * d, smem);
+        // unique compaction (order preserving) through nbr_tmp
+        int* tmpo = nbr_tmp + 2 * (size_t)s;
+        int base = 0, nup = 0;
+        for (int c0 = 0; c0 < 2 * d; c0 += blockDim.x) {
+            int i = c0 + threadIdx.x;
+            int keep = 0, x = 0;
+            if (i < 2 * d) {
+                x = cand[i];
+                keep = (i == 0) || (x != cand[i - 1]);
+            }
+            int tot;
+            int pos = block_excl_scan(keep, s_scan, &tot);
+            if (keep) tmpo[base + pos] = x;
+            int upk = keep && x > v;
+            int totu;
+            block_excl_scan(upk, s_scan, &totu);
+            base += tot;
+            nup += totu;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < base; i += blockDim.x) cand[i] = tmpo[i];
+        if (threadIdx.x == 0) {
+            ucnt[v] = base;
+            upcnt[v] = nup;
+        }
+        __syncthreads();
+    }
+}
+
+// Pair cost (quadrics.py:117-132 + evaluate 53-58) for 'average' placement.
+MF_DEV double pair_cost(const Q10& qi, const Q10& qj, double pix, double piy, double piz, double pjx, double pjy,
+                        double pjz, int order) {
+    double a00 = qi.a00 + qj.a00, a01 = qi.a01 + qj.a01, a02 = qi.a02 + qj.a02;
+    double a11 = qi.a11 + qj.a11, a12 = qi.a12 + qj.a12, a22 = qi.a22 + qj.a22;
+    double b0 = qi.b0 + qj.b0, b1 = qi.b1 + qj.b1, b2 = qi.b2 + qj.b2, c = qi.c + qj.c;
+    double x0 = 0.5 * (pix + pjx), x1 = 0.5 * (piy + pjy), x2 = 0.5 * (piz + pjz);
+    double quad = 0.0;
+    quad = quad + (x0 * a00) * x0;
+    quad = quad + (x0 * a01) * x1;
+    quad = quad + (x0 * a02) * x2;
+    quad = quad + (x1 * a01) * x0;
+    quad = quad + (x1 * a11) * x1;
+    quad = quad + (x1 * a12) * x2;
+    quad = quad + (x2 * a02) * x0;
+    quad = quad + (x2 * a12) * x1;
+    quad = quad + (x2 * a22) * x2;
+    double lin = 2.0 * dot3(b0, b1, b2, x0, x1, x2, order);
+    return (quad + lin) + c;
+}
+
+// K4: lexicographic edge list + pair cost + rank key + adjacency edge ids.
+// Edge id of (v, u>v) = eoff[v] + rank of u among v's upper neighbours, which
+// is exactly np.unique(axis=0)'s lexicographic order (mesh.py:131-134).
+__global__ void __launch_bounds__(128) k_edges(int N, const int* __restrict__ inc_off, const int* __restrict__ nbr,
+                                               const int* __restrict__ ucnt, const int* __restrict__ upcnt,
+                                               const int* __restrict__ eoff, const double* __restrict__ vq,
+                                               const double* __restrict__ P, int* __restrict__ e0,
+                                               int* __restrict__ e1, double* __restrict__ cost,
+                                               uint64_t* __restrict__ key_hi, int* __restrict__ adj_eid,
+                                               int* __restrict__ mate, int* __restrict__ minrep,
+                                               int* __restrict__ absorbed, int order) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        mate[v] = -1;
+        minrep[v] = v;
+        absorbed[v] = -1;
+        int nu = ucnt[v];
+        if (nu == 0) continue;
+        size_t s2 = 2 * (size_t)inc_off[v];
+        int nlow = nu - upcnt[v];
+        int eb = eoff[v];
+        Q10 qv;
+        q_load(vq, v, qv);
+        double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
+        for (int j = 0; j < nu; j++) {
+            int u = nbr[s2 + j];
+            int eid;
+            if (u > v) {
+                eid = eb + (j - nlow);
+                Q10 qu;
+                q_load(vq, u, qu);
+                double c = pair_cost(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
+                e0[eid] = v;
+                e1[eid] = u;
+                cost[eid] = c;
+                key_hi[eid] = f64_key(c);
+            } else {
+                // edge (u, v) lives in u's upper list: binary search v there
+                size_t su = 2 * (size_t)inc_off[u];
+                int nuu = ucnt[u];
+                int lo = nuu - upcnt[u], hi = nuu;
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (nbr[su + mid] < v) lo = mid + 1; else hi = mid;
+                }
+                eid = eoff[u] + (lo - (nuu - upcnt[u]));
+            }
+            adj_eid[s2 + j] = eid;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// Seeded shuffle keys (decimate.py:184-191).
+__global__ void k_cost_minmax(const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
+                              const int* __restrict__ vmesh, unsigned long long* __restrict__ mlo,
+                              unsigned long long* __restrict__ mhi) {
+    const int E = *dE;
+    uint64_t lo = ~0ull, hi = 0ull;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        int b = mesh_of(vmesh, e0[e]);
+        uint64_t k = f64_key(cost[e]);
+        if (vmesh) {
+            atomicMin(mlo + b, (unsigned long long)k);
+            atomicMax(mhi + b, (unsigned long long)k);
+        } else {
+            lo = k < lo ? k : lo;
+            hi = k > hi ? k : hi;
+        }
+    }
+    if (!vmesh) {
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+            lo = a < lo ? a : lo;
+            hi = b > hi ? b : hi;
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(mlo, (unsigned long long)lo);
+            atomicMax(mhi, (unsigned long long)hi);
+        }
+    }
+}
+
+typedef unsigned __int128 u128;
+MF_DEV u128 pcg_mult() { return ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull; }
+
+// state after `delta` LCG steps: s' = A s + C with (A, C) from square-and-multiply.
+MF_DEV u128 pcg_advance(u128 s, u128 inc, uint64_t delta) {
+    u128 cur_m = pcg_mult(), cur_p = inc, acc_m = 1, acc_p = 0;
+    while (delta) {
+        if (delta & 1) {
+            acc_m *= cur_m;
+            acc_p = acc_p * cur_m + cur_p;
+        }
+        cur_p = (cur_m + 1) * cur_p;
+        cur_m *= cur_m;
+        delta >>= 1;
+    }
+    return acc_m * s + acc_p;
+}
+MF_DEV uint64_t pcg_out(u128 s) {
+    uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    uint64_t x = hi ^ lo;
+    unsigned rot = (unsigned)(hi >> 58);
+    return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// One thread per run of kSeedRun consecutive edges: jump once, then step.
+constexpr int kSeedRun = 16;
+__global__ void k_seed_keys(const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
+                            const int* __restrict__ vmesh, const int* __restrict__ eoff, const int* __restrict__ voff,
+                            const unsigned long long* __restrict__ mlo, const unsigned long long* __restrict__ mhi,
+                            uint64_t s_hi, uint64_t s_lo, uint64_t i_hi,
+                            uint64_t i_lo, uint64_t* __restrict__ key_hi, uint64_t* __restrict__ key_lo) {
+    const int E = *dE;
+    const u128 s0 = ((u128)s_hi << 64) | s_lo, inc = ((u128)i_hi << 64) | i_lo;
+    const u128 M = pcg_mult();
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r * kSeedRun < E;
+         r += (long long)gridDim.x * blockDim.x) {
+        int e = (int)(r * kSeedRun);
+        int eend = min(E, e + kSeedRun);
+        int cur_b = -1;
+        u128 st = 0;
+        double lo = 0.0, width = 0.0;
+        for (; e < eend; e++) {
+            int b = mesh_of(vmesh, e0[e]);
+            if (b != cur_b) {
+                cur_b = b;
+                int local = e - (vmesh ? eoff[voff[b]] : 0);
+                st = pcg_advance(s0, inc, (uint64_t)local + 1ull);
+                lo = f64_unkey(mlo[b]);
+                double hi = f64_unkey(mhi[b]);
+                width = 1e-12 * (hi - lo);
+            } else {
+                st = st * M + inc;
+            }
+            double c = cost[e];
+            long long bucket = (width > 0.0) ? (long long)floor((c - lo) / width) : 0ll;
+            uint64_t k53 = pcg_out(st) >> 11;
+            key_hi[e] = ((uint64_t)bucket << 24) | (k53 >> 29);
+            key_lo[e] = ((k53 & ((1ull << 29) - 1ull)) << 35) | (uint64_t)e;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// K5: locally-dominant matching (persistent, grid barrier between phases).
+// An edge is matched when it is the lowest-ranked live edge at both of its
+// endpoints; the fixed point equals the sequential greedy scan over the
+// rank order (decimate.py:256-263) run to exhaustion.
+struct MatchArgs {
+    int N;
+    const int* inc_off;
+    const int* ucnt;
+    const int* nbr;
+    const int* adj_eid;
+    const int* e0;
+    const int* e1;
+    const uint64_t* key_hi;
+    const uint64_t* key_lo;  // nullptr -> secondary key is the edge id
+    int* mate;
+    int* best;
+    int* front0;
+    int* front1;
+    int* counters;  // [2] frontier sizes, [2] iteration count (diagnostic)
+    unsigned* bar;
+};
+
+__global__ void __launch_bounds__(256) k_match(MatchArgs a) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int v = tid; v < a.N; v += nth)
+        if (a.ucnt[v] > 0) a.front0[append_slot(a.counters)] = v;
+    grid_sync(a.bar);
+    int cur = 0;
+    for (int iter = 0;; iter++) {
+        int* Fc = cur ? a.front1 : a.front0;
+        int* Fn = cur ? a.front0 : a.front1;
+        const int n = __ldcg(a.counters + cur);
+        if (n == 0) {
+            if (tid == 0) a.counters[2] = iter;
+            break;
+        }
+        for (int i = tid; i < n; i += nth) {
+            int v = __ldcg(Fc + i);
+            size_t s = 2 * (size_t)a.inc_off[v];
+            int nu = a.ucnt[v];
+            int be = -1;
+            uint64_t bh = ~0ull, bl = ~0ull;
+            for (int j = 0; j < nu; j++) {
+                int u = a.nbr[s + j];
+                if (__ldcg(a.mate + u) >= 0) continue;
+                int e = a.adj_eid[s + j];
+                uint64_t kh = a.key_hi[e];
+                uint64_t kl = a.key_lo ? a.key_lo[e] : (uint64_t)e;
+                if (key_lt(kh, kl, bh, bl)) { bh = kh; bl = kl; be = e; }
+            }
+            a.best[v] = be;
+        }
+        if (tid == 0) a.counters[cur ^ 1] = 0;
+        grid_sync(a.bar);
+        for (int i = tid; i < n; i += nth) {
+            int v = __ldcg(Fc + i);
+            int e = __ldcg(a.best + v);
+            if (e < 0) continue;
+            int u = a.e0[e] == v ? a.e1[e] : a.e0[e];
+            if (__ldcg(a.best + u) == e) a.mate[v] = e;
+            else Fn[append_slot(a.counters + (cur ^ 1))] = v;
+        }
+        grid_sync(a.bar);
+        cur ^= 1;
+    }
+}
+
+// ------------------------------------------------------------------------
+// K6: per-segment MSD radix select over unique 128-bit keys.  For each
+// segment s, selects the k_s smallest candidates: mode 1 = all, 2 = none,
+// 3 = key <= threshold.  k_s = min(want_s, count_s), want_s = budget_s - removed_s.
+struct SelectArgs {
+    const int* n;  // candidate count
+    const uint64_t* chi;
+    const uint64_t* clo;
+    const int* cseg;
+    int B;
+    const int* seg_cnt;
+    const int* act;
+    const int* budget;
+    const int* removed;  // nullable
+    int* ksel;           // out: number selected per segment
+    int* mode;           // out
+    uint64_t* p_hi;      // prefix / threshold
+    uint64_t* p_lo;
+    int* krem;
+    int* hist;     // B*256, zero on entry, zero on exit
+    int* notdone;  // [16], zero on entry
+    unsigned* bar;
+};
+
+MF_DEV int key_digit(uint64_t hi, uint64_t lo, int shift) {
+    return (int)((shift >= 64 ? (hi >> (shift - 64)) : (lo >> shift)) & 255ull);
+}
+MF_DEV bool prefix_match(uint64_t hi, uint64_t lo, uint64_t phi, uint64_t plo, int top) {
+    if (top >= 128) return true;
+    if (top >= 64) return (hi >> (top - 64)) == (phi >> (top - 64));
+    if (hi != phi) return false;
+    return top == 0 ? lo == plo : (lo >> top) == (plo >> top);
+}
+
+__global__ void __launch_bounds__(256) k_select(SelectArgs a) {
+    __shared__ int s_hist[256];
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    const int n = *a.n;
+    for (int b = tid; b < a.B; b += nth) {
+        int want = a.act[b] ? a.budget[b] - (a.removed ? a.removed[b] : 0) : 0;
+        int cnt = a.seg_cnt[b];
+        int k = want < cnt ? want : cnt;
+        if (k < 0) k = 0;
+        a.ksel[b] = k;
+        a.p_hi[b] = 0;
+        a.p_lo[b] = 0;
+        a.krem[b] = k;
+        a.mode[b] = (k == 0) ? 2 : (k >= cnt ? 1 : 0);
+    }
+    grid_sync(a.bar);
+    for (int pass = 0; pass < 16; pass++) {
+        const int shift = 120 - 8 * pass;
+        if (a.B == 1) {
+            if (__ldcg(a.mode) == 0) {
+                for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
+                __syncthreads();
+                uint64_t phi = __ldcg(a.p_hi), plo = __ldcg(a.p_lo);
+                for (int i = tid; i < n; i += nth) {
+                    uint64_t h = a.chi[i], l = a.clo[i];
+                    if (prefix_match(h, l, phi, plo, shift + 8)) atomicAdd(s_hist + key_digit(h, l, shift), 1);
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < 256; i += blockDim.x)
+                    if (s_hist[i]) atomicAdd(a.hist + i, s_hist[i]);
+            }
+        } else {
+            for (int i = tid; i < n; i += nth) {
+                int b = a.cseg[i];
+                if (__ldcg(a.mode + b) != 0) continue;
+                uint64_t h = a.chi[i], l = a.clo[i];
+                if (prefix_match(h, l, __ldcg(a.p_hi + b), __ldcg(a.p_lo + b), shift + 8))
+                    atomicAdd(a.hist + 256 * b + key_digit(h, l, shift), 1);
+            }
+        }
+        grid_sync(a.bar);
+        for (int b = tid; b < a.B; b += nth) {
+            if (a.mode[b] != 0) continue;
+            int* hb = a.hist + 256 * b;
+            int kr = a.krem[b], cum = 0, dsel = 255, hsel = 0;
+            for (int d = 0; d < 256; d++) {
+                int h = __ldcg(hb + d);
+                if (cum + h >= kr) { dsel = d; hsel = h; break; }
+                cum += h;
+            }
+            for (int d = 0; d < 256; d++) hb[d] = 0;
+            kr -= cum;
+            a.krem[b] = kr;
+            uint64_t phi = a.p_hi[b], plo = a.p_lo[b];
+            if (shift >= 64) phi |= (uint64_t)dsel << (shift - 64);
+            else plo |= (uint64_t)dsel << shift;
+            if (hsel == kr) {  // every candidate under this prefix is selected
+                if (shift >= 64) {
+                    phi |= (shift - 64 > 0) ? ((1ull << (shift - 64)) - 1ull) : 0ull;
+                    plo = ~0ull;
+                } else {
+                    plo |= (shift > 0) ? ((1ull << shift) - 1ull) : 0ull;
+                }
+                a.mode[b] = 3;
+            } else {
+                atomicAdd(a.notdone + pass, 1);
+            }
+            a.p_hi[b] = phi;
+            a.p_lo[b] = plo;
+        }
+        grid_sync(a.bar);
+        if (__ldcg(a.notdone + pass) == 0) break;
+    }
+}
+
+MF_DEV bool is_selected(int mode, uint64_t h, uint64_t l, uint64_t th, uint64_t tl) {
+    return mode == 1 || (mode == 3 && !key_lt(th, tl, h, l));
+}
+
+// Candidates for budget truncation: the matched edges (one per pair, from its e0 end).
+__global__ void k_trunc_cand(int N, const int* __restrict__ mate, const int* __restrict__ e0,
+                             const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
+                             const int* __restrict__ vmesh, int* __restrict__ ncand, uint64_t* __restrict__ chi,
+                             uint64_t* __restrict__ clo, int* __restrict__ cseg, int* __restrict__ cpay,
+                             int* __restrict__ seg_cnt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        int e = mate[v];
+        if (e < 0 || e0[e] != v) continue;
+        int b = mesh_of(vmesh, v);
+        int slot = append_slot(ncand);
+        chi[slot] = key_hi[e];
+        clo[slot] = key_lo ? key_lo[e] : (uint64_t)e;
+        cseg[slot] = b;
+        cpay[slot] = e;
+        if (vmesh) atomicAdd(seg_cnt + b, 1);
+        else append_slot(seg_cnt);
+    }
+}
+
+__global__ void k_trunc_apply(const int* __restrict__ ncand, const uint64_t* __restrict__ chi,
+                              const uint64_t* __restrict__ clo, const int* __restrict__ cseg,
+                              const int* __restrict__ cpay, const int* __restrict__ mode,
+                              const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
+                              const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate, int B,
+                              const int* __restrict__ ksel, int* __restrict__ removed) {
+    const int n = *ncand;
+    int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int b = tid; b < B; b += nth) removed[b] = ksel[b];
+    for (int i = tid; i < n; i += nth) {
+        int b = cseg[i];
+        if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) continue;
+        int e = cpay[i];
+        mate[e0[e]] = -1;
+        mate[e1[e]] = -1;
+    }
+}
+
+// Absorb candidates (decimate.py:207-221): every unmatched vertex with edges
+// picks its lowest (cost, rep) incident edge; the matching is maximal here so
+// every neighbour is clustered and one pass suffices.
+__global__ void k_absorb_cand(int N, const int* __restrict__ inc_off, const int* __restrict__ ucnt,
+                              const int* __restrict__ nbr, const int* __restrict__ adj_eid,
+                              const double* __restrict__ cost, const int* __restrict__ mate,
+                              const int* __restrict__ e0, const int* __restrict__ vmesh, const int* __restrict__ act,
+                              const int* __restrict__ budget, const int* __restrict__ removed,
+                              int* __restrict__ ncand, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
+                              int* __restrict__ cseg, int* __restrict__ cpay, int* __restrict__ caux,
+                              int* __restrict__ seg_cnt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        int nu = ucnt[v];
+        if (nu == 0 || mate[v] >= 0) continue;
+        int b = mesh_of(vmesh, v);
+        if (!act[b] || removed[b] >= budget[b]) continue;
+        size_t s = 2 * (size_t)inc_off[v];
+        uint64_t bk = ~0ull;
+        int brep = 0x7fffffff;
+        for (int j = 0; j < nu; j++) {
+            int u = nbr[s + j];
+            int mu = mate[u];
+            if (mu < 0) continue;  // cannot happen for a maximal matching
+            int rep = e0[mu];
+            uint64_t k = f64_key(cost[adj_eid[s + j]]);
+            if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
+        }
+        if (brep == 0x7fffffff) continue;
+        int slot = append_slot(ncand);
+        chi[slot] = bk;
+        clo[slot] = ((uint64_t)(unsigned)brep << 32) | (unsigned)v;
+        cseg[slot] = b;
+        cpay[slot] = v;
+        caux[slot] = brep;
+        if (vmesh) atomicAdd(seg_cnt + b, 1);
+        else append_slot(seg_cnt);
+    }
+}
+
+struct RoundFail {
+    int* abort;
+    int* fail_ach;     // per mesh: achievable vertices (first failure), -1 = ok
+    int* fail_round;   // per mesh
+    int* fail_noedge;  // per mesh: the failing round had no edges (decimate.py:239-244)
+};
+
+__global__ void k_absorb_apply(const int* __restrict__ ncand, const uint64_t* __restrict__ chi,
+                               const uint64_t* __restrict__ clo, const int* __restrict__ cseg,
+                               const int* __restrict__ cpay, const int* __restrict__ caux,
+                               const int* __restrict__ mode, const uint64_t* __restrict__ thi,
+                               const uint64_t* __restrict__ tlo, int* __restrict__ absorbed, int B,
+                               const int* __restrict__ act, const int* __restrict__ budget,
+                               const int* __restrict__ nin, const int* __restrict__ ksel, int* __restrict__ removed,
+                               const int* __restrict__ eoff, const int* __restrict__ voff, RoundFail fail, int round) {
+    const int n = *ncand;
+    int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int i = tid; i < n; i += nth) {
+        int b = cseg[i];
+        if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) absorbed[cpay[i]] = caux[i];
+    }
+    for (int b = tid; b < B; b += nth) {
+        if (!act[b]) continue;
+        int r = removed[b] + ksel[b];
+        removed[b] = r;
+        if (r < budget[b]) {
+            if (fail.fail_ach[b] < 0) {
+                fail.fail_ach[b] = nin[b] - r;
+                fail.fail_round[b] = round;
+                fail.fail_noedge[b] = (eoff[voff[b + 1]] == eoff[voff[b]]);
+            }
+            atomicExch(fail.abort, 1);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// K7: relabel (decimate.py:130-137, 275-278).  Cluster anchor = lower end of
+// the matched pair; output index = rank of the cluster's lowest member.
+__global__ void k_relabel1(int N, const int* __restrict__ abort_flag, const int* __restrict__ mate,
+                           const int* __restrict__ e0, const int* __restrict__ absorbed, int* __restrict__ anchor,
+                           int* __restrict__ minrep) {
+    if (*abort_flag) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        int m = mate[v], a = v;
+        if (m >= 0) a = e0[m];
+        else if (absorbed[v] >= 0) {
+            a = absorbed[v];
+            atomicMin(minrep + a, v);
+        }
+        anchor[v] = a;
+    }
+}
+__global__ void k_relabel2(int N, const int* __restrict__ abort_flag, const int* __restrict__ anchor,
+                           const int* __restrict__ minrep, int* __restrict__ isrep) {
+    if (*abort_flag) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x)
+        isrep[v] = (minrep[anchor[v]] == v);
+}
+__global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int* __restrict__ anchor,
+                           const int* __restrict__ minrep, const int* __restrict__ outidx, int* __restrict__ rstep,
+                           int* __restrict__ ccount) {
+    if (*abort_flag) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        int r = outidx[minrep[anchor[v]]];
+        rstep[v] = r;
+        atomicAdd(ccount + r, 1);
+    }
+}
+
+// Generic CSR scatter of items by key (order fixed afterwards by the segment sort).
+__global__ void k_csr_scatter(int n, const int* __restrict__ abort_flag, const int* __restrict__ key,
+                              const int* __restrict__ off, int* __restrict__ cursor, int* __restrict__ members) {
+    if (abort_flag && *abort_flag) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        int r = key[v];
+        members[off[r] + atomicAdd(cursor + r, 1)] = v;
+    }
+}
+
+// Thread tier of the member sort; longer segments go to the heavy list.
+__global__ void k_seg_sort_small(int nseg, const int* __restrict__ abort_flag, const int* __restrict__ off,
+                                 int* __restrict__ members, int* __restrict__ heavy, int* __restrict__ heavy_count) {
+    if (abort_flag && *abort_flag) return;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nseg; r += gridDim.x * blockDim.x) {
+        int s = off[r], d = off[r + 1] - s;
+        if (d <= 1) continue;
+        if (d > kSmallDeg) {
+            heavy[append_slot(heavy_count)] = r;
+            continue;
+        }
+        int k[kSmallDeg];
+        for (int i = 0; i < d; i++) k[i] = members[s + i];
+        isort<kSmallDeg>(k, d);
+        for (int i = 0; i < d; i++) members[s + i] = k[i];
+    }
+}
+__global__ void __launch_bounds__(256) k_seg_sort_heavy(const int* __restrict__ abort_flag,
+                                                        const int* __restrict__ off, int* __restrict__ members,
+                                                        int* __restrict__ tmp, const int* __restrict__ heavy,
+                                                        const int* __restrict__ heavy_count) {
+    __shared__ int smem[kChunk];
+    if (abort_flag && *abort_flag) return;
+    const int H = *heavy_count;
+    for (int h = blockIdx.x; h < H; h += gridDim.x) {
+        int r = heavy[h];
+        int s = off[r], d = off[r + 1] - s;
+        block_sort_ints(members + s, tmp + s, d, smem);
+    }
+}
+
+// K8: contraction by member mean (decimate.py:280-283) and feature mean
+// (decimate.py:142-145): fold from +0.0 in ascending member order, then
+// divide by the count.  Inactive (bypassed) meshes copy rows verbatim.
+__global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const int* __restrict__ coff,
+                           const int* __restrict__ members, const int* __restrict__ vmesh,
+                           const int* __restrict__ act, const double* __restrict__ P, const double* __restrict__ X,
+                           int C, double* __restrict__ Pout, double* __restrict__ Xout) {
+    if (*abort_flag) return;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < Nout; r += gridDim.x * blockDim.x) {
+        int s = coff[r], d = coff[r + 1] - s;
+        int v0 = members[s];
+        if (!act[mesh_of(vmesh, v0)]) {
+            Pout[3 * r] = P[3 * v0];
+            Pout[3 * r + 1] = P[3 * v0 + 1];
+            Pout[3 * r + 2] = P[3 * v0 + 2];
+            if (X)
+                for (int k = 0; k < C; k++) Xout[(size_t)r * C + k] = X[(size_t)v0 * C + k];
+            continue;
+        }
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        for (int i = 0; i < d; i++) {
+            int v = members[s + i];
+            sx = sx + P[3 * v];
+            sy = sy + P[3 * v + 1];
+            sz = sz + P[3 * v + 2];
+        }
+        double cnt = (double)d;
+        Pout[3 * r] = sx / cnt;
+        Pout[3 * r + 1] = sy / cnt;
+        Pout[3 * r + 2] = sz / cnt;
+        if (X) {
+            for (int k = 0; k < C; k++) {
+                double acc = 0.0;
+                for (int i = 0; i < d; i++) acc = acc + X[(size_t)members[s + i] * C + k];
+                Xout[(size_t)r * C + k] = acc / cnt;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// K9: output facets (decimate.py:147-167).
+MF_DEV uint32_t tri_hash(int a, int b, int c) {
+    uint32_t h = (uint32_t)a * 0x9E3779B1u;
+    h ^= (uint32_t)b * 0x85EBCA77u + (h << 6) + (h >> 2);
+    h ^= (uint32_t)c * 0xC2B2AE3Du + (h << 6) + (h >> 2);
+    h ^= h >> 16;
+    h *= 0x7feb352du;
+    h ^= h >> 15;
+    h *= 0x846ca68bu;
+    h ^= h >> 16;
+    return h;
+}
+
+__global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict__ abort_flag,
+                              const int* __restrict__ F, const int* __restrict__ rstep, const int* __restrict__ vmesh,
+                              const int* __restrict__ act, int* __restrict__ mapped, int4* __restrict__ canon,
+                              int* __restrict__ slot, unsigned char* __restrict__ has_live, int* __restrict__ table,
+                              unsigned tmask) {
+    if (*abort_flag) return;
+    const int M = *dM;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
+        int ia = F[3 * f], ib = F[3 * f + 1], ic = F[3 * f + 2];
+        int a = rstep[ia], b = rstep[ib], c = rstep[ic];
+        mapped[3 * f] = a;
+        mapped[3 * f + 1] = b;
+        mapped[3 * f + 2] = c;
+        if (!act[mesh_of(vmesh, ia)]) {  // bypass: kept verbatim (identity round keeps duplicates)
+            slot[f] = -2;
+            continue;
+        }
+        if (a == b || b == c || a == c) {
+            slot[f] = -1;
+            continue;
+        }
+        has_live[ia] = 1;
+        has_live[ib] = 1;
+        has_live[ic] = 1;
+        int lo = min(a, min(b, c)), hi = max(a, max(b, c)), mid = a + b + c - lo - hi;
+        canon[f] = make_int4(lo, mid, hi, 0);
+        __threadfence();
+        unsigned h = tri_hash(lo, mid, hi) & tmask;
+        while (true) {
+            int cur = __ldcg(table + h);
+            if (cur < 0) {
+                int prev = atomicCAS(table + h, -1, f);
+                if (prev < 0) break;
+                cur = prev;
+            }
+            int4 oc = __ldcg(canon + cur);
+            if (oc.x == lo && oc.y == mid && oc.z == hi) {
+                atomicMin(table + h, f);
+                break;
+            }
+            h = (h + 1) & tmask;
+        }
+        slot[f] = (int)h;
+    }
+}
+
+__global__ void k_facet_keep(const int* __restrict__ dM, int Mcap, const int* __restrict__ abort_flag,
+                             const int* __restrict__ slot, const int* __restrict__ table, int* __restrict__ keep) {
+    if (*abort_flag) return;
+    const int M = *dM;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < Mcap; f += gridDim.x * blockDim.x) {
+        int k = 0;
+        if (f < M) {
+            int s = slot[f];
+            k = (s == -2) ? 1 : (s >= 0 && table[s] == f);
+        }
+        keep[f] = k;  // zero tail: the scan runs over the host bound Mcap
+    }
+}
+
+__global__ void k_identity_index(int n, int* __restrict__ a, int* __restrict__ b) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = b[i] = i;
+}
+
+__global__ void k_facet_write(const int* __restrict__ dM, const int* __restrict__ abort_flag,
+                              const int* __restrict__ keep, const int* __restrict__ kout,
+                              const int* __restrict__ mapped, int* __restrict__ Fout, int B,
+                              const int* __restrict__ foff_in, int* __restrict__ foff_out) {
+    if (*abort_flag) return;
+    const int M = *dM;
+    int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int b = tid; b <= B; b += nth) foff_out[b] = kout[foff_in[b]];
+    for (int f = tid; f < M; f += nth) {
+        if (!keep[f]) continue;
+        int o = kout[f];
+        Fout[3 * o] = mapped[3 * f];
+        Fout[3 * o + 1] = mapped[3 * f + 1];
+        Fout[3 * o + 2] = mapped[3 * f + 2];
+    }
+}
+
+// K10: chain replace / mapping across rounds (decimate.py:380-381); the
+// round's mapping (decimate.py:159-167) is formed on the fly.
+__global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int* __restrict__ rstep,
+                          const int* __restrict__ inc_off, const unsigned char* __restrict__ has_live,
+                          const int* __restrict__ vmesh, const int* __restrict__ act, int* __restrict__ rt,
+                          int* __restrict__ mt, int first_round) {
+    if (*abort_flag) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N0; i += gridDim.x * blockDim.x) {
+        int r = first_round ? i : rt[i];
+        rt[i] = rstep[r];
+        int m = first_round ? i : mt[i];
+        if (m < 0) {
+            mt[i] = -1;
+            continue;
+        }
+        int ms = rstep[m];
+        if (act[mesh_of(vmesh, m)] && inc_off[m + 1] > inc_off[m] && !has_live[m]) ms = -1;
+        mt[i] = ms;
+    }
+}
+
+// ------------------------------------------------------------------------
+// boundary conversion / validation
+__global__ void k_facets_in(int64_t M, const int64_t* __restrict__ F64, int* __restrict__ F32, int B,
+                            const int64_t* __restrict__ voff, const int64_t* __restrict__ foff,
+                            int* __restrict__ bad) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < M; f += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = B;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (foff[mid] <= f) lo = mid; else hi = mid;
+        }
+        int64_t vlo = voff[lo], vhi = voff[lo + 1];
+        int64_t a = F64[3 * f], b = F64[3 * f + 1], c = F64[3 * f + 2];
+        bool ok = a >= vlo && a < vhi && b >= vlo && b < vhi && c >= vlo && c < vhi && a != b && b != c && a != c;
+        if (!ok) atomicMin(bad, (int)min(f, (int64_t)0x7ffffffe));
+        F32[3 * f] = (int)a;
+        F32[3 * f + 1] = (int)b;
+        F32[3 * f + 2] = (int)c;
+    }
+}
+__global__ void k_check_finite(int64_t n, const double* __restrict__ P, int* __restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(P[i])) atomicExch(bad, 1);
+}
+__global__ void k_f32_to_f64(int64_t n, const float* __restrict__ a, double* __restrict__ b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (double)a[i];
+}
+__global__ void k_i32_to_i64(int64_t n, const int* __restrict__ a, int64_t* __restrict__ b, int64_t add) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (int64_t)a[i] + add;
+}
+__global__ void k_f64_to_f32(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (float)a[i];
+}
+
+}  // namespace mf

@@ -1,0 +1,193 @@
+"""decimate_parallel on the GPU -- drop-in for the reference's decimate.py:45-382.
+
+`DecimationConfig`, `DecimationResult`, `VertexCluster`, `clusters`,
+`representative_vertices` and `decimate_parallel` keep the reference
+signatures, validation order, exception types and output dtypes
+(int64 replace/mapping/facets, float64 positions/features).  All compute runs
+in libmfgpu.so: one call decimates a TriMesh or a whole BatchedMesh through
+every round of its chain on one device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .mesh import BatchedMesh, TriMesh
+from .numerics import einsum_order
+
+SHUFFLE_BUCKET_FRACTION = 1e-12  # decimate.py:42 (the kernels use the same constant)
+
+
+@dataclass(frozen=True)
+class DecimationConfig:
+    """Settings of decimate_parallel (decimate.py:45-71)."""
+
+    target_vertices: int
+    placement: str = "average"
+    shuffle_seed: int | None = None
+    rounds: int | str = "auto"
+
+    def __post_init__(self):
+        if self.target_vertices < 1:
+            raise ValueError("target_vertices must be >= 1")
+        if self.placement not in ("average", "inverse"):
+            raise ValueError(f"unknown placement {self.placement!r}")
+        if self.rounds != "auto" and (not isinstance(self.rounds, int) or self.rounds < 0):
+            raise ValueError("rounds must be 'auto' or a non-negative integer")
+
+
+@dataclass
+class DecimationResult:
+    """Decimated mesh and the cluster tensors over the input vertices (decimate.py:74-92)."""
+
+    mesh: TriMesh | BatchedMesh
+    replace: np.ndarray
+    mapping: np.ndarray
+    reached_target: bool = True
+    _native: object = field(default=None, repr=False, compare=False)
+
+    @property
+    def n_vertices_in(self) -> int:
+        return len(self.replace)
+
+    @property
+    def n_vertices_out(self) -> int:
+        return self.mesh.n_vertices
+
+    def cluster_sizes(self) -> np.ndarray:
+        return np.bincount(self.replace, minlength=self.n_vertices_out)
+
+
+@dataclass(frozen=True)
+class VertexCluster:
+    members: tuple
+    representative: int
+
+
+def clusters(result: DecimationResult) -> list:
+    """Clusters ordered by output index, members ascending (decimate.py:103-115)."""
+    order = np.argsort(result.replace, kind="stable")
+    ids = result.replace[order]
+    cuts = np.flatnonzero(np.diff(ids)) + 1
+    groups = np.split(order, cuts) if len(order) else []
+    return [VertexCluster(tuple(int(v) for v in np.sort(g)), int(result.replace[g[0]])) for g in groups]
+
+
+def representative_vertices(result: DecimationResult) -> np.ndarray:
+    """Lowest input index of every output vertex's cluster (decimate.py:118-123)."""
+    n_in = len(result.replace)
+    rep = np.full(result.n_vertices_out, n_in, dtype=np.int64)
+    np.minimum.at(rep, result.replace, np.arange(n_in, dtype=np.int64))
+    return rep
+
+
+def round_targets(n_in: int, target: int, rounds) -> list:
+    """_round_targets (decimate.py:294-316), computed by the library."""
+    cap = 4096
+    buf = (ctypes.c_int64 * cap)()
+    k = _native.lib().mf_round_targets(n_in, target, -1 if rounds == "auto" else int(rounds), buf, cap)
+    return [int(buf[i]) for i in range(min(k, cap))]
+
+
+def pcg_state(seed) -> tuple:
+    """(state_hi, state_lo, inc_hi, inc_lo) of np.random.default_rng(seed) -- host setup of the
+    device PCG64 jump-ahead (decimate.py:190)."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m = (1 << 64) - 1
+    return (s >> 64, s & m, inc >> 64, inc & m)
+
+
+def _trusted_trimesh(positions, facets, features) -> TriMesh:
+    # outputs are valid by construction (no degenerate / out-of-range facets)
+    t = TriMesh.__new__(TriMesh)
+    t.positions, t.facets, t.features = positions, facets, features
+    return t
+
+
+def _make_config(config: DecimationConfig) -> _native.Config:
+    cfg = _native.Config()
+    cfg.target_vertices = int(config.target_vertices)
+    cfg.rounds = -1 if config.rounds == "auto" else int(config.rounds)
+    cfg.placement = 0 if config.placement == "average" else 1
+    cfg.seeded = 0 if config.shuffle_seed is None else 1
+    cfg.einsum_order = einsum_order()
+    if config.shuffle_seed is not None:
+        for i, w in enumerate(pcg_state(config.shuffle_seed)):
+            cfg.pcg_state[i] = w
+    return cfg
+
+
+def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None) -> DecimationResult:
+    """Cluster decimation to an exact vertex count (decimate.py:344-382), on the GPU.
+
+    Accepts a TriMesh or a BatchedMesh (every entry decimated to
+    config.target_vertices); raises InfeasibleTargetError naming the
+    achievable minimum, ValueError / StructuralError as the reference does.
+    """
+    batched = isinstance(mesh, BatchedMesh)
+    base = mesh.mesh if batched else mesh
+    P = np.ascontiguousarray(base.positions, dtype=np.float64)
+    F = np.ascontiguousarray(base.facets, dtype=np.int64)
+    X = base.features
+    same = X.dtype == np.float64 and X.shape == P.shape and np.array_equal(X.view(np.uint64), P.view(np.uint64))
+    Xc = None if same else np.ascontiguousarray(X)
+    view = _native.MeshView()
+    view.positions = P.ctypes.data
+    view.facets = F.ctypes.data if F.size else None
+    view.features = None if Xc is None else Xc.ctypes.data
+    view.features_dtype = _native.DTYPE_F32 if (Xc is not None and Xc.dtype == np.float32) else _native.DTYPE_F64
+    view.n, view.m = P.shape[0], F.shape[0]
+    view.c = X.shape[1]
+    if batched:
+        vo = np.ascontiguousarray(mesh.vertex_offsets, dtype=np.int64)
+        fo = np.ascontiguousarray(mesh.facet_offsets, dtype=np.int64)
+        view.vertex_offsets, view.facet_offsets, view.n_meshes = vo.ctypes.data, fo.ctypes.data, len(vo) - 1
+    cfg = _make_config(config)
+    if device is None:
+        device = _native.default_device()
+    ctx = _native.context(device)
+    handle = ctypes.c_void_p()
+    st = _native.Status()
+    _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(handle), ctypes.byref(st))
+    _native.raise_for(st)
+    dec = _native.Decimation(handle, device)
+    n_out, m_out, c = dec.n_out, dec.m_out, view.c
+    pos = np.empty((n_out, 3))
+    fac = np.empty((m_out, 3), dtype=np.int64)
+    feats_dtype = np.float64
+    # the identity result keeps the input feature dtype (decimate.py:172-174); any real round folds into float64
+    if Xc is not None and Xc.dtype == np.float32 and _all_identity(mesh, config):
+        feats_dtype = np.float32
+    feats = np.empty((n_out, c), dtype=feats_dtype)
+    rep = np.empty(dec.n_in, dtype=np.int64)
+    mp = np.empty(dec.n_in, dtype=np.int64)
+    B = dec.n_meshes
+    vo_out = np.empty(B + 1, dtype=np.int64)
+    fo_out = np.empty(B + 1, dtype=np.int64)
+    st = _native.Status()
+    _native.lib().mf_decimation_copy(
+        dec.handle, pos.ctypes.data, fac.ctypes.data if fac.size else None, feats.ctypes.data if feats.size else None,
+        _native.DTYPE_F32 if feats_dtype == np.float32 else _native.DTYPE_F64,
+        rep.ctypes.data if rep.size else None, mp.ctypes.data if mp.size else None,
+        vo_out.ctypes.data, fo_out.ctypes.data, None, ctypes.byref(st),
+    )
+    _native.raise_for(st)
+    rep.flags.writeable = False
+    out_mesh = _trusted_trimesh(pos, fac, feats)
+    if batched:
+        bm = BatchedMesh.__new__(BatchedMesh)
+        bm.mesh, bm.vertex_offsets, bm.facet_offsets = out_mesh, vo_out, fo_out
+        out_mesh = bm
+    return DecimationResult(mesh=out_mesh, replace=rep, mapping=mp, _native=dec)
+
+
+def _all_identity(mesh, config) -> bool:
+    if isinstance(mesh, BatchedMesh):
+        nv = np.diff(mesh.vertex_offsets)
+        return bool(np.all(nv == config.target_vertices))
+    return mesh.n_vertices == config.target_vertices

@@ -1,0 +1,28 @@
+"""Host numpy reduction-order probe.
+
+numpy's einsum('ij,ij->i') reduction order depends on the SIMD kernel the
+host dispatches to: on AVX-512 hosts a 3-term dot product is evaluated as
+(t0 + t2) + t1, elsewhere sequentially.  The reference's facet intercepts and
+pair costs inherit that order, so the CUDA kernels take it as a flag and the
+drop-in API probes the local numpy once, making results bit-identical to the
+reference run on the same host.
+"""
+
+import functools
+
+import numpy as np
+
+ORDER_LANE_SPLIT = 0  # (t0 + t2) + t1
+ORDER_SEQUENTIAL = 1  # (t0 + t1) + t2
+
+
+@functools.lru_cache(maxsize=None)
+def einsum_order() -> int:
+    ones = np.ones((1, 3))
+    a = float(np.einsum("ij,ij->i", np.array([[1e16, 1.0, -1e16]]), ones)[0])
+    b = float(np.einsum("ij,ij->i", np.array([[1.0, 1e16, -1e16]]), ones)[0])
+    if a == 1.0 and b == 0.0:
+        return ORDER_LANE_SPLIT
+    if a == 0.0 and b == 0.0:
+        return ORDER_SEQUENTIAL
+    raise RuntimeError(f"unsupported numpy einsum reduction order (probe {a}, {b})")
