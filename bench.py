@@ -1,0 +1,409 @@
+"""Benchmark of the decimation hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+One "step" = one decimate_parallel call from input to target, including every
+internal round; facets/s = input facets / step time.  The
+default workload is BASELINE.json configs[1]: delaunay_terrain(115_114,
+noise=0.02, seed=12) decimated to 41,449 vertices (paper Fig. 1 size).  With
+N > 1 GPUs (one process per GPU, torchrun) every rank decimates its own copy
+of the workload with no inter-GPU traffic ("scaling": "weak"); `value` is the
+whole-job facets/s over the max-over-ranks device time.
+
+Reported: `value` (device-resident inputs, CUDA events on the launching stream,
+L2 flushed between steps), `e2e` (public numpy API with pinned host inputs,
+H2D + D2H inside the timed region), `roofline` of the dominant kernel (timed
+live with CUDA events inside the timed region; algorithmic bytes from the
+per-round counts), `cpu_baseline` (the C oracle port of the reference on this
+host), `clocks` sampled during the timed region, `gpu_launches`.
+`--impl reference` times the reference's CPU algorithm (oracle port, all
+usable host threads) on the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per decimation step and facets/sec (1/2/4/8 B200) vs ref CPU; % HBM peak"
+# Picasso GPU decimation of the Fig. 1 mesh (115,114 v / 231,293 f -> 41,449 v) in 65 ms.
+PUBLISHED_FIG1_MS = 65.0
+PUBLISHED_FIG1_FACETS = 231_293
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+# ---------------------------------------------------------------- workloads
+def workload(name: str, rank: int):
+    from paper_2103_15076_b200 import synthetic as S
+    from paper_2103_15076_b200.mesh import concat_batch
+
+    if name == "cfg2":
+        return dict(mesh=S.delaunay_terrain(115_114, noise=0.02, seed=12), target=41_449,
+                    desc="delaunay_terrain(115114, noise=0.02, seed=12) -> 41449 vertices (BASELINE configs[1])")
+    if name == "cfg1":
+        return dict(mesh=S.icosphere(5), target=3585, desc="icosphere(5) -> 3585 vertices (configs[0])")
+    if name == "cfg4":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        per = 256 // world
+        meshes = [S.delaunay_terrain(2500, noise=0.02, seed=b) for b in range(rank * per, (rank + 1) * per)]
+        return dict(mesh=concat_batch(meshes), target=1250,
+                    desc=f"batch of {per} delaunay_terrain(2500, 0.02, seed=b) -> 1250 each (configs[3] slice)")
+    raise SystemExit(f"unknown --config {name}")
+
+
+# ---------------------------------------------------------------- helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+REASON_FIELDS = ["clocks_event_reasons.sw_power_cap", "clocks_event_reasons.hw_slowdown",
+                 "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown"]
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 50 ms while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = "index,clocks.sm,clocks.max.sm,utilization.gpu," + ",".join(REASON_FIELDS)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms",
+                 "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 4 + len(REASON_FIELDS):
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[4:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [r for r in rows if r[2] > 0] or rows
+        reasons = set()
+        for r in rows:
+            for name, val in zip(REASON_FIELDS, r[3]):
+                if val.lower().startswith("active"):
+                    reasons.add(name.split(".")[-1])
+        return {"sm_mhz": float(np.median([r[0] for r in loaded])), "sm_max_mhz": rows[0][1],
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+# Algorithmic bytes per launch of the main kernels, from one round's counts
+# (N, M, E vertices/facets/edges in, Nn/Mn out; int32 indices, float64 values).
+# Each byte a kernel must move at least once -- see DESIGN.md "Kernels".
+def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
+    N, M, E, Nn, Mn = r["N"], r["M"], r["E"], r["N_out"], r["M_out"]
+    table = {
+        "k_facet_plane": 12 * M + 24 * N + 32 * M + 4 * N,
+        "k_inc_scatter": 12 * M + 4 * N + 12 * M,
+        "k_vertex": 4 * N + 12 * M + 32 * M + 12 * M + 80 * N + 8 * E + 8 * N,
+        "k_edges": 8 * E + 16 * N + 80 * N + 24 * N + 8 * E + 8 * E + 8 * E + 8 * E + 12 * N,
+        "k_match": 8 * E + 8 * E + 8 * E + 8 * N + 8 * N,
+        "k_contract": 4 * N + 4 * Nn + 24 * N + 24 * Nn,
+        "k_facet_remap": 12 * M + 4 * N + 12 * M + 16 * M + 4 * M + N,
+        "k_compose": 8 * r.get("N0", N) + 4 * N,
+    }
+    v = table.get(name)
+    return None if v is None else float(v)
+
+
+def step_bytes(rounds: list, n0: int, C: int = 3) -> float:
+    """SURVEY.md §8(d) whole-step model: Σ_r 24N+24M+8CN+160N+48E+24N'+24M'+8CN' + 16·N0."""
+    b = 16.0 * n0
+    for r in rounds:
+        N, M, E, Nn, Mn = r["N"], r["M"], r["E"], r["N_out"], r["M_out"]
+        b += 24 * N + 24 * M + 8 * C * N + 160 * N + 48 * E + 24 * Nn + 24 * Mn + 8 * C * Nn
+    return b
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    wl = workload(args.config, 0)
+    mesh, target = wl["mesh"], wl["target"]
+    batched = hasattr(mesh, "vertex_offsets")
+    threads = os.cpu_count() or 1
+    base = mesh.mesh if batched else mesh
+    kw = dict(target=target, seed=None, threads=threads)
+    if batched:
+        kw.update(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets)
+    for _ in range(args.warmup):
+        O.decimate(base.positions, base.facets, None, **kw)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        O.decimate(base.positions, base.facets, None, **kw)
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * float(np.mean(times))
+    value = base.n_facets / (ms / 1e3)
+    cores = threads if batched else 1
+    sample = f"full {args.config} workload per step ({base.n_facets} facets), oracle port of the reference"
+    line = {"metric": METRIC, "value": value, "unit": "facets/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["desc"], "facets_in": base.n_facets, "vertices_in": base.n_vertices},
+            "cpu_baseline": {"value": value, "unit": "facets/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "facets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(mesh, target, budget_s=12.0):
+    """The C oracle (port of the reference path) on this host, single thread, bounded sample."""
+    from oracle import oracle as O
+
+    base = mesh.mesh if hasattr(mesh, "vertex_offsets") else mesh
+    kw = dict(target=target)
+    if hasattr(mesh, "vertex_offsets"):
+        kw.update(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets)
+    times = []
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s and len(times) < 50:
+        t = time.perf_counter()
+        O.decimate(base.positions, base.facets, None, **kw)
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * float(np.median(times))
+    return {"value": base.n_facets / (ms / 1e3), "unit": "facets/s", "cores": 1, "kind": "port",
+            "sample": f"{len(times)} full decimations of the same workload (median {ms:.1f} ms)"}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    import paper_2103_15076_b200 as mfg
+    from paper_2103_15076_b200 import _native
+    from paper_2103_15076_b200 import tensor as T
+
+    wl = workload(args.config, rank)
+    mesh, target = wl["mesh"], wl["target"]
+    batched = hasattr(mesh, "vertex_offsets")
+    base = mesh.mesh if batched else mesh
+    n_in, m_in = base.n_vertices, base.n_facets
+    V = torch.from_numpy(base.positions).to(dev)
+    Fd = torch.from_numpy(base.facets).to(dev)
+    nv = np.diff(mesh.vertex_offsets) if batched else None
+    nf = np.diff(mesh.facet_offsets) if batched else None
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        return T.decimate(V, Fd, nv, nf, target=target)
+
+    # warm-up (first one with every kernel timed, to name the dominant kernel)
+    _native.profile(1)
+    dd = step()
+    torch.cuda.synchronize()
+    breakdown = _native.profile_read()
+    _native.profile(0)
+    rounds = dd.round_stats()
+    for r in rounds:
+        r["N0"] = n_in
+    for _ in range(max(0, args.warmup - 1)):
+        step()
+    torch.cuda.synchronize()
+    total_ms = sum(v[0] for v in breakdown.values())
+    dominant = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
+
+    # ---------------- timed region: device-resident inputs
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    _native.launch_count(reset=True)
+    _native.profile(2, dominant)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    phys = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    with ClockSampler(phys) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[k].record()
+            step()
+            ends[k].record()
+        torch.cuda.synchronize()
+    launches = _native.launch_count() // args.steps
+    dom = _native.profile_read().get(dominant, (0.0, 0))
+    _native.profile(0)
+    if dist:
+        dist.barrier()
+    step_ms = float(np.sum([s.elapsed_time(e) for s, e in zip(starts, ends)])) / args.steps
+    t = torch.tensor([step_ms], device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t.item())
+    value = world * m_in / (step_ms_max / 1e3)
+
+    # ---------------- e2e: public numpy API, pinned host inputs, H2D + D2H inside
+    Pp = torch.empty((n_in, 3), dtype=torch.float64, pin_memory=True).numpy()
+    Fp = torch.empty((m_in, 3), dtype=torch.int64, pin_memory=True).numpy()
+    Pp[:] = base.positions
+    Fp[:] = base.facets
+    pm = mfg.TriMesh(Pp, Fp)
+    host_mesh = mfg.BatchedMesh(pm, mesh.vertex_offsets, mesh.facet_offsets) if batched else pm
+    cfg = mfg.DecimationConfig(target_vertices=target)
+    res = mfg.decimate_parallel(host_mesh, cfg)
+    e2e_t = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = mfg.decimate_parallel(host_mesh, cfg)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_ms = 1e3 * float(np.mean(e2e_t))
+    t = torch.tensor([e2e_ms], device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    out = res.mesh.mesh if batched else res.mesh
+    h2d = Pp.nbytes + Fp.nbytes
+    d2h = out.positions.nbytes + out.facets.nbytes + out.features.nbytes + res.replace.nbytes + res.mapping.nbytes
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_kind = load_peaks()
+    per_round = [kernel_bytes(dominant, r) for r in rounds]
+    dom_ms_per_step = dom[0] / args.steps if dom[1] else None
+    roof = {"kernel": dominant, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_kind}
+    if dom_ms_per_step and all(b is not None for b in per_round):
+        alg = float(sum(per_round))
+        achieved = alg / (dom_ms_per_step / 1e3) / 1e9
+        roof.update({"achieved": achieved, "frac": achieved / peak, "alg_bytes_per_step": alg,
+                     "launches_per_step": dom[1] / args.steps, "ms_per_step": dom_ms_per_step,
+                     "share_of_step": dom_ms_per_step / step_ms})
+    else:
+        roof.update({"achieved": None, "frac": None})
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(args.config, {}).get(dominant)
+    roof["traffic"] = traffic
+    whole = step_bytes(rounds, n_in)
+    roof["step_alg_bytes"] = whole
+    roof["step_frac"] = whole / (step_ms / 1e3) / 1e9 / peak
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(mesh, target)
+
+    vs = None
+    if args.config == "cfg2":
+        vs = value / (PUBLISHED_FIG1_FACETS / (PUBLISHED_FIG1_MS / 1e3))
+    line = {
+        "metric": METRIC, "value": value, "unit": "facets/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": vs, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "facets_in": m_in, "vertices_in": n_in, "target": target,
+                   "rounds": len(rounds), "l2": "flushed between timed steps (512 MiB memset, outside events)",
+                   "parallelism": f"replicas x{world}, one mesh per GPU, no collective" if world > 1 else "1 GPU"},
+        "clocks": clk.summary(),
+        "e2e": {"value": world * m_in / (e2e_ms / 1e3), "unit": "facets/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "paper_2103_15076_b200.decimate_parallel(TriMesh numpy, pinned) -> numpy"},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "kernels": {k: {"ms": round(v[0], 4), "share": round(v[0] / total_ms, 4), "launches": v[1]}
+                    for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:8]},
+        "round_stats": rounds,
+    }
+    if vs is not None:
+        line["vs_baseline_note"] = "value / (231,293 facets / 65 ms): Picasso Fig. 1 GPU decimation (RTX 2080 Ti)"
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and world == 1 and args.impl == "ours":
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", "--master-port=29533", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

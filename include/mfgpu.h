@@ -103,6 +103,9 @@ int mf_decimation_copy(const mf_decimation *res, double *positions, int64_t *fac
                        int32_t features_dtype, int64_t *replace, int64_t *mapping, int64_t *vertex_offsets,
                        int64_t *facet_offsets, void *stream, mf_status *status);
 void mf_decimation_free(mf_decimation *res);
+/* Per-round counts of the call (rows of 6: N, M, E, N_out, M_out, matching iterations);
+ * returns the number of rounds. */
+int32_t mf_decimation_round_stats(const mf_decimation *res, int64_t *out, int32_t cap_rounds);
 
 /* pool over a replace tensor (host/device int64[n]) or over a decimation's
  * own replace (res != NULL, replace ignored: reuses its device cluster CSR). */
@@ -113,6 +116,10 @@ int mf_unpool(mf_context *ctx, const mf_decimation *res, const int64_t *replace,
               const void *coarse, int32_t dtype, int64_t c, void *out, void *stream, mf_status *status);
 
 int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t *chain, int64_t cap);
+
+/* Per-kernel CUDA-event timing on the launching stream (mode 0 off, 1 all, 2 only `only`). */
+void mf_profile(int32_t mode, const char *only);
+int32_t mf_profile_read(char *names, int32_t name_cap, double *total_ms, int64_t *launches, int32_t cap);
 
 /* Number of kernels this library launched on the calling thread since the last reset. */
 int64_t mf_kernel_launch_count(int32_t reset);

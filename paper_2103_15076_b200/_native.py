@@ -100,6 +100,12 @@ def lib():
         L.mf_kernel_launch_count.argtypes = [_i32]
         L.mf_kernel_launch_count.restype = _i64
         L.mf_version.restype = ctypes.c_char_p
+        L.mf_profile.argtypes = [_i32, ctypes.c_char_p]
+        L.mf_profile_read.argtypes = [ctypes.c_char_p, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
+                                      _i32]
+        L.mf_profile_read.restype = _i32
+        L.mf_decimation_round_stats.argtypes = [_vp, ctypes.POINTER(_i64), _i32]
+        L.mf_decimation_round_stats.restype = _i32
         _lib = L
     return _lib
 
@@ -171,6 +177,34 @@ class Decimation:
             except Exception:
                 pass
             self.handle = None
+
+
+def round_stats(dec) -> list:
+    """Per-round dicts {N, M, E, N_out, M_out, ld_iters} of a decimation handle."""
+    cap = 256
+    buf = (_i64 * (6 * cap))()
+    k = lib().mf_decimation_round_stats(dec.handle, buf, cap)
+    keys = ("N", "M", "E", "N_out", "M_out", "ld_iters")
+    return [dict(zip(keys, (int(buf[6 * r + j]) for j in range(6)))) for r in range(k)]
+
+
+def profile(mode: int, only: str | None = None) -> None:
+    """Per-kernel CUDA-event timing: 0 off, 1 every kernel, 2 only the kernel named `only`."""
+    lib().mf_profile(mode, only.encode() if only else None)
+
+
+def profile_read() -> dict:
+    """{kernel: (total_ms, launches)} of the launches recorded since profile() was enabled."""
+    cap, width = 128, 64
+    names = ctypes.create_string_buffer(cap * width)
+    ms = (ctypes.c_double * cap)()
+    cnt = (_i64 * cap)()
+    k = lib().mf_profile_read(names, width, ms, cnt, cap)
+    out = {}
+    for i in range(min(k, cap)):
+        nm = names.raw[i * width:(i + 1) * width].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[i]), int(cnt[i]))
+    return out
 
 
 def launch_count(reset: bool = False) -> int:

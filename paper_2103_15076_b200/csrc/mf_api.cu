@@ -36,15 +36,13 @@ static int grid_n(int64_t n) {
 static int copy_i32_as_i64(const int* src, int64_t n, int64_t* dst, cudaStream_t s, mf_status* st) {
     if (!dst || n <= 0) return MF_OK;
     if (is_device_ptr(dst)) {
-        k_i32_to_i64<<<grid_n(n), 256, 0, s>>>(n, src, dst, 0);
-        g_launches++;
+        LAUNCH(k_i32_to_i64, grid_n(n), 256, 0, s, n, src, dst, 0);
         MF_CUDA_TRY(cudaGetLastError());
         return MF_OK;
     }
     int64_t* tmp = nullptr;
     MF_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * 8, s));
-    k_i32_to_i64<<<grid_n(n), 256, 0, s>>>(n, src, tmp, 0);
-    g_launches++;
+    LAUNCH(k_i32_to_i64, grid_n(n), 256, 0, s, n, src, tmp, 0);
     MF_CUDA_TRY(cudaMemcpyAsync(dst, tmp, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
     MF_CUDA_TRY(cudaFreeAsync(tmp, s));
     return MF_OK;
@@ -57,14 +55,12 @@ static int copy_f64_as(const double* src, int64_t n, void* dst, int dtype, cudaS
         return MF_OK;
     }
     if (is_device_ptr(dst)) {
-        k_f64_to_f32<<<grid_n(n), 256, 0, s>>>(n, src, (float*)dst);
-        g_launches++;
+        LAUNCH(k_f64_to_f32, grid_n(n), 256, 0, s, n, src, (float*)dst);
         return MF_OK;
     }
     float* tmp = nullptr;
     MF_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * 4, s));
-    k_f64_to_f32<<<grid_n(n), 256, 0, s>>>(n, src, tmp);
-    g_launches++;
+    LAUNCH(k_f64_to_f32, grid_n(n), 256, 0, s, n, src, tmp);
     MF_CUDA_TRY(cudaMemcpyAsync(dst, tmp, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
     MF_CUDA_TRY(cudaFreeAsync(tmp, s));
     return MF_OK;
@@ -263,6 +259,14 @@ int mf_unpool(mf_context* ctx, const mf_decimation* res, const int64_t* replace,
     return rc;
 }
 
+int32_t mf_decimation_round_stats(const mf_decimation* res, int64_t* out, int32_t cap_rounds) {
+    if (!res) return -1;
+    int32_t R = (int32_t)(res->r.round_stats.size() / 6);
+    for (int32_t i = 0; i < R && i < cap_rounds; i++)
+        for (int k = 0; k < 6; k++) out[6 * i + k] = res->r.round_stats[6 * i + k];
+    return R;
+}
+
 int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t* chain, int64_t cap) {
     std::vector<int64_t> v;
     round_targets(n_in, target, rounds, v);
@@ -277,5 +281,43 @@ int64_t mf_kernel_launch_count(int32_t reset) {
 }
 
 const char* mf_version(void) { return "mfgpu 0.1.0 (sm_100a)"; }
+
+/* Per-kernel CUDA-event timing on the launching stream.  mode 0 = off,
+ * 1 = every kernel, 2 = only the kernel named `only` (e.g. "k_match").
+ * Enabling clears earlier records. */
+void mf_profile(int32_t mode, const char* only) {
+    g_prof_mode = mode;
+    g_prof_only = only ? only : "";
+    g_prof_recs.clear();
+    g_prof_pool_used = 0;
+}
+/* Aggregate the recorded launches (synchronises the device): fills up to
+ * `cap` rows of names / total milliseconds / launch counts, returns the
+ * number of distinct kernels. */
+int32_t mf_profile_read(char* names, int32_t name_cap, double* total_ms, int64_t* launches, int32_t cap) {
+    cudaDeviceSynchronize();
+    std::vector<std::string> keys;
+    std::vector<double> ms;
+    std::vector<int64_t> cnt;
+    for (const ProfRec& r : g_prof_recs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        size_t k = 0;
+        while (k < keys.size() && keys[k] != r.name) k++;
+        if (k == keys.size()) {
+            keys.push_back(r.name);
+            ms.push_back(0.0);
+            cnt.push_back(0);
+        }
+        ms[k] += t;
+        cnt[k]++;
+    }
+    for (size_t k = 0; k < keys.size() && (int32_t)k < cap; k++) {
+        snprintf(names + k * name_cap, name_cap, "%s", keys[k].c_str());
+        total_ms[k] = ms[k];
+        launches[k] = cnt[k];
+    }
+    return (int32_t)keys.size();
+}
 
 }  // extern "C"

@@ -26,10 +26,46 @@ namespace mf {
 
 thread_local int64_t g_launches = 0;
 
+// ---- optional per-kernel timing (CUDA events on the launching stream) ----
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+thread_local int g_prof_mode = 0;  // 0 off, 1 every launch, 2 only kernels named g_prof_only
+thread_local std::string g_prof_only;
+thread_local std::vector<ProfRec> g_prof_recs;
+thread_local std::vector<cudaEvent_t> g_prof_pool;
+thread_local size_t g_prof_pool_used = 0;
+
+static cudaEvent_t prof_event() {
+    if (g_prof_pool_used == g_prof_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        g_prof_pool.push_back(e);
+    }
+    return g_prof_pool[g_prof_pool_used++];
+}
+static bool prof_on(const char* name) {
+    if (g_prof_mode == 1) return true;
+    return g_prof_mode == 2 && g_prof_only == name;
+}
+void prof_pre(const char* name, cudaStream_t s) {
+    if (!prof_on(name)) return;
+    ProfRec r{name, prof_event(), prof_event()};
+    cudaEventRecord(r.a, s);
+    g_prof_recs.push_back(r);
+}
+void prof_post(const char* name, cudaStream_t s) {
+    if (!prof_on(name)) return;
+    cudaEventRecord(g_prof_recs.back().b, s);
+}
+
 #ifndef LAUNCH
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                 \
     do {                                                               \
+        prof_pre(#kernel, stream);                                     \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);    \
+        prof_post(#kernel, stream);                                    \
         g_launches++;                                                  \
     } while (0)
 #endif
@@ -84,9 +120,11 @@ static void run_scan(const Context* ctx, ScanBuf& sb, const int* in, int* out, i
     (void)ctx;
 }
 
-static int coop_launch(const void* fn, int blocks, int threads, void* arg, cudaStream_t s) {
+static int coop_launch(const char* name, const void* fn, int blocks, int threads, void* arg, cudaStream_t s) {
     void* args[] = {arg};
+    prof_pre(name, s);
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(threads), args, 0, s);
+    prof_post(name, s);
     g_launches++;
     return e == cudaSuccess ? 0 : (int)e;
 }
@@ -305,6 +343,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         W.fo64 = A.template take<int64_t>((size_t)B + 1);
         W.F64 = A.template take<int64_t>((size_t)Mcap * 3);
         W.Xf32 = A.template take<float>((size_t)N0 * C);
+        W.stats = A.template take<int>((size_t)std::max(R, 1) * 4);
     };
     struct WS {
         int* params; int* F0; double* P0; double* X0; double *Pa, *Pb, *Xa, *Xb; int *Fa, *Fb, *foff_a, *foff_b;
@@ -315,7 +354,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         uint64_t *chi, *clo; int *cseg, *cpay, *caux, *seg_cnt, *ksel, *mode, *krem; uint64_t *p_hi, *p_lo;
         int *hist, *removed, *fail, *absorbed, *minrep, *anchor, *isrep, *outidx, *rstep, *ccount, *coff, *cmem;
         unsigned char* has_live; int* mapped; int4* canon; int *slot, *keep, *kout; unsigned tsize; int* table;
-        ScanBuf scan; int64_t *vo64, *fo64, *F64; float* Xf32;
+        ScanBuf scan; int64_t *vo64, *fo64, *F64; float* Xf32; int* stats;
     } W;
     {
         Arena meas;
@@ -342,7 +381,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     // ---- params upload (one pinned H2D): act | budget | nin(R+1) | voff(R+1)
     size_t pw = (size_t)nParamR * B * 3 + (size_t)(R + 1) * (B + 1) + (size_t)(R + 1) * B;
     size_t pin_need = pw * sizeof(int) + 8 * sizeof(int64_t) * (size_t)(B + 1) + 4096 + (size_t)(B + 1) * 8 +
-                      (size_t)B * 12;
+                      (size_t)B * 12 + (size_t)R * 16 + 64;
     if (ctx->pinned_bytes < pin_need) {
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         ctx->pinned = nullptr;
@@ -477,7 +516,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.e0, W.e1, W.key_hi, seeded ? W.key_lo : nullptr,
                          W.mate, W.best, W.front0, W.front1, d_ninc, W.bar};
             int blocks = std::max(1, std::min(ctx->coop_blocks_match, (N + 255) / 256));
-            coop_err |= coop_launch((const void*)k_match, blocks, 256, &ma, stream);
+            coop_err |= coop_launch("k_match", (const void*)k_match, blocks, 256, &ma, stream);
         }
         // budget truncation (select the `budget` lowest-ranked matched edges per mesh)
         auto select = [&](const int* removed_in) {
@@ -487,7 +526,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             SelectArgs sa{d_ncand, W.chi, W.clo, W.cseg, B, W.seg_cnt, act, budget, removed_in, W.ksel, W.mode,
                           W.p_hi, W.p_lo, W.krem, W.hist, d_notdone, W.bar};
             int blocks = std::max(1, std::min(ctx->coop_blocks_select, (N / 2 + 255) / 256));
-            coop_err |= coop_launch((const void*)k_select, blocks, 256, &sa, stream);
+            coop_err |= coop_launch("k_select", (const void*)k_select, blocks, 256, &sa, stream);
         };
         cudaMemsetAsync(W.seg_cnt, 0, (size_t)B * sizeof(int), stream);
         LAUNCH(k_trunc_cand, grid_for(ctx, N), 256, 0, stream, N, W.mate, W.e0, W.key_hi, seeded ? W.key_lo : nullptr,
@@ -534,6 +573,10 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
                foff_c, foff_n);
         LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
                res->replace, res->mapping, r == 0);
+        cudaMemcpyAsync(W.stats + 4 * r + 0, foff_c + B, sizeof(int), cudaMemcpyDeviceToDevice, stream);
+        cudaMemcpyAsync(W.stats + 4 * r + 1, W.eoff + N, sizeof(int), cudaMemcpyDeviceToDevice, stream);
+        cudaMemcpyAsync(W.stats + 4 * r + 2, foff_n + B, sizeof(int), cudaMemcpyDeviceToDevice, stream);
+        cudaMemcpyAsync(W.stats + 4 * r + 3, d_ninc + 2, sizeof(int), cudaMemcpyDeviceToDevice, stream);
         Pc = Pn;
         Xc = Xn;
         Fc = Fn;
@@ -563,6 +606,9 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     MF_CUDA_TRY(cudaMemcpyAsync(h_st + 8, foff_c, (B + 1) * sizeof(int), cudaMemcpyDeviceToHost, stream));
     MF_CUDA_TRY(cudaMemcpyAsync(h_st + 8 + B + 1, W.fail, (size_t)B * 3 * sizeof(int), cudaMemcpyDeviceToHost,
                                 stream));
+    int* h_stats = h_st + 8 + B + 1 + 3 * B;
+    if (R > 0)
+        MF_CUDA_TRY(cudaMemcpyAsync(h_stats, W.stats, (size_t)R * 4 * sizeof(int), cudaMemcpyDeviceToHost, stream));
     MF_CUDA_TRY(cudaStreamSynchronize(stream));
     MF_CUDA_TRY(cudaGetLastError());
     const int* h_fo = h_st + 8;
@@ -611,6 +657,11 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         return st->code;
     }
     res->m_out = (R == 0) ? m : h_fo[B];
+    for (int r = 0; r < R; r++) {
+        int64_t row[6] = {h_N[r], h_stats[4 * r], h_stats[4 * r + 1], h_N[r + 1], h_stats[4 * r + 2],
+                          h_stats[4 * r + 3]};
+        res->round_stats.insert(res->round_stats.end(), row, row + 6);
+    }
     res->vertex_offsets.resize(B + 1);
     res->facet_offsets.resize(B + 1);
     for (int b = 0; b <= B; b++) {

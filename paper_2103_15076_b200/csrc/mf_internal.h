@@ -61,6 +61,7 @@ struct Result {
     int* replace = nullptr;       // n_in
     int* mapping = nullptr;       // n_in
     std::vector<int64_t> vertex_offsets, facet_offsets;
+    std::vector<int64_t> round_stats;  // per round: N, M, E, N', M', LD iterations
     void* block = nullptr;        // single allocation backing all arrays
     // cluster CSR of `replace` for pooling (built lazily)
     int* csr_off = nullptr;

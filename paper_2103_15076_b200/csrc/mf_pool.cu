@@ -15,13 +15,7 @@
 
 namespace mf {
 
-#ifndef LAUNCH
-#define LAUNCH(kernel, grid, block, smem, stream, ...)              \
-    do {                                                            \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__); \
-        g_launches++;                                               \
-    } while (0)
-#endif
+
 
 static int grid_of(const Context* ctx, int64_t n, int block = 256) {
     int64_t g = (n + block - 1) / block;

@@ -1,0 +1,137 @@
+"""Device-tensor API: decimation and pooling on CUDA tensors (no host copies).
+
+`decimate(vertices, faces, nv, mf, target, ...)` takes batched float64
+vertices [N,3] and int64 faces [M,3] resident on a CUDA device plus per-mesh
+vertex / facet counts, and returns decimated vertices / faces / counts and
+the cluster `replace` / `mapping` index tensors on the same device -- the
+north-star interface ("batched vertices/faces/nv/mf go in, decimated
+vertices/faces plus cluster representative and map indices come out").
+torch is only the allocator / stream here; all compute runs in libmfgpu.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .decimate import DecimationConfig, _make_config
+
+_POOL_MODES = ("average", "max", "weighted", "sum")
+
+
+class DeviceDecimation:
+    """Outputs of one device decimation plus the library handle (reused by pool/unpool)."""
+
+    def __init__(self, dec, vertices, faces, features, nv, mf, replace, mapping):
+        self._dec = dec
+        self.vertices, self.faces, self.features = vertices, faces, features
+        self.nv, self.mf = nv, mf
+        self.replace, self.mapping = replace, mapping
+
+    @property
+    def n_vertices_out(self) -> int:
+        return self._dec.n_out
+
+    def round_stats(self) -> list:
+        return _native.round_stats(self._dec)
+
+
+def _offsets(counts, total) -> np.ndarray:
+    if counts is None:
+        return None
+    c = np.asarray(counts.cpu() if torch.is_tensor(counts) else counts, dtype=np.int64)
+    off = np.zeros(len(c) + 1, dtype=np.int64)
+    np.cumsum(c, out=off[1:])
+    if off[-1] != total:
+        raise ValueError(f"counts sum to {off[-1]}, expected {total}")
+    return off
+
+
+def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, target: int = 1,
+             placement: str = "average", seed=None, rounds="auto", features: torch.Tensor | None = None,
+             copy_outputs: bool = True) -> DeviceDecimation:
+    if not vertices.is_cuda or not faces.is_cuda:
+        raise ValueError("vertices / faces must be CUDA tensors")
+    if vertices.dtype != torch.float64 or faces.dtype != torch.int64:
+        raise ValueError("vertices must be float64 and faces int64")
+    vertices = vertices.contiguous()
+    faces = faces.contiguous()
+    dev = vertices.device
+    view = _native.MeshView()
+    view.positions = vertices.data_ptr()
+    view.facets = faces.data_ptr() if faces.numel() else None
+    view.n, view.m = vertices.shape[0], faces.shape[0]
+    if features is not None:
+        features = features.contiguous()
+        view.features = features.data_ptr()
+        view.features_dtype = _native.DTYPE_F32 if features.dtype == torch.float32 else _native.DTYPE_F64
+        view.c = features.shape[1]
+    else:
+        view.c = 3
+    vo = _offsets(nv, view.n)
+    fo = _offsets(mf, view.m)
+    if vo is not None:
+        view.vertex_offsets, view.facet_offsets, view.n_meshes = vo.ctypes.data, fo.ctypes.data, len(vo) - 1
+    cfg = _make_config(DecimationConfig(target_vertices=target, placement=placement, shuffle_seed=seed,
+                                        rounds=rounds))
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ctx = _native.context(dev.index)
+    handle = ctypes.c_void_p()
+    st = _native.Status()
+    _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), ctypes.c_void_p(stream),
+                              ctypes.byref(handle), ctypes.byref(st))
+    _native.raise_for(st)
+    dec = _native.Decimation(handle, dev.index)
+    if not copy_outputs:
+        return DeviceDecimation(dec, None, None, None, None, None, None, None)
+    B = dec.n_meshes
+    V = torch.empty((dec.n_out, 3), dtype=torch.float64, device=dev)
+    Fo = torch.empty((dec.m_out, 3), dtype=torch.int64, device=dev)
+    X = torch.empty((dec.n_out, dec.c), dtype=torch.float64, device=dev)
+    R = torch.empty(dec.n_in, dtype=torch.int64, device=dev)
+    Mp = torch.empty(dec.n_in, dtype=torch.int64, device=dev)
+    vo_out = np.empty(B + 1, dtype=np.int64)
+    fo_out = np.empty(B + 1, dtype=np.int64)
+    st = _native.Status()
+    _native.lib().mf_decimation_copy(
+        dec.handle, V.data_ptr() if V.numel() else None, Fo.data_ptr() if Fo.numel() else None,
+        X.data_ptr() if X.numel() else None, _native.DTYPE_F64, R.data_ptr() if R.numel() else None,
+        Mp.data_ptr() if Mp.numel() else None, vo_out.ctypes.data, fo_out.ctypes.data, ctypes.c_void_p(stream),
+        ctypes.byref(st))
+    _native.raise_for(st)
+    nv_out = torch.from_numpy(np.diff(vo_out))
+    mf_out = torch.from_numpy(np.diff(fo_out))
+    return DeviceDecimation(dec, V, Fo, X, nv_out, mf_out, R, Mp)
+
+
+def pool(features: torch.Tensor, dd: DeviceDecimation, mode: str = "average", weights=None) -> torch.Tensor:
+    if mode not in _POOL_MODES:
+        raise ValueError(f"mode must be one of {_POOL_MODES}, got {mode!r}")
+    features = features.contiguous()
+    dev = features.device
+    out = torch.empty((dd.n_vertices_out, features.shape[1]), dtype=features.dtype, device=dev)
+    w = None if weights is None else weights.to(dtype=features.dtype).contiguous()
+    st = _native.Status()
+    _native.lib().mf_pool(
+        _native.context(dev.index), dd._dec.handle, None, dd._dec.n_in, dd._dec.n_out, features.data_ptr(),
+        _native.DTYPE_F32 if features.dtype == torch.float32 else _native.DTYPE_F64, features.shape[1],
+        _POOL_MODES.index(mode), None if w is None else w.data_ptr(), out.data_ptr(),
+        ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), ctypes.byref(st))
+    _native.raise_for(st)
+    return out
+
+
+def unpool(coarse: torch.Tensor, dd: DeviceDecimation) -> torch.Tensor:
+    coarse = coarse.contiguous()
+    dev = coarse.device
+    out = torch.empty((dd._dec.n_in, coarse.shape[1]), dtype=coarse.dtype, device=dev)
+    st = _native.Status()
+    _native.lib().mf_unpool(
+        _native.context(dev.index), dd._dec.handle, None, dd._dec.n_in, dd._dec.n_out, coarse.data_ptr(),
+        _native.DTYPE_F32 if coarse.dtype == torch.float32 else _native.DTYPE_F64, coarse.shape[1],
+        out.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), ctypes.byref(st))
+    _native.raise_for(st)
+    return out
