@@ -254,7 +254,11 @@ def run_ours(args):
     def step():
         return T.decimate(V, Fd, nv, nf, target=target)
 
-    # warm-up (first one with every kernel timed, to name the dominant kernel)
+    # warm-up; the last warm-up step times every kernel to name the dominant one
+    for _ in range(max(0, args.warmup - 1)):
+        step()
+    torch.cuda.synchronize()
+    flush.zero_()
     _native.profile(1)
     dd = step()
     torch.cuda.synchronize()
@@ -263,9 +267,6 @@ def run_ours(args):
     rounds = dd.round_stats()
     for r in rounds:
         r["N0"] = n_in
-    for _ in range(max(0, args.warmup - 1)):
-        step()
-    torch.cuda.synchronize()
     total_ms = sum(v[0] for v in breakdown.values())
     dominant = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
 

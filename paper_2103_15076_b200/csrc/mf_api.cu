@@ -91,12 +91,7 @@ int mf_context_create(int device, mf_context** out) {
         return MF_ERR_CUDA;
     }
     c->c.sm_count = prop.multiProcessorCount;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_match, 256, 0);
-    c->c.coop_blocks_match = std::max(1, occ) * prop.multiProcessorCount;
-    occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_select, 256, 0);
-    c->c.coop_blocks_select = std::max(1, occ) * prop.multiProcessorCount;
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmem);
     // keep freed stream-ordered allocations cached in the device pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -111,6 +106,7 @@ int mf_context_create(int device, mf_context** out) {
 void mf_context_destroy(mf_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
+    drop_graphs(&ctx->c);
     if (ctx->c.arena) cudaFree(ctx->c.arena);
     if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
     delete ctx;
@@ -283,33 +279,35 @@ int64_t mf_kernel_launch_count(int32_t reset) {
 const char* mf_version(void) { return "mfgpu 0.1.0 (sm_100a)"; }
 
 /* Per-kernel CUDA-event timing on the launching stream.  mode 0 = off,
- * 1 = every kernel, 2 = only the kernel named `only` (e.g. "k_match").
- * Enabling clears earlier records. */
+ * 1 = every kernel, 2 = only the kernel named `only` (e.g. "k_suitor").
+ * Enabling clears earlier records.  Graph replays are timed through event
+ * nodes captured with the graph. */
 void mf_profile(int32_t mode, const char* only) {
+    cudaDeviceSynchronize();
+    prof_collect_pending();
     g_prof_mode = mode;
     g_prof_only = only ? only : "";
     g_prof_recs.clear();
-    g_prof_pool_used = 0;
+    g_prof_done.clear();
 }
-/* Aggregate the recorded launches (synchronises the device): fills up to
- * `cap` rows of names / total milliseconds / launch counts, returns the
- * number of distinct kernels. */
+/* Aggregate the timed launches (synchronises the device): fills up to `cap`
+ * rows of names / total milliseconds / launch counts, returns the number of
+ * distinct kernels. */
 int32_t mf_profile_read(char* names, int32_t name_cap, double* total_ms, int64_t* launches, int32_t cap) {
     cudaDeviceSynchronize();
+    prof_collect_pending();
     std::vector<std::string> keys;
     std::vector<double> ms;
     std::vector<int64_t> cnt;
-    for (const ProfRec& r : g_prof_recs) {
-        float t = 0.f;
-        cudaEventElapsedTime(&t, r.a, r.b);
+    for (const auto& r : g_prof_done) {
         size_t k = 0;
-        while (k < keys.size() && keys[k] != r.name) k++;
+        while (k < keys.size() && keys[k] != r.first) k++;
         if (k == keys.size()) {
-            keys.push_back(r.name);
+            keys.push_back(r.first);
             ms.push_back(0.0);
             cnt.push_back(0);
         }
-        ms[k] += t;
+        ms[k] += r.second;
         cnt[k]++;
     }
     for (size_t k = 0; k < keys.size() && (int32_t)k < cap; k++) {

@@ -101,7 +101,9 @@ constexpr unsigned long long kFlagPre = 2ull << 32;
 
 template <typename LoadOp>
 __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, int* __restrict__ out,
-                                                          unsigned long long* status, int* ticket) {
+                                                          unsigned long long* status, int* ticket,
+                                                          const int* __restrict__ abort_flag) {
+    if (abort_flag && *abort_flag) return;  // a failed round: every later stage is skipped
     __shared__ int s_tile;
     __shared__ int s_warp[kScanBlock / 32];
     __shared__ int s_prefix;

@@ -4,8 +4,11 @@
 // launch sequence with no host synchronisation until the end: vertex counts
 // per round are known on the host (they are the round targets), facet and
 // edge counts stay on the device and every kernel reads them from there
-// (grids are sized from host upper bounds).  The single readback at the end
-// carries the status words and the output facet offsets.
+// (grids are sized from host upper bounds).  The sequence is captured once
+// per call shape into a CUDA graph and replayed: inputs are staged into fixed
+// workspace buffers, outputs copied into the result allocation, and one small
+// readback at the end carries status words, output facet offsets and the
+// per-round counts.
 //
 // Batches (BatchedMesh, decimate.py:354-361) are processed as one segmented
 // pipeline over the concatenated arrays: per-mesh budgets, per-mesh rank
@@ -17,6 +20,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "mf_internal.h"
@@ -33,7 +38,8 @@ struct ProfRec {
 };
 thread_local int g_prof_mode = 0;  // 0 off, 1 every launch, 2 only kernels named g_prof_only
 thread_local std::string g_prof_only;
-thread_local std::vector<ProfRec> g_prof_recs;
+thread_local std::vector<ProfRec> g_prof_recs;                         // recorded, not yet read
+thread_local std::vector<std::pair<std::string, float>> g_prof_done;  // (kernel, ms)
 thread_local std::vector<cudaEvent_t> g_prof_pool;
 thread_local size_t g_prof_pool_used = 0;
 
@@ -49,22 +55,55 @@ static bool prof_on(const char* name) {
     if (g_prof_mode == 1) return true;
     return g_prof_mode == 2 && g_prof_only == name;
 }
+// inside stream capture a plain cudaEventRecord only adds a dependency; the
+// External flag turns it into an event-record node that fires on every replay
+static void prof_record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
+}
 void prof_pre(const char* name, cudaStream_t s) {
     if (!prof_on(name)) return;
     ProfRec r{name, prof_event(), prof_event()};
-    cudaEventRecord(r.a, s);
+    prof_record(r.a, s);
     g_prof_recs.push_back(r);
 }
 void prof_post(const char* name, cudaStream_t s) {
     if (!prof_on(name)) return;
-    cudaEventRecord(g_prof_recs.back().b, s);
+    prof_record(g_prof_recs.back().b, s);
 }
+// after the stream synchronised: fold event pairs into the tallies
+static void prof_collect(const std::vector<ProfRec>& recs) {
+    for (const ProfRec& r : recs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        g_prof_done.emplace_back(r.name, t);
+    }
+}
+void prof_collect_pending() {
+    prof_collect(g_prof_recs);
+    g_prof_recs.clear();
+}
+
+// first failing runtime call of the current recording (error attribution)
+thread_local cudaError_t g_rec_err = cudaSuccess;
+thread_local int g_rec_line = 0;
+static void rec_check(cudaError_t e, int line) {
+    if (e != cudaSuccess && g_rec_err == cudaSuccess) {
+        g_rec_err = e;
+        g_rec_line = line;
+    }
+}
+#define RC(expr) rec_check((expr), __LINE__)
+#define RCK() rec_check(cudaGetLastError(), __LINE__)
 
 #ifndef LAUNCH
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                 \
     do {                                                               \
         prof_pre(#kernel, stream);                                     \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);    \
+        rec_check(cudaGetLastError(), __LINE__);                       \
         prof_post(#kernel, stream);                                    \
         g_launches++;                                                  \
     } while (0)
@@ -108,25 +147,451 @@ int64_t round_targets(int64_t n_in, int64_t target, int rounds, std::vector<int6
 
 struct ScanBuf {
     unsigned long long* status = nullptr;
-    int* ticket = nullptr;
-    size_t words = 0;
 };
 
-static void run_scan(const Context* ctx, ScanBuf& sb, const int* in, int* out, int n, cudaStream_t s) {
+template <typename LoadOp>
+static void run_scan(ScanBuf& sb, LoadOp op, int* out, int n, cudaStream_t s, const char* name,
+                     const int* abort_flag) {
     int tiles = std::max(1, (n + kScanTile - 1) / kScanTile);
-    cudaMemsetAsync(sb.status, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), s);
-    LAUNCH(k_scan_excl<LoadArr>, tiles, kScanBlock, 0, s, LoadArr{in}, n, out, sb.status,
-           reinterpret_cast<int*>(sb.status + tiles));
-    (void)ctx;
-}
-
-static int coop_launch(const char* name, const void* fn, int blocks, int threads, void* arg, cudaStream_t s) {
-    void* args[] = {arg};
+    RC(cudaMemsetAsync(sb.status, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), s));
     prof_pre(name, s);
-    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(threads), args, 0, s);
+    k_scan_excl<LoadOp><<<tiles, kScanBlock, 0, s>>>(op, n, out, sb.status, reinterpret_cast<int*>(sb.status + tiles),
+                                                     abort_flag);
+    RCK();
     prof_post(name, s);
     g_launches++;
-    return e == cudaSuccess ? 0 : (int)e;
+}
+
+// ------------------------------------------------------------------------
+// plan: everything the host knows before touching the device
+struct Plan {
+    int64_t n = 0, m = 0, C = 3;
+    bool alias = true;
+    int fdtype = MF_DTYPE_F64;
+    int B = 1, R = 0, first_err = 1, err_code = MF_OK;
+    char err_msg[256] = {0};
+    std::vector<int64_t> voff, foff;
+    std::vector<std::vector<int64_t>> chains;
+    std::vector<int> h_nin, h_act, h_budget, h_voff, h_N;
+    int N0 = 0, M0 = 0, Nfin = 0, Mcap = 1, Ecap = 3, N1 = 0, nParamR = 1;
+    bool seeded = false;
+    int order = 0;
+    uint64_t pcg[4] = {0, 0, 0, 0};
+    size_t params_words = 0;
+};
+
+static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan& p, mf_status* st) {
+    p.n = mv->n;
+    p.m = mv->m;
+    if (cfg->placement != 0) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "placement 'inverse' is not supported by the CUDA path yet");
+        return st->code;
+    }
+    if (p.n < 0 || p.m < 0 || p.n >= (int64_t)INT32_MAX - 1 || 3 * p.m >= (int64_t)INT32_MAX - 1) {
+        st->code = MF_ERR_LIMIT;
+        snprintf(st->message, sizeof(st->message), "mesh too large for 32-bit device indices (n=%lld, m=%lld)",
+                 (long long)p.n, (long long)p.m);
+        return st->code;
+    }
+    p.alias = (mv->features == nullptr);
+    p.C = p.alias ? 3 : mv->c;
+    p.fdtype = p.alias ? MF_DTYPE_F64 : mv->features_dtype;
+    p.B = mv->vertex_offsets ? (int)mv->n_meshes : 1;
+    const int B = p.B;
+    p.voff.assign(B + 1, 0);
+    p.foff.assign(B + 1, 0);
+    if (mv->vertex_offsets) {
+        for (int b = 0; b <= B; b++) {
+            p.voff[b] = mv->vertex_offsets[b];
+            p.foff[b] = mv->facet_offsets[b];
+        }
+        bool ok = p.voff[0] == 0 && p.foff[0] == 0 && p.voff[B] == p.n && p.foff[B] == p.m;
+        for (int b = 0; b < B && ok; b++) ok = p.voff[b + 1] >= p.voff[b] && p.foff[b + 1] >= p.foff[b];
+        if (!ok) {
+            st->code = MF_ERR_STRUCTURAL;
+            snprintf(st->message, sizeof(st->message), "vertex/facet offsets must be monotone from 0 to n/m");
+            return st->code;
+        }
+    } else {
+        p.voff[1] = p.n;
+        p.foff[1] = p.m;
+    }
+    // per-mesh chains and host-side errors, in batch order (decimate.py:363-371)
+    const int64_t target = cfg->target_vertices;
+    p.first_err = B;
+    p.chains.assign(B, {});
+    for (int b = 0; b < B; b++) {
+        int64_t nb = p.voff[b + 1] - p.voff[b], mb = p.foff[b + 1] - p.foff[b];
+        if (target > nb) {
+            p.err_code = MF_ERR_VALUE;
+            snprintf(p.err_msg, sizeof(p.err_msg), "target_vertices=%lld exceeds the input size %lld",
+                     (long long)target, (long long)nb);
+        } else if (cfg->rounds == 0 || target == nb) {
+            if (target != nb) {
+                p.err_code = MF_ERR_VALUE;
+                snprintf(p.err_msg, sizeof(p.err_msg), "rounds=0 requires target_vertices == input vertex count");
+            }
+        } else if (nb < 3 || mb < 1) {
+            p.err_code = MF_ERR_STRUCTURAL;
+            snprintf(p.err_msg, sizeof(p.err_msg),
+                     "decimate_parallel requires a mesh with at least 3 vertices and 1 facet, got %lld vertices / "
+                     "%lld facets",
+                     (long long)nb, (long long)mb);
+        } else {
+            round_targets(nb, target, cfg->rounds, p.chains[b]);
+        }
+        if (p.err_code != MF_OK) {
+            p.first_err = b;
+            break;
+        }
+    }
+    p.R = 0;
+    for (int b = 0; b < p.first_err; b++) p.R = std::max(p.R, (int)p.chains[b].size());
+    const int R = p.R;
+    p.nParamR = std::max(R, 1);
+    p.h_nin.assign((size_t)(R + 1) * B, 0);
+    p.h_act.assign((size_t)p.nParamR * B, 0);
+    p.h_budget.assign((size_t)p.nParamR * B, 0);
+    p.h_voff.assign((size_t)(R + 1) * (B + 1), 0);
+    for (int b = 0; b < B; b++) p.h_nin[b] = (int)(p.voff[b + 1] - p.voff[b]);
+    for (int r = 0; r < R; r++)
+        for (int b = 0; b < B; b++) {
+            int nin = p.h_nin[(size_t)r * B + b];
+            bool a = b < p.first_err && r < (int)p.chains[b].size();
+            p.h_act[(size_t)r * B + b] = a;
+            int tgt = a ? (int)p.chains[b][r] : nin;
+            p.h_budget[(size_t)r * B + b] = nin - tgt;
+            p.h_nin[(size_t)(r + 1) * B + b] = tgt;
+        }
+    for (int r = 0; r <= R; r++) {
+        int acc = 0;
+        for (int b = 0; b < B; b++) {
+            acc += p.h_nin[(size_t)r * B + b];
+            p.h_voff[(size_t)r * (B + 1) + b + 1] = acc;
+        }
+    }
+    p.h_N.assign(R + 1, 0);
+    for (int r = 0; r <= R; r++) p.h_N[r] = p.h_voff[(size_t)r * (B + 1) + B];
+    p.N0 = (int)p.n;
+    p.M0 = (int)p.m;
+    p.Nfin = p.h_N[R];
+    p.Mcap = std::max(p.M0, 1);
+    p.Ecap = 3 * p.Mcap;
+    p.N1 = R > 0 ? p.h_N[1] : p.N0;
+    p.seeded = cfg->seeded != 0;
+    p.order = cfg->einsum_order;
+    for (int i = 0; i < 4; i++) p.pcg[i] = cfg->pcg_state[i];
+    // device params: act | budget | nin | voff | foff0 (int32)
+    p.params_words = (size_t)p.nParamR * B * 2 + (size_t)(R + 1) * B + (size_t)(R + 1) * (B + 1) + (B + 1);
+    return MF_OK;
+}
+
+// ------------------------------------------------------------------------
+// workspace
+struct WS {
+    int* params;
+    int64_t *vo64, *fo64, *F64;
+    float* Xf32;
+    int* F0;
+    double *P0, *X0, *Pa, *Pb, *Xa, *Xb, *Pfin, *Xfin;
+    int *Fa, *Fb, *Ffin, *rt, *mt;
+    int *foff_a, *foff_b;
+    int* vmesh;
+    Plane* plane;
+    int *deg, *inc_off, *cursor, *inc, *inc_tmp;
+    double* vq;
+    int *nbr, *nbr_tmp, *adj_eid, *ucnt, *upcnt, *eoff, *heavy, *counters, *e0, *e1;
+    double* cost;
+    uint64_t *key_hi, *key_lo;
+    unsigned long long *mlo, *mhi;
+    int *mate, *best;
+    uint64_t *chi, *clo;
+    int *cpay, *caux, *ksel, *mode;
+    uint64_t *p_hi, *p_lo;
+    int *coffc, *removed, *absorbed, *minrep, *anchor, *outidx, *rstep, *ccount, *coff, *cmem;
+    unsigned char* has_live;
+    int* mapped;
+    int4* canon;
+    int *slot, *kout;
+    unsigned tsize;
+    int* table;
+    ScanBuf scan;
+    int* status;  // [8] flags | foff_final[B+1] | fail[3B] | stats[4R]
+    size_t status_words;
+};
+
+static void layout(Arena& A, WS& W, const Plan& p) {
+    const int B = p.B, R = p.R, N0 = p.N0, N1 = p.N1, Mcap = p.Mcap, Ecap = p.Ecap, Nfin = p.Nfin;
+    const int64_t C = p.C;
+    const bool alias = p.alias;
+    W.params = A.take<int>(p.params_words);
+    W.vo64 = A.take<int64_t>((size_t)2 * (B + 1));
+    W.fo64 = W.vo64 ? W.vo64 + (B + 1) : nullptr;
+    W.F64 = A.take<int64_t>((size_t)Mcap * 3);
+    W.Xf32 = (!alias && p.fdtype == MF_DTYPE_F32) ? A.take<float>((size_t)N0 * C) : nullptr;
+    W.F0 = A.take<int>((size_t)Mcap * 3);
+    W.P0 = A.take<double>((size_t)N0 * 3);
+    W.X0 = alias ? nullptr : A.take<double>((size_t)N0 * C);
+    W.Pa = A.take<double>((size_t)N1 * 3);
+    W.Pb = A.take<double>((size_t)N1 * 3);
+    W.Xa = alias ? nullptr : A.take<double>((size_t)N1 * C);
+    W.Xb = alias ? nullptr : A.take<double>((size_t)N1 * C);
+    W.Pfin = A.take<double>((size_t)Nfin * 3);
+    W.Xfin = alias ? nullptr : A.take<double>((size_t)Nfin * C);
+    W.Fa = A.take<int>((size_t)Mcap * 3);
+    W.Fb = A.take<int>((size_t)Mcap * 3);
+    W.Ffin = A.take<int>((size_t)Mcap * 3);
+    W.rt = A.take<int>((size_t)N0);
+    W.mt = A.take<int>((size_t)N0);
+    W.foff_a = A.take<int>((size_t)B + 1);
+    W.foff_b = A.take<int>((size_t)B + 1);
+    W.vmesh = (B > 1) ? A.take<int>((size_t)N0) : nullptr;
+    W.plane = A.take<Plane>((size_t)Mcap);
+    W.deg = A.take<int>((size_t)N0 + 1);
+    W.inc_off = A.take<int>((size_t)N0 + 1);
+    W.cursor = A.take<int>((size_t)N0 + 1);
+    W.inc = A.take<int>((size_t)Ecap);
+    W.inc_tmp = A.take<int>((size_t)Ecap);
+    W.vq = A.take<double>((size_t)N0 * 10);
+    W.nbr = A.take<int>((size_t)2 * Ecap);
+    W.nbr_tmp = A.take<int>((size_t)2 * Ecap);
+    W.adj_eid = A.take<int>((size_t)2 * Ecap);
+    W.ucnt = A.take<int>((size_t)N0);
+    W.upcnt = A.take<int>((size_t)N0);
+    W.eoff = A.take<int>((size_t)N0 + 1);
+    W.heavy = A.take<int>((size_t)N0);
+    W.counters = A.take<int>(64);
+    W.e0 = A.take<int>((size_t)Ecap);
+    W.e1 = A.take<int>((size_t)Ecap);
+    W.cost = A.take<double>((size_t)Ecap);
+    W.key_hi = A.take<uint64_t>((size_t)Ecap);
+    W.key_lo = p.seeded ? A.take<uint64_t>((size_t)Ecap) : nullptr;
+    W.mlo = A.take<unsigned long long>((size_t)B);
+    W.mhi = A.take<unsigned long long>((size_t)B);
+    W.mate = A.take<int>((size_t)N0);
+    W.best = A.take<int>((size_t)N0);
+    W.chi = A.take<uint64_t>((size_t)N0);
+    W.clo = A.take<uint64_t>((size_t)N0);
+    W.cpay = A.take<int>((size_t)N0);
+    W.caux = A.take<int>((size_t)N0);
+    W.ksel = A.take<int>((size_t)B);
+    W.mode = A.take<int>((size_t)B);
+    W.p_hi = A.take<uint64_t>((size_t)B);
+    W.p_lo = A.take<uint64_t>((size_t)B);
+    W.coffc = A.take<int>((size_t)N0 + 1);
+    W.removed = A.take<int>((size_t)B);
+    W.absorbed = A.take<int>((size_t)N0);
+    W.minrep = A.take<int>((size_t)N0);
+    W.anchor = A.take<int>((size_t)N0);
+    W.outidx = A.take<int>((size_t)N0 + 1);
+    W.rstep = A.take<int>((size_t)N0);
+    W.ccount = A.take<int>((size_t)N0 + 1);
+    W.coff = A.take<int>((size_t)N0 + 1);
+    W.cmem = A.take<int>((size_t)N0);
+    W.has_live = A.take<unsigned char>((size_t)N0);
+    W.mapped = A.take<int>((size_t)Mcap * 3);
+    W.canon = A.take<int4>((size_t)Mcap);
+    W.slot = A.take<int>((size_t)Mcap);
+    W.kout = A.take<int>((size_t)Mcap + 1);
+    W.tsize = 1u;
+    while (W.tsize < (unsigned)(2 * Mcap)) W.tsize <<= 1;
+    W.table = A.take<int>((size_t)W.tsize);
+    size_t maxn = (size_t)std::max(N0, Mcap) + 1;
+    W.scan.status = A.take<unsigned long long>(maxn / kScanTile + 4);
+    W.status_words = 8 + (size_t)(B + 1) + 3 * (size_t)B + 4 * (size_t)std::max(R, 1);
+    W.status = A.take<int>(W.status_words);
+}
+
+// ------------------------------------------------------------------------
+// the device sequence (captured into a graph); inputs already staged in W
+static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream) {
+    const int B = p.B, R = p.R, N0 = p.N0, Mcap = p.Mcap, Ecap = p.Ecap;
+    const int64_t n = p.n, m = p.m, C = p.C;
+    const bool seeded = p.seeded;
+    int* d_abort = W.status;  // [0] abort, [1] bad facet, [2] bad position
+    int* d_badf = W.status + 1;
+    int* d_badp = W.status + 2;
+    int* d_foff_fin = W.status + 8;
+    int* d_fail = W.status + 8 + (B + 1);
+    int* d_stats = d_fail + 3 * B;
+    int* d_act = W.params;
+    int* d_budget = W.params + (size_t)p.nParamR * B;
+    int* d_nin = W.params + (size_t)p.nParamR * B * 2;
+    int* d_voff = d_nin + (size_t)(R + 1) * B;
+    int* d_foff0 = d_voff + (size_t)(R + 1) * (B + 1);
+
+    RC(cudaMemsetAsync(W.status, 0, W.status_words * sizeof(int), stream));
+    RC(cudaMemsetAsync(d_fail, 0xFF, (size_t)B * 3 * sizeof(int), stream));
+    RC(cudaMemsetAsync(d_badf, 0x7f, sizeof(int), stream));
+    if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, W.F0, B, W.vo64, W.fo64, d_badf);
+    if (n > 0) LAUNCH(k_check_finite, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, W.P0, d_badp);
+    if (W.Xf32 && n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, W.X0);
+    RC(cudaMemcpyAsync(W.foff_a, d_foff0, (B + 1) * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+
+    const double* Pc = W.P0;
+    const double* Xc = p.alias ? nullptr : W.X0;
+    const int* Fc = W.F0;
+    int* foff_c = W.foff_a;
+    int* foff_n = W.foff_b;
+    const int order = p.order;
+    int* d_heavy_n = W.counters + 4;
+    int* d_heavy_c = W.counters + 12;
+    for (int r = 0; r < R; r++) {
+        const int N = p.h_N[r];
+        const int Nn = p.h_N[r + 1];
+        const int* act = d_act + (size_t)r * B;
+        const int* budget = d_budget + (size_t)r * B;
+        const int* nin = d_nin + (size_t)r * B;
+        const int* voff_r = d_voff + (size_t)r * (B + 1);
+        const int* dM = foff_c + B;
+        const bool last = (r == R - 1);
+        double* Pn = last ? W.Pfin : ((r & 1) ? W.Pb : W.Pa);
+        double* Xn = p.alias ? nullptr : (last ? W.Xfin : ((r & 1) ? W.Xb : W.Xa));
+        int* Fn = last ? W.Ffin : ((r & 1) ? W.Fb : W.Fa);
+        int* vmesh = nullptr;
+        if (B > 1) {
+            vmesh = W.vmesh;
+            LAUNCH(k_vmesh, grid_for(ctx, N), 256, 0, stream, d_abort, N, voff_r, B, vmesh);
+        }
+        RC(cudaMemsetAsync(W.deg, 0, (size_t)(N + 1) * sizeof(int), stream));
+        RC(cudaMemsetAsync(W.cursor, 0, (size_t)(N + 1) * sizeof(int), stream));
+        RC(cudaMemsetAsync(W.counters, 0, 64 * sizeof(int), stream));
+        // facet planes + incidence CSR (corner-major order)
+        LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, Pc, dM, vmesh, act, W.plane, W.deg, order);
+        run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", d_abort);
+        LAUNCH(k_inc_scatter, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, dM, Mcap, vmesh, act, W.inc_off, W.cursor,
+               W.inc);
+        // vertex quadrics + unique neighbour lists
+        LAUNCH(k_vertex, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap, W.vq, W.nbr,
+               W.ucnt, W.upcnt, W.heavy, d_heavy_n);
+        LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
+               W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
+        // lexicographic edges + pair costs + rank keys
+        run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
+        LAUNCH(k_edges, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
+               W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed, order);
+        const int* dE = W.eoff + N;
+        if (seeded) {
+            RC(cudaMemsetAsync(W.mlo, 0xFF, (size_t)B * sizeof(unsigned long long), stream));
+            RC(cudaMemsetAsync(W.mhi, 0, (size_t)B * sizeof(unsigned long long), stream));
+            LAUNCH(k_cost_minmax, grid_for(ctx, Ecap), 256, 0, stream, d_abort, dE, W.cost, W.e0, vmesh, W.mlo, W.mhi);
+            LAUNCH(k_seed_keys, grid_for(ctx, (Ecap + kSeedRun - 1) / kSeedRun), 256, 0, stream, d_abort, dE, W.cost, W.e0,
+                   vmesh, W.eoff, voff_r, W.mlo, W.mhi, p.pcg[0], p.pcg[1], p.pcg[2], p.pcg[3], W.key_hi, W.key_lo);
+        }
+        // greedy matching (Suitor proposals) -> mutual proposals are the matched pairs
+        RC(cudaMemsetAsync(W.best, 0xFF, (size_t)N * sizeof(int), stream));
+        {
+            MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.e0, W.e1, W.key_hi, seeded ? W.key_lo : nullptr,
+                         W.best, d_abort};
+            LAUNCH(k_suitor, grid_for(ctx, N), 256, 0, stream, ma);
+        }
+        LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.best, W.e0, W.e1, W.mate);
+        auto select = [&](const int* removed_in) {
+            SelectArgs sa{W.chi, W.clo, W.coffc, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
+                          d_abort};
+            LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelSmem, stream, sa);
+        };
+        // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
+        run_scan(W.scan, LoadTruncFlag{W.mate, W.e0}, W.coffc, N, stream, "k_scan<trunc>", d_abort);
+        LAUNCH(k_trunc_write, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.mate, W.e0, W.key_hi,
+               seeded ? W.key_lo : nullptr, W.coffc, W.chi, W.clo, W.cpay);
+        select(nullptr);
+        LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, W.coffc, W.chi, W.clo, W.cpay, W.mode,
+               W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed);
+        // absorb leftovers (one pass is exact: the matching is maximal when the budget is unmet)
+        run_scan(W.scan, LoadAbsorbFlag{W.inc_off, W.ucnt, W.nbr, W.mate, vmesh, act, budget, W.removed}, W.coffc,
+                 N, stream, "k_scan<absorb>", d_abort);
+        LAUNCH(k_absorb_write, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.cost,
+               W.mate, W.e0, W.coffc, W.chi, W.clo, W.caux);
+        select(W.removed);
+        RoundFail rf{d_abort, d_fail, d_fail + B, d_fail + 2 * B};
+        LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, W.coffc, W.chi, W.clo, W.caux, W.mode,
+               W.p_hi, W.p_lo, W.absorbed, B, act, budget, nin, W.ksel, W.removed, W.eoff, voff_r, rf, r);
+        // relabel: output index = rank of the cluster's lowest member
+        LAUNCH(k_relabel1, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.mate, W.e0, W.absorbed, W.anchor,
+               W.minrep);
+        run_scan(W.scan, LoadIsRep{W.anchor, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
+        RC(cudaMemsetAsync(W.ccount, 0, (size_t)(Nn + 1) * sizeof(int), stream));
+        LAUNCH(k_relabel3, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.anchor, W.minrep, W.outidx, W.rstep,
+               W.ccount);
+        // cluster CSR + contraction
+        run_scan(W.scan, LoadArr{W.ccount}, W.coff, Nn, stream, "k_scan<clusters>", d_abort);
+        RC(cudaMemsetAsync(W.cursor, 0, (size_t)(Nn + 1) * sizeof(int), stream));
+        LAUNCH(k_csr_scatter, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.rstep, W.coff, W.cursor, W.cmem);
+        LAUNCH(k_seg_sort_small, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.coff, W.cmem, W.heavy, d_heavy_c);
+        LAUNCH(k_seg_sort_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.coff, W.cmem, W.best, W.heavy,
+               d_heavy_c);
+        LAUNCH(k_contract, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.coff, W.cmem, vmesh, act, Pc, Xc,
+               (int)C, Pn, Xn);
+        // output facets: remap, drop degenerate, drop later duplicates (hash, min facet id wins)
+        RC(cudaMemsetAsync(W.table, 0xFF, (size_t)W.tsize * sizeof(int), stream));
+        RC(cudaMemsetAsync(W.has_live, 0, (size_t)N, stream));
+        LAUNCH(k_facet_remap, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh, act, W.mapped,
+               W.canon, W.slot, W.has_live, W.table, W.tsize - 1);
+        run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort);
+        LAUNCH(k_facet_write, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, W.kout, W.mapped, Fn, B, foff_c,
+               foff_n);
+        LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
+               W.rt, W.mt, r == 0);
+        RC(cudaMemcpyAsync(d_stats + 4 * r + 0, foff_c + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        RC(cudaMemcpyAsync(d_stats + 4 * r + 1, W.eoff + N, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        RC(cudaMemcpyAsync(d_stats + 4 * r + 2, foff_n + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        Pc = Pn;
+        Xc = Xn;
+        Fc = Fn;
+        std::swap(foff_c, foff_n);
+    }
+    RC(cudaMemcpyAsync(d_foff_fin, foff_c, (B + 1) * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+}
+
+// ------------------------------------------------------------------------
+// graph cache (per context): key = every host value baked into the sequence
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<ProfRec> prof;
+    int64_t kernels = 0;  // kernel nodes (launch accounting on replay)
+};
+struct GraphCache {
+    std::map<std::vector<int64_t>, GraphEntry> entries;
+    void* arena = nullptr;
+    cudaStream_t capture = nullptr;
+    ~GraphCache() { clear(); }
+    void clear() {
+        for (auto& kv : entries)
+            if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        entries.clear();
+    }
+};
+static std::map<const Context*, GraphCache>& caches() {
+    static thread_local std::map<const Context*, GraphCache> c;
+    return c;
+}
+void drop_graphs(const Context* ctx) {
+    auto& c = caches();
+    auto it = c.find(ctx);
+    if (it != c.end()) {
+        if (it->second.capture) cudaStreamDestroy(it->second.capture);
+        c.erase(it);
+    }
+}
+
+static std::vector<int64_t> graph_key(const Plan& p) {
+    std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
+                              (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
+                              g_prof_mode};
+    k.insert(k.end(), p.h_N.begin(), p.h_N.end());
+    for (char ch : g_prof_only) k.push_back(ch);
+    return k;
+}
+
+static bool use_graphs() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_GRAPHS");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
 }
 
 int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,
@@ -135,232 +600,21 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     st->mesh_index = -1;
     st->achievable_vertices = 0;
     st->message[0] = 0;
-    const int64_t n = mv->n, m = mv->m;
-    if (cfg->placement != 0) {
-        st->code = MF_ERR_VALUE;
-        snprintf(st->message, sizeof(st->message), "placement 'inverse' is not supported by the CUDA path yet");
-        return st->code;
-    }
-    if (n < 0 || m < 0 || n >= (int64_t)INT32_MAX - 1 || 3 * m >= (int64_t)INT32_MAX - 1) {
-        st->code = MF_ERR_LIMIT;
-        snprintf(st->message, sizeof(st->message), "mesh too large for 32-bit device indices (n=%lld, m=%lld)",
-                 (long long)n, (long long)m);
-        return st->code;
-    }
-    const bool alias = (mv->features == nullptr);
-    const int64_t C = alias ? 3 : mv->c;
-    const int B = mv->vertex_offsets ? (int)mv->n_meshes : 1;
-    std::vector<int64_t> voff(B + 1), foff(B + 1);
-    if (mv->vertex_offsets) {
-        for (int b = 0; b <= B; b++) { voff[b] = mv->vertex_offsets[b]; foff[b] = mv->facet_offsets[b]; }
-        bool ok = voff[0] == 0 && foff[0] == 0 && voff[B] == n && foff[B] == m;
-        for (int b = 0; b < B && ok; b++) ok = voff[b + 1] >= voff[b] && foff[b + 1] >= foff[b];
-        if (!ok) {
-            st->code = MF_ERR_STRUCTURAL;
-            snprintf(st->message, sizeof(st->message), "vertex/facet offsets must be monotone from 0 to n/m");
-            return st->code;
-        }
-    } else {
-        voff[0] = 0; voff[1] = n; foff[0] = 0; foff[1] = m;
-    }
-    // ---- per-mesh chains and host-side errors, in batch order (decimate.py:363-371)
-    const int64_t target = cfg->target_vertices;
-    int first_err = B;
-    int err_code = MF_OK;
-    char err_msg[256] = {0};
-    std::vector<std::vector<int64_t>> chains(B);
-    for (int b = 0; b < B; b++) {
-        int64_t nb = voff[b + 1] - voff[b], mb = foff[b + 1] - foff[b];
-        if (target > nb) {
-            err_code = MF_ERR_VALUE;
-            snprintf(err_msg, sizeof(err_msg), "target_vertices=%lld exceeds the input size %lld", (long long)target,
-                     (long long)nb);
-        } else if (cfg->rounds == 0 || target == nb) {
-            if (target != nb) {
-                err_code = MF_ERR_VALUE;
-                snprintf(err_msg, sizeof(err_msg), "rounds=0 requires target_vertices == input vertex count");
-            }
-        } else if (nb < 3 || mb < 1) {
-            err_code = MF_ERR_STRUCTURAL;
-            snprintf(err_msg, sizeof(err_msg),
-                     "decimate_parallel requires a mesh with at least 3 vertices and 1 facet, got %lld vertices / "
-                     "%lld facets",
-                     (long long)nb, (long long)mb);
-        } else {
-            round_targets(nb, target, cfg->rounds, chains[b]);
-        }
-        if (err_code != MF_OK) {
-            first_err = b;
-            break;
-        }
-    }
-    int R = 0;
-    for (int b = 0; b < first_err; b++) R = std::max(R, (int)chains[b].size());
-
-    // ---- per-round host tables: nin, act, budget, voff
-    std::vector<int> h_nin((size_t)(R + 1) * B), h_act((size_t)std::max(R, 1) * B, 0),
-        h_budget((size_t)std::max(R, 1) * B, 0), h_voff((size_t)(R + 1) * (B + 1));
-    for (int b = 0; b < B; b++) h_nin[b] = (int)(voff[b + 1] - voff[b]);
-    for (int r = 0; r < R; r++) {
-        for (int b = 0; b < B; b++) {
-            int nin = h_nin[(size_t)r * B + b];
-            bool a = b < first_err && r < (int)chains[b].size();
-            h_act[(size_t)r * B + b] = a;
-            int tgt = a ? (int)chains[b][r] : nin;
-            h_budget[(size_t)r * B + b] = nin - tgt;
-            h_nin[(size_t)(r + 1) * B + b] = tgt;
-        }
-    }
-    for (int r = 0; r <= R; r++) {
-        int acc = 0;
-        h_voff[(size_t)r * (B + 1)] = 0;
-        for (int b = 0; b < B; b++) {
-            acc += h_nin[(size_t)r * B + b];
-            h_voff[(size_t)r * (B + 1) + b + 1] = acc;
-        }
-    }
-    std::vector<int> h_N(R + 1);
-    for (int r = 0; r <= R; r++) h_N[r] = h_voff[(size_t)r * (B + 1) + B];
-    const int N0 = (int)n, M0 = (int)m;
-    const int Nfin = h_N[R];
-    const int Mcap = std::max(M0, 1);
-    const int Ecap = 3 * Mcap;
-    const int N1 = R > 0 ? h_N[1] : N0;
-
+    Plan p;
+    if (make_plan(mv, cfg, p, st) != MF_OK) return st->code;
+    const int B = p.B, R = p.R;
+    const int64_t n = p.n, m = p.m, C = p.C;
     MF_CUDA_TRY(cudaSetDevice(ctx->device));
 
-    // ---- result allocation (stream ordered)
-    Result* res = new Result();
-    res->device = ctx->device;
-    res->n_in = n;
-    res->n_out = Nfin;
-    res->c = C;
-    res->n_meshes = B;
-    res->features_alias = alias;
-    {
-        Arena ra;
-        ra.measuring = true;
-        ra.take<double>((size_t)Nfin * 3);
-        if (!alias) ra.take<double>((size_t)Nfin * C);
-        ra.take<int>((size_t)Mcap * 3);
-        ra.take<int>((size_t)N0);
-        ra.take<int>((size_t)N0);
-        cudaError_t e = cudaMallocAsync(&res->block, ra.off, stream);
-        if (e != cudaSuccess) {
-            delete res;
-            MF_CUDA_TRY(e);
-        }
-        Arena rb;
-        rb.base = (char*)res->block;
-        rb.cap = ra.off;
-        res->positions = rb.take<double>((size_t)Nfin * 3);
-        res->features = alias ? nullptr : rb.take<double>((size_t)Nfin * C);
-        res->facets = rb.take<int>((size_t)Mcap * 3);
-        res->replace = rb.take<int>((size_t)N0);
-        res->mapping = rb.take<int>((size_t)N0);
-    }
-
-    // ---- workspace layout (measured, then carved from the context arena)
-    const bool seeded = cfg->seeded != 0;
-    const int nParamR = std::max(R, 1);
-    auto layout = [&](Arena& A, auto& W) {
-        W.params = A.template take<int>((size_t)nParamR * B * 3 + (size_t)(R + 1) * (B + 1) + (size_t)(R + 1) * B);
-        W.F0 = A.template take<int>((size_t)Mcap * 3);
-        W.P0 = A.template take<double>((size_t)N0 * 3);
-        W.X0 = alias ? nullptr : A.template take<double>((size_t)N0 * C);
-        W.Pa = A.template take<double>((size_t)N1 * 3);
-        W.Pb = A.template take<double>((size_t)N1 * 3);
-        W.Xa = alias ? nullptr : A.template take<double>((size_t)N1 * C);
-        W.Xb = alias ? nullptr : A.template take<double>((size_t)N1 * C);
-        W.Fa = A.template take<int>((size_t)Mcap * 3);
-        W.Fb = A.template take<int>((size_t)Mcap * 3);
-        W.foff_a = A.template take<int>((size_t)B + 1);
-        W.foff_b = A.template take<int>((size_t)B + 1);
-        W.vmesh = (B > 1) ? A.template take<int>((size_t)N0) : nullptr;
-        W.plane = A.template take<Plane>((size_t)Mcap);
-        W.deg = A.template take<int>((size_t)N0 + 1);
-        W.inc_off = A.template take<int>((size_t)N0 + 1);
-        W.cursor = A.template take<int>((size_t)N0 + 1);
-        W.inc = A.template take<int>((size_t)Ecap);
-        W.inc_tmp = A.template take<int>((size_t)Ecap);
-        W.vq = A.template take<double>((size_t)N0 * 10);
-        W.nbr = A.template take<int>((size_t)2 * Ecap);
-        W.nbr_tmp = A.template take<int>((size_t)2 * Ecap);
-        W.adj_eid = A.template take<int>((size_t)2 * Ecap);
-        W.ucnt = A.template take<int>((size_t)N0);
-        W.upcnt = A.template take<int>((size_t)N0);
-        W.eoff = A.template take<int>((size_t)N0 + 1);
-        W.heavy = A.template take<int>((size_t)N0);
-        W.counters = A.template take<int>(64);
-        W.e0 = A.template take<int>((size_t)Ecap);
-        W.e1 = A.template take<int>((size_t)Ecap);
-        W.cost = A.template take<double>((size_t)Ecap);
-        W.key_hi = A.template take<uint64_t>((size_t)Ecap);
-        W.key_lo = seeded ? A.template take<uint64_t>((size_t)Ecap) : nullptr;
-        W.mlo = A.template take<unsigned long long>((size_t)B);
-        W.mhi = A.template take<unsigned long long>((size_t)B);
-        W.mate = A.template take<int>((size_t)N0);
-        W.best = A.template take<int>((size_t)N0);
-        W.front0 = A.template take<int>((size_t)N0);
-        W.front1 = A.template take<int>((size_t)N0);
-        W.bar = A.template take<unsigned>(64);
-        W.chi = A.template take<uint64_t>((size_t)N0);
-        W.clo = A.template take<uint64_t>((size_t)N0);
-        W.cseg = A.template take<int>((size_t)N0);
-        W.cpay = A.template take<int>((size_t)N0);
-        W.caux = A.template take<int>((size_t)N0);
-        W.seg_cnt = A.template take<int>((size_t)B);
-        W.ksel = A.template take<int>((size_t)B);
-        W.mode = A.template take<int>((size_t)B);
-        W.krem = A.template take<int>((size_t)B);
-        W.p_hi = A.template take<uint64_t>((size_t)B);
-        W.p_lo = A.template take<uint64_t>((size_t)B);
-        W.hist = A.template take<int>((size_t)B * 256);
-        W.removed = A.template take<int>((size_t)B);
-        W.fail = A.template take<int>((size_t)B * 3 + 8);
-        W.absorbed = A.template take<int>((size_t)N0);
-        W.minrep = A.template take<int>((size_t)N0);
-        W.anchor = A.template take<int>((size_t)N0);
-        W.isrep = A.template take<int>((size_t)N0 + 1);
-        W.outidx = A.template take<int>((size_t)N0 + 1);
-        W.rstep = A.template take<int>((size_t)N0);
-        W.ccount = A.template take<int>((size_t)N0 + 1);
-        W.coff = A.template take<int>((size_t)N0 + 1);
-        W.cmem = A.template take<int>((size_t)N0);
-        W.has_live = A.template take<unsigned char>((size_t)N0);
-        W.mapped = A.template take<int>((size_t)Mcap * 3);
-        W.canon = A.template take<int4>((size_t)Mcap);
-        W.slot = A.template take<int>((size_t)Mcap);
-        W.keep = A.template take<int>((size_t)Mcap + 1);
-        W.kout = A.template take<int>((size_t)Mcap + 1);
-        W.tsize = 1u;
-        while (W.tsize < (unsigned)(2 * Mcap)) W.tsize <<= 1;
-        W.table = A.template take<int>((size_t)W.tsize);
-        size_t maxn = (size_t)std::max(N0, Mcap) + 1;
-        W.scan.words = maxn / kScanTile + 4;
-        W.scan.status = A.template take<unsigned long long>(W.scan.words);
-        W.vo64 = A.template take<int64_t>((size_t)B + 1);
-        W.fo64 = A.template take<int64_t>((size_t)B + 1);
-        W.F64 = A.template take<int64_t>((size_t)Mcap * 3);
-        W.Xf32 = A.template take<float>((size_t)N0 * C);
-        W.stats = A.template take<int>((size_t)std::max(R, 1) * 4);
-    };
-    struct WS {
-        int* params; int* F0; double* P0; double* X0; double *Pa, *Pb, *Xa, *Xb; int *Fa, *Fb, *foff_a, *foff_b;
-        int* vmesh; Plane* plane; int *deg, *inc_off, *cursor, *inc, *inc_tmp; double* vq;
-        int *nbr, *nbr_tmp, *adj_eid, *ucnt, *upcnt, *eoff, *heavy, *counters, *e0, *e1;
-        double* cost; uint64_t *key_hi, *key_lo; unsigned long long *mlo, *mhi;
-        int *mate, *best, *front0, *front1; unsigned* bar;
-        uint64_t *chi, *clo; int *cseg, *cpay, *caux, *seg_cnt, *ksel, *mode, *krem; uint64_t *p_hi, *p_lo;
-        int *hist, *removed, *fail, *absorbed, *minrep, *anchor, *isrep, *outidx, *rstep, *ccount, *coff, *cmem;
-        unsigned char* has_live; int* mapped; int4* canon; int *slot, *keep, *kout; unsigned tsize; int* table;
-        ScanBuf scan; int64_t *vo64, *fo64, *F64; float* Xf32; int* stats;
-    } W;
+    // ---- workspace (grown on demand; cached graphs are tied to the arena address)
+    WS W;
     {
         Arena meas;
         meas.measuring = true;
-        layout(meas, W);
+        layout(meas, W, p);
         if (ctx->arena_bytes < meas.off) {
+            MF_CUDA_TRY(cudaStreamSynchronize(stream));
+            drop_graphs(ctx);
             if (ctx->arena) cudaFree(ctx->arena);
             ctx->arena = nullptr;
             ctx->arena_bytes = 0;
@@ -371,269 +625,178 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         Arena A;
         A.base = (char*)ctx->arena;
         A.cap = ctx->arena_bytes;
-        layout(A, W);
+        layout(A, W, p);
     }
-    int* d_abort = W.fail + 3 * B;      // [0] abort, [1] bad facet, [2] bad position, [3] limit
-    int* d_fail_ach = W.fail;
-    int* d_fail_round = W.fail + B;
-    int* d_fail_noedge = W.fail + 2 * B;
-
-    // ---- params upload (one pinned H2D): act | budget | nin(R+1) | voff(R+1)
-    size_t pw = (size_t)nParamR * B * 3 + (size_t)(R + 1) * (B + 1) + (size_t)(R + 1) * B;
-    size_t pin_need = pw * sizeof(int) + 8 * sizeof(int64_t) * (size_t)(B + 1) + 4096 + (size_t)(B + 1) * 8 +
-                      (size_t)B * 12 + (size_t)R * 16 + 64;
+    // ---- pinned staging: params + readback
+    size_t pin_need = p.params_words * 4 + 2 * (size_t)(B + 1) * 8 + W.status_words * 4 + 1024;
     if (ctx->pinned_bytes < pin_need) {
+        MF_CUDA_TRY(cudaStreamSynchronize(stream));
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         ctx->pinned = nullptr;
         MF_CUDA_TRY(cudaMallocHost(&ctx->pinned, pin_need * 2));
         ctx->pinned_bytes = pin_need * 2;
     }
     int* hp = (int*)ctx->pinned;
-    int* h_actp = hp;
-    int* h_budp = hp + (size_t)nParamR * B;
-    int* h_ninp = hp + (size_t)nParamR * B * 2;
-    int* h_voffp = h_ninp + (size_t)(R + 1) * B;
-    std::copy(h_act.begin(), h_act.begin() + (size_t)nParamR * B, h_actp);
-    std::copy(h_budget.begin(), h_budget.begin() + (size_t)nParamR * B, h_budp);
-    std::copy(h_nin.begin(), h_nin.end(), h_ninp);
-    std::copy(h_voff.begin(), h_voff.end(), h_voffp);
-    // nin table is (R+1)*B; the layout above reserved nParamR*B*3 + ... words in order act, budget, nin, voff.
-    int* d_act = W.params;
-    int* d_budget = W.params + (size_t)nParamR * B;
-    int* d_nin = W.params + (size_t)nParamR * B * 2;
-    int* d_voff = d_nin + (size_t)(R + 1) * B;
-    MF_CUDA_TRY(cudaMemcpyAsync(W.params, hp, pw * sizeof(int), cudaMemcpyHostToDevice, stream));
-    int64_t* h_o64 = (int64_t*)((char*)ctx->pinned + ((pw * sizeof(int) + 255) & ~size_t(255)));
-    for (int b = 0; b <= B; b++) { h_o64[b] = voff[b]; h_o64[B + 1 + b] = foff[b]; }
-    MF_CUDA_TRY(cudaMemcpyAsync(W.vo64, h_o64, (B + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
-    MF_CUDA_TRY(cudaMemcpyAsync(W.fo64, h_o64 + B + 1, (B + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
-    MF_CUDA_TRY(cudaMemsetAsync(W.fail, 0xFF, (size_t)B * 3 * sizeof(int), stream));
-    MF_CUDA_TRY(cudaMemsetAsync(d_abort, 0, 8 * sizeof(int), stream));
-    int* d_badf = d_abort + 1;
-    int* d_badp = d_abort + 2;
-    MF_CUDA_TRY(cudaMemsetAsync(d_badf, 0x7f, sizeof(int), stream));
-
-    // ---- inputs -> device (int64 facets -> int32 with validation)
-    const double* dP = mv->positions;
-    if (!is_device_ptr(mv->positions)) {
-        MF_CUDA_TRY(cudaMemcpyAsync(W.P0, mv->positions, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice,
-                                    stream));
-        dP = W.P0;
-    }
-    const int64_t* dF64 = mv->facets;
-    if (m > 0 && !is_device_ptr(mv->facets)) {
-        MF_CUDA_TRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 3 * sizeof(int64_t), cudaMemcpyHostToDevice,
-                                    stream));
-        dF64 = W.F64;
-    }
-    if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, dF64, W.F0, B, W.vo64, W.fo64, d_badf);
-    if (n > 0) LAUNCH(k_check_finite, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, dP, d_badp);
-    const double* dX = nullptr;
-    if (!alias) {
-        if (mv->features_dtype == MF_DTYPE_F64) {
-            if (is_device_ptr(mv->features)) dX = (const double*)mv->features;
-            else {
-                MF_CUDA_TRY(cudaMemcpyAsync(W.X0, mv->features, (size_t)n * C * sizeof(double),
-                                            cudaMemcpyHostToDevice, stream));
-                dX = W.X0;
-            }
-        } else {
-            const float* xf = (const float*)mv->features;
-            if (!is_device_ptr(xf)) {
-                MF_CUDA_TRY(cudaMemcpyAsync(W.Xf32, xf, (size_t)n * C * sizeof(float), cudaMemcpyHostToDevice,
-                                            stream));
-                xf = W.Xf32;
-            }
-            if (n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, xf, W.X0);
-            dX = W.X0;
-        }
-    }
-    // facet offsets of round 0 (int32)
     {
-        std::vector<int> f32(B + 1);
-        for (int b = 0; b <= B; b++) f32[b] = (int)foff[b];
-        int* hf = (int*)(h_o64 + 2 * (B + 1));
-        std::copy(f32.begin(), f32.end(), hf);
-        MF_CUDA_TRY(cudaMemcpyAsync(W.foff_a, hf, (B + 1) * sizeof(int), cudaMemcpyHostToDevice, stream));
+        int* q = hp;
+        q = std::copy(p.h_act.begin(), p.h_act.end(), q);
+        q = std::copy(p.h_budget.begin(), p.h_budget.end(), q);
+        q = std::copy(p.h_nin.begin(), p.h_nin.end(), q);
+        q = std::copy(p.h_voff.begin(), p.h_voff.end(), q);
+        for (int b = 0; b <= B; b++) *q++ = (int)p.foff[b];
     }
-
-    // ---- rounds
-    const double* Pc = dP;
-    const double* Xc = dX;
-    const int* Fc = W.F0;
-    int* foff_c = W.foff_a;
-    int* foff_n = W.foff_b;
-    const int order = cfg->einsum_order;
-    int* d_ninc = W.counters;       // [0] frontier 0, [1] frontier 1, [2] LD iterations
-    int* d_heavy_n = W.counters + 4;
-    int* d_ncand = W.counters + 8;
-    int* d_heavy_c = W.counters + 12;
-    int* d_notdone = W.counters + 16;  // 16 words
-    int coop_err = 0;
-    for (int r = 0; r < R; r++) {
-        const int N = h_N[r];
-        const int Nn = h_N[r + 1];
-        const int* act = d_act + (size_t)r * B;
-        const int* budget = d_budget + (size_t)r * B;
-        const int* nin = d_nin + (size_t)r * B;
-        const int* voff_r = d_voff + (size_t)r * (B + 1);
-        const int* dM = foff_c + B;
-        const bool last = (r == R - 1);
-        double* Pn = last ? res->positions : ((r & 1) ? W.Pb : W.Pa);
-        double* Xn = alias ? nullptr : (last ? res->features : ((r & 1) ? W.Xb : W.Xa));
-        int* Fn = last ? res->facets : ((r & 1) ? W.Fb : W.Fa);
-        int* vmesh = nullptr;
-        if (B > 1) {
-            vmesh = W.vmesh;
-            LAUNCH(k_vmesh, grid_for(ctx, N), 256, 0, stream, N, voff_r, B, vmesh);
-        }
-        cudaMemsetAsync(W.deg, 0, (size_t)(N + 1) * sizeof(int), stream);
-        cudaMemsetAsync(W.cursor, 0, (size_t)(N + 1) * sizeof(int), stream);
-        cudaMemsetAsync(W.counters, 0, 64 * sizeof(int), stream);
-        LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, Fc, Pc, dM, vmesh, act, W.plane, W.deg, order);
-        run_scan(ctx, W.scan, W.deg, W.inc_off, N, stream);
-        LAUNCH(k_inc_scatter, grid_for(ctx, Mcap), 256, 0, stream, Fc, dM, Mcap, vmesh, act, W.inc_off, W.cursor,
-               W.inc);
-        LAUNCH(k_vertex, grid_for(ctx, N, 128), 128, 0, stream, N, W.inc_off, W.inc, Fc, W.plane, Mcap, W.vq, W.nbr,
-               W.ucnt, W.upcnt, W.heavy, d_heavy_n);
-        LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
-               W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
-        run_scan(ctx, W.scan, W.upcnt, W.eoff, N, stream);
-        LAUNCH(k_edges, grid_for(ctx, N, 128), 128, 0, stream, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
-               W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed, order);
-        const int* dE = W.eoff + N;
-        if (seeded) {
-            cudaMemsetAsync(W.mlo, 0xFF, (size_t)B * sizeof(unsigned long long), stream);
-            cudaMemsetAsync(W.mhi, 0, (size_t)B * sizeof(unsigned long long), stream);
-            LAUNCH(k_cost_minmax, grid_for(ctx, Ecap), 256, 0, stream, dE, W.cost, W.e0, vmesh, W.mlo, W.mhi);
-            LAUNCH(k_seed_keys, grid_for(ctx, (Ecap + kSeedRun - 1) / kSeedRun), 256, 0, stream, dE, W.cost, W.e0,
-                   vmesh, W.eoff, voff_r, W.mlo, W.mhi, cfg->pcg_state[0], cfg->pcg_state[1], cfg->pcg_state[2],
-                   cfg->pcg_state[3], W.key_hi, W.key_lo);
-        }
-        // locally-dominant matching
-        {
-            cudaMemsetAsync(W.bar, 0, 2 * sizeof(unsigned), stream);
-            MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.e0, W.e1, W.key_hi, seeded ? W.key_lo : nullptr,
-                         W.mate, W.best, W.front0, W.front1, d_ninc, W.bar};
-            int blocks = std::max(1, std::min(ctx->coop_blocks_match, (N + 255) / 256));
-            coop_err |= coop_launch("k_match", (const void*)k_match, blocks, 256, &ma, stream);
-        }
-        // budget truncation (select the `budget` lowest-ranked matched edges per mesh)
-        auto select = [&](const int* removed_in) {
-            cudaMemsetAsync(W.bar, 0, 2 * sizeof(unsigned), stream);
-            cudaMemsetAsync(d_notdone, 0, 16 * sizeof(int), stream);
-            cudaMemsetAsync(W.hist, 0, (size_t)B * 256 * sizeof(int), stream);
-            SelectArgs sa{d_ncand, W.chi, W.clo, W.cseg, B, W.seg_cnt, act, budget, removed_in, W.ksel, W.mode,
-                          W.p_hi, W.p_lo, W.krem, W.hist, d_notdone, W.bar};
-            int blocks = std::max(1, std::min(ctx->coop_blocks_select, (N / 2 + 255) / 256));
-            coop_err |= coop_launch("k_select", (const void*)k_select, blocks, 256, &sa, stream);
-        };
-        cudaMemsetAsync(W.seg_cnt, 0, (size_t)B * sizeof(int), stream);
-        LAUNCH(k_trunc_cand, grid_for(ctx, N), 256, 0, stream, N, W.mate, W.e0, W.key_hi, seeded ? W.key_lo : nullptr,
-               vmesh, d_ncand, W.chi, W.clo, W.cseg, W.cpay, W.seg_cnt);
-        select(nullptr);
-        LAUNCH(k_trunc_apply, grid_for(ctx, N / 2 + B), 256, 0, stream, d_ncand, W.chi, W.clo, W.cseg, W.cpay, W.mode,
-               W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed);
-        // absorb leftovers (one pass is exact: the matching is maximal when budget is unmet)
-        cudaMemsetAsync(W.seg_cnt, 0, (size_t)B * sizeof(int), stream);
-        cudaMemsetAsync(d_ncand, 0, sizeof(int), stream);
-        LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.cost,
-               W.mate, W.e0, vmesh, act, budget, W.removed, d_ncand, W.chi, W.clo, W.cseg, W.cpay, W.caux,
-               W.seg_cnt);
-        select(W.removed);
-        RoundFail rf{d_abort, d_fail_ach, d_fail_round, d_fail_noedge};
-        LAUNCH(k_absorb_apply, grid_for(ctx, N / 2 + B), 256, 0, stream, d_ncand, W.chi, W.clo, W.cseg, W.cpay,
-               W.caux, W.mode, W.p_hi, W.p_lo, W.absorbed, B, act, budget, nin, W.ksel, W.removed, W.eoff, voff_r, rf,
-               r);
-        // relabel
-        LAUNCH(k_relabel1, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.mate, W.e0, W.absorbed, W.anchor,
-               W.minrep);
-        LAUNCH(k_relabel2, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.anchor, W.minrep, W.isrep);
-        run_scan(ctx, W.scan, W.isrep, W.outidx, N, stream);
-        cudaMemsetAsync(W.ccount, 0, (size_t)(Nn + 1) * sizeof(int), stream);
-        LAUNCH(k_relabel3, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.anchor, W.minrep, W.outidx, W.rstep,
-               W.ccount);
-        // cluster CSR + contraction
-        run_scan(ctx, W.scan, W.ccount, W.coff, Nn, stream);
-        cudaMemsetAsync(W.cursor, 0, (size_t)(Nn + 1) * sizeof(int), stream);
-        LAUNCH(k_csr_scatter, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.rstep, W.coff, W.cursor, W.cmem);
-        LAUNCH(k_seg_sort_small, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.coff, W.cmem, W.heavy, d_heavy_c);
-        LAUNCH(k_seg_sort_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.coff, W.cmem, W.front0, W.heavy,
-               d_heavy_c);
-        LAUNCH(k_contract, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.coff, W.cmem, vmesh, act, Pc, Xc,
-               (int)C, Pn, Xn);
-        // output facets
-        cudaMemsetAsync(W.table, 0xFF, (size_t)W.tsize * sizeof(int), stream);
-        cudaMemsetAsync(W.has_live, 0, (size_t)N, stream);
-        LAUNCH(k_facet_remap, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh, act, W.mapped,
-               W.canon, W.slot, W.has_live, W.table, W.tsize - 1);
-        LAUNCH(k_facet_keep, grid_for(ctx, Mcap), 256, 0, stream, dM, Mcap, d_abort, W.slot, W.table, W.keep);
-        run_scan(ctx, W.scan, W.keep, W.kout, Mcap, stream);
-        LAUNCH(k_facet_write, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, W.keep, W.kout, W.mapped, Fn, B,
-               foff_c, foff_n);
-        LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
-               res->replace, res->mapping, r == 0);
-        cudaMemcpyAsync(W.stats + 4 * r + 0, foff_c + B, sizeof(int), cudaMemcpyDeviceToDevice, stream);
-        cudaMemcpyAsync(W.stats + 4 * r + 1, W.eoff + N, sizeof(int), cudaMemcpyDeviceToDevice, stream);
-        cudaMemcpyAsync(W.stats + 4 * r + 2, foff_n + B, sizeof(int), cudaMemcpyDeviceToDevice, stream);
-        cudaMemcpyAsync(W.stats + 4 * r + 3, d_ninc + 2, sizeof(int), cudaMemcpyDeviceToDevice, stream);
-        Pc = Pn;
-        Xc = Xn;
-        Fc = Fn;
-        std::swap(foff_c, foff_n);
+    int64_t* h_o64 = (int64_t*)((char*)ctx->pinned + ((p.params_words * 4 + 255) & ~size_t(255)));
+    for (int b = 0; b <= B; b++) {
+        h_o64[b] = p.voff[b];
+        h_o64[B + 1 + b] = p.foff[b];
     }
-    if (coop_err) {
+    int* h_status = (int*)(h_o64 + 2 * (B + 1));
+    // ---- stage params + inputs (outside the graph: host pointers / caller buffers change per call)
+    MF_CUDA_TRY(cudaMemcpyAsync(W.params, hp, p.params_words * 4, cudaMemcpyHostToDevice, stream));
+    MF_CUDA_TRY(cudaMemcpyAsync(W.vo64, h_o64, 2 * (size_t)(B + 1) * 8, cudaMemcpyHostToDevice, stream));
+    if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, mv->positions, (size_t)n * 24, cudaMemcpyDefault, stream));
+    if (m) MF_CUDA_TRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 24, cudaMemcpyDefault, stream));
+    if (!p.alias && n * C > 0) {
+        if (p.fdtype == MF_DTYPE_F64)
+            MF_CUDA_TRY(cudaMemcpyAsync(W.X0, mv->features, (size_t)(n * C) * 8, cudaMemcpyDefault, stream));
+        else
+            MF_CUDA_TRY(cudaMemcpyAsync(W.Xf32, mv->features, (size_t)(n * C) * 4, cudaMemcpyDefault, stream));
+    }
+    // ---- the round chain: replay (or capture once) the graph of this call shape
+    g_rec_err = cudaSuccess;
+    auto rec_fail = [&]() {
         st->code = MF_ERR_CUDA;
-        snprintf(st->message, sizeof(st->message), "cooperative launch failed (%d)", coop_err);
-        cudaFreeAsync(res->block, stream);
-        delete res;
+        snprintf(st->message, sizeof(st->message), "recording the round chain failed at mf_decimate.cu:%d: %s",
+                 g_rec_line, cudaGetErrorString(g_rec_err));
+        cudaGetLastError();
         return st->code;
+    };
+    std::vector<ProfRec>* graph_prof = nullptr;
+    if (use_graphs()) {
+        GraphCache& gc = caches()[ctx];
+        if (gc.arena != ctx->arena) {
+            gc.clear();
+            gc.arena = ctx->arena;
+        }
+        if (!gc.capture) MF_CUDA_TRY(cudaStreamCreateWithFlags(&gc.capture, cudaStreamNonBlocking));
+        std::vector<int64_t> key = graph_key(p);
+        auto it = gc.entries.find(key);
+        if (it == gc.entries.end()) {
+            if (gc.entries.size() >= 16) gc.clear();
+            size_t rec0 = g_prof_recs.size();
+            int64_t l0 = g_launches;
+            MF_CUDA_TRY(cudaStreamBeginCapture(gc.capture, cudaStreamCaptureModeThreadLocal));
+            record(ctx, p, W, gc.capture);
+            int64_t nk = g_launches - l0;
+            g_launches = l0;
+            cudaGraph_t g = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(gc.capture, &g);
+            if (g_rec_err != cudaSuccess) {
+                if (g) cudaGraphDestroy(g);
+                return rec_fail();
+            }
+            MF_CUDA_TRY(ce);
+            GraphEntry e;
+            cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+            cudaGraphDestroy(g);
+            MF_CUDA_TRY(ie);
+            e.prof.assign(g_prof_recs.begin() + rec0, g_prof_recs.end());
+            e.kernels = nk;
+            g_prof_recs.resize(rec0);
+            it = gc.entries.emplace(key, std::move(e)).first;
+        }
+        MF_CUDA_TRY(cudaGraphLaunch(it->second.exec, stream));
+        g_launches += it->second.kernels;
+        graph_prof = &it->second.prof;
+    } else {
+        record(ctx, p, W, stream);
+        if (g_rec_err != cudaSuccess) return rec_fail();
     }
-    if (R == 0) {
-        // identity (decimate.py:172-174, 367-370): copy inputs, replace = mapping = arange
-        MF_CUDA_TRY(cudaMemcpyAsync(res->positions, dP, (size_t)n * 3 * sizeof(double), cudaMemcpyDeviceToDevice,
-                                    stream));
-        if (!alias && n * C > 0)
-            MF_CUDA_TRY(cudaMemcpyAsync(res->features, dX, (size_t)n * C * sizeof(double), cudaMemcpyDeviceToDevice,
-                                        stream));
-        if (m) MF_CUDA_TRY(cudaMemcpyAsync(res->facets, W.F0, (size_t)m * 3 * sizeof(int), cudaMemcpyDeviceToDevice,
-                                           stream));
-        LAUNCH(k_identity_index, grid_for(ctx, n), 256, 0, stream, (int)n, res->replace, res->mapping);
+    // ---- result: copy outputs out of the workspace
+    Result* res = new Result();
+    res->device = ctx->device;
+    res->n_in = n;
+    res->n_out = p.Nfin;
+    res->c = C;
+    res->n_meshes = B;
+    res->features_alias = p.alias;
+    {
+        Arena ra;
+        ra.measuring = true;
+        ra.take<double>((size_t)p.Nfin * 3);
+        if (!p.alias) ra.take<double>((size_t)p.Nfin * C);
+        ra.take<int>((size_t)p.Mcap * 3);
+        ra.take<int>((size_t)p.N0);
+        ra.take<int>((size_t)p.N0);
+        cudaError_t e = cudaMallocAsync(&res->block, ra.off, stream);
+        if (e != cudaSuccess) {
+            delete res;
+            MF_CUDA_TRY(e);
+        }
+        Arena rb;
+        rb.base = (char*)res->block;
+        rb.cap = ra.off;
+        res->positions = rb.take<double>((size_t)p.Nfin * 3);
+        res->features = p.alias ? nullptr : rb.take<double>((size_t)p.Nfin * C);
+        res->facets = rb.take<int>((size_t)p.Mcap * 3);
+        res->replace = rb.take<int>((size_t)p.N0);
+        res->mapping = rb.take<int>((size_t)p.N0);
     }
-    // ---- single readback: status words + final facet offsets + per-mesh failures
-    int* h_st = (int*)(h_o64 + 4 * (B + 1));
-    MF_CUDA_TRY(cudaMemcpyAsync(h_st, d_abort, 8 * sizeof(int), cudaMemcpyDeviceToHost, stream));
-    MF_CUDA_TRY(cudaMemcpyAsync(h_st + 8, foff_c, (B + 1) * sizeof(int), cudaMemcpyDeviceToHost, stream));
-    MF_CUDA_TRY(cudaMemcpyAsync(h_st + 8 + B + 1, W.fail, (size_t)B * 3 * sizeof(int), cudaMemcpyDeviceToHost,
-                                stream));
-    int* h_stats = h_st + 8 + B + 1 + 3 * B;
-    if (R > 0)
-        MF_CUDA_TRY(cudaMemcpyAsync(h_stats, W.stats, (size_t)R * 4 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    if (R > 0) {
+        if (p.Nfin) cudaMemcpyAsync(res->positions, W.Pfin, (size_t)p.Nfin * 24, cudaMemcpyDeviceToDevice, stream);
+        if (!p.alias && p.Nfin * C > 0)
+            cudaMemcpyAsync(res->features, W.Xfin, (size_t)(p.Nfin * C) * 8, cudaMemcpyDeviceToDevice, stream);
+        cudaMemcpyAsync(res->facets, W.Ffin, (size_t)p.Mcap * 12, cudaMemcpyDeviceToDevice, stream);
+        if (n) {
+            cudaMemcpyAsync(res->replace, W.rt, (size_t)n * 4, cudaMemcpyDeviceToDevice, stream);
+            cudaMemcpyAsync(res->mapping, W.mt, (size_t)n * 4, cudaMemcpyDeviceToDevice, stream);
+        }
+    } else {
+        // identity (decimate.py:172-174, 367-370): inputs verbatim, replace = mapping = arange
+        if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, res->facets, B, W.vo64, W.fo64,
+                          W.counters);
+        if (n) cudaMemcpyAsync(res->positions, W.P0, (size_t)n * 24, cudaMemcpyDeviceToDevice, stream);
+        if (!p.alias && n * C > 0) {
+            if (W.Xf32) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, res->features);
+            else cudaMemcpyAsync(res->features, W.X0, (size_t)(n * C) * 8, cudaMemcpyDeviceToDevice, stream);
+        }
+        if (n) LAUNCH(k_identity_index, grid_for(ctx, n), 256, 0, stream, (int)n, res->replace, res->mapping);
+    }
+    // ---- single readback
+    MF_CUDA_TRY(cudaMemcpyAsync(h_status, W.status, W.status_words * 4, cudaMemcpyDeviceToHost, stream));
     MF_CUDA_TRY(cudaStreamSynchronize(stream));
     MF_CUDA_TRY(cudaGetLastError());
-    const int* h_fo = h_st + 8;
-    const int* h_fail = h_st + 8 + B + 1;
-    if (h_st[1] != 0x7f7f7f7f || h_st[2] != 0) {
-        st->code = MF_ERR_STRUCTURAL;
-        if (h_st[2]) snprintf(st->message, sizeof(st->message), "positions contain NaN or infinite values");
+    if (graph_prof) prof_collect(*graph_prof);
+    prof_collect_pending();
+    const int* h_fo = h_status + 8;
+    const int* h_fail = h_status + 8 + (B + 1);
+    const int* h_stats = h_fail + 3 * B;
+    auto fail_out = [&](int code) {
+        st->code = code;
+        cudaFree(res->block);
+        delete res;
+        return code;
+    };
+    if (R > 0 && (h_status[1] != 0x7f7f7f7f || h_status[2] != 0)) {
+        if (h_status[2]) snprintf(st->message, sizeof(st->message), "positions contain NaN or infinite values");
         else
             snprintf(st->message, sizeof(st->message),
                      "facet %d references an out-of-range vertex (or one outside its batch entry) or repeats a vertex",
-                     h_st[1]);
-        cudaFreeAsync(res->block, stream);
-        delete res;
-        return st->code;
+                     h_status[1]);
+        return fail_out(MF_ERR_STRUCTURAL);
     }
-    if (h_st[0]) {
+    if (R > 0 && h_status[0]) {
         int bf = -1;
         for (int b = 0; b < B; b++)
-            if (h_fail[b] >= 0) { bf = b; break; }
-        st->code = MF_ERR_INFEASIBLE;
+            if (h_fail[b] >= 0) {
+                bf = b;
+                break;
+            }
         st->mesh_index = bf;
         if (bf >= 0) {
             st->achievable_vertices = h_fail[bf];
             int rr = h_fail[B + bf];
-            st->target_vertices = chains[bf][rr];
+            st->target_vertices = p.chains[bf][rr];
             st->no_edges = h_fail[2 * B + bf];
             if (st->no_edges)
                 snprintf(st->message, sizeof(st->message),
@@ -644,29 +807,23 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
                          "cannot reach %lld vertices in one pass; achievable minimum is %d",
                          (long long)st->target_vertices, h_fail[bf]);
         }
-        cudaFreeAsync(res->block, stream);
-        delete res;
-        return st->code;
+        return fail_out(MF_ERR_INFEASIBLE);
     }
-    if (first_err < B) {
-        st->code = err_code;
-        st->mesh_index = first_err;
-        snprintf(st->message, sizeof(st->message), "%s", err_msg);
-        cudaFreeAsync(res->block, stream);
-        delete res;
-        return st->code;
+    if (p.first_err < B) {
+        st->mesh_index = p.first_err;
+        snprintf(st->message, sizeof(st->message), "%s", p.err_msg);
+        return fail_out(p.err_code);
     }
     res->m_out = (R == 0) ? m : h_fo[B];
-    for (int r = 0; r < R; r++) {
-        int64_t row[6] = {h_N[r], h_stats[4 * r], h_stats[4 * r + 1], h_N[r + 1], h_stats[4 * r + 2],
-                          h_stats[4 * r + 3]};
-        res->round_stats.insert(res->round_stats.end(), row, row + 6);
-    }
     res->vertex_offsets.resize(B + 1);
     res->facet_offsets.resize(B + 1);
     for (int b = 0; b <= B; b++) {
-        res->vertex_offsets[b] = h_voff[(size_t)R * (B + 1) + b];
-        res->facet_offsets[b] = (R == 0) ? foff[b] : h_fo[b];
+        res->vertex_offsets[b] = p.h_voff[(size_t)R * (B + 1) + b];
+        res->facet_offsets[b] = (R == 0) ? p.foff[b] : h_fo[b];
+    }
+    for (int r = 0; r < R; r++) {
+        int64_t row[6] = {p.h_N[r], h_stats[4 * r], h_stats[4 * r + 1], p.h_N[r + 1], h_stats[4 * r + 2], 0};
+        res->round_stats.insert(res->round_stats.end(), row, row + 6);
     }
     *out = res;
     return MF_OK;

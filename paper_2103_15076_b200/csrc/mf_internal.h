@@ -22,8 +22,6 @@ struct DevStatus {
 struct Context {
     int device = 0;
     int sm_count = 148;
-    int coop_blocks_match = 0;   // co-resident blocks of the matching kernel
-    int coop_blocks_select = 0;  // co-resident blocks of the selection kernel
     // workspace arena (grown on demand, kept across calls)
     void* arena = nullptr;
     size_t arena_bytes = 0;
@@ -102,4 +100,6 @@ int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64
                void* out, cudaStream_t stream, mf_status* st);
 int64_t round_targets(int64_t n_in, int64_t target, int rounds, std::vector<int64_t>& chain);
 extern thread_local int64_t g_launches;
+void drop_graphs(const Context* ctx);
+void prof_collect_pending();
 }  // namespace mf

@@ -6,9 +6,9 @@
 //                                         sequential per-vertex quadric fold, unique neighbour lists
 //   mesh.py:125-134 + quadrics.py:117-132 k_edges             lexicographic edge ids, pair cost, rank keys
 //   decimate.py:181-191 (seeded)         k_cost_minmax + k_seed_keys  PCG64 jump-ahead keys, buckets
-//   decimate.py:248-263 (greedy)         k_match (persistent)  locally-dominant matching rounds
-//   decimate.py:256-263 (budget stop)    k_select (persistent) MSD radix select of the budget lowest ranks
-//   decimate.py:194-226 (absorb)         k_absorb_cand + k_select + k_absorb_apply
+//   decimate.py:248-263 (greedy)         k_suitor + k_mates    proposal (Suitor) greedy matching, CAS only
+//   decimate.py:256-263 (budget stop)    k_trunc_* + k_select  per-mesh MSD radix select of the lowest ranks
+//   decimate.py:194-226 (absorb)         k_absorb_* + k_select one-pass absorption of the leftovers
 //   decimate.py:130-137, 275-278         k_relabel{1,2,3}      min-member flags + exclusive scan
 //   decimate.py:142-145, 280-283         k_contract{,_heavy}   ascending-member fold from +0.0, / count
 //   decimate.py:147-167                  k_facet_remap / keep / write   remap, degenerate drop, hash dedupe
@@ -116,7 +116,8 @@ MF_DEV int mesh_of(const int* __restrict__ vmesh, int v) { return vmesh ? vmesh[
 
 // ------------------------------------------------------------------------
 // K0: batch bookkeeping -- owning mesh of every vertex of this round.
-__global__ void k_vmesh(int N, const int* __restrict__ voff, int B, int* __restrict__ vmesh) {
+__global__ void k_vmesh(const int* __restrict__ abort_flag, int N, const int* __restrict__ voff, int B, int* __restrict__ vmesh) {
+    if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int lo = 0, hi = B;  // find b with voff[b] <= v < voff[b+1]
         while (hi - lo > 1) {
@@ -128,9 +129,10 @@ __global__ void k_vmesh(int N, const int* __restrict__ voff, int B, int* __restr
 }
 
 // K1: facet plane (mesh.py:77-87) + incidence degrees.
-__global__ void k_facet_plane(const int* __restrict__ F, const double* __restrict__ P, const int* __restrict__ dM,
+__global__ void k_facet_plane(const int* __restrict__ abort_flag, const int* __restrict__ F, const double* __restrict__ P, const int* __restrict__ dM,
                               const int* __restrict__ vmesh, const int* __restrict__ act, Plane* __restrict__ plane,
                               int* __restrict__ deg, int order) {
+    if (*abort_flag) return;
     const int M = *dM;
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
         int ia = F[3 * f], ib = F[3 * f + 1], ic = F[3 * f + 2];
@@ -158,9 +160,10 @@ __global__ void k_facet_plane(const int* __restrict__ F, const double* __restric
 
 // K2: corner-major incidence scatter; key k = corner*Mcap + f keeps the
 // np.add.at order (corner 0 facets ascending, then corner 1, then 2).
-__global__ void k_inc_scatter(const int* __restrict__ F, const int* __restrict__ dM, int Mcap,
+__global__ void k_inc_scatter(const int* __restrict__ abort_flag, const int* __restrict__ F, const int* __restrict__ dM, int Mcap,
                               const int* __restrict__ vmesh, const int* __restrict__ act,
                               const int* __restrict__ inc_off, int* __restrict__ cursor, int* __restrict__ inc) {
+    if (*abort_flag) return;
     const int M = *dM;
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
         int t[3] = {F[3 * f], F[3 * f + 1], F[3 * f + 2]};
@@ -211,11 +214,12 @@ MF_DEV void other_two(const int* __restrict__ F, int f, int corner, int& a, int&
 // K3: per-vertex quadric fold + unique neighbour list (thread tier, deg <= kSmallDeg).
 // Neighbours are written sorted & unique to nbr[2*inc_off[v] ...]; ucnt = count,
 // upcnt = count of neighbours > v (the vertex's lexicographic edges).
-__global__ void __launch_bounds__(128) k_vertex(int N, const int* __restrict__ inc_off, const int* __restrict__ inc,
+__global__ void __launch_bounds__(128) k_vertex(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off, const int* __restrict__ inc,
                                                 const int* __restrict__ F, const Plane* __restrict__ plane, int Mcap,
                                                 double* __restrict__ vq, int* __restrict__ nbr, int* __restrict__ ucnt,
                                                 int* __restrict__ upcnt, int* __restrict__ heavy,
                                                 int* __restrict__ heavy_count) {
+    if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int s = inc_off[v], d = inc_off[v + 1] - s;
         if (d > kSmallDeg) {
@@ -254,12 +258,13 @@ __global__ void __launch_bounds__(128) k_vertex(int N, const int* __restrict__ i
 }
 
 // K3h: heavy tier -- one block per high-degree vertex (any degree).
-__global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ heavy, const int* __restrict__ heavy_count,
+__global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ abort_flag, const int* __restrict__ heavy, const int* __restrict__ heavy_count,
                                                       const int* __restrict__ inc_off, int* __restrict__ inc,
                                                       int* __restrict__ inc_tmp, const int* __restrict__ F,
                                                       const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
                                                       int* __restrict__ nbr, int* __restrict__ nbr_tmp,
                                                       int* __restrict__ ucnt, int* __restrict__ upcnt) {
+    if (*abort_flag) return;
     __shared__ int smem[kChunk];
     __shared__ Plane s_pl[256];
     __shared__ int s_scan[33];
@@ -348,7 +353,7 @@ MF_DEV double pair_cost(const Q10& qi, const Q10& qj, double pix, double piy, do
 // K4: lexicographic edge list + pair cost + rank key + adjacency edge ids.
 // Edge id of (v, u>v) = eoff[v] + rank of u among v's upper neighbours, which
 // is exactly np.unique(axis=0)'s lexicographic order (mesh.py:131-134).
-__global__ void __launch_bounds__(128) k_edges(int N, const int* __restrict__ inc_off, const int* __restrict__ nbr,
+__global__ void __launch_bounds__(128) k_edges(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off, const int* __restrict__ nbr,
                                                const int* __restrict__ ucnt, const int* __restrict__ upcnt,
                                                const int* __restrict__ eoff, const double* __restrict__ vq,
                                                const double* __restrict__ P, int* __restrict__ e0,
@@ -356,6 +361,7 @@ __global__ void __launch_bounds__(128) k_edges(int N, const int* __restrict__ in
                                                uint64_t* __restrict__ key_hi, int* __restrict__ adj_eid,
                                                int* __restrict__ mate, int* __restrict__ minrep,
                                                int* __restrict__ absorbed, int order) {
+    if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         mate[v] = -1;
         minrep[v] = v;
@@ -398,9 +404,10 @@ __global__ void __launch_bounds__(128) k_edges(int N, const int* __restrict__ in
 
 // ------------------------------------------------------------------------
 // Seeded shuffle keys (decimate.py:184-191).
-__global__ void k_cost_minmax(const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
+__global__ void k_cost_minmax(const int* __restrict__ abort_flag, const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
                               const int* __restrict__ vmesh, unsigned long long* __restrict__ mlo,
                               unsigned long long* __restrict__ mhi) {
+    if (*abort_flag) return;
     const int E = *dE;
     uint64_t lo = ~0ull, hi = 0ull;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
@@ -453,11 +460,12 @@ MF_DEV uint64_t pcg_out(u128 s) {
 
 // One thread per run of kSeedRun consecutive edges: jump once, then step.
 constexpr int kSeedRun = 16;
-__global__ void k_seed_keys(const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
+__global__ void k_seed_keys(const int* __restrict__ abort_flag, const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
                             const int* __restrict__ vmesh, const int* __restrict__ eoff, const int* __restrict__ voff,
                             const unsigned long long* __restrict__ mlo, const unsigned long long* __restrict__ mhi,
                             uint64_t s_hi, uint64_t s_lo, uint64_t i_hi,
                             uint64_t i_lo, uint64_t* __restrict__ key_hi, uint64_t* __restrict__ key_lo) {
+    if (*abort_flag) return;
     const int E = *dE;
     const u128 s0 = ((u128)s_hi << 64) | s_lo, inc = ((u128)i_hi << 64) | i_lo;
     const u128 M = pcg_mult();
@@ -490,10 +498,13 @@ __global__ void k_seed_keys(const int* __restrict__ dE, const double* __restrict
 }
 
 // ------------------------------------------------------------------------
-// K5: locally-dominant matching (persistent, grid barrier between phases).
-// An edge is matched when it is the lowest-ranked live edge at both of its
-// endpoints; the fixed point equals the sequential greedy scan over the
-// rank order (decimate.py:256-263) run to exhaustion.
+// K5: greedy matching by proposals (Suitor algorithm, Manne & Halappanavar).
+// Every vertex proposes to the neighbour whose incident edge ranks best among
+// those it can win (the neighbour's current suitor edge ranks worse); a
+// successful 32-bit CAS on suitor[v] may displace an earlier suitor, which
+// then proposes again.  Keys are unique, so the fixed point is the unique
+// greedy matching of the rank order -- exactly the sequential scan of
+// decimate.py:256-263 run to exhaustion -- with no grid-wide barrier.
 struct MatchArgs {
     int N;
     const int* inc_off;
@@ -504,203 +515,299 @@ struct MatchArgs {
     const int* e1;
     const uint64_t* key_hi;
     const uint64_t* key_lo;  // nullptr -> secondary key is the edge id
-    int* mate;
-    int* best;
-    int* front0;
-    int* front1;
-    int* counters;  // [2] frontier sizes, [2] iteration count (diagnostic)
-    unsigned* bar;
+    int* suitor;             // per vertex: edge of the best proposal received (-1 none)
+    const int* abort_flag;
 };
 
-__global__ void __launch_bounds__(256) k_match(MatchArgs a) {
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    for (int v = tid; v < a.N; v += nth)
-        if (a.ucnt[v] > 0) a.front0[append_slot(a.counters)] = v;
-    grid_sync(a.bar);
-    int cur = 0;
-    for (int iter = 0;; iter++) {
-        int* Fc = cur ? a.front1 : a.front0;
-        int* Fn = cur ? a.front0 : a.front1;
-        const int n = __ldcg(a.counters + cur);
-        if (n == 0) {
-            if (tid == 0) a.counters[2] = iter;
-            break;
-        }
-        for (int i = tid; i < n; i += nth) {
-            int v = __ldcg(Fc + i);
-            size_t s = 2 * (size_t)a.inc_off[v];
-            int nu = a.ucnt[v];
-            int be = -1;
+MF_DEV void edge_key(const MatchArgs& a, int e, uint64_t& h, uint64_t& l) {
+    h = a.key_hi[e];
+    l = a.key_lo ? a.key_lo[e] : (uint64_t)(unsigned)e;
+}
+
+__global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
+    if (*a.abort_flag) return;
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < a.N; u += gridDim.x * blockDim.x) {
+        int cur = u;
+        while (cur >= 0) {
+            const size_t s = 2 * (size_t)a.inc_off[cur];
+            const int nu = a.ucnt[cur];
+            int be = -1, bv = -1;
             uint64_t bh = ~0ull, bl = ~0ull;
             for (int j = 0; j < nu; j++) {
-                int u = a.nbr[s + j];
-                if (__ldcg(a.mate + u) >= 0) continue;
                 int e = a.adj_eid[s + j];
-                uint64_t kh = a.key_hi[e];
-                uint64_t kl = a.key_lo ? a.key_lo[e] : (uint64_t)e;
-                if (key_lt(kh, kl, bh, bl)) { bh = kh; bl = kl; be = e; }
+                uint64_t kh, kl;
+                edge_key(a, e, kh, kl);
+                if (!key_lt(kh, kl, bh, bl)) continue;
+                int v = a.nbr[s + j];
+                int sv = ld_volatile(a.suitor + v);
+                if (sv >= 0) {
+                    uint64_t sh, sl;
+                    edge_key(a, sv, sh, sl);
+                    if (!key_lt(kh, kl, sh, sl)) continue;
+                }
+                bh = kh; bl = kl; be = e; bv = v;
             }
-            a.best[v] = be;
+            if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
+            int sv = ld_volatile(a.suitor + bv);
+            int next = -2;  // -2: re-scan cur
+            while (true) {
+                if (sv >= 0) {
+                    uint64_t sh, sl;
+                    edge_key(a, sv, sh, sl);
+                    if (!key_lt(bh, bl, sh, sl)) break;  // lost the race: re-scan
+                }
+                int old = atomicCAS(a.suitor + bv, sv, be);
+                if (old == sv) {
+                    next = (sv < 0) ? -1 : (a.e0[sv] == bv ? a.e1[sv] : a.e0[sv]);
+                    break;
+                }
+                sv = old;
+            }
+            if (next != -2) cur = next;
         }
-        if (tid == 0) a.counters[cur ^ 1] = 0;
-        grid_sync(a.bar);
-        for (int i = tid; i < n; i += nth) {
-            int v = __ldcg(Fc + i);
-            int e = __ldcg(a.best + v);
-            if (e < 0) continue;
-            int u = a.e0[e] == v ? a.e1[e] : a.e0[e];
-            if (__ldcg(a.best + u) == e) a.mate[v] = e;
-            else Fn[append_slot(a.counters + (cur ^ 1))] = v;
+    }
+}
+
+// mate = the suitor edge when the proposal is mutual.
+__global__ void k_mates(const int* __restrict__ abort_flag, int N, const int* __restrict__ suitor, const int* __restrict__ e0,
+                        const int* __restrict__ e1, int* __restrict__ mate) {
+    if (*abort_flag) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        int e = suitor[v];
+        int m = -1;
+        if (e >= 0) {
+            int u = e0[e] == v ? e1[e] : e0[e];
+            if (suitor[u] == e) m = e;
         }
-        grid_sync(a.bar);
-        cur ^= 1;
+        mate[v] = m;
     }
 }
 
 // ------------------------------------------------------------------------
-// K6: per-segment MSD radix select over unique 128-bit keys.  For each
-// segment s, selects the k_s smallest candidates: mode 1 = all, 2 = none,
-// 3 = key <= threshold.  k_s = min(want_s, count_s), want_s = budget_s - removed_s.
+// K6: per-segment selection of the k smallest unique 128-bit keys.
+// Candidates are compacted in vertex order (so each mesh's candidates are
+// contiguous); one block per segment runs an MSD radix select with 11-bit
+// digits and shared-memory histograms, first streaming the segment from
+// global memory (L2-resident at these sizes) and switching to a shared-memory
+// copy of the surviving prefix bucket as soon as it fits.
+// Output per segment: mode 1 = all, 2 = none, 3 = keys <= (thr_hi, thr_lo).
+constexpr int kSelBits = 11;
+constexpr int kSelBins = 1 << kSelBits;
+constexpr int kSelCap = 4096;  // keys held in shared memory (64 KiB)
+constexpr int kSelThreads = 1024;
+constexpr int kSelSmem = kSelBins * 4 + 2 * kSelCap * 8;
+
+MF_DEV int sel_digit(uint64_t hi, uint64_t lo, int shift, int width) {
+    // bits [shift, shift+width) of the 128-bit key (may straddle the 64-bit boundary)
+    unsigned __int128 k = ((unsigned __int128)hi << 64) | lo;
+    return (int)((k >> shift) & ((1u << width) - 1u));
+}
+MF_DEV bool sel_prefix(uint64_t hi, uint64_t lo, uint64_t phi, uint64_t plo, int top) {
+    if (top >= 128) return true;
+    unsigned __int128 k = ((unsigned __int128)hi << 64) | lo;
+    unsigned __int128 p = ((unsigned __int128)phi << 64) | plo;
+    return (k >> top) == (p >> top);
+}
+
 struct SelectArgs {
-    const int* n;  // candidate count
     const uint64_t* chi;
     const uint64_t* clo;
-    const int* cseg;
+    const int* cand_off;  // exclusive scan of candidate flags over the round's vertices
+    const int* voff;      // segment b owns candidates [cand_off[voff[b]], cand_off[voff[b+1]])
     int B;
-    const int* seg_cnt;
     const int* act;
     const int* budget;
     const int* removed;  // nullable
-    int* ksel;           // out: number selected per segment
-    int* mode;           // out
-    uint64_t* p_hi;      // prefix / threshold
-    uint64_t* p_lo;
-    int* krem;
-    int* hist;     // B*256, zero on entry, zero on exit
-    int* notdone;  // [16], zero on entry
-    unsigned* bar;
+    int* ksel;
+    int* mode;
+    uint64_t* thr_hi;
+    uint64_t* thr_lo;
+    const int* abort_flag;
 };
 
-MF_DEV int key_digit(uint64_t hi, uint64_t lo, int shift) {
-    return (int)((shift >= 64 ? (hi >> (shift - 64)) : (lo >> shift)) & 255ull);
-}
-MF_DEV bool prefix_match(uint64_t hi, uint64_t lo, uint64_t phi, uint64_t plo, int top) {
-    if (top >= 128) return true;
-    if (top >= 64) return (hi >> (top - 64)) == (phi >> (top - 64));
-    if (hi != phi) return false;
-    return top == 0 ? lo == plo : (lo >> top) == (plo >> top);
-}
-
-__global__ void __launch_bounds__(256) k_select(SelectArgs a) {
-    __shared__ int s_hist[256];
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    const int n = *a.n;
-    for (int b = tid; b < a.B; b += nth) {
+__global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
+    if (*a.abort_flag) return;
+    extern __shared__ unsigned char s_raw[];
+    int* hist = reinterpret_cast<int*>(s_raw);                          // kSelBins
+    uint64_t* sh = reinterpret_cast<uint64_t*>(s_raw + kSelBins * 4);   // kSelCap
+    uint64_t* sl = sh + kSelCap;                                        // kSelCap
+    __shared__ int s_scan[33];
+    __shared__ int s_sel[4];
+    __shared__ int s_ncomp;
+    for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+        const int c0 = a.cand_off[a.voff[b]], c1 = a.cand_off[a.voff[b + 1]];
+        const int cnt = c1 - c0;
         int want = a.act[b] ? a.budget[b] - (a.removed ? a.removed[b] : 0) : 0;
-        int cnt = a.seg_cnt[b];
         int k = want < cnt ? want : cnt;
         if (k < 0) k = 0;
-        a.ksel[b] = k;
-        a.p_hi[b] = 0;
-        a.p_lo[b] = 0;
-        a.krem[b] = k;
-        a.mode[b] = (k == 0) ? 2 : (k >= cnt ? 1 : 0);
-    }
-    grid_sync(a.bar);
-    for (int pass = 0; pass < 16; pass++) {
-        const int shift = 120 - 8 * pass;
-        if (a.B == 1) {
-            if (__ldcg(a.mode) == 0) {
-                for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
-                __syncthreads();
-                uint64_t phi = __ldcg(a.p_hi), plo = __ldcg(a.p_lo);
-                for (int i = tid; i < n; i += nth) {
-                    uint64_t h = a.chi[i], l = a.clo[i];
-                    if (prefix_match(h, l, phi, plo, shift + 8)) atomicAdd(s_hist + key_digit(h, l, shift), 1);
-                }
-                __syncthreads();
-                for (int i = threadIdx.x; i < 256; i += blockDim.x)
-                    if (s_hist[i]) atomicAdd(a.hist + i, s_hist[i]);
+        if (k == 0 || k >= cnt) {
+            if (threadIdx.x == 0) {
+                a.ksel[b] = k;
+                a.mode[b] = (k == 0) ? 2 : 1;
             }
-        } else {
-            for (int i = tid; i < n; i += nth) {
-                int b = a.cseg[i];
-                if (__ldcg(a.mode + b) != 0) continue;
-                uint64_t h = a.chi[i], l = a.clo[i];
-                if (prefix_match(h, l, __ldcg(a.p_hi + b), __ldcg(a.p_lo + b), shift + 8))
-                    atomicAdd(a.hist + 256 * b + key_digit(h, l, shift), 1);
-            }
+            continue;
         }
-        grid_sync(a.bar);
-        for (int b = tid; b < a.B; b += nth) {
-            if (a.mode[b] != 0) continue;
-            int* hb = a.hist + 256 * b;
-            int kr = a.krem[b], cum = 0, dsel = 255, hsel = 0;
-            for (int d = 0; d < 256; d++) {
-                int h = __ldcg(hb + d);
-                if (cum + h >= kr) { dsel = d; hsel = h; break; }
-                cum += h;
-            }
-            for (int d = 0; d < 256; d++) hb[d] = 0;
-            kr -= cum;
-            a.krem[b] = kr;
-            uint64_t phi = a.p_hi[b], plo = a.p_lo[b];
-            if (shift >= 64) phi |= (uint64_t)dsel << (shift - 64);
-            else plo |= (uint64_t)dsel << shift;
-            if (hsel == kr) {  // every candidate under this prefix is selected
-                if (shift >= 64) {
-                    phi |= (shift - 64 > 0) ? ((1ull << (shift - 64)) - 1ull) : 0ull;
-                    plo = ~0ull;
-                } else {
-                    plo |= (shift > 0) ? ((1ull << shift) - 1ull) : 0ull;
-                }
-                a.mode[b] = 3;
+        uint64_t phi = 0, plo = 0;
+        int kr = k;
+        bool in_smem = false;
+        int n_s = 0;
+        int top = 128;
+        bool done = false;
+        while (!done) {
+            int width = top >= kSelBits ? kSelBits : top;
+            int shift = top - width;
+            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+            if (in_smem) {
+                for (int i = threadIdx.x; i < n_s; i += blockDim.x)
+                    if (sel_prefix(sh[i], sl[i], phi, plo, top)) atomicAdd(hist + sel_digit(sh[i], sl[i], shift, width), 1);
             } else {
-                atomicAdd(a.notdone + pass, 1);
+#pragma unroll 4
+                for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+                    uint64_t h = a.chi[i], l = a.clo[i];
+                    if (sel_prefix(h, l, phi, plo, top)) atomicAdd(hist + sel_digit(h, l, shift, width), 1);
+                }
             }
-            a.p_hi[b] = phi;
-            a.p_lo[b] = plo;
+            __syncthreads();
+            // block scan over the bins: find digit d with cum(d) < kr <= cum(d) + hist[d]
+            const int per = kSelBins / kSelThreads;  // 2 bins per thread
+            int loc = 0;
+            for (int j = 0; j < per; j++) loc += hist[threadIdx.x * per + j];
+            int tot;
+            int ex = block_excl_scan(loc, s_scan, &tot);
+            if (ex < kr && kr <= ex + loc) {
+                int cum = ex;
+                for (int j = 0; j < per; j++) {
+                    int h = hist[threadIdx.x * per + j];
+                    if (cum + h >= kr) {
+                        s_sel[0] = threadIdx.x * per + j;
+                        s_sel[1] = cum;
+                        s_sel[2] = h;
+                        break;
+                    }
+                    cum += h;
+                }
+            }
+            __syncthreads();
+            const int d = s_sel[0];
+            kr -= s_sel[1];
+            const int hd = s_sel[2];
+            unsigned __int128 p = ((unsigned __int128)phi << 64) | plo;
+            p |= ((unsigned __int128)d) << shift;
+            phi = (uint64_t)(p >> 64);
+            plo = (uint64_t)p;
+            top = shift;
+            if (hd == kr) {
+                unsigned __int128 ones = (shift == 0) ? 0 : ((((unsigned __int128)1) << shift) - 1);
+                p |= ones;
+                if (threadIdx.x == 0) {
+                    a.thr_hi[b] = (uint64_t)(p >> 64);
+                    a.thr_lo[b] = (uint64_t)p;
+                    a.mode[b] = 3;
+                    a.ksel[b] = k;
+                }
+                done = true;
+            } else if (!in_smem && hd <= kSelCap) {
+                // compact the surviving bucket into shared memory
+                if (threadIdx.x == 0) s_ncomp = 0;
+                __syncthreads();
+                for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+                    uint64_t h = a.chi[i], l = a.clo[i];
+                    if (sel_prefix(h, l, phi, plo, top)) {
+                        int slot = atomicAdd(&s_ncomp, 1);
+                        sh[slot] = h;
+                        sl[slot] = l;
+                    }
+                }
+                __syncthreads();
+                n_s = s_ncomp;
+                in_smem = true;
+            }
+            __syncthreads();
         }
-        grid_sync(a.bar);
-        if (__ldcg(a.notdone + pass) == 0) break;
     }
 }
+
+// ---- flag producers fused into the decoupled look-back scan (LoadOp functors)
+struct LoadTruncFlag {  // matched pair, counted at its e0 end
+    const int* mate;
+    const int* e0;
+    MF_DEV int operator()(int v) const {
+        int e = mate[v];
+        return e >= 0 && e0[e] == v;
+    }
+};
+struct LoadAbsorbFlag {  // unmatched vertex with a clustered neighbour in a mesh still short of budget
+    const int* inc_off;
+    const int* ucnt;
+    const int* nbr;
+    const int* mate;
+    const int* vmesh;
+    const int* act;
+    const int* budget;
+    const int* removed;
+    MF_DEV int operator()(int v) const {
+        int nu = ucnt[v];
+        if (nu == 0 || mate[v] >= 0) return 0;
+        int b = vmesh ? vmesh[v] : 0;
+        if (!act[b] || removed[b] >= budget[b]) return 0;
+        size_t s = 2 * (size_t)inc_off[v];
+        for (int j = 0; j < nu; j++)
+            if (mate[nbr[s + j]] >= 0) return 1;
+        return 0;
+    }
+};
+struct LoadIsRep {  // v is the lowest member of its cluster
+    const int* anchor;
+    const int* minrep;
+    MF_DEV int operator()(int v) const { return minrep[anchor[v]] == v; }
+};
+struct LoadKeep {  // facet survives: bypassed, or first occurrence of its non-degenerate triple
+    const int* dM;
+    const int* slot;
+    const int* table;
+    MF_DEV int operator()(int f) const {
+        if (f >= *dM) return 0;
+        int s = slot[f];
+        return s == -2 ? 1 : (s >= 0 && table[s] == f);
+    }
+};
 
 MF_DEV bool is_selected(int mode, uint64_t h, uint64_t l, uint64_t th, uint64_t tl) {
     return mode == 1 || (mode == 3 && !key_lt(th, tl, h, l));
 }
 
-// Candidates for budget truncation: the matched edges (one per pair, from its e0 end).
-__global__ void k_trunc_cand(int N, const int* __restrict__ mate, const int* __restrict__ e0,
-                             const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
-                             const int* __restrict__ vmesh, int* __restrict__ ncand, uint64_t* __restrict__ chi,
-                             uint64_t* __restrict__ clo, int* __restrict__ cseg, int* __restrict__ cpay,
-                             int* __restrict__ seg_cnt) {
+// Candidate flags (pass 1) and ordered writes (pass 2) for budget truncation:
+// the matched edges, one per pair from its e0 end.
+__global__ void k_trunc_write(const int* __restrict__ abort_flag, int N, const int* __restrict__ mate, const int* __restrict__ e0,
+                              const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
+                              const int* __restrict__ coff, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
+                              int* __restrict__ cpay) {
+    if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int e = mate[v];
         if (e < 0 || e0[e] != v) continue;
-        int b = mesh_of(vmesh, v);
-        int slot = append_slot(ncand);
+        int slot = coff[v];
         chi[slot] = key_hi[e];
         clo[slot] = key_lo ? key_lo[e] : (uint64_t)e;
-        cseg[slot] = b;
         cpay[slot] = e;
-        if (vmesh) atomicAdd(seg_cnt + b, 1);
-        else append_slot(seg_cnt);
     }
 }
 
-__global__ void k_trunc_apply(const int* __restrict__ ncand, const uint64_t* __restrict__ chi,
-                              const uint64_t* __restrict__ clo, const int* __restrict__ cseg,
+// Unmatch the pairs beyond the budget; removed = number kept.
+__global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const int* __restrict__ vmesh, const int* __restrict__ coff,
+                              const uint64_t* __restrict__ chi, const uint64_t* __restrict__ clo,
                               const int* __restrict__ cpay, const int* __restrict__ mode,
                               const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
                               const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate, int B,
                               const int* __restrict__ ksel, int* __restrict__ removed) {
-    const int n = *ncand;
+    if (*abort_flag) return;
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int b = tid; b < B; b += nth) removed[b] = ksel[b];
-    for (int i = tid; i < n; i += nth) {
-        int b = cseg[i];
+    for (int v = tid; v < N; v += nth) {
+        int i = coff[v];
+        if (coff[v + 1] == i) continue;  // not a candidate
+        int b = mesh_of(vmesh, v);
         if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) continue;
         int e = cpay[i];
         mate[e0[e]] = -1;
@@ -711,39 +818,37 @@ __global__ void k_trunc_apply(const int* __restrict__ ncand, const uint64_t* __r
 // Absorb candidates (decimate.py:207-221): every unmatched vertex with edges
 // picks its lowest (cost, rep) incident edge; the matching is maximal here so
 // every neighbour is clustered and one pass suffices.
-__global__ void k_absorb_cand(int N, const int* __restrict__ inc_off, const int* __restrict__ ucnt,
-                              const int* __restrict__ nbr, const int* __restrict__ adj_eid,
-                              const double* __restrict__ cost, const int* __restrict__ mate,
-                              const int* __restrict__ e0, const int* __restrict__ vmesh, const int* __restrict__ act,
-                              const int* __restrict__ budget, const int* __restrict__ removed,
-                              int* __restrict__ ncand, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
-                              int* __restrict__ cseg, int* __restrict__ cpay, int* __restrict__ caux,
-                              int* __restrict__ seg_cnt) {
+MF_DEV bool absorb_best(int v, const int* __restrict__ inc_off, const int* __restrict__ ucnt,
+                        const int* __restrict__ nbr, const int* __restrict__ adj_eid, const double* __restrict__ cost,
+                        const int* __restrict__ mate, const int* __restrict__ e0, uint64_t& bk, int& brep) {
+    int nu = ucnt[v];
+    size_t s = 2 * (size_t)inc_off[v];
+    bk = ~0ull;
+    brep = 0x7fffffff;
+    for (int j = 0; j < nu; j++) {
+        int mu = mate[nbr[s + j]];
+        if (mu < 0) continue;  // cannot happen for a maximal matching
+        int rep = e0[mu];
+        uint64_t k = f64_key(cost[adj_eid[s + j]]);
+        if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
+    }
+    return brep != 0x7fffffff;
+}
+__global__ void k_absorb_write(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off, const int* __restrict__ ucnt,
+                               const int* __restrict__ nbr, const int* __restrict__ adj_eid,
+                               const double* __restrict__ cost, const int* __restrict__ mate,
+                               const int* __restrict__ e0, const int* __restrict__ coff, uint64_t* __restrict__ chi,
+                               uint64_t* __restrict__ clo, int* __restrict__ caux) {
+    if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int nu = ucnt[v];
-        if (nu == 0 || mate[v] >= 0) continue;
-        int b = mesh_of(vmesh, v);
-        if (!act[b] || removed[b] >= budget[b]) continue;
-        size_t s = 2 * (size_t)inc_off[v];
-        uint64_t bk = ~0ull;
-        int brep = 0x7fffffff;
-        for (int j = 0; j < nu; j++) {
-            int u = nbr[s + j];
-            int mu = mate[u];
-            if (mu < 0) continue;  // cannot happen for a maximal matching
-            int rep = e0[mu];
-            uint64_t k = f64_key(cost[adj_eid[s + j]]);
-            if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
-        }
-        if (brep == 0x7fffffff) continue;
-        int slot = append_slot(ncand);
-        chi[slot] = bk;
-        clo[slot] = ((uint64_t)(unsigned)brep << 32) | (unsigned)v;
-        cseg[slot] = b;
-        cpay[slot] = v;
-        caux[slot] = brep;
-        if (vmesh) atomicAdd(seg_cnt + b, 1);
-        else append_slot(seg_cnt);
+        int i = coff[v];
+        if (coff[v + 1] == i) continue;
+        uint64_t bk;
+        int brep;
+        absorb_best(v, inc_off, ucnt, nbr, adj_eid, cost, mate, e0, bk, brep);
+        chi[i] = bk;
+        clo[i] = ((uint64_t)(unsigned)brep << 32) | (unsigned)v;
+        caux[i] = brep;
     }
 }
 
@@ -754,19 +859,21 @@ struct RoundFail {
     int* fail_noedge;  // per mesh: the failing round had no edges (decimate.py:239-244)
 };
 
-__global__ void k_absorb_apply(const int* __restrict__ ncand, const uint64_t* __restrict__ chi,
-                               const uint64_t* __restrict__ clo, const int* __restrict__ cseg,
-                               const int* __restrict__ cpay, const int* __restrict__ caux,
-                               const int* __restrict__ mode, const uint64_t* __restrict__ thi,
-                               const uint64_t* __restrict__ tlo, int* __restrict__ absorbed, int B,
-                               const int* __restrict__ act, const int* __restrict__ budget,
-                               const int* __restrict__ nin, const int* __restrict__ ksel, int* __restrict__ removed,
-                               const int* __restrict__ eoff, const int* __restrict__ voff, RoundFail fail, int round) {
-    const int n = *ncand;
+__global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* __restrict__ coff,
+                               const uint64_t* __restrict__ chi, const uint64_t* __restrict__ clo,
+                               const int* __restrict__ caux, const int* __restrict__ mode,
+                               const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
+                               int* __restrict__ absorbed, int B, const int* __restrict__ act,
+                               const int* __restrict__ budget, const int* __restrict__ nin,
+                               const int* __restrict__ ksel, int* __restrict__ removed, const int* __restrict__ eoff,
+                               const int* __restrict__ voff, RoundFail fail, int round) {
+    if (*fail.abort) return;
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    for (int i = tid; i < n; i += nth) {
-        int b = cseg[i];
-        if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) absorbed[cpay[i]] = caux[i];
+    for (int v = tid; v < N; v += nth) {
+        int i = coff[v];
+        if (coff[v + 1] == i) continue;
+        int b = mesh_of(vmesh, v);
+        if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) absorbed[v] = caux[i];
     }
     for (int b = tid; b < B; b += nth) {
         if (!act[b]) continue;
@@ -799,12 +906,6 @@ __global__ void k_relabel1(int N, const int* __restrict__ abort_flag, const int*
         }
         anchor[v] = a;
     }
-}
-__global__ void k_relabel2(int N, const int* __restrict__ abort_flag, const int* __restrict__ anchor,
-                           const int* __restrict__ minrep, int* __restrict__ isrep) {
-    if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x)
-        isrep[v] = (minrep[anchor[v]] == v);
 }
 __global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int* __restrict__ anchor,
                            const int* __restrict__ minrep, const int* __restrict__ outidx, int* __restrict__ rstep,
@@ -958,26 +1059,13 @@ __global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict_
     }
 }
 
-__global__ void k_facet_keep(const int* __restrict__ dM, int Mcap, const int* __restrict__ abort_flag,
-                             const int* __restrict__ slot, const int* __restrict__ table, int* __restrict__ keep) {
-    if (*abort_flag) return;
-    const int M = *dM;
-    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < Mcap; f += gridDim.x * blockDim.x) {
-        int k = 0;
-        if (f < M) {
-            int s = slot[f];
-            k = (s == -2) ? 1 : (s >= 0 && table[s] == f);
-        }
-        keep[f] = k;  // zero tail: the scan runs over the host bound Mcap
-    }
-}
 
 __global__ void k_identity_index(int n, int* __restrict__ a, int* __restrict__ b) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = b[i] = i;
 }
 
 __global__ void k_facet_write(const int* __restrict__ dM, const int* __restrict__ abort_flag,
-                              const int* __restrict__ keep, const int* __restrict__ kout,
+                              const int* __restrict__ kout,
                               const int* __restrict__ mapped, int* __restrict__ Fout, int B,
                               const int* __restrict__ foff_in, int* __restrict__ foff_out) {
     if (*abort_flag) return;
@@ -985,8 +1073,8 @@ __global__ void k_facet_write(const int* __restrict__ dM, const int* __restrict_
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int b = tid; b <= B; b += nth) foff_out[b] = kout[foff_in[b]];
     for (int f = tid; f < M; f += nth) {
-        if (!keep[f]) continue;
         int o = kout[f];
+        if (kout[f + 1] == o) continue;
         Fout[3 * o] = mapped[3 * f];
         Fout[3 * o + 1] = mapped[3 * f + 1];
         Fout[3 * o + 2] = mapped[3 * f + 2];

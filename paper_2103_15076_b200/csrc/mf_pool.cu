@@ -45,6 +45,52 @@ __global__ void k_check_cover(int64_t n_out, const int* __restrict__ count, int*
         if (count[i] == 0) atomicExch(empty, 1);
 }
 
+// x86 SSE NaN semantics for the folds: a NaN operand propagates with its
+// payload (quieted), the first operand winning when both are NaN; NVIDIA FP32
+// arithmetic would return the canonical 0x7fffffff instead.
+MF_DEV float qnan_of(float a) { return __int_as_float(__float_as_int(a) | 0x00400000); }
+MF_DEV double qnan_of(double a) {
+    return __longlong_as_double(__double_as_longlong(a) | 0x0008000000000000ll);
+}
+template <typename T>
+MF_DEV T x86_add(T a, T b) {
+    if (a != a) return qnan_of(a);
+    if (b != b) return qnan_of(b);
+    return a + b;
+}
+template <typename T>
+MF_DEV T x86_mul(T a, T b) {
+    if (a != a) return qnan_of(a);
+    if (b != b) return qnan_of(b);
+    return a * b;
+}
+template <typename T>
+MF_DEV T x86_div(T a, T b) {
+    if (a != a) return qnan_of(a);
+    if (b != b) return qnan_of(b);
+    return a / b;
+}
+// cvtss2sd / cvtsd2ss keep the NaN payload (shifted into the wider mantissa)
+MF_DEV double widen(float a) {
+    if (a != a) {
+        unsigned u = (unsigned)__float_as_int(a);
+        unsigned long long d = ((unsigned long long)(u >> 31) << 63) | 0x7FF0000000000000ull |
+                               ((unsigned long long)(u & 0x7FFFFF) << 29) | 0x0008000000000000ull;
+        return __longlong_as_double((long long)d);
+    }
+    return (double)a;
+}
+MF_DEV float narrow(double a) {
+    if (a != a) {
+        unsigned long long d = (unsigned long long)__double_as_longlong(a);
+        unsigned u = ((unsigned)(d >> 63) << 31) | 0x7F800000u | (unsigned)((d >> 29) & 0x7FFFFF) | 0x00400000u;
+        return __int_as_float((int)u);
+    }
+    return (float)a;
+}
+MF_DEV double avg_div(double acc, int cnt) { return x86_div(acc, (double)cnt); }
+MF_DEV float avg_div(float acc, int cnt) { return narrow(x86_div(widen(acc), (double)cnt)); }
+
 // pooling.py:36-71.  max: numpy maximum.at from -inf (later element wins ties,
 // NaN sticky); average/sum: sequential fold in the input dtype,
 // average divides in float64 and rounds back (in-place `/= int64 counts`);
@@ -71,15 +117,15 @@ __global__ void k_pool(int64_t n_out, int C, const int* __restrict__ off, const 
             acc = (T)0;
             for (int i = s; i < e; i++) {
                 int m = members[i];
-                acc = acc + X[(int64_t)m * C + k] * w[m];
-                den = den + w[m];
+                acc = x86_add(acc, x86_mul(X[(int64_t)m * C + k], w[m]));
+                den = x86_add(den, w[m]);
             }
             if (den == (T)0) atomicExch(zero_weight, 1);
-            acc = acc / den;
+            acc = x86_div(acc, den);
         } else {
             acc = (T)0;
-            for (int i = s; i < e; i++) acc = acc + X[(int64_t)members[i] * C + k];
-            if (mode == MF_POOL_AVERAGE) acc = (T)((double)acc / (double)(e - s));
+            for (int i = s; i < e; i++) acc = x86_add(acc, X[(int64_t)members[i] * C + k]);
+            if (mode == MF_POOL_AVERAGE) acc = avg_div(acc, e - s);
         }
         out[idx] = acc;
     }
@@ -111,7 +157,7 @@ static void scan_into(const Context* ctx, unsigned long long* status, const int*
     int tiles = std::max(1, (n + kScanTile - 1) / kScanTile);
     cudaMemsetAsync(status, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), s);
     LAUNCH(k_scan_excl<LoadArr>, tiles, kScanBlock, 0, s, LoadArr{in}, n, out, status,
-           reinterpret_cast<int*>(status + tiles));
+           reinterpret_cast<int*>(status + tiles), nullptr);
     (void)ctx;
 }
 

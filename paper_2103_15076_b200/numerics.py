@@ -8,6 +8,7 @@ drop-in API probes the local numpy once, making results bit-identical to the
 reference run on the same host.
 """
 
+import contextlib
 import functools
 
 import numpy as np
@@ -16,8 +17,26 @@ ORDER_LANE_SPLIT = 0  # (t0 + t2) + t1
 ORDER_SEQUENTIAL = 1  # (t0 + t1) + t2
 
 
-@functools.lru_cache(maxsize=None)
+_override = None
+
+
+@contextlib.contextmanager
+def forced_order(order: int):
+    """Pin the reduction order (e.g. to replay fixtures recorded on another host)."""
+    global _override
+    prev, _override = _override, order
+    try:
+        yield
+    finally:
+        _override = prev
+
+
 def einsum_order() -> int:
+    return _override if _override is not None else _probe()
+
+
+@functools.lru_cache(maxsize=None)
+def _probe() -> int:
     ones = np.ones((1, 3))
     a = float(np.einsum("ij,ij->i", np.array([[1e16, 1.0, -1e16]]), ones)[0])
     b = float(np.einsum("ij,ij->i", np.array([[1.0, 1e16, -1e16]]), ones)[0])

@@ -114,3 +114,58 @@ def test_features_float32_and_channels(oracle):
     feats = np.random.default_rng(0).standard_normal((800, 7)).astype(np.float32)
     m2 = mfg.TriMesh(mesh.positions, mesh.facets, feats)
     run_both(oracle, m2, 300, seed=2)
+
+
+def fan_mesh(k, seed=0, lift=0.0):
+    """One hub vertex of degree k (heavy tier when k > 32) inside a ring."""
+    rng = np.random.default_rng(seed)
+    ang = np.sort(rng.random(k)) * 2 * np.pi
+    ring = np.stack([np.cos(ang), np.sin(ang), lift * rng.standard_normal(k)], axis=1)
+    P = np.concatenate([[[0.0, 0.0, 0.3]], ring])
+    F = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)])
+    return mfg.TriMesh(P, F)
+
+
+@pytest.mark.parametrize("k,target,seed", [(40, 20, None), (300, 100, None), (3000, 1000, 4), (5000, 2600, None)])
+def test_heavy_hub(oracle, k, target, seed):
+    run_both(oracle, fan_mesh(k, seed=k, lift=0.05), target, seed=seed)
+
+
+def test_fan_absorb_to_achievable(oracle):
+    # one round down to the achievable minimum: maximal matching + absorption
+    run_both(oracle, fan_mesh(200, seed=1, lift=0.0), 88, rounds=1)
+    with pytest.raises(mfg.InfeasibleTargetError) as err:
+        mfg.decimate_parallel(fan_mesh(200, seed=1), mfg.DecimationConfig(87, rounds=1))
+    assert err.value.achievable_vertices == 88
+
+
+@pytest.mark.parametrize("seed", [None, 2])
+def test_flat_grid_sweep(oracle, seed):
+    run_both(oracle, S.flat_grid(150), 11250, seed=seed)
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_random_small(oracle, i):
+    rng = np.random.default_rng(100 + i)
+    n = int(rng.integers(5, 400))
+    mesh = S.delaunay_terrain(n, noise=float(rng.random()), seed=1000 + i)
+    target = int(rng.integers(1, n))
+    seed = None if i % 2 else int(rng.integers(0, 1000))
+    rounds = ["auto", 1, 2, 3][i % 4]
+    try:
+        ref = oracle.decimate(mesh.positions, mesh.facets, None, target=target, rounds=rounds, seed=seed,
+                              order=einsum_order())
+    except oracle.OracleInfeasible as e:
+        with pytest.raises(mfg.InfeasibleTargetError) as err:
+            mfg.decimate_parallel(mesh, mfg.DecimationConfig(target, shuffle_seed=seed, rounds=rounds))
+        assert err.value.achievable_vertices == e.achievable_vertices
+        return
+    res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target, shuffle_seed=seed, rounds=rounds))
+    assert_same(res, ref)
+
+
+def test_big_batch_random(oracle):
+    rng = np.random.default_rng(5)
+    meshes = [S.delaunay_terrain(int(rng.integers(40, 900)), seed=int(s)) for s in rng.integers(0, 10**6, 40)]
+    run_both(oracle, mfg.concat_batch(meshes), 40, seed=13)
+    run_both(oracle, mfg.concat_batch(meshes), 40)

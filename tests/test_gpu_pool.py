@@ -1,0 +1,89 @@
+"""GPU pooling / unpooling vs the oracle, bitwise: all modes x float32/float64,
+signed zeros, NaN payloads, exact ties, clusters from 1 to 100k members
+(thread tier and heavy tier of the member sort), host and device buffers."""
+
+import numpy as np
+import pytest
+
+import paper_2103_15076_b200 as mfg
+from paper_2103_15076_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def hand_result(replace, n_out):
+    replace = np.asarray(replace, dtype=np.int64)
+    return mfg.DecimationResult(mesh=mfg.TriMesh(np.zeros((n_out, 3)), np.zeros((0, 3))), replace=replace,
+                                mapping=replace.copy())
+
+
+def bits_equal(a, b):
+    return a.shape == b.shape and a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("sizes", [(400, 60), (5000, 1), (100_000, 3), (70_000, 20_000)])
+def test_pool_modes(oracle, dtype, sizes):
+    n, n_out = sizes
+    rng = np.random.default_rng(n + n_out)
+    rep = rng.integers(0, n_out, n)
+    rep[:n_out] = np.arange(n_out)
+    c = 5 if n < 10_000 else 33
+    X = rng.standard_normal((n, c)).astype(dtype)
+    X[rng.integers(0, n, 7), 0] = np.nan
+    X[rep == rep[7], 1] = 0.0
+    X[7, 1] = -0.0
+    X[9, 2] = X[10, 2]
+    w = (0.5 + rng.random(n)).astype(dtype)
+    res = hand_result(rep, n_out)
+    for mode in mfg.POOL_MODES:
+        got = mfg.pool(X, res, mode=mode, weights=w)
+        exp = oracle.pool(X, rep, n_out, mode, w)
+        assert bits_equal(got, exp), mode
+    coarse = oracle.pool(X, rep, n_out, "max")
+    assert bits_equal(mfg.unpool(coarse, res), oracle.unpool(coarse, rep))
+
+
+def test_pool_on_decimation_handle(oracle):
+    mesh = S.delaunay_terrain(30_000, noise=0.02, seed=3)
+    res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=7_500))
+    feats = np.random.default_rng(0).standard_normal((mesh.n_vertices, 64)).astype(np.float32)
+    for mode in ("max", "average", "sum"):
+        assert bits_equal(mfg.pool(feats, res, mode=mode), oracle.pool(feats, res.replace, 7_500, mode))
+    coarse = mfg.pool(feats, res, mode="max")
+    assert bits_equal(mfg.unpool(coarse, res), coarse[res.replace])
+
+
+def test_pool_errors():
+    res = hand_result([0, 0, 2], 3)
+    with pytest.raises(RuntimeError, match="cover"):
+        mfg.pool(np.zeros((3, 1)), res, mode="sum")
+    ok = hand_result([0, 1, 1], 2)
+    with pytest.raises(ValueError, match="weights"):
+        mfg.pool(np.zeros((3, 1)), ok, mode="weighted")
+    with pytest.raises(ValueError, match="mode"):
+        mfg.pool(np.zeros((3, 1)), ok, mode="median")
+    with pytest.raises(ValueError, match="zero total weight"):
+        mfg.pool(np.ones((3, 1)), ok, mode="weighted", weights=np.array([0.0, 1.0, -1.0]))
+    with pytest.raises(mfg.StructuralError):
+        mfg.unpool(np.zeros((5, 2)), ok)
+
+
+def test_tensor_api_pool_unpool(oracle):
+    import torch
+
+    from paper_2103_15076_b200 import tensor as T
+
+    mesh = S.delaunay_terrain(5000, noise=0.02, seed=1)
+    V = torch.from_numpy(mesh.positions).cuda()
+    F = torch.from_numpy(mesh.facets).cuda()
+    dd = T.decimate(V, F, target=1200)
+    ref = oracle.decimate(mesh.positions, mesh.facets, target=1200)
+    np.testing.assert_array_equal(dd.replace.cpu().numpy(), ref["replace"])
+    np.testing.assert_array_equal(dd.faces.cpu().numpy(), ref["facets"])
+    assert bits_equal(dd.vertices.cpu().numpy(), ref["positions"])
+    X = torch.randn(5000, 64, device="cuda", dtype=torch.float32)
+    pooled = T.pool(X, dd, mode="max")
+    assert bits_equal(pooled.cpu().numpy(), oracle.pool(X.cpu().numpy(), ref["replace"], 1200, "max"))
+    up = T.unpool(pooled, dd)
+    assert torch.equal(up, pooled[dd.replace])
