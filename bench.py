@@ -141,7 +141,9 @@ def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
         "k_inc_scatter": 12 * M + 4 * N + 12 * M,
         "k_vertex": 4 * N + 12 * M + 32 * M + 12 * M + 80 * N + 8 * E + 8 * N,
         "k_edges": 8 * E + 16 * N + 80 * N + 24 * N + 8 * E + 8 * E + 8 * E + 8 * E + 12 * N,
-        "k_match": 8 * E + 8 * E + 8 * E + 8 * N + 8 * N,
+        # adjacency (nbr + edge id) + rank key per slot, suitor word per vertex
+        "k_suitor": 8 * E + 8 * E + 16 * E + 8 * N,
+        "k_select": 16 * Nn,
         "k_contract": 4 * N + 4 * Nn + 24 * N + 24 * Nn,
         "k_facet_remap": 12 * M + 4 * N + 12 * M + 16 * M + 4 * M + N,
         "k_compose": 8 * r.get("N0", N) + 4 * N,
@@ -270,12 +272,17 @@ def run_ours(args):
     total_ms = sum(v[0] for v in breakdown.values())
     dominant = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
 
+    # the timed region times the dominant kernel live: warm that graph variant first
+    _native.profile(2, dominant)
+    step()
+    torch.cuda.synchronize()
+    _native.profile(2, dominant)  # clears the warm-up record
+
     # ---------------- timed region: device-resident inputs
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     _native.launch_count(reset=True)
-    _native.profile(2, dominant)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     phys = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \

@@ -309,7 +309,7 @@ struct WS {
     uint64_t *chi, *clo;
     int *cpay, *caux, *ksel, *mode;
     uint64_t *p_hi, *p_lo;
-    int *coffc, *removed, *absorbed, *minrep, *anchor, *outidx, *rstep, *ccount, *coff, *cmem;
+    int *segA, *segB, *removed, *absorbed, *minrep, *anchor, *outidx, *rstep, *ccount, *coff, *cmem;
     unsigned char* has_live;
     int* mapped;
     int4* canon;
@@ -379,7 +379,8 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.mode = A.take<int>((size_t)B);
     W.p_hi = A.take<uint64_t>((size_t)B);
     W.p_lo = A.take<uint64_t>((size_t)B);
-    W.coffc = A.take<int>((size_t)N0 + 1);
+    W.segA = A.take<int>((size_t)B);
+    W.segB = A.take<int>((size_t)B);
     W.removed = A.take<int>((size_t)B);
     W.absorbed = A.take<int>((size_t)N0);
     W.minrep = A.take<int>((size_t)N0);
@@ -463,13 +464,13 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         LAUNCH(k_inc_scatter, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, dM, Mcap, vmesh, act, W.inc_off, W.cursor,
                W.inc);
         // vertex quadrics + unique neighbour lists
-        LAUNCH(k_vertex, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap, W.vq, W.nbr,
+        LAUNCH(k_vertex, grid_for(ctx, (int64_t)N * kGrp), 256, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap, W.vq, W.nbr,
                W.ucnt, W.upcnt, W.heavy, d_heavy_n);
         LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
                W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
         // lexicographic edges + pair costs + rank keys
         run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
-        LAUNCH(k_edges, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
+        LAUNCH(k_edges, grid_for(ctx, (int64_t)N * kGrp), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
                W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed, order);
         const int* dE = W.eoff + N;
         if (seeded) {
@@ -484,30 +485,27 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         {
             MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.e0, W.e1, W.key_hi, seeded ? W.key_lo : nullptr,
                          W.best, d_abort};
-            LAUNCH(k_suitor, grid_for(ctx, N), 256, 0, stream, ma);
+            LAUNCH(k_suitor, grid_for(ctx, (int64_t)N * 16), 256, 0, stream, ma);
         }
-        LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.best, W.e0, W.e1, W.mate);
-        auto select = [&](const int* removed_in) {
-            SelectArgs sa{W.chi, W.clo, W.coffc, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
+        LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.best, W.e0, W.e1, W.mate, B, W.segA);
+        auto select = [&](const int* seg_cnt, const int* removed_in) {
+            SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
                           d_abort};
             LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelSmem, stream, sa);
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
-        run_scan(W.scan, LoadTruncFlag{W.mate, W.e0}, W.coffc, N, stream, "k_scan<trunc>", d_abort);
-        LAUNCH(k_trunc_write, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.mate, W.e0, W.key_hi,
-               seeded ? W.key_lo : nullptr, W.coffc, W.chi, W.clo, W.cpay);
-        select(nullptr);
-        LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, W.coffc, W.chi, W.clo, W.cpay, W.mode,
-               W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed);
+        LAUNCH(k_trunc_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.mate, W.e0, W.key_hi,
+               seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay);
+        select(W.segA, nullptr);
+        LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, voff_r, W.segA, W.chi, W.clo,
+               W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB);
         // absorb leftovers (one pass is exact: the matching is maximal when the budget is unmet)
-        run_scan(W.scan, LoadAbsorbFlag{W.inc_off, W.ucnt, W.nbr, W.mate, vmesh, act, budget, W.removed}, W.coffc,
-                 N, stream, "k_scan<absorb>", d_abort);
-        LAUNCH(k_absorb_write, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.cost,
-               W.mate, W.e0, W.coffc, W.chi, W.clo, W.caux);
-        select(W.removed);
+        LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.nbr, W.adj_eid,
+               W.cost, W.mate, W.e0, vmesh, voff_r, act, budget, W.removed, W.segB, W.chi, W.clo, W.caux);
+        select(W.segB, W.removed);
         RoundFail rf{d_abort, d_fail, d_fail + B, d_fail + 2 * B};
-        LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, W.coffc, W.chi, W.clo, W.caux, W.mode,
-               W.p_hi, W.p_lo, W.absorbed, B, act, budget, nin, W.ksel, W.removed, W.eoff, voff_r, rf, r);
+        LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, voff_r, W.segB, W.chi, W.clo, W.caux,
+               W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.eoff, rf, r);
         // relabel: output index = rank of the cluster's lowest member
         LAUNCH(k_relabel1, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.mate, W.e0, W.absorbed, W.anchor,
                W.minrep);

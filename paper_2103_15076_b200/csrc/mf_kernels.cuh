@@ -211,49 +211,194 @@ MF_DEV void other_two(const int* __restrict__ F, int f, int corner, int& a, int&
     b = corner == 0 ? z : (corner == 1 ? x : y);
 }
 
-// K3: per-vertex quadric fold + unique neighbour list (thread tier, deg <= kSmallDeg).
+
+// Pair cost (quadrics.py:117-132 + evaluate 53-58, SURVEY A.2) for 'average' placement.
+MF_DEV double pair_cost(const Q10& qi, const Q10& qj, double pix, double piy, double piz, double pjx, double pjy,
+                        double pjz, int order) {
+    double a00 = qi.a00 + qj.a00, a01 = qi.a01 + qj.a01, a02 = qi.a02 + qj.a02;
+    double a11 = qi.a11 + qj.a11, a12 = qi.a12 + qj.a12, a22 = qi.a22 + qj.a22;
+    double b0 = qi.b0 + qj.b0, b1 = qi.b1 + qj.b1, b2 = qi.b2 + qj.b2, c = qi.c + qj.c;
+    double x0 = 0.5 * (pix + pjx), x1 = 0.5 * (piy + pjy), x2 = 0.5 * (piz + pjz);
+    double quad = 0.0;
+    quad = quad + (x0 * a00) * x0;
+    quad = quad + (x0 * a01) * x1;
+    quad = quad + (x0 * a02) * x2;
+    quad = quad + (x1 * a01) * x0;
+    quad = quad + (x1 * a11) * x1;
+    quad = quad + (x1 * a12) * x2;
+    quad = quad + (x2 * a02) * x0;
+    quad = quad + (x2 * a12) * x1;
+    quad = quad + (x2 * a22) * x2;
+    double lin = 2.0 * dot3(b0, b1, b2, x0, x1, x2, order);
+    return (quad + lin) + c;
+}
+
+// ------------------------------------------------------------------------
+// Group-cooperative tier: 16 lanes per vertex (two vertices per warp).  The
+// incidence list (deg <= 16) is spread over the lanes, sorted with a shuffle
+// bitonic network, every lane gathers its facet's plane and corner vertices
+// in parallel, the ten quadric products are staged in shared memory and
+// folded by ten lanes (one component each) in incidence order, and the
+// 2*deg neighbour candidates are sorted / de-duplicated in shared memory.
 // Neighbours are written sorted & unique to nbr[2*inc_off[v] ...]; ucnt = count,
 // upcnt = count of neighbours > v (the vertex's lexicographic edges).
-__global__ void __launch_bounds__(128) k_vertex(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off, const int* __restrict__ inc,
-                                                const int* __restrict__ F, const Plane* __restrict__ plane, int Mcap,
-                                                double* __restrict__ vq, int* __restrict__ nbr, int* __restrict__ ucnt,
-                                                int* __restrict__ upcnt, int* __restrict__ heavy,
-                                                int* __restrict__ heavy_count) {
+constexpr int kGrp = 16;
+constexpr int kGrpWarps = 8;  // 256-thread blocks
+
+MF_DEV unsigned grp_mask() { return 0xFFFFu << (threadIdx.x & 16); }
+
+MF_DEV int grp_bitonic16(int x, unsigned mask) {
+    const int l = threadIdx.x & 15;
+#pragma unroll
+    for (int k = 2; k <= 16; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            int y = __shfl_xor_sync(mask, x, j, kGrp);
+            bool up = ((l & k) == 0);
+            bool lower = ((l & j) == 0);
+            x = (lower == up) ? min(x, y) : max(x, y);
+        }
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __restrict__ abort_flag, int N,
+                                                                 const int* __restrict__ inc_off,
+                                                                 const int* __restrict__ inc,
+                                                                 const int* __restrict__ F,
+                                                                 const Plane* __restrict__ plane, int Mcap,
+                                                                 double* __restrict__ vq, int* __restrict__ nbr,
+                                                                 int* __restrict__ ucnt, int* __restrict__ upcnt,
+                                                                 int* __restrict__ heavy,
+                                                                 int* __restrict__ heavy_count) {
     if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int s = inc_off[v], d = inc_off[v + 1] - s;
-        if (d > kSmallDeg) {
-            heavy[append_slot(heavy_count)] = v;
+    __shared__ double s_q[2 * kGrpWarps][kGrp][10];
+    __shared__ int s_c[2 * kGrpWarps][2 * kGrp];
+    const int g = threadIdx.x >> 4;  // group within block
+    const int l = threadIdx.x & 15;
+    const unsigned mask = grp_mask();
+    const int groups = gridDim.x * (blockDim.x >> 4);
+    for (int v = blockIdx.x * (blockDim.x >> 4) + g; v < N; v += groups) {
+        const int s = inc_off[v], d = inc_off[v + 1] - s;
+        if (d > kGrp) {
+            if (l == 0) heavy[atomicAdd(heavy_count, 1)] = v;
             continue;
         }
-        int k[kSmallDeg];
-        for (int i = 0; i < d; i++) k[i] = inc[s + i];
-        isort<kSmallDeg>(k, d);
-        Q10 q;
-        q_zero(q);
-        int cand[2 * kSmallDeg];
-        int nc = 0;
-        for (int i = 0; i < d; i++) {
+        int k = (l < d) ? inc[s + l] : 0x7fffffff;
+        k = grp_bitonic16(k, mask);
+        int a = 0x7fffffff, b = 0x7fffffff;
+        if (l < d) {
             int corner, f;
-            decode_inc(k[i], Mcap, corner, f);
+            decode_inc(k, Mcap, corner, f);
             Plane p = plane[f];
-            q_add_plane(q, p);
-            int a, b;
             other_two(F, f, corner, a, b);
-            cand[nc++] = a;
-            cand[nc++] = b;
+            double* q = s_q[g][l];
+            q[0] = p.n0 * p.n0; q[1] = p.n0 * p.n1; q[2] = p.n0 * p.n2;
+            q[3] = p.n1 * p.n1; q[4] = p.n1 * p.n2; q[5] = p.n2 * p.n2;
+            q[6] = p.d * p.n0; q[7] = p.d * p.n1; q[8] = p.d * p.n2;
+            q[9] = p.d * p.d;
         }
-        q_store(vq, v, q);
-        isort<2 * kSmallDeg>(cand, nc);
-        int nu = 0, nup = 0;
+        s_c[g][2 * l] = a;
+        s_c[g][2 * l + 1] = b;
+        __syncwarp(mask);
+        if (l < 10) {  // quadrics.py:72-76: fold each component in incidence order from +0.0
+            double acc = 0.0;
+            for (int i = 0; i < d; i++) acc = acc + s_q[g][i][l];
+            vq[10 * (size_t)v + l] = acc;
+        }
+        // bitonic sort of the 32 candidates (16 lanes, one compare-exchange each per stage)
+        int* c = s_c[g];
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                int i = ((l & ~(j - 1)) << 1) | (l & (j - 1));  // l-th pair (i, i + j)
+                int x = c[i], y = c[i + j];
+                bool up = ((i & kk) == 0);
+                if ((x > y) == up) { c[i] = y; c[i + j] = x; }
+                __syncwarp(mask);
+            }
+        }
+        // unique (keep first of each run), order preserving, among the 2d real values
+        int x0 = c[2 * l], x1 = c[2 * l + 1];
+        int prev = (l == 0) ? -1 : c[2 * l - 1];
+        bool k0 = (2 * l < 2 * d) && x0 != prev;
+        bool k1 = (2 * l + 1 < 2 * d) && x1 != x0;
+        unsigned b0 = __ballot_sync(mask, k0), b1 = __ballot_sync(mask, k1);
+        unsigned u0 = __ballot_sync(mask, k0 && x0 > v), u1 = __ballot_sync(mask, k1 && x1 > v);
+        const unsigned sh = threadIdx.x & 16;
+        b0 >>= sh; b1 >>= sh; u0 >>= sh; u1 >>= sh;
+        unsigned below = (1u << l) - 1u;
+        int pos = __popc(b0 & below) + __popc(b1 & below);
         int* out = nbr + 2 * (size_t)s;
-        for (int i = 0; i < nc; i++) {
-            if (i > 0 && cand[i] == cand[i - 1]) continue;
-            out[nu++] = cand[i];
-            nup += cand[i] > v;
+        if (k0) out[pos++] = x0;
+        if (k1) out[pos] = x1;
+        if (l == 0) {
+            ucnt[v] = __popc(b0) + __popc(b1);
+            upcnt[v] = __popc(u0) + __popc(u1);
         }
-        ucnt[v] = nu;
-        upcnt[v] = nup;
+        __syncwarp(mask);
+    }
+}
+
+// K4: lexicographic edge list + pair cost + rank key + adjacency edge ids.
+// Edge id of (v, u>v) = eoff[v] + rank of u among v's upper neighbours, which
+// is exactly np.unique(axis=0)'s lexicographic order (mesh.py:131-134).
+// One lane per neighbour of v.  Lower-indexed neighbours
+// resolve their edge id by binary search in the neighbour's upper list.
+__global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __restrict__ abort_flag, int N,
+                                                                const int* __restrict__ inc_off,
+                                                                const int* __restrict__ nbr,
+                                                                const int* __restrict__ ucnt,
+                                                                const int* __restrict__ upcnt,
+                                                                const int* __restrict__ eoff,
+                                                                const double* __restrict__ vq,
+                                                                const double* __restrict__ P, int* __restrict__ e0,
+                                                                int* __restrict__ e1, double* __restrict__ cost,
+                                                                uint64_t* __restrict__ key_hi,
+                                                                int* __restrict__ adj_eid, int* __restrict__ mate,
+                                                                int* __restrict__ minrep, int* __restrict__ absorbed,
+                                                                int order) {
+    if (*abort_flag) return;
+    const int g = threadIdx.x >> 4;
+    const int l = threadIdx.x & 15;
+    const int groups = gridDim.x * (blockDim.x >> 4);
+    for (int v = blockIdx.x * (blockDim.x >> 4) + g; v < N; v += groups) {
+        if (l == 0) {
+            mate[v] = -1;
+            minrep[v] = v;
+            absorbed[v] = -1;
+        }
+        const int nu = ucnt[v];
+        if (nu == 0) continue;
+        const size_t s2 = 2 * (size_t)inc_off[v];
+        const int nlow = nu - upcnt[v];
+        const int eb = eoff[v];
+        Q10 qv;
+        q_load(vq, v, qv);
+        const double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
+        for (int j = l; j < nu; j += kGrp) {
+            int u = nbr[s2 + j];
+            int eid;
+            if (u > v) {
+                eid = eb + (j - nlow);
+                Q10 qu;
+                q_load(vq, u, qu);
+                double c = pair_cost(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
+                e0[eid] = v;
+                e1[eid] = u;
+                cost[eid] = c;
+                key_hi[eid] = f64_key(c);
+            } else {
+                size_t su = 2 * (size_t)inc_off[u];
+                int nuu = ucnt[u];
+                int lo = nuu - upcnt[u], hi = nuu;
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (nbr[su + mid] < v) lo = mid + 1; else hi = mid;
+                }
+                eid = eoff[u] + (lo - (nuu - upcnt[u]));
+            }
+            adj_eid[s2 + j] = eid;
+        }
     }
 }
 
@@ -329,78 +474,7 @@ __global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ ab
     }
 }
 
-// Pair cost (quadrics.py:117-132 + evaluate 53-58, SURVEY A.2) for 'average' placement.
-MF_DEV double pair_cost(const Q10& qi, const Q10& qj, double pix, double piy, double piz, double pjx, double pjy,
-                        double pjz, int order) {
-    double a00 = qi.a00 + qj.a00, a01 = qi.a01 + qj.a01, a02 = qi.a02 + qj.a02;
-    double a11 = qi.a11 + qj.a11, a12 = qi.a12 + qj.a12, a22 = qi.a22 + qj.a22;
-    double b0 = qi.b0 + qj.b0, b1 = qi.b1 + qj.b1, b2 = qi.b2 + qj.b2, c = qi.c + qj.c;
-    double x0 = 0.5 * (pix + pjx), x1 = 0.5 * (piy + pjy), x2 = 0.5 * (piz + pjz);
-    double quad = 0.0;
-    quad = quad + (x0 * a00) * x0;
-    quad = quad + (x0 * a01) * x1;
-    quad = quad + (x0 * a02) * x2;
-    quad = quad + (x1 * a01) * x0;
-    quad = quad + (x1 * a11) * x1;
-    quad = quad + (x1 * a12) * x2;
-    quad = quad + (x2 * a02) * x0;
-    quad = quad + (x2 * a12) * x1;
-    quad = quad + (x2 * a22) * x2;
-    double lin = 2.0 * dot3(b0, b1, b2, x0, x1, x2, order);
-    return (quad + lin) + c;
-}
 
-// K4: lexicographic edge list + pair cost + rank key + adjacency edge ids.
-// Edge id of (v, u>v) = eoff[v] + rank of u among v's upper neighbours, which
-// is exactly np.unique(axis=0)'s lexicographic order (mesh.py:131-134).
-__global__ void __launch_bounds__(128) k_edges(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off, const int* __restrict__ nbr,
-                                               const int* __restrict__ ucnt, const int* __restrict__ upcnt,
-                                               const int* __restrict__ eoff, const double* __restrict__ vq,
-                                               const double* __restrict__ P, int* __restrict__ e0,
-                                               int* __restrict__ e1, double* __restrict__ cost,
-                                               uint64_t* __restrict__ key_hi, int* __restrict__ adj_eid,
-                                               int* __restrict__ mate, int* __restrict__ minrep,
-                                               int* __restrict__ absorbed, int order) {
-    if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        mate[v] = -1;
-        minrep[v] = v;
-        absorbed[v] = -1;
-        int nu = ucnt[v];
-        if (nu == 0) continue;
-        size_t s2 = 2 * (size_t)inc_off[v];
-        int nlow = nu - upcnt[v];
-        int eb = eoff[v];
-        Q10 qv;
-        q_load(vq, v, qv);
-        double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
-        for (int j = 0; j < nu; j++) {
-            int u = nbr[s2 + j];
-            int eid;
-            if (u > v) {
-                eid = eb + (j - nlow);
-                Q10 qu;
-                q_load(vq, u, qu);
-                double c = pair_cost(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
-                e0[eid] = v;
-                e1[eid] = u;
-                cost[eid] = c;
-                key_hi[eid] = f64_key(c);
-            } else {
-                // edge (u, v) lives in u's upper list: binary search v there
-                size_t su = 2 * (size_t)inc_off[u];
-                int nuu = ucnt[u];
-                int lo = nuu - upcnt[u], hi = nuu;
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (nbr[su + mid] < v) lo = mid + 1; else hi = mid;
-                }
-                eid = eoff[u] + (lo - (nuu - upcnt[u]));
-            }
-            adj_eid[s2 + j] = eid;
-        }
-    }
-}
 
 // ------------------------------------------------------------------------
 // Seeded shuffle keys (decimate.py:184-191).
@@ -526,14 +600,21 @@ MF_DEV void edge_key(const MatchArgs& a, int e, uint64_t& h, uint64_t& l) {
 
 __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
     if (*a.abort_flag) return;
-    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < a.N; u += gridDim.x * blockDim.x) {
+    // 16 lanes per proposer: the adjacency of `cur` is scanned in parallel
+    // (one neighbour per lane), the best winnable edge is an argmin over the
+    // group, and lane 0 issues the CAS.  Control flow is uniform per group.
+    const int g = threadIdx.x >> 4;
+    const int l = threadIdx.x & 15;
+    const unsigned mask = 0xFFFFu << (threadIdx.x & 16);
+    const int groups = gridDim.x * (blockDim.x >> 4);
+    for (int u = blockIdx.x * (blockDim.x >> 4) + g; u < a.N; u += groups) {
         int cur = u;
         while (cur >= 0) {
             const size_t s = 2 * (size_t)a.inc_off[cur];
             const int nu = a.ucnt[cur];
             int be = -1, bv = -1;
             uint64_t bh = ~0ull, bl = ~0ull;
-            for (int j = 0; j < nu; j++) {
+            for (int j = l; j < nu; j += 16) {
                 int e = a.adj_eid[s + j];
                 uint64_t kh, kl;
                 edge_key(a, e, kh, kl);
@@ -547,22 +628,31 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                 }
                 bh = kh; bl = kl; be = e; bv = v;
             }
-            if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
-            int sv = ld_volatile(a.suitor + bv);
-            int next = -2;  // -2: re-scan cur
-            while (true) {
-                if (sv >= 0) {
-                    uint64_t sh, sl;
-                    edge_key(a, sv, sh, sl);
-                    if (!key_lt(bh, bl, sh, sl)) break;  // lost the race: re-scan
-                }
-                int old = atomicCAS(a.suitor + bv, sv, be);
-                if (old == sv) {
-                    next = (sv < 0) ? -1 : (a.e0[sv] == bv ? a.e1[sv] : a.e0[sv]);
-                    break;
-                }
-                sv = old;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {
+                uint64_t oh = __shfl_xor_sync(mask, bh, o, 16), ol = __shfl_xor_sync(mask, bl, o, 16);
+                int oe = __shfl_xor_sync(mask, be, o, 16), ov = __shfl_xor_sync(mask, bv, o, 16);
+                if (key_lt(oh, ol, bh, bl)) { bh = oh; bl = ol; be = oe; bv = ov; }
             }
+            if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
+            int next = -2;      // -2: lost a race, re-scan cur
+            if (l == 0) {
+                int sv = ld_volatile(a.suitor + bv);
+                while (true) {
+                    if (sv >= 0) {
+                        uint64_t sh, sl;
+                        edge_key(a, sv, sh, sl);
+                        if (!key_lt(bh, bl, sh, sl)) break;
+                    }
+                    int old = atomicCAS(a.suitor + bv, sv, be);
+                    if (old == sv) {
+                        next = (sv < 0) ? -1 : (a.e0[sv] == bv ? a.e1[sv] : a.e0[sv]);
+                        break;
+                    }
+                    sv = old;
+                }
+            }
+            next = __shfl_sync(mask, next, 0, 16);
             if (next != -2) cur = next;
         }
     }
@@ -570,8 +660,9 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
 
 // mate = the suitor edge when the proposal is mutual.
 __global__ void k_mates(const int* __restrict__ abort_flag, int N, const int* __restrict__ suitor, const int* __restrict__ e0,
-                        const int* __restrict__ e1, int* __restrict__ mate) {
+                        const int* __restrict__ e1, int* __restrict__ mate, int B, int* __restrict__ seg_cnt) {
     if (*abort_flag) return;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) seg_cnt[b] = 0;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int e = suitor[v];
         int m = -1;
@@ -612,8 +703,8 @@ MF_DEV bool sel_prefix(uint64_t hi, uint64_t lo, uint64_t phi, uint64_t plo, int
 struct SelectArgs {
     const uint64_t* chi;
     const uint64_t* clo;
-    const int* cand_off;  // exclusive scan of candidate flags over the round's vertices
-    const int* voff;      // segment b owns candidates [cand_off[voff[b]], cand_off[voff[b+1]])
+    const int* seg_cnt;   // candidates of segment b: [voff[b], voff[b] + seg_cnt[b])
+    const int* voff;      // (a mesh never has more candidates than vertices)
     int B;
     const int* act;
     const int* budget;
@@ -635,7 +726,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     __shared__ int s_sel[4];
     __shared__ int s_ncomp;
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-        const int c0 = a.cand_off[a.voff[b]], c1 = a.cand_off[a.voff[b + 1]];
+        const int c0 = a.voff[b], c1 = c0 + a.seg_cnt[b];
         const int cnt = c1 - c0;
         int want = a.act[b] ? a.budget[b] - (a.removed ? a.removed[b] : 0) : 0;
         int k = want < cnt ? want : cnt;
@@ -729,34 +820,6 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
 }
 
 // ---- flag producers fused into the decoupled look-back scan (LoadOp functors)
-struct LoadTruncFlag {  // matched pair, counted at its e0 end
-    const int* mate;
-    const int* e0;
-    MF_DEV int operator()(int v) const {
-        int e = mate[v];
-        return e >= 0 && e0[e] == v;
-    }
-};
-struct LoadAbsorbFlag {  // unmatched vertex with a clustered neighbour in a mesh still short of budget
-    const int* inc_off;
-    const int* ucnt;
-    const int* nbr;
-    const int* mate;
-    const int* vmesh;
-    const int* act;
-    const int* budget;
-    const int* removed;
-    MF_DEV int operator()(int v) const {
-        int nu = ucnt[v];
-        if (nu == 0 || mate[v] >= 0) return 0;
-        int b = vmesh ? vmesh[v] : 0;
-        if (!act[b] || removed[b] >= budget[b]) return 0;
-        size_t s = 2 * (size_t)inc_off[v];
-        for (int j = 0; j < nu; j++)
-            if (mate[nbr[s + j]] >= 0) return 1;
-        return 0;
-    }
-};
 struct LoadIsRep {  // v is the lowest member of its cluster
     const int* anchor;
     const int* minrep;
@@ -779,35 +842,60 @@ MF_DEV bool is_selected(int mode, uint64_t h, uint64_t l, uint64_t th, uint64_t 
 
 // Candidate flags (pass 1) and ordered writes (pass 2) for budget truncation:
 // the matched edges, one per pair from its e0 end.
-__global__ void k_trunc_write(const int* __restrict__ abort_flag, int N, const int* __restrict__ mate, const int* __restrict__ e0,
-                              const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
-                              const int* __restrict__ coff, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
-                              int* __restrict__ cpay) {
+// Candidates are appended into their mesh's own vertex-index range, so each
+// segment is contiguous without a scan (order inside a segment is irrelevant:
+// the selection is by unique key).
+MF_DEV int seg_slot(const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt, int v,
+                    int& b) {
+    if (!vmesh) {
+        b = 0;
+        return append_slot(seg_cnt);
+    }
+    b = vmesh[v];
+    return voff[b] + atomicAdd(seg_cnt + b, 1);
+}
+
+// Budget truncation candidates: the matched edges, one per pair from its e0 end.
+__global__ void k_trunc_cand(const int* __restrict__ abort_flag, int N, const int* __restrict__ mate,
+                             const int* __restrict__ e0, const uint64_t* __restrict__ key_hi,
+                             const uint64_t* __restrict__ key_lo, const int* __restrict__ vmesh,
+                             const int* __restrict__ voff, int* __restrict__ seg_cnt, uint64_t* __restrict__ chi,
+                             uint64_t* __restrict__ clo, int* __restrict__ cpay) {
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int e = mate[v];
         if (e < 0 || e0[e] != v) continue;
-        int slot = coff[v];
+        int b;
+        int slot = seg_slot(vmesh, voff, seg_cnt, v, b);
         chi[slot] = key_hi[e];
         clo[slot] = key_lo ? key_lo[e] : (uint64_t)e;
         cpay[slot] = e;
     }
 }
 
+MF_DEV bool seg_valid(const int* __restrict__ vmesh, const int* __restrict__ voff, const int* __restrict__ seg_cnt,
+                      int i, int& b) {
+    b = vmesh ? vmesh[i] : 0;
+    return i - voff[b] < seg_cnt[b];
+}
+
 // Unmatch the pairs beyond the budget; removed = number kept.
-__global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const int* __restrict__ vmesh, const int* __restrict__ coff,
+__global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const int* __restrict__ vmesh,
+                              const int* __restrict__ voff, const int* __restrict__ seg_cnt,
                               const uint64_t* __restrict__ chi, const uint64_t* __restrict__ clo,
                               const int* __restrict__ cpay, const int* __restrict__ mode,
                               const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
                               const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate, int B,
-                              const int* __restrict__ ksel, int* __restrict__ removed) {
+                              const int* __restrict__ ksel, int* __restrict__ removed, int* __restrict__ seg_cnt2) {
     if (*abort_flag) return;
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    for (int b = tid; b < B; b += nth) removed[b] = ksel[b];
-    for (int v = tid; v < N; v += nth) {
-        int i = coff[v];
-        if (coff[v + 1] == i) continue;  // not a candidate
-        int b = mesh_of(vmesh, v);
+    for (int b = tid; b < B; b += nth) {
+        removed[b] = ksel[b];
+        seg_cnt2[b] = 0;
+    }
+    for (int i = tid; i < N; i += nth) {
+        int b;
+        if (!seg_valid(vmesh, voff, seg_cnt, i, b)) continue;
         if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) continue;
         int e = cpay[i];
         mate[e0[e]] = -1;
@@ -818,37 +906,36 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
 // Absorb candidates (decimate.py:207-221): every unmatched vertex with edges
 // picks its lowest (cost, rep) incident edge; the matching is maximal here so
 // every neighbour is clustered and one pass suffices.
-MF_DEV bool absorb_best(int v, const int* __restrict__ inc_off, const int* __restrict__ ucnt,
-                        const int* __restrict__ nbr, const int* __restrict__ adj_eid, const double* __restrict__ cost,
-                        const int* __restrict__ mate, const int* __restrict__ e0, uint64_t& bk, int& brep) {
-    int nu = ucnt[v];
-    size_t s = 2 * (size_t)inc_off[v];
-    bk = ~0ull;
-    brep = 0x7fffffff;
-    for (int j = 0; j < nu; j++) {
-        int mu = mate[nbr[s + j]];
-        if (mu < 0) continue;  // cannot happen for a maximal matching
-        int rep = e0[mu];
-        uint64_t k = f64_key(cost[adj_eid[s + j]]);
-        if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
-    }
-    return brep != 0x7fffffff;
-}
-__global__ void k_absorb_write(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off, const int* __restrict__ ucnt,
-                               const int* __restrict__ nbr, const int* __restrict__ adj_eid,
-                               const double* __restrict__ cost, const int* __restrict__ mate,
-                               const int* __restrict__ e0, const int* __restrict__ coff, uint64_t* __restrict__ chi,
-                               uint64_t* __restrict__ clo, int* __restrict__ caux) {
+__global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off,
+                              const int* __restrict__ ucnt, const int* __restrict__ nbr,
+                              const int* __restrict__ adj_eid, const double* __restrict__ cost,
+                              const int* __restrict__ mate, const int* __restrict__ e0, const int* __restrict__ vmesh,
+                              const int* __restrict__ voff, const int* __restrict__ act,
+                              const int* __restrict__ budget, const int* __restrict__ removed,
+                              int* __restrict__ seg_cnt, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
+                              int* __restrict__ caux) {
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int i = coff[v];
-        if (coff[v + 1] == i) continue;
-        uint64_t bk;
-        int brep;
-        absorb_best(v, inc_off, ucnt, nbr, adj_eid, cost, mate, e0, bk, brep);
-        chi[i] = bk;
-        clo[i] = ((uint64_t)(unsigned)brep << 32) | (unsigned)v;
-        caux[i] = brep;
+        int nu = ucnt[v];
+        if (nu == 0 || mate[v] >= 0) continue;
+        int bm = mesh_of(vmesh, v);
+        if (!act[bm] || removed[bm] >= budget[bm]) continue;
+        size_t s = 2 * (size_t)inc_off[v];
+        uint64_t bk = ~0ull;
+        int brep = 0x7fffffff;
+        for (int j = 0; j < nu; j++) {
+            int mu = mate[nbr[s + j]];
+            if (mu < 0) continue;  // cannot happen for a maximal matching
+            int rep = e0[mu];
+            uint64_t k = f64_key(cost[adj_eid[s + j]]);
+            if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
+        }
+        if (brep == 0x7fffffff) continue;
+        int b;
+        int slot = seg_slot(vmesh, voff, seg_cnt, v, b);
+        chi[slot] = bk;
+        clo[slot] = ((uint64_t)(unsigned)brep << 32) | (unsigned)v;
+        caux[slot] = brep;
     }
 }
 
@@ -859,21 +946,25 @@ struct RoundFail {
     int* fail_noedge;  // per mesh: the failing round had no edges (decimate.py:239-244)
 };
 
-__global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* __restrict__ coff,
-                               const uint64_t* __restrict__ chi, const uint64_t* __restrict__ clo,
-                               const int* __restrict__ caux, const int* __restrict__ mode,
-                               const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
-                               int* __restrict__ absorbed, int B, const int* __restrict__ act,
+__global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* __restrict__ voff,
+                               const int* __restrict__ seg_cnt, const uint64_t* __restrict__ chi,
+                               const uint64_t* __restrict__ clo, const int* __restrict__ caux,
+                               const int* __restrict__ mode, const uint64_t* __restrict__ thi,
+                               const uint64_t* __restrict__ tlo, int* __restrict__ absorbed,
+                               int* __restrict__ minrep, int B, const int* __restrict__ act,
                                const int* __restrict__ budget, const int* __restrict__ nin,
                                const int* __restrict__ ksel, int* __restrict__ removed, const int* __restrict__ eoff,
-                               const int* __restrict__ voff, RoundFail fail, int round) {
+                               RoundFail fail, int round) {
     if (*fail.abort) return;
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    for (int v = tid; v < N; v += nth) {
-        int i = coff[v];
-        if (coff[v + 1] == i) continue;
-        int b = mesh_of(vmesh, v);
-        if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) absorbed[v] = caux[i];
+    for (int i = tid; i < N; i += nth) {
+        int b;
+        if (!seg_valid(vmesh, voff, seg_cnt, i, b)) continue;
+        if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) {
+            int v = (int)(clo[i] & 0xffffffffull), rep = caux[i];
+            absorbed[v] = rep;
+            atomicMin(minrep + rep, v);  // cluster's lowest member (decimate.py:224)
+        }
     }
     for (int b = tid; b < B; b += nth) {
         if (!act[b]) continue;
@@ -900,10 +991,7 @@ __global__ void k_relabel1(int N, const int* __restrict__ abort_flag, const int*
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int m = mate[v], a = v;
         if (m >= 0) a = e0[m];
-        else if (absorbed[v] >= 0) {
-            a = absorbed[v];
-            atomicMin(minrep + a, v);
-        }
+        else if (absorbed[v] >= 0) a = absorbed[v];
         anchor[v] = a;
     }
 }
