@@ -44,20 +44,39 @@ L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
 
 # ---------------------------------------------------------------- workloads
 def workload(name: str, rank: int):
+    """Synthetic input of a BASELINE.json config.  `levels` = successive
+    decimate_parallel targets of one step (a hierarchy for cfg3 / cfg5);
+    `pool_channels` > 0 adds max-pool down / unpool up of float32 features."""
     from paper_2103_15076_b200 import synthetic as S
     from paper_2103_15076_b200.mesh import concat_batch
 
     if name == "cfg2":
-        return dict(mesh=S.delaunay_terrain(115_114, noise=0.02, seed=12), target=41_449,
+        return dict(mesh=S.delaunay_terrain(115_114, noise=0.02, seed=12), levels=[41_449], pool_channels=0,
                     desc="delaunay_terrain(115114, noise=0.02, seed=12) -> 41449 vertices (BASELINE configs[1])")
     if name == "cfg1":
-        return dict(mesh=S.icosphere(5), target=3585, desc="icosphere(5) -> 3585 vertices (configs[0])")
+        return dict(mesh=S.icosphere(5), levels=[3585], pool_channels=0,
+                    desc="icosphere(5) -> 3585 vertices (configs[0])")
+    if name == "cfg3":
+        return dict(mesh=S.delaunay_terrain(500_000, noise=0.02, seed=3), levels=[125_000, 62_500, 31_250, 15_625],
+                    pool_channels=64,
+                    desc="delaunay_terrain(500000, 0.02, seed=3): 4 decimations 125000/62500/31250/15625 + "
+                         "max-pool down / unpool up of C=64 float32 features (configs[2])")
     if name == "cfg4":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         per = 256 // world
         meshes = [S.delaunay_terrain(2500, noise=0.02, seed=b) for b in range(rank * per, (rank + 1) * per)]
-        return dict(mesh=concat_batch(meshes), target=1250,
-                    desc=f"batch of {per} delaunay_terrain(2500, 0.02, seed=b) -> 1250 each (configs[3] slice)")
+        return dict(mesh=concat_batch(meshes), levels=[1250], pool_channels=0,
+                    desc=f"batch of {per} delaunay_terrain(2500, 0.02, seed=b) -> 1250 each (configs[3] slice "
+                         f"of 256 over {world} GPU(s))")
+    if name == "cfg5":
+        mesh = S.perturbed_grid(3163, noise=0.02, seed=rank)
+        n, lv = mesh.n_vertices, []
+        for _ in range(4):
+            n = -(-n // 2)
+            lv.append(n)
+        return dict(mesh=mesh, levels=lv, pool_channels=0,
+                    desc="perturbed_grid(3163, 0.02, seed=rank): 4 levels by ceil-halving "
+                         + "/".join(str(x) for x in lv) + " (configs[4], one mesh per GPU)")
     raise SystemExit(f"unknown --config {name}")
 
 
@@ -168,59 +187,99 @@ def dist_setup():
     return world, rank, local
 
 
-# ---------------------------------------------------------------- reference arm
+# ---------------------------------------------------------------- CPU arm (oracle port of the reference)
+def cpu_sample(name: str, wl: dict) -> dict:
+    """Bounded CPU sample of a workload: the same workload when one oracle step
+    takes a few seconds, else the same generator at reduced size."""
+    if name == "cfg5":
+        from paper_2103_15076_b200 import synthetic as S
+
+        mesh = S.perturbed_grid(700, noise=0.02, seed=0)
+        n, lv = mesh.n_vertices, []
+        for _ in range(4):
+            n = -(-n // 2)
+            lv.append(n)
+        return dict(mesh=mesh, levels=lv, pool_channels=0,
+                    desc="perturbed_grid(700, 0.02, seed=0), same 4-level ceil-halving hierarchy (reduced size)")
+    return wl
+
+
+def oracle_step(wl: dict, threads: int = 1) -> None:
+    """One step on the C oracle: the level chain, plus max-pool down / unpool up when configured."""
+    from oracle import oracle as O
+
+    mesh = wl["mesh"]
+    batched = hasattr(mesh, "vertex_offsets")
+    base = mesh.mesh if batched else mesh
+    P, F, X = base.positions, base.facets, None
+    kw = dict(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets, threads=threads) if batched \
+        else {}
+    feats = wl.get("_features")
+    reps = []
+    for tgt in wl["levels"]:
+        out = O.decimate(P, F, X, target=tgt, **kw)
+        if feats is not None:
+            reps.append((out["replace"], len(out["positions"])))
+            feats = O.pool(feats, out["replace"], len(out["positions"]), "max")
+        P, F, X = out["positions"], out["facets"], out["features"]
+        if batched:
+            kw.update(vertex_offsets=out["vertex_offsets"], facet_offsets=out["facet_offsets"])
+    for rep, _ in reversed(reps):
+        feats = O.unpool(feats, rep)
+
+
+def with_features(wl: dict) -> dict:
+    if wl.get("pool_channels"):
+        n = (wl["mesh"].mesh if hasattr(wl["mesh"], "vertex_offsets") else wl["mesh"]).n_vertices
+        wl["_features"] = np.random.default_rng(0).standard_normal((n, wl["pool_channels"])).astype(np.float32)
+    return wl
+
+
+def facets_in(wl: dict) -> int:
+    m = wl["mesh"]
+    return (m.mesh if hasattr(m, "vertex_offsets") else m).n_facets
+
+
 def run_reference(args):
     world, rank, _ = dist_setup()
     if rank != 0:
         return 0
-    from oracle import oracle as O
-
-    wl = workload(args.config, 0)
-    mesh, target = wl["mesh"], wl["target"]
-    batched = hasattr(mesh, "vertex_offsets")
+    wl = with_features(cpu_sample(args.config, workload(args.config, 0)))
     threads = os.cpu_count() or 1
-    base = mesh.mesh if batched else mesh
-    kw = dict(target=target, seed=None, threads=threads)
-    if batched:
-        kw.update(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets)
     for _ in range(args.warmup):
-        O.decimate(base.positions, base.facets, None, **kw)
+        oracle_step(wl, threads)
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        O.decimate(base.positions, base.facets, None, **kw)
+        oracle_step(wl, threads)
         times.append(time.perf_counter() - t)
     ms = 1e3 * float(np.mean(times))
-    value = base.n_facets / (ms / 1e3)
+    value = facets_in(wl) / (ms / 1e3)
+    batched = hasattr(wl["mesh"], "vertex_offsets")
     cores = threads if batched else 1
-    sample = f"full {args.config} workload per step ({base.n_facets} facets), oracle port of the reference"
+    sample = f"{wl['desc']}; oracle port of the reference, {'%d threads over meshes' % threads if batched else '1 thread'}"
     line = {"metric": METRIC, "value": value, "unit": "facets/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl["desc"], "facets_in": base.n_facets, "vertices_in": base.n_vertices},
+            "config": {"workload": wl["desc"], "facets_in": facets_in(wl)},
             "cpu_baseline": {"value": value, "unit": "facets/s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "facets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline(mesh, target, budget_s=12.0):
+def cpu_baseline(name: str, wl: dict, budget_s: float = 12.0) -> dict:
     """The C oracle (port of the reference path) on this host, single thread, bounded sample."""
-    from oracle import oracle as O
-
-    base = mesh.mesh if hasattr(mesh, "vertex_offsets") else mesh
-    kw = dict(target=target)
-    if hasattr(mesh, "vertex_offsets"):
-        kw.update(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets)
+    sw = with_features(dict(cpu_sample(name, wl)))
     times = []
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < budget_s and len(times) < 50:
         t = time.perf_counter()
-        O.decimate(base.positions, base.facets, None, **kw)
+        oracle_step(sw, 1)
         times.append(time.perf_counter() - t)
     ms = 1e3 * float(np.median(times))
-    return {"value": base.n_facets / (ms / 1e3), "unit": "facets/s", "cores": 1, "kind": "port",
-            "sample": f"{len(times)} full decimations of the same workload (median {ms:.1f} ms)"}
+    return {"value": facets_in(sw) / (ms / 1e3), "unit": "facets/s", "cores": 1, "kind": "port",
+            "sample": f"{len(times)} step(s) of {sw['desc']} (median {ms:.1f} ms)"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -242,19 +301,33 @@ def run_ours(args):
     from paper_2103_15076_b200 import _native
     from paper_2103_15076_b200 import tensor as T
 
-    wl = workload(args.config, rank)
-    mesh, target = wl["mesh"], wl["target"]
+    wl = with_features(workload(args.config, rank))
+    mesh, levels = wl["mesh"], wl["levels"]
     batched = hasattr(mesh, "vertex_offsets")
     base = mesh.mesh if batched else mesh
     n_in, m_in = base.n_vertices, base.n_facets
-    V = torch.from_numpy(base.positions).to(dev)
-    Fd = torch.from_numpy(base.facets).to(dev)
+    V0 = torch.from_numpy(base.positions).to(dev)
+    F0 = torch.from_numpy(base.facets).to(dev)
+    X0 = torch.from_numpy(wl["_features"]).to(dev) if wl.get("_features") is not None else None
     nv = np.diff(mesh.vertex_offsets) if batched else None
     nf = np.diff(mesh.facet_offsets) if batched else None
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def step():
-        return T.decimate(V, Fd, nv, nf, target=target)
+        dds = []
+        V, F, X, cnv, cnf = V0, F0, X0, nv, nf
+        for tgt in levels:
+            dd = T.decimate(V, F, cnv, cnf, target=tgt)
+            dds.append(dd)
+            if X is not None:
+                X = T.pool(X, dd, mode="max")
+            V, F = dd.vertices, dd.faces
+            if batched:
+                cnv, cnf = dd.nv.numpy(), dd.mf.numpy()
+        if X is not None:
+            for dd in reversed(dds):
+                X = T.unpool(X, dd)
+        return dds
 
     # warm-up; the last warm-up step times every kernel to name the dominant one
     for _ in range(max(0, args.warmup - 1)):
@@ -262,16 +335,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     flush.zero_()
     _native.profile(1)
-    dd = step()
+    dds = step()
     torch.cuda.synchronize()
     breakdown = _native.profile_read()
     _native.profile(0)
-    rounds = dd.round_stats()
-    for r in rounds:
-        r["N0"] = n_in
+    rounds = []
+    for dd in dds:
+        for r in dd.round_stats():
+            r["N0"] = dd._dec.n_in
+            rounds.append(r)
     total_ms = sum(v[0] for v in breakdown.values())
     dominant = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
-
     # the timed region times the dominant kernel live: warm that graph variant first
     _native.profile(2, dominant)
     step()
@@ -311,25 +385,44 @@ def run_ours(args):
     Fp = torch.empty((m_in, 3), dtype=torch.int64, pin_memory=True).numpy()
     Pp[:] = base.positions
     Fp[:] = base.facets
+    Xp = None
+    if wl.get("_features") is not None:
+        Xp = torch.empty(wl["_features"].shape, dtype=torch.float32, pin_memory=True).numpy()
+        Xp[:] = wl["_features"]
     pm = mfg.TriMesh(Pp, Fp)
     host_mesh = mfg.BatchedMesh(pm, mesh.vertex_offsets, mesh.facet_offsets) if batched else pm
-    cfg = mfg.DecimationConfig(target_vertices=target)
-    res = mfg.decimate_parallel(host_mesh, cfg)
+
+    def e2e_step():
+        cur, X, outs, d2h = host_mesh, Xp, [], 0
+        for tgt in levels:
+            res = mfg.decimate_parallel(cur, mfg.DecimationConfig(target_vertices=tgt))
+            outs.append(res)
+            o = res.mesh.mesh if batched else res.mesh
+            d2h += o.positions.nbytes + o.facets.nbytes + o.features.nbytes + res.replace.nbytes + res.mapping.nbytes
+            if X is not None:
+                X = mfg.pool(X, res, mode="max")
+                d2h += X.nbytes
+            cur = res.mesh
+        if X is not None:
+            for res in reversed(outs):
+                X = mfg.unpool(X, res)
+                d2h += X.nbytes
+        return d2h
+
+    d2h = e2e_step()
     e2e_t = []
-    for _ in range(args.steps):
+    for _ in range(max(3, min(args.steps, 20))):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = mfg.decimate_parallel(host_mesh, cfg)
+        e2e_step()
         e2e_t.append(time.perf_counter() - t0)
     e2e_ms = 1e3 * float(np.mean(e2e_t))
     t = torch.tensor([e2e_ms], device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
-    out = res.mesh.mesh if batched else res.mesh
-    h2d = Pp.nbytes + Fp.nbytes
-    d2h = out.positions.nbytes + out.facets.nbytes + out.features.nbytes + res.replace.nbytes + res.mapping.nbytes
+    h2d = Pp.nbytes + Fp.nbytes + (Xp.nbytes if Xp is not None else 0)
 
     if rank != 0:
         if dist:
@@ -348,20 +441,20 @@ def run_ours(args):
                      "launches_per_step": dom[1] / args.steps, "ms_per_step": dom_ms_per_step,
                      "share_of_step": dom_ms_per_step / step_ms})
     else:
-        roof.update({"achieved": None, "frac": None})
+        roof.update({"achieved": None, "frac": None, "ms_per_step": dom_ms_per_step})
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
             traffic = json.load(fh).get(args.config, {}).get(dominant)
     roof["traffic"] = traffic
-    whole = step_bytes(rounds, n_in)
+    whole = sum(step_bytes([r], r["N0"]) - 16.0 * r["N0"] for r in rounds) + 16.0 * n_in
     roof["step_alg_bytes"] = whole
     roof["step_frac"] = whole / (step_ms / 1e3) / 1e9 / peak
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(mesh, target)
+        cpu = cpu_baseline(args.config, wl)
 
     vs = None
     if args.config == "cfg2":
@@ -370,18 +463,18 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "facets/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": vs, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "facets_in": m_in, "vertices_in": n_in, "target": target,
+        "config": {"workload": wl["desc"], "facets_in": m_in, "vertices_in": n_in, "levels": levels,
                    "rounds": len(rounds), "l2": "flushed between timed steps (512 MiB memset, outside events)",
-                   "parallelism": f"replicas x{world}, one mesh per GPU, no collective" if world > 1 else "1 GPU"},
+                   "parallelism": f"{world} GPUs, independent work per GPU, no collective" if world > 1 else "1 GPU"},
         "clocks": clk.summary(),
         "e2e": {"value": world * m_in / (e2e_ms / 1e3), "unit": "facets/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "paper_2103_15076_b200.decimate_parallel(TriMesh numpy, pinned) -> numpy"},
+                "path": "paper_2103_15076_b200.decimate_parallel / pool / unpool (numpy in, numpy out; pinned inputs)"},
         "gpu_launches": int(launches),
         "roofline": roof,
         "cpu_baseline": cpu,
         "kernels": {k: {"ms": round(v[0], 4), "share": round(v[0] / total_ms, 4), "launches": v[1]}
-                    for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:8]},
+                    for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:10]},
         "round_stats": rounds,
     }
     if vs is not None:
