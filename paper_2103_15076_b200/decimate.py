@@ -129,7 +129,7 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     config.target_vertices); raises InfeasibleTargetError naming the
     achievable minimum, ValueError / StructuralError as the reference does.
     """
-    batched = isinstance(mesh, BatchedMesh)
+    batched = hasattr(mesh, "vertex_offsets")  # duck-typed: the reference's containers work too
     base = mesh.mesh if batched else mesh
     P = np.ascontiguousarray(base.positions, dtype=np.float64)
     F = np.ascontiguousarray(base.facets, dtype=np.int64)
@@ -187,7 +187,7 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
 
 
 def _all_identity(mesh, config) -> bool:
-    if isinstance(mesh, BatchedMesh):
+    if hasattr(mesh, "vertex_offsets"):
         nv = np.diff(mesh.vertex_offsets)
         return bool(np.all(nv == config.target_vertices))
     return mesh.n_vertices == config.target_vertices
