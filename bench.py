@@ -163,6 +163,11 @@ def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
         # adjacency (nbr + edge id) + rank key per slot, suitor word per vertex
         "k_suitor": 8 * E + 8 * E + 16 * E + 8 * N,
         "k_select": 16 * Nn,
+        # one pass over the adjacency (nbr + edge id + key prefix) + pick / mate words: the matching
+        # must read every incidence at least once; all LD-round launches of the round share it
+        "k_ld_pick": 24 * E + 12 * N,
+        "k_vertex_t": 4 * N + 12 * M + 32 * M + 12 * M + 80 * N + 8 * E + 8 * N,
+        "k_adj_keys": 16 * E + 8 * E,
         "k_contract": 4 * N + 4 * Nn + 24 * N + 24 * Nn,
         "k_facet_remap": 12 * M + 4 * N + 12 * M + 16 * M + 4 * M + N,
         "k_compose": 8 * r.get("N0", N) + 4 * N,

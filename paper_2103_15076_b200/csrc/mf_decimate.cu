@@ -178,6 +178,7 @@ struct Plan {
     int order = 0;
     uint64_t pcg[4] = {0, 0, 0, 0};
     size_t params_words = 0;
+    int ld_min = kLDMinVertices;  // rounds with at least this many vertices start with LD rounds
 };
 
 static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan& p, mf_status* st) {
@@ -281,6 +282,7 @@ static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan
     p.N1 = R > 0 ? p.h_N[1] : p.N0;
     p.seeded = cfg->seeded != 0;
     p.order = cfg->einsum_order;
+    if (const char* e = getenv("MF_LD_MIN")) p.ld_min = atoi(e);
     for (int i = 0; i < 4; i++) p.pcg[i] = cfg->pcg_state[i];
     // device params: act | budget | nin | voff | foff0 (int32)
     p.params_words = (size_t)p.nParamR * B * 2 + (size_t)(R + 1) * B + (size_t)(R + 1) * (B + 1) + (B + 1);
@@ -301,7 +303,13 @@ struct WS {
     Plane* plane;
     int *deg, *inc_off, *cursor, *inc, *inc_tmp;
     double* vq;
-    int *nbr, *nbr_tmp, *adj_eid, *ucnt, *upcnt, *eoff, *heavy, *counters, *e0, *e1;
+    unsigned* adj_k32;
+    unsigned long long* suitor;
+    int *bestu, *front0, *front1, *ldc;
+    unsigned* bar;
+    int* selstate;
+    int* ghist;
+    int *nbr, *nbr_tmp, *adj_eid, *ucnt, *upcnt, *eoff, *heavy, *mid, *counters, *e0, *e1;
     double* cost;
     uint64_t *key_hi, *key_lo;
     unsigned long long *mlo, *mhi;
@@ -357,10 +365,20 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.nbr = A.take<int>((size_t)2 * Ecap);
     W.nbr_tmp = A.take<int>((size_t)2 * Ecap);
     W.adj_eid = A.take<int>((size_t)2 * Ecap);
+    W.adj_k32 = A.take<unsigned>((size_t)2 * Ecap);
+    W.suitor = A.take<unsigned long long>((size_t)N0);
+    W.bestu = A.take<int>((size_t)N0);
+    W.front0 = A.take<int>((size_t)N0);
+    W.front1 = A.take<int>((size_t)N0);
+    W.ldc = A.take<int>(8);
+    W.bar = A.take<unsigned>(8);
+    W.selstate = A.take<int>((size_t)2 * B);
+    W.ghist = A.take<int>(kSelBins);
     W.ucnt = A.take<int>((size_t)N0);
     W.upcnt = A.take<int>((size_t)N0);
     W.eoff = A.take<int>((size_t)N0 + 1);
     W.heavy = A.take<int>((size_t)N0);
+    W.mid = A.take<int>((size_t)N0);
     W.counters = A.take<int>(64);
     W.e0 = A.take<int>((size_t)Ecap);
     W.e1 = A.take<int>((size_t)Ecap);
@@ -425,6 +443,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     RC(cudaMemsetAsync(W.status, 0, W.status_words * sizeof(int), stream));
     RC(cudaMemsetAsync(d_fail, 0xFF, (size_t)B * 3 * sizeof(int), stream));
     RC(cudaMemsetAsync(d_badf, 0x7f, sizeof(int), stream));
+    RC(cudaMemsetAsync(W.ghist, 0, kSelBins * sizeof(int), stream));
     if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, W.F0, B, W.vo64, W.fo64, d_badf);
     if (n > 0) LAUNCH(k_check_finite, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, W.P0, d_badp);
     if (W.Xf32 && n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, W.X0);
@@ -438,6 +457,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     const int order = p.order;
     int* d_heavy_n = W.counters + 4;
     int* d_heavy_c = W.counters + 12;
+    int* d_mid_n = W.counters + 20;
     for (int r = 0; r < R; r++) {
         const int N = p.h_N[r];
         const int Nn = p.h_N[r + 1];
@@ -464,13 +484,15 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         LAUNCH(k_inc_scatter, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, dM, Mcap, vmesh, act, W.inc_off, W.cursor,
                W.inc);
         // vertex quadrics + unique neighbour lists
-        LAUNCH(k_vertex, grid_for(ctx, (int64_t)N * kGrp), 256, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap, W.vq, W.nbr,
-               W.ucnt, W.upcnt, W.heavy, d_heavy_n);
+        LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap,
+               W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
+        LAUNCH(k_vertex, ctx->sm_count * 8, 256, 0, stream, d_abort, W.mid, d_mid_n, W.inc_off, W.inc, Fc, W.plane,
+               Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.heavy, d_heavy_n);
         LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
                W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
         // lexicographic edges + pair costs + rank keys
         run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
-        LAUNCH(k_edges, grid_for(ctx, (int64_t)N * kGrp), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
+        LAUNCH(k_edges, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
                W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed, order);
         const int* dE = W.eoff + N;
         if (seeded) {
@@ -481,16 +503,45 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                    vmesh, W.eoff, voff_r, W.mlo, W.mhi, p.pcg[0], p.pcg[1], p.pcg[2], p.pcg[3], W.key_hi, W.key_lo);
         }
         // greedy matching (Suitor proposals) -> mutual proposals are the matched pairs
-        RC(cudaMemsetAsync(W.best, 0xFF, (size_t)N * sizeof(int), stream));
-        {
-            MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.e0, W.e1, W.key_hi, seeded ? W.key_lo : nullptr,
-                         W.best, d_abort};
-            LAUNCH(k_suitor, grid_for(ctx, (int64_t)N * 16), 256, 0, stream, ma);
+        LAUNCH(k_adj_keys, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.adj_eid,
+               W.key_hi, W.adj_k32);
+        // large meshes: locally-dominant rounds (persistent) first, then Suitor proposals on the
+        // residual frontier; small meshes: Suitor only (the grid barriers would dominate)
+        const bool use_ld = N >= p.ld_min;
+        RC(cudaMemsetAsync(W.ldc, 0, 8 * sizeof(int), stream));
+        RC(cudaMemsetAsync(W.bar, 0, 8 * sizeof(unsigned), stream));
+        if (!use_ld) {
+            RC(cudaMemsetAsync(W.mate, 0xFF, (size_t)N * sizeof(int), stream));
+        } else {
+            LDArgs la{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
+                      W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, kLDRounds, d_abort};
+            LAUNCH(k_ld_init, grid_for(ctx, N), 256, 0, stream, la);
+            for (int round = 0; round < kLDRounds; round++) {
+                LAUNCH(k_ld_pick, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, la, round);
+                LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, round);
+            }
         }
-        LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.best, W.e0, W.e1, W.mate, B, W.segA);
+        RC(cudaMemsetAsync(W.suitor, 0xFF, (size_t)N * sizeof(unsigned long long), stream));
+        {
+            MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.adj_k32, W.e0, W.e1, W.key_hi,
+                         seeded ? W.key_lo : nullptr, W.suitor, d_abort, use_ld ? W.mate : nullptr,
+                         use_ld ? W.front0 : nullptr, W.front1, W.ldc};
+            LAUNCH(k_suitor, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, ma);
+        }
+        LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, B, W.segA);
+        // per-mesh selection; one big mesh first narrows its rank prefix with multi-block passes
+        const bool big = (B == 1 && N > (1 << 16));
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
-                          d_abort};
+                          d_abort, W.selstate, W.selstate + B, 0};
+            if (big) {
+                for (int pass = 0; pass < 2; pass++) {
+                    LAUNCH(k_sel_hist, std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2), 512, 0, stream, sa,
+                           W.ghist, pass);
+                    LAUNCH(k_sel_decide, 1, kSelThreads, 0, stream, sa, W.ghist, pass);
+                }
+                sa.resume = 1;
+            }
             LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelSmem, stream, sa);
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
@@ -526,7 +577,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         RC(cudaMemsetAsync(W.table, 0xFF, (size_t)W.tsize * sizeof(int), stream));
         RC(cudaMemsetAsync(W.has_live, 0, (size_t)N, stream));
         LAUNCH(k_facet_remap, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh, act, W.mapped,
-               W.canon, W.slot, W.has_live, W.table, W.tsize - 1);
+               W.canon, W.slot, W.has_live, W.table, W.tsize - 1, std::max(1u, W.tsize / (unsigned)std::max(Nn, 1)));
         run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort);
         LAUNCH(k_facet_write, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, W.kout, W.mapped, Fn, B, foff_c,
                foff_n);
@@ -535,6 +586,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         RC(cudaMemcpyAsync(d_stats + 4 * r + 0, foff_c + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));
         RC(cudaMemcpyAsync(d_stats + 4 * r + 1, W.eoff + N, sizeof(int), cudaMemcpyDeviceToDevice, stream));
         RC(cudaMemcpyAsync(d_stats + 4 * r + 2, foff_n + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        RC(cudaMemcpyAsync(d_stats + 4 * r + 3, W.ldc + 2, sizeof(int), cudaMemcpyDeviceToDevice, stream));
         Pc = Pn;
         Xc = Xn;
         Fc = Fn;
@@ -577,7 +629,7 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode};
+                              g_prof_mode, p.ld_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
     return k;
@@ -820,7 +872,8 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         res->facet_offsets[b] = (R == 0) ? p.foff[b] : h_fo[b];
     }
     for (int r = 0; r < R; r++) {
-        int64_t row[6] = {p.h_N[r], h_stats[4 * r], h_stats[4 * r + 1], p.h_N[r + 1], h_stats[4 * r + 2], 0};
+        int64_t row[6] = {p.h_N[r], h_stats[4 * r], h_stats[4 * r + 1], p.h_N[r + 1], h_stats[4 * r + 2],
+                          h_stats[4 * r + 3]};
         res->round_stats.insert(res->round_stats.end(), row, row + 6);
     }
     *out = res;

@@ -262,7 +262,88 @@ MF_DEV int grp_bitonic16(int x, unsigned mask) {
     return x;
 }
 
-__global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __restrict__ abort_flag, int N,
+// In-register bitonic network (fully unrolled: the array stays in registers).
+template <int L>
+MF_DEV void reg_sort(int (&a)[L]) {
+#pragma unroll
+    for (int k = 2; k <= L; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < L; i++) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    int x = a[i], y = a[ixj];
+                    bool up = ((i & k) == 0);
+                    int lo = min(x, y), hi = max(x, y);
+                    a[i] = up ? lo : hi;
+                    a[ixj] = up ? hi : lo;
+                }
+            }
+        }
+    }
+}
+
+// K3 thread tier (deg <= 8): one thread per vertex, incidences and the 16
+// neighbour candidates sorted by register networks, every plane / facet gather
+// issued before the ordered fold.  Degree 9..16 goes to the 16-lane group
+// kernel (list `mid`), larger to the block tier (list `heavy`).
+constexpr int kThreadDeg = 8;
+__global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_flag, int N,
+                                                  const int* __restrict__ inc_off, const int* __restrict__ inc,
+                                                  const int* __restrict__ F, const Plane* __restrict__ plane,
+                                                  int Mcap, double* __restrict__ vq, int* __restrict__ nbr,
+                                                  int* __restrict__ ucnt, int* __restrict__ upcnt,
+                                                  int* __restrict__ mid, int* __restrict__ mid_count,
+                                                  int* __restrict__ heavy, int* __restrict__ heavy_count) {
+    if (*abort_flag) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        const int s = inc_off[v], d = inc_off[v + 1] - s;
+        if (d > kThreadDeg) {
+            if (d <= kGrp) mid[append_slot(mid_count)] = v;
+            else heavy[append_slot(heavy_count)] = v;
+            continue;
+        }
+        int k[kThreadDeg];
+#pragma unroll
+        for (int i = 0; i < kThreadDeg; i++) k[i] = (i < d) ? inc[s + i] : 0x7fffffff;
+        reg_sort(k);
+        Q10 q;
+        q_zero(q);
+        int c[2 * kThreadDeg];
+#pragma unroll
+        for (int i = 0; i < kThreadDeg; i++) {
+            c[2 * i] = 0x7fffffff;
+            c[2 * i + 1] = 0x7fffffff;
+            if (i < d) {
+                int corner, f;
+                decode_inc(k[i], Mcap, corner, f);
+                Plane p = plane[f];
+                q_add_plane(q, p);
+                other_two(F, f, corner, c[2 * i], c[2 * i + 1]);
+            }
+        }
+        q_store(vq, v, q);
+        reg_sort(c);
+        int nu = 0, nup = 0;
+        int* out = nbr + 2 * (size_t)s;
+#pragma unroll
+        for (int i = 0; i < 2 * kThreadDeg; i++) {
+            const int x = c[i];
+            const bool keep = (x != 0x7fffffff) && (i == 0 || x != c[i > 0 ? i - 1 : 0]);
+            if (keep) {
+                out[nu++] = x;
+                nup += x > v;
+            }
+        }
+        ucnt[v] = nu;
+        upcnt[v] = nup;
+    }
+}
+
+__global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __restrict__ abort_flag,
+                                                                 const int* __restrict__ list,
+                                                                 const int* __restrict__ list_count,
                                                                  const int* __restrict__ inc_off,
                                                                  const int* __restrict__ inc,
                                                                  const int* __restrict__ F,
@@ -278,12 +359,10 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __re
     const int l = threadIdx.x & 15;
     const unsigned mask = grp_mask();
     const int groups = gridDim.x * (blockDim.x >> 4);
-    for (int v = blockIdx.x * (blockDim.x >> 4) + g; v < N; v += groups) {
+    const int N = *list_count;
+    for (int vi = blockIdx.x * (blockDim.x >> 4) + g; vi < N; vi += groups) {
+        const int v = list[vi];
         const int s = inc_off[v], d = inc_off[v + 1] - s;
-        if (d > kGrp) {
-            if (l == 0) heavy[atomicAdd(heavy_count, 1)] = v;
-            continue;
-        }
         int k = (l < d) ? inc[s + l] : 0x7fffffff;
         k = grp_bitonic16(k, mask);
         int a = 0x7fffffff, b = 0x7fffffff;
@@ -354,14 +433,15 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
                                                                 const double* __restrict__ P, int* __restrict__ e0,
                                                                 int* __restrict__ e1, double* __restrict__ cost,
                                                                 uint64_t* __restrict__ key_hi,
-                                                                int* __restrict__ adj_eid, int* __restrict__ mate,
+                                                                int* __restrict__ adj_eid,
+                                                                int* __restrict__ mate,
                                                                 int* __restrict__ minrep, int* __restrict__ absorbed,
                                                                 int order) {
     if (*abort_flag) return;
-    const int g = threadIdx.x >> 4;
-    const int l = threadIdx.x & 15;
-    const int groups = gridDim.x * (blockDim.x >> 4);
-    for (int v = blockIdx.x * (blockDim.x >> 4) + g; v < N; v += groups) {
+    const int g = threadIdx.x >> 3;  // 8 lanes per vertex (typical degree ~6)
+    const int l = threadIdx.x & 7;
+    const int groups = gridDim.x * (blockDim.x >> 3);
+    for (int v = blockIdx.x * (blockDim.x >> 3) + g; v < N; v += groups) {
         if (l == 0) {
             mate[v] = -1;
             minrep[v] = v;
@@ -375,7 +455,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
         Q10 qv;
         q_load(vq, v, qv);
         const double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
-        for (int j = l; j < nu; j += kGrp) {
+        for (int j = l; j < nu; j += 8) {
             int u = nbr[s2 + j];
             int eid;
             if (u > v) {
@@ -585,90 +665,260 @@ struct MatchArgs {
     const int* ucnt;
     const int* nbr;
     const int* adj_eid;
+    const unsigned* adj_k32;  // top 32 bits of each adjacency slot's rank key
     const int* e0;
     const int* e1;
     const uint64_t* key_hi;
     const uint64_t* key_lo;  // nullptr -> secondary key is the edge id
-    int* suitor;             // per vertex: edge of the best proposal received (-1 none)
+    unsigned long long* suitor;  // per vertex: (k32 << 32) | edge of the best proposal received, ~0 = none
     const int* abort_flag;
+    const int* mate;       // nullable: vertices matched by the LD rounds are not eligible
+    const int* front0;     // nullable: proposers = residual LD frontier, else all vertices
+    const int* front1;
+    const int* counters;
 };
 
 MF_DEV void edge_key(const MatchArgs& a, int e, uint64_t& h, uint64_t& l) {
     h = a.key_hi[e];
     l = a.key_lo ? a.key_lo[e] : (uint64_t)(unsigned)e;
 }
+// strict rank order of edge e (prefix ke) against edge f (prefix kf); the full
+// 128-bit keys are only gathered when the 32-bit prefixes tie
+MF_DEV bool edge_lt(const MatchArgs& a, unsigned ke, int e, unsigned kf, int f) {
+    if (ke != kf) return ke < kf;
+    uint64_t h1, l1, h2, l2;
+    edge_key(a, e, h1, l1);
+    edge_key(a, f, h2, l2);
+    return key_lt(h1, l1, h2, l2);
+}
 
 __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
     if (*a.abort_flag) return;
-    // 16 lanes per proposer: the adjacency of `cur` is scanned in parallel
+    // 8 lanes per proposer: the adjacency of `cur` is scanned in parallel
     // (one neighbour per lane), the best winnable edge is an argmin over the
-    // group, and lane 0 issues the CAS.  Control flow is uniform per group.
-    const int g = threadIdx.x >> 4;
-    const int l = threadIdx.x & 15;
-    const unsigned mask = 0xFFFFu << (threadIdx.x & 16);
-    const int groups = gridDim.x * (blockDim.x >> 4);
-    for (int u = blockIdx.x * (blockDim.x >> 4) + g; u < a.N; u += groups) {
-        int cur = u;
+    // group, and lane 0 issues a 64-bit CAS of (key prefix | edge id) on the
+    // neighbour's suitor word.  Control flow is uniform per group.
+    const int g = threadIdx.x >> 3;
+    const int l = threadIdx.x & 7;
+    const unsigned mask = 0xFFu << (threadIdx.x & 24);
+    const int groups = gridDim.x * (blockDim.x >> 3);
+    const int* list = nullptr;
+    int nprop = a.N;
+    if (a.front0) {
+        const int which = __ldcg(a.counters + 3);
+        list = which ? a.front1 : a.front0;
+        nprop = __ldcg(a.counters + which);
+    }
+    for (int ui = blockIdx.x * (blockDim.x >> 3) + g; ui < nprop; ui += groups) {
+        int cur = list ? __ldcg(list + ui) : ui;
+        if (a.mate && __ldcg(a.mate + cur) >= 0) continue;
         while (cur >= 0) {
             const size_t s = 2 * (size_t)a.inc_off[cur];
             const int nu = a.ucnt[cur];
             int be = -1, bv = -1;
-            uint64_t bh = ~0ull, bl = ~0ull;
-            for (int j = l; j < nu; j += 16) {
-                int e = a.adj_eid[s + j];
-                uint64_t kh, kl;
-                edge_key(a, e, kh, kl);
-                if (!key_lt(kh, kl, bh, bl)) continue;
-                int v = a.nbr[s + j];
-                int sv = ld_volatile(a.suitor + v);
-                if (sv >= 0) {
-                    uint64_t sh, sl;
-                    edge_key(a, sv, sh, sl);
-                    if (!key_lt(kh, kl, sh, sl)) continue;
-                }
-                bh = kh; bl = kl; be = e; bv = v;
+            unsigned bk = 0xffffffffu;
+            for (int j = l; j < nu; j += 8) {
+                const int e = a.adj_eid[s + j];
+                const unsigned ke = a.adj_k32[s + j];
+                if (be >= 0 && !edge_lt(a, ke, e, bk, be)) continue;
+                const int v = a.nbr[s + j];
+                if (a.mate && __ldcg(a.mate + v) >= 0) continue;
+                const unsigned long long sw = ld_volatile(a.suitor + v);
+                if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
+                bk = ke; be = e; bv = v;
             }
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                uint64_t oh = __shfl_xor_sync(mask, bh, o, 16), ol = __shfl_xor_sync(mask, bl, o, 16);
-                int oe = __shfl_xor_sync(mask, be, o, 16), ov = __shfl_xor_sync(mask, bv, o, 16);
-                if (key_lt(oh, ol, bh, bl)) { bh = oh; bl = ol; be = oe; bv = ov; }
+            for (int o = 4; o > 0; o >>= 1) {
+                unsigned ok = __shfl_xor_sync(mask, bk, o, 8);
+                int oe = __shfl_xor_sync(mask, be, o, 8), ov = __shfl_xor_sync(mask, bv, o, 8);
+                if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bv = ov; }
             }
             if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
             int next = -2;      // -2: lost a race, re-scan cur
             if (l == 0) {
-                int sv = ld_volatile(a.suitor + bv);
+                const unsigned long long mine = ((unsigned long long)bk << 32) | (unsigned)be;
+                unsigned long long sw = ld_volatile(a.suitor + bv);
                 while (true) {
-                    if (sv >= 0) {
-                        uint64_t sh, sl;
-                        edge_key(a, sv, sh, sl);
-                        if (!key_lt(bh, bl, sh, sl)) break;
-                    }
-                    int old = atomicCAS(a.suitor + bv, sv, be);
-                    if (old == sv) {
-                        next = (sv < 0) ? -1 : (a.e0[sv] == bv ? a.e1[sv] : a.e0[sv]);
+                    if (sw != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw >> 32), (int)(unsigned)sw)) break;
+                    unsigned long long old = atomicCAS(a.suitor + bv, sw, mine);
+                    if (old == sw) {
+                        if (sw == ~0ull) next = -1;
+                        else {
+                            int se = (int)(unsigned)sw;
+                            next = (a.e0[se] == bv) ? a.e1[se] : a.e0[se];
+                        }
                         break;
                     }
-                    sv = old;
+                    sw = old;
                 }
             }
-            next = __shfl_sync(mask, next, 0, 16);
+            next = __shfl_sync(mask, next, 0, 8);
             if (next != -2) cur = next;
         }
     }
 }
 
+// Locally-dominant rounds (persistent, cooperative launch, grid barrier).
+// Each round every frontier vertex (8 lanes) picks its best live incident
+// edge (lowest rank among edges to unmatched neighbours); an edge that is the
+// pick of both endpoints is matched -- it is then the first of its
+// neighbourhood in rank order, so the sequential greedy scan accepts it too.
+// Matched / exhausted vertices leave the frontier.  After `max_rounds` the
+// remaining frontier is finished by k_suitor on the residual graph.
+constexpr int kLDRounds = 12;  // fixed in the graph; rounds after convergence exit at once
+constexpr int kLDMinVertices = 1 << 19;
+struct LDArgs {
+    int N;
+    const int* inc_off;
+    const int* ucnt;
+    const int* nbr;
+    const int* adj_eid;
+    const unsigned* adj_k32;
+    const uint64_t* key_hi;
+    const uint64_t* key_lo;
+    int* mate;     // -1 unmatched
+    int* best;     // per vertex: picked edge
+    int* bestu;    // per vertex: the other endpoint of the pick
+    int* front0;
+    int* front1;
+    int* counters;  // [0],[1] frontier sizes, [2] rounds run, [3] which frontier holds the residual
+    unsigned* bar;
+    int max_rounds;
+    const int* abort_flag;
+};
+
+MF_DEV bool ld_lt(const LDArgs& a, unsigned ke, int e, unsigned kf, int f) {
+    if (ke != kf) return ke < kf;
+    uint64_t h1 = a.key_hi[e], h2 = a.key_hi[f];
+    uint64_t l1 = a.key_lo ? a.key_lo[e] : (uint64_t)(unsigned)e, l2 = a.key_lo ? a.key_lo[f] : (uint64_t)(unsigned)f;
+    return key_lt(h1, l1, h2, l2);
+}
+
+// Block-ordered append: survivors of one block keep their relative order and
+// land in one contiguous chunk (one atomic per block), so the frontier stays
+// roughly sorted by vertex id and the next round streams the adjacency.
+MF_DEV void block_append(bool keep, int v, int* __restrict__ out, int* __restrict__ counter) {
+    __shared__ int s_scan[33];
+    __shared__ int s_base;
+    int tot;
+    int pos = block_excl_scan(keep ? 1 : 0, s_scan, &tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(counter, tot) : 0;
+    __syncthreads();
+    if (keep) out[s_base + pos] = v;
+    __syncthreads();
+}
+
+// initial frontier: every vertex with an edge (mate reset)
+__global__ void __launch_bounds__(256) k_ld_init(LDArgs a) {
+    if (*a.abort_flag) return;
+    const int nb = (a.N + blockDim.x - 1) / blockDim.x;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int v = b * blockDim.x + threadIdx.x;
+        bool keep = false;
+        if (v < a.N) {
+            a.mate[v] = -1;
+            keep = a.ucnt[v] > 0;
+        }
+        block_append(keep, v, a.front0, a.counters);
+    }
+}
+
+// phase A of round `round`: each frontier vertex picks its best live edge
+__global__ void __launch_bounds__(256) k_ld_pick(LDArgs a, int round) {
+    if (*a.abort_flag) return;
+    const int cur = round & 1;
+    const int n = a.counters[cur];
+    if (n == 0) return;
+    const int* Fc = cur ? a.front1 : a.front0;
+    const int l = threadIdx.x & 7;
+    const unsigned mask = 0xFFu << (threadIdx.x & 24);
+    const int ngroups = (gridDim.x * blockDim.x) >> 3;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 3; i < n; i += ngroups) {
+        const int v = Fc[i];
+        const size_t s = 2 * (size_t)a.inc_off[v];
+        const int nu = a.ucnt[v];
+        int be = -1, bu = -1;
+        unsigned bk = 0xffffffffu;
+        for (int j = l; j < nu; j += 8) {
+            const int u = a.nbr[s + j];
+            if (a.mate[u] >= 0) continue;
+            const int e = a.adj_eid[s + j];
+            const unsigned ke = a.adj_k32[s + j];
+            if (be < 0 || ld_lt(a, ke, e, bk, be)) { bk = ke; be = e; bu = u; }
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            unsigned ok = __shfl_xor_sync(mask, bk, o, 8);
+            int oe = __shfl_xor_sync(mask, be, o, 8), ou = __shfl_xor_sync(mask, bu, o, 8);
+            if (oe >= 0 && (be < 0 || ld_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bu = ou; }
+        }
+        if (l == 0) {
+            a.best[v] = be;
+            a.bestu[v] = bu;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[cur ^ 1] = 0;
+}
+
+// phase B: mutual picks are matched; the rest (with a live edge) survive
+__global__ void __launch_bounds__(256) k_ld_match(LDArgs a, int round) {
+    if (*a.abort_flag) return;
+    const int cur = round & 1;
+    const int n = a.counters[cur];
+    if (n && blockIdx.x == 0 && threadIdx.x == 0) {
+        a.counters[3] = cur ^ 1;  // the residual frontier lives here after this round
+        a.counters[2] = round + 1;
+    }
+    if (n == 0) return;
+    const int* Fc = cur ? a.front1 : a.front0;
+    int* Fn = cur ? a.front0 : a.front1;
+    const int nb = (n + blockDim.x - 1) / blockDim.x;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int i = b * blockDim.x + threadIdx.x;
+        bool keep = false;
+        int v = 0;
+        if (i < n) {
+            v = Fc[i];
+            const int e = a.best[v];
+            if (e >= 0) {
+                if (a.best[a.bestu[v]] == e) a.mate[v] = e;
+                else keep = true;
+            }
+        }
+        block_append(keep, v, Fn, a.counters + (cur ^ 1));
+    }
+}
+
+// 32-bit rank-key prefix per adjacency slot (after the keys are final), so the
+// matching scans contiguous prefixes instead of gathering 8-byte keys.
+__global__ void __launch_bounds__(256) k_adj_keys(const int* __restrict__ abort_flag, int N,
+                                                  const int* __restrict__ inc_off, const int* __restrict__ ucnt,
+                                                  const int* __restrict__ adj_eid, const uint64_t* __restrict__ key_hi,
+                                                  unsigned* __restrict__ adj_k32) {
+    if (*abort_flag) return;
+    const int l = threadIdx.x & 7;
+    const int groups = gridDim.x * (blockDim.x >> 3);
+    for (int v = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); v < N; v += groups) {
+        const size_t s = 2 * (size_t)inc_off[v];
+        const int nu = ucnt[v];
+        for (int j = l; j < nu; j += 8) adj_k32[s + j] = (unsigned)(key_hi[adj_eid[s + j]] >> 32);
+    }
+}
+
 // mate = the suitor edge when the proposal is mutual.
-__global__ void k_mates(const int* __restrict__ abort_flag, int N, const int* __restrict__ suitor, const int* __restrict__ e0,
+__global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigned long long* __restrict__ suitor,
+                        const int* __restrict__ e0,
                         const int* __restrict__ e1, int* __restrict__ mate, int B, int* __restrict__ seg_cnt) {
     if (*abort_flag) return;
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) seg_cnt[b] = 0;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int e = suitor[v];
-        int m = -1;
-        if (e >= 0) {
+        int m = mate[v];
+        if (m >= 0) continue;  // matched by the LD rounds
+        unsigned long long w = suitor[v];
+        if (w != ~0ull) {
+            int e = (int)(unsigned)w;
             int u = e0[e] == v ? e1[e] : e0[e];
-            if (suitor[u] == e) m = e;
+            if ((int)(unsigned)suitor[u] == e && suitor[u] != ~0ull) m = e;
         }
         mate[v] = m;
     }
@@ -711,9 +961,12 @@ struct SelectArgs {
     const int* removed;  // nullable
     int* ksel;
     int* mode;
-    uint64_t* thr_hi;
+    uint64_t* thr_hi;   // prefix while selecting, threshold once decided
     uint64_t* thr_lo;
     const int* abort_flag;
+    int* krem;          // resumable state (after the multi-block passes)
+    int* top;
+    int resume;
 };
 
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
@@ -728,21 +981,30 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         const int c0 = a.voff[b], c1 = c0 + a.seg_cnt[b];
         const int cnt = c1 - c0;
-        int want = a.act[b] ? a.budget[b] - (a.removed ? a.removed[b] : 0) : 0;
-        int k = want < cnt ? want : cnt;
-        if (k < 0) k = 0;
-        if (k == 0 || k >= cnt) {
-            if (threadIdx.x == 0) {
-                a.ksel[b] = k;
-                a.mode[b] = (k == 0) ? 2 : 1;
-            }
-            continue;
-        }
         uint64_t phi = 0, plo = 0;
-        int kr = k;
+        int kr, top = 128, k;
+        if (a.resume) {
+            if (a.mode[b] != 0) continue;  // decided by the multi-block passes
+            phi = a.thr_hi[b];
+            plo = a.thr_lo[b];
+            kr = a.krem[b];
+            top = a.top[b];
+            k = a.ksel[b];
+        } else {
+            int want = a.act[b] ? a.budget[b] - (a.removed ? a.removed[b] : 0) : 0;
+            k = want < cnt ? want : cnt;
+            if (k < 0) k = 0;
+            if (k == 0 || k >= cnt) {
+                if (threadIdx.x == 0) {
+                    a.ksel[b] = k;
+                    a.mode[b] = (k == 0) ? 2 : 1;
+                }
+                continue;
+            }
+            kr = k;
+        }
         bool in_smem = false;
         int n_s = 0;
-        int top = 128;
         bool done = false;
         while (!done) {
             int width = top >= kSelBits ? kSelBits : top;
@@ -817,6 +1079,95 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
             __syncthreads();
         }
     }
+}
+
+// Multi-block MSD passes for one large segment (a single big mesh): every
+// block histograms its slice of the candidates under the current prefix in
+// shared memory and flushes non-zero bins; one block then picks the digit.
+// The single-CTA k_select resumes from the resulting state.
+__global__ void __launch_bounds__(512) k_sel_hist(SelectArgs a, int* __restrict__ ghist, int pass) {
+    if (*a.abort_flag) return;
+    __shared__ int h[kSelBins];
+    if (pass > 0 && a.mode[0] != 0) return;
+    const int top = 128 - kSelBits * pass;
+    const int width = top >= kSelBits ? kSelBits : top;
+    const int shift = top - width;
+    const uint64_t phi = pass ? a.thr_hi[0] : 0, plo = pass ? a.thr_lo[0] : 0;
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int c0 = a.voff[0], c1 = c0 + a.seg_cnt[0];
+    for (int i = c0 + blockIdx.x * blockDim.x + threadIdx.x; i < c1; i += gridDim.x * blockDim.x) {
+        uint64_t hh = a.chi[i], ll = a.clo[i];
+        if (sel_prefix(hh, ll, phi, plo, top)) atomicAdd(h + sel_digit(hh, ll, shift, width), 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+        if (h[i]) atomicAdd(ghist + i, h[i]);
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* __restrict__ ghist, int pass) {
+    __shared__ int s_scan[33];
+    __shared__ int s_sel[3];
+    if (*a.abort_flag) return;
+    const int cnt = a.seg_cnt[0];
+    int kr;
+    uint64_t phi = 0, plo = 0;
+    if (pass == 0) {
+        int want = a.act[0] ? a.budget[0] - (a.removed ? a.removed[0] : 0) : 0;
+        int k = want < cnt ? want : cnt;
+        if (k < 0) k = 0;
+        if (threadIdx.x == 0) a.ksel[0] = k;
+        if (k == 0 || k >= cnt) {
+            if (threadIdx.x == 0) a.mode[0] = (k == 0) ? 2 : 1;
+            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) ghist[i] = 0;
+            return;
+        }
+        kr = k;
+    } else {
+        if (a.mode[0] != 0) return;
+        kr = a.krem[0];
+        phi = a.thr_hi[0];
+        plo = a.thr_lo[0];
+    }
+    const int top = 128 - kSelBits * pass;
+    const int width = top >= kSelBits ? kSelBits : top;
+    const int shift = top - width;
+    const int per = kSelBins / kSelThreads;
+    int loc = 0;
+    for (int j = 0; j < per; j++) loc += ghist[threadIdx.x * per + j];
+    int tot;
+    int ex = block_excl_scan(loc, s_scan, &tot);
+    if (ex < kr && kr <= ex + loc) {
+        int cum = ex;
+        for (int j = 0; j < per; j++) {
+            int hv = ghist[threadIdx.x * per + j];
+            if (cum + hv >= kr) {
+                s_sel[0] = threadIdx.x * per + j;
+                s_sel[1] = cum;
+                s_sel[2] = hv;
+                break;
+            }
+            cum += hv;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) ghist[i] = 0;
+    if (threadIdx.x != 0) return;
+    const int d = s_sel[0];
+    kr -= s_sel[1];
+    unsigned __int128 p = ((unsigned __int128)phi << 64) | plo;
+    p |= ((unsigned __int128)d) << shift;
+    if (s_sel[2] == kr) {
+        unsigned __int128 ones = (shift == 0) ? 0 : ((((unsigned __int128)1) << shift) - 1);
+        p |= ones;
+        a.mode[0] = 3;
+    } else {
+        a.mode[0] = 0;
+    }
+    a.thr_hi[0] = (uint64_t)(p >> 64);
+    a.thr_lo[0] = (uint64_t)p;
+    a.krem[0] = kr;
+    a.top[0] = shift;
 }
 
 // ---- flag producers fused into the decoupled look-back scan (LoadOp functors)
@@ -1101,11 +1452,14 @@ MF_DEV uint32_t tri_hash(int a, int b, int c) {
     return h;
 }
 
+// Base slot = min vertex * (slots per output vertex) + a small hash of the
+// other two: facets sharing their lowest vertex land in one short run of the
+// table, and consecutive facets (spatially coherent) probe neighbouring lines.
 __global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict__ abort_flag,
                               const int* __restrict__ F, const int* __restrict__ rstep, const int* __restrict__ vmesh,
                               const int* __restrict__ act, int* __restrict__ mapped, int4* __restrict__ canon,
                               int* __restrict__ slot, unsigned char* __restrict__ has_live, int* __restrict__ table,
-                              unsigned tmask) {
+                              unsigned tmask, unsigned per_vertex) {
     if (*abort_flag) return;
     const int M = *dM;
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
@@ -1128,7 +1482,7 @@ __global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict_
         int lo = min(a, min(b, c)), hi = max(a, max(b, c)), mid = a + b + c - lo - hi;
         canon[f] = make_int4(lo, mid, hi, 0);
         __threadfence();
-        unsigned h = tri_hash(lo, mid, hi) & tmask;
+        unsigned h = ((unsigned)lo * per_vertex + (tri_hash(lo, mid, hi) & 7u)) & tmask;
         while (true) {
             int cur = __ldcg(table + h);
             if (cur < 0) {

@@ -1,4 +1,4 @@
-"""Run W warm-up decimation steps then exactly one more (for ncu -s/-c windows).
+"""Run W warm-up decimation calls (first level of the config) then exactly one more (ncu windows).
 
     python scripts/one_step.py [--config cfg2] [--warmup 3]
 
@@ -33,7 +33,7 @@ F = torch.from_numpy(base.facets).cuda()
 torch.cuda.synchronize()
 for _ in range(args.warmup):
     _native.launch_count(reset=True)
-    T.decimate(V, F, nv, nf, target=wl["target"])
+    T.decimate(V, F, nv, nf, target=wl["levels"][0])
 print(f"launches_per_step {_native.launch_count()}", file=sys.stderr)
-T.decimate(V, F, nv, nf, target=wl["target"])
+T.decimate(V, F, nv, nf, target=wl["levels"][0])
 torch.cuda.synchronize()

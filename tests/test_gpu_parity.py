@@ -169,3 +169,25 @@ def test_big_batch_random(oracle):
     meshes = [S.delaunay_terrain(int(rng.integers(40, 900)), seed=int(s)) for s in rng.integers(0, 10**6, 40)]
     run_both(oracle, mfg.concat_batch(meshes), 40, seed=13)
     run_both(oracle, mfg.concat_batch(meshes), 40)
+
+
+@pytest.mark.parametrize("seed", [None, 5])
+def test_large_grid_ld_path(oracle, seed):
+    # >= 512k vertices: locally-dominant rounds + Suitor residual
+    mesh = S.perturbed_grid(760, noise=0.02, seed=1)
+    run_both(oracle, mesh, -(-mesh.n_vertices // 2), seed=seed)
+
+
+def test_large_flat_grid_ld_then_suitor(oracle):
+    # all costs tie: LD rounds sweep slowly, the residual frontier goes to Suitor
+    mesh = S.flat_grid(730)
+    run_both(oracle, mesh, -(-mesh.n_vertices // 2))
+
+
+@pytest.mark.parametrize("seed", [None, 7])
+def test_forced_ld_small(oracle, seed, monkeypatch):
+    monkeypatch.setenv("MF_LD_MIN", "0")
+    run_both(oracle, S.delaunay_terrain(20_000, noise=0.02, seed=4), 6_000, seed=seed)
+    run_both(oracle, S.flat_grid(60), 1_800, seed=seed)
+    meshes = [S.delaunay_terrain(300 + 40 * b, seed=b) for b in range(6)]
+    run_both(oracle, mfg.concat_batch(meshes), 150, seed=seed)
