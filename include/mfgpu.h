@@ -11,6 +11,7 @@
  *   mf_decimation_*    <- DecimationResult fields mesh / replace / mapping   decimate.py:74-92
  *   mf_pool            <- pooling.pool(features, result, mode, weights)      pooling.py:49-71
  *   mf_unpool          <- pooling.unpool(coarse, result)                     pooling.py:74-77
+ *   mf_pool_backward   <- pooling.pool_backward / unpool_backward            pooling.py:80-102
  *   mf_round_targets   <- decimate._round_targets                            decimate.py:294-316
  *
  * Plain pointers and sizes only.  Array pointers may be host or device memory
@@ -112,6 +113,13 @@ int32_t mf_decimation_round_stats(const mf_decimation *res, int64_t *out, int32_
 int mf_pool(mf_context *ctx, const mf_decimation *res, const int64_t *replace, int64_t n, int64_t n_out,
             const void *features, int32_t dtype, int64_t c, int32_t mode, const void *weights, void *out,
             void *stream, mf_status *status);
+/* pooling.pool_backward (pooling.py:80-97).  out dtype follows numpy: average -> float64,
+ * sum -> grad dtype, weighted -> promote(grad, features), max -> features dtype.
+ * unpool_backward (pooling.py:100-102) = mf_pool(mode = MF_POOL_SUM). */
+int mf_pool_backward(mf_context *ctx, const mf_decimation *res, const int64_t *replace, int64_t n, int64_t n_out,
+                     const void *grad_output, int32_t grad_dtype, const void *features, int32_t features_dtype,
+                     int64_t c, int32_t mode, const void *weights, void *out, int32_t out_dtype, void *stream,
+                     mf_status *status);
 int mf_unpool(mf_context *ctx, const mf_decimation *res, const int64_t *replace, int64_t n, int64_t n_out,
               const void *coarse, int32_t dtype, int64_t c, void *out, void *stream, mf_status *status);
 

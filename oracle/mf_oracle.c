@@ -19,6 +19,8 @@
  *   contraction + output      decimate.py:140-169, 275-291
  *   round chain               decimate.py:294-316
  *   pool / unpool             pooling.py:36-77
+ *   'inverse' placement       quadrics.py:89-114, decimate.py:284-286 (mf_inverse.h;
+ *                             tolerance-only vs LAPACK, see that header)
  *
  * Floating-point order follows the numpy calls bit for bit:
  * products and sums are separately rounded (compile with -ffp-contract=off),
@@ -40,6 +42,7 @@
 #include <string.h>
 
 #include "mf_oracle.h"
+#include "mf_inverse.h"
 
 /* ------------------------------------------------------------------ */
 /* small helpers                                                        */
@@ -222,6 +225,10 @@ static void vertex_quadrics(const omesh *g, int order, double *Q /* n*QW */) {
         }
     }
     free(plane); free(degen);
+}
+
+static void q13_a6(const double *q, double a6[6]) {
+    a6[0] = q[0]; a6[1] = q[1]; a6[2] = q[2]; a6[3] = q[4]; a6[4] = q[5]; a6[5] = q[8];
 }
 
 /* Quadric.evaluate (quadrics.py:53-58) of Q at x */
@@ -435,7 +442,7 @@ static void build_output(const omesh *g, const int64_t *replace, int64_t n_out, 
 
 /* ---- _decimate_round: decimate.py:229-291 ('average' placement) ---- */
 static int decimate_round(const omesh *g, int64_t target, int seeded, const uint64_t pcg[4], int order,
-                          omesh *out, int64_t *replace, int64_t *mapping, int64_t *achievable) {
+                          int placement, omesh *out, int64_t *replace, int64_t *mapping, int64_t *achievable) {
     int64_t n = g->n;
     if (target == n) { /* _identity_result */
         out->n = n; out->m = g->m; out->c = g->c;
@@ -465,6 +472,12 @@ static int decimate_round(const omesh *g, int64_t target, int seeded, const uint
         for (int k = 0; k < QW; k++) q[k] = qi[k] + qj[k];
         const double *pi = g->P + 3 * E[2 * e], *pj = g->P + 3 * E[2 * e + 1];
         double x[3] = {0.5 * (pi[0] + pj[0]), 0.5 * (pi[1] + pj[1]), 0.5 * (pi[2] + pj[2])};
+        if (placement) { /* optimal_positions(q, midpoints, 'inverse'), quadrics.py:131 */
+            double a6[6], t[3];
+            q13_a6(q, a6);
+            mf_optimal_position(a6, q + 9, x, t);
+            x[0] = t[0]; x[1] = t[1]; x[2] = t[2];
+        }
         cost[e] = q_evaluate(q, q + 9, q[12], x, order);
     }
     int64_t *ord = (int64_t *)xmalloc((size_t)ne * sizeof(int64_t));
@@ -521,6 +534,18 @@ static int decimate_round(const omesh *g, int64_t target, int seeded, const uint
     }
     for (int64_t r = 0; r < nc; r++)
         for (int k = 0; k < 3; k++) Pout[3 * r + k] = Pout[3 * r + k] / (double)counts[r];
+    if (placement) { /* accumulate_quadrics + optimal_positions(..., 'inverse'), decimate.py:284-286 */
+        double *Qc = (double *)xcalloc((size_t)nc * QW, sizeof(double));
+        for (int64_t v = 0; v < n; v++)
+            for (int k = 0; k < QW; k++) Qc[QW * replace[v] + k] += Q[QW * v + k];
+        for (int64_t r = 0; r < nc; r++) {
+            double a6[6], t[3];
+            q13_a6(Qc + QW * r, a6);
+            mf_optimal_position(a6, Qc + QW * r + 9, Pout + 3 * r, t);
+            Pout[3 * r] = t[0]; Pout[3 * r + 1] = t[1]; Pout[3 * r + 2] = t[2];
+        }
+        free(Qc);
+    }
     build_output(g, replace, nc, Pout, out, mapping);
     free(counts); free(Q); free(E); free(cost); free(cluster);
     return 0;
@@ -529,7 +554,7 @@ static int decimate_round(const omesh *g, int64_t target, int seeded, const uint
 /* ---- decimate_parallel for one mesh: decimate.py:363-382 ---- */
 int mfo_decimate_mesh(const double *P, int64_t n, const int64_t *F, int64_t m, const double *X, int64_t c,
                       const int64_t *chain, int64_t nchain, int seeded, const uint64_t pcg[4], int order,
-                      mfo_result **res_out, int64_t *achievable) {
+                      int placement, mfo_result **res_out, int64_t *achievable) {
     omesh cur;
     cur.n = n; cur.m = m; cur.c = c;
     cur.P = (double *)xmalloc((size_t)n * 3 * sizeof(double));
@@ -545,7 +570,7 @@ int mfo_decimate_mesh(const double *P, int64_t n, const int64_t *F, int64_t m, c
     int64_t *sm = (int64_t *)xmalloc((size_t)n * sizeof(int64_t));
     for (int64_t r = 0; r < nchain; r++) {
         omesh nxt;
-        int st = decimate_round(&cur, chain[r], seeded, pcg, order, &nxt, sr, sm, achievable);
+        int st = decimate_round(&cur, chain[r], seeded, pcg, order, placement, &nxt, sr, sm, achievable);
         if (st) {
             omesh_free(&cur); free(replace); free(mapping); free(sr); free(sm);
             return st;

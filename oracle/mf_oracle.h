@@ -18,7 +18,7 @@ typedef struct mfo_result {
 int64_t mfo_round_targets(int64_t n_in, int64_t target, int64_t rounds, int64_t *chain, int64_t cap);
 int mfo_decimate_mesh(const double *P, int64_t n, const int64_t *F, int64_t m, const double *X, int64_t c,
                       const int64_t *chain, int64_t nchain, int seeded, const uint64_t pcg[4], int order,
-                      mfo_result **res_out, int64_t *achievable);
+                      int placement, mfo_result **res_out, int64_t *achievable);
 void mfo_result_sizes(const mfo_result *r, int64_t *n_in, int64_t *n_out, int64_t *m_out, int64_t *c);
 void mfo_result_copy(const mfo_result *r, double *positions, int64_t *facets, double *features, int64_t *replace,
                      int64_t *mapping);

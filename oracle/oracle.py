@@ -61,7 +61,7 @@ def lib():
         L.mfo_decimate_mesh.restype = ctypes.c_int
         L.mfo_decimate_mesh.argtypes = [
             _f64p, ctypes.c_int64, _i64p, ctypes.c_int64, _f64p, ctypes.c_int64,
-            _i64p, ctypes.c_int64, ctypes.c_int, _u64p, ctypes.c_int,
+            _i64p, ctypes.c_int64, ctypes.c_int, _u64p, ctypes.c_int, ctypes.c_int,
             ctypes.POINTER(ctypes.c_void_p), _i64p,
         ]
         L.mfo_result_sizes.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _i64p]
@@ -125,7 +125,7 @@ def pcg64_random(seed, n) -> np.ndarray:
     return out
 
 
-def _decimate_one(P, F, X, target, rounds, seed, order):
+def _decimate_one(P, F, X, target, rounds, seed, order, placement="average"):
     """decimate_parallel on one TriMesh (decimate.py:363-382)."""
     n = len(P)
     if target > n:
@@ -146,7 +146,7 @@ def _decimate_one(P, F, X, target, rounds, seed, order):
     st = lib().mfo_decimate_mesh(
         _p(P, _f64p), n, _p(F, _i64p), len(F), _p(Xd, _f64p), c,
         _p(chain, _i64p), len(chain), int(seed is not None), _p(words, _u64p), order,
-        ctypes.byref(res), ctypes.byref(ach),
+        int(placement == "inverse"), ctypes.byref(res), ctypes.byref(ach),
     )
     if st == 4:
         raise OracleInfeasible(f"achievable minimum is {ach.value}", ach.value)
@@ -170,7 +170,7 @@ def _decimate_one(P, F, X, target, rounds, seed, order):
 
 
 def decimate(positions, facets, features=None, target=None, rounds="auto", seed=None, order=0,
-             vertex_offsets=None, facet_offsets=None, threads=1):
+             vertex_offsets=None, facet_offsets=None, threads=1, placement="average"):
     """Oracle decimate_parallel; batch when offsets are given.
 
     Returns a dict with positions, facets, features, replace, mapping and,
@@ -182,11 +182,11 @@ def decimate(positions, facets, features=None, target=None, rounds="auto", seed=
     if X.ndim == 1:
         X = X[:, None]
     if vertex_offsets is None:
-        return _decimate_one(P, F, X, target, rounds, seed, order)
+        return _decimate_one(P, F, X, target, rounds, seed, order, placement)
     vo = np.asarray(vertex_offsets, dtype=np.int64)
     fo = np.asarray(facet_offsets, dtype=np.int64)
     parts = [(P[vo[b]:vo[b + 1]], F[fo[b]:fo[b + 1]] - vo[b], X[vo[b]:vo[b + 1]]) for b in range(len(vo) - 1)]
-    run = lambda p: _decimate_one(p[0], p[1], p[2], target, rounds, seed, order)  # noqa: E731
+    run = lambda p: _decimate_one(p[0], p[1], p[2], target, rounds, seed, order, placement)  # noqa: E731
     if threads > 1 and len(parts) > 1:
         with ThreadPoolExecutor(max_workers=min(threads, len(parts))) as ex:
             results = list(ex.map(run, parts))
@@ -243,3 +243,48 @@ def unpool(coarse, replace):
     if c.ndim == 1:
         c = c[:, None]
     return c[np.asarray(replace, dtype=np.int64)]
+
+
+def pool_backward(grad_output, features, replace, n_out, mode="average", weights=None):
+    """pooling.pool_backward (pooling.py:80-97) restated with explicit loops (small inputs only)."""
+    X = np.asarray(features)
+    if X.dtype not in (np.float32, np.float64):
+        X = X.astype(np.float64)
+    X = X.reshape(len(X), -1)
+    G = np.asarray(grad_output)
+    if G.dtype not in (np.float32, np.float64):
+        G = G.astype(np.float64)
+    G = G.reshape(n_out, -1)
+    r = np.asarray(replace, dtype=np.int64)
+    n, c = X.shape
+    members = [[] for _ in range(n_out)]
+    for v in range(n):
+        members[r[v]].append(v)
+    if mode == "sum":
+        return np.array([G[r[v]] for v in range(n)], dtype=G.dtype).reshape(n, c)
+    if mode == "average":
+        return np.array([[np.float64(G[r[v], k]) / np.float64(len(members[r[v]])) for k in range(c)]
+                         for v in range(n)], dtype=np.float64).reshape(n, c)
+    if mode == "weighted":
+        w = np.asarray(weights, dtype=X.dtype)
+        den = np.zeros(n_out, dtype=X.dtype)
+        for v in range(n):
+            den[r[v]] = den[r[v]] + w[v]
+        odt = np.result_type(G.dtype, X.dtype)
+        out = np.zeros((n, c), dtype=odt)
+        for v in range(n):
+            q = w[v] / den[r[v]]
+            for k in range(c):
+                out[v, k] = odt.type(G[r[v], k]) * odt.type(q)
+        return out
+    out = np.zeros((n, c), dtype=X.dtype)
+    for cl in range(n_out):
+        for k in range(c):
+            acc = X.dtype.type(-np.inf)
+            for v in members[cl]:
+                acc = acc if (np.isnan(acc) or acc > X[v, k]) else X[v, k]
+            for v in members[cl]:
+                if X[v, k] == acc:
+                    out[v, k] = X.dtype.type(0) + X.dtype.type(G[cl, k])
+                    break
+    return out

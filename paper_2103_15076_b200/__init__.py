@@ -16,7 +16,7 @@ from .decimate import (
 )
 from .errors import InfeasibleTargetError, MeshError, NativeError, StructuralError
 from .mesh import BatchedMesh, TriMesh, concat_batch
-from .pooling import POOL_MODES, pool, unpool
+from .pooling import POOL_MODES, pool, pool_backward, unpool, unpool_backward
 
 __version__ = "0.1.0"
 
@@ -35,7 +35,9 @@ __all__ = [
     "concat_batch",
     "decimate_parallel",
     "pool",
+    "pool_backward",
     "representative_vertices",
     "round_targets",
     "unpool",
+    "unpool_backward",
 ]

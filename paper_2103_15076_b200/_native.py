@@ -93,6 +93,9 @@ def lib():
         L.mf_decimation_free.argtypes = [_vp]
         L.mf_pool.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp, _vp, _vp, ctypes.POINTER(Status)]
         L.mf_pool.restype = ctypes.c_int
+        L.mf_pool_backward.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _vp, _i32,
+                                       _vp, ctypes.POINTER(Status)]
+        L.mf_pool_backward.restype = ctypes.c_int
         L.mf_unpool.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _i32, _i64, _vp, _vp, ctypes.POINTER(Status)]
         L.mf_unpool.restype = ctypes.c_int
         L.mf_round_targets.argtypes = [_i64, _i64, _i32, ctypes.POINTER(_i64), _i64]

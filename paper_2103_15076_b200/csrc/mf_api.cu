@@ -234,6 +234,60 @@ done:
     return rc;
 }
 
+/* pooling.pool_backward (pooling.py:80-97); unpool_backward = mf_pool(..., MF_POOL_SUM) (pooling.py:100-102). */
+int mf_pool_backward(mf_context* ctx, const mf_decimation* res, const int64_t* replace, int64_t n, int64_t n_out,
+                     const void* grad_output, int32_t grad_dtype, const void* features, int32_t features_dtype,
+                     int64_t c, int32_t mode, const void* weights, void* out, int32_t out_dtype, void* stream,
+                     mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || mode < 0 || mode > 3) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "mode must be one of ('average', 'max', 'weighted', 'sum')");
+        return st->code;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    const int *d_off = nullptr, *d_mem = nullptr, *d_rep = nullptr;
+    void *blk_r = nullptr, *blk_csr = nullptr;
+    int rc = MF_OK;
+    if (res) {
+        Result& r = const_cast<mf_decimation*>(res)->r;
+        n = r.n_in;
+        n_out = r.n_out;
+        if (!r.csr_block) {
+            int *o, *mm;
+            if ((rc = build_cluster_csr(&ctx->c, r.replace, r.n_in, r.n_out, &o, &mm, &r.csr_block, s, st)))
+                return rc;
+            r.csr_off = o;
+            r.csr_members = mm;
+        }
+        d_off = r.csr_off;
+        d_mem = r.csr_members;
+        d_rep = r.replace;
+    } else {
+        int *r32, *cnt;
+        if ((rc = upload_replace(&ctx->c, replace, n, n_out, 1, &r32, &cnt, &blk_r, s, st))) goto done;
+        int *o, *mm;
+        if ((rc = build_cluster_csr(&ctx->c, r32, n, n_out, &o, &mm, &blk_csr, s, st))) goto done;
+        d_off = o;
+        d_mem = mm;
+        d_rep = r32;
+    }
+    if (mode == MF_POOL_WEIGHTED && !weights) {
+        st->code = rc = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "weighted pooling requires per-input-vertex weights");
+        goto done;
+    }
+    rc = pool_backward_run(&ctx->c, grad_output, grad_dtype, features, features_dtype, n, c, d_rep, d_off, d_mem,
+                           n_out, mode, weights, out, out_dtype, s, st);
+done:
+    if (blk_r) cudaFreeAsync(blk_r, s);
+    if (blk_csr) cudaFreeAsync(blk_csr, s);
+    return rc;
+}
+
 int mf_unpool(mf_context* ctx, const mf_decimation* res, const int64_t* replace, int64_t n, int64_t n_out,
               const void* coarse, int32_t dtype, int64_t c, void* out, void* stream, mf_status* status) {
     mf_status local;

@@ -179,25 +179,29 @@ struct Plan {
     uint64_t pcg[4] = {0, 0, 0, 0};
     size_t params_words = 0;
     int ld_min = kLDMinVertices;  // rounds with at least this many vertices start with LD rounds
+    int placement = 0;            // 0 = average, 1 = inverse (quadrics.py:89-114)
 };
 
 static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan& p, mf_status* st) {
     p.n = mv->n;
     p.m = mv->m;
-    if (cfg->placement != 0) {
+    if (cfg->placement != 0 && cfg->placement != 1) {
         st->code = MF_ERR_VALUE;
-        snprintf(st->message, sizeof(st->message), "placement 'inverse' is not supported by the CUDA path yet");
+        snprintf(st->message, sizeof(st->message), "unknown placement %d", cfg->placement);
         return st->code;
     }
+    p.placement = cfg->placement;
     if (p.n < 0 || p.m < 0 || p.n >= (int64_t)INT32_MAX - 1 || 3 * p.m >= (int64_t)INT32_MAX - 1) {
         st->code = MF_ERR_LIMIT;
         snprintf(st->message, sizeof(st->message), "mesh too large for 32-bit device indices (n=%lld, m=%lld)",
                  (long long)p.n, (long long)p.m);
         return st->code;
     }
-    p.alias = (mv->features == nullptr);
-    p.C = p.alias ? 3 : mv->c;
-    p.fdtype = p.alias ? MF_DTYPE_F64 : mv->features_dtype;
+    // features omitted = a copy of the positions (mesh.py:28-29); their fold equals the position fold
+    // only for 'average' placement, so 'inverse' carries them as a separate array
+    p.alias = (mv->features == nullptr) && p.placement == 0;
+    p.C = mv->features ? mv->c : 3;
+    p.fdtype = mv->features ? mv->features_dtype : MF_DTYPE_F64;
     p.B = mv->vertex_offsets ? (int)mv->n_meshes : 1;
     const int B = p.B;
     p.voff.assign(B + 1, 0);
@@ -493,7 +497,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // lexicographic edges + pair costs + rank keys
         run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
         LAUNCH(k_edges, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
-               W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed, order);
+               W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed, order, p.placement);
         const int* dE = W.eoff + N;
         if (seeded) {
             RC(cudaMemsetAsync(W.mlo, 0xFF, (size_t)B * sizeof(unsigned long long), stream));
@@ -572,7 +576,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         LAUNCH(k_seg_sort_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.coff, W.cmem, W.best, W.heavy,
                d_heavy_c);
         LAUNCH(k_contract, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.coff, W.cmem, vmesh, act, Pc, Xc,
-               (int)C, Pn, Xn);
+               (int)C, Pn, Xn, W.vq, p.placement);
         // output facets: remap, drop degenerate, drop later duplicates (hash, min facet id wins)
         RC(cudaMemsetAsync(W.table, 0xFF, (size_t)W.tsize * sizeof(int), stream));
         RC(cudaMemsetAsync(W.has_live, 0, (size_t)N, stream));
@@ -629,7 +633,7 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode, p.ld_min};
+                              g_prof_mode, p.ld_min, p.placement};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
     return k;
@@ -707,7 +711,9 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, mv->positions, (size_t)n * 24, cudaMemcpyDefault, stream));
     if (m) MF_CUDA_TRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 24, cudaMemcpyDefault, stream));
     if (!p.alias && n * C > 0) {
-        if (p.fdtype == MF_DTYPE_F64)
+        if (!mv->features)
+            MF_CUDA_TRY(cudaMemcpyAsync(W.X0, mv->positions, (size_t)n * 24, cudaMemcpyDefault, stream));
+        else if (p.fdtype == MF_DTYPE_F64)
             MF_CUDA_TRY(cudaMemcpyAsync(W.X0, mv->features, (size_t)(n * C) * 8, cudaMemcpyDefault, stream));
         else
             MF_CUDA_TRY(cudaMemcpyAsync(W.Xf32, mv->features, (size_t)(n * C) * 4, cudaMemcpyDefault, stream));

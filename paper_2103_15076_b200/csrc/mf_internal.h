@@ -99,6 +99,9 @@ int upload_replace(Context* ctx, const int64_t* replace, int64_t n, int64_t n_ou
 int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64_t c, const int* d_replace, int64_t n,
                void* out, cudaStream_t stream, mf_status* st);
 int64_t round_targets(int64_t n_in, int64_t target, int rounds, std::vector<int64_t>& chain);
+int pool_backward_run(Context* ctx, const void* grad, int gdtype, const void* features, int fdtype, int64_t n,
+                      int64_t c, const int* d_replace, const int* d_off, const int* d_members, int64_t n_out, int mode,
+                      const void* weights, void* out, int odtype, cudaStream_t stream, mf_status* st);
 extern thread_local int64_t g_launches;
 void drop_graphs(const Context* ctx);
 void prof_collect_pending();

@@ -21,6 +21,7 @@
 #pragma once
 
 #include "mf_common.cuh"
+#include "mf_inverse.cuh"
 
 namespace mf {
 
@@ -214,11 +215,17 @@ MF_DEV void other_two(const int* __restrict__ F, int f, int corner, int& a, int&
 
 // Pair cost (quadrics.py:117-132 + evaluate 53-58) for 'average' placement.
 MF_DEV double pair_cost(const Q10& qi, const Q10& qj, double pix, double piy, double piz, double pjx, double pjy,
-                        double pjz, int order) {
+                        double pjz, int order, int placement) {
     double a00 = qi.a00 + qj.a00, a01 = qi.a01 + qj.a01, a02 = qi.a02 + qj.a02;
     double a11 = qi.a11 + qj.a11, a12 = qi.a12 + qj.a12, a22 = qi.a22 + qj.a22;
     double b0 = qi.b0 + qj.b0, b1 = qi.b1 + qj.b1, b2 = qi.b2 + qj.b2, c = qi.c + qj.c;
     double x0 = 0.5 * (pix + pjx), x1 = 0.5 * (piy + pjy), x2 = 0.5 * (piz + pjz);
+    if (placement) {  // optimal_positions(q, midpoints, 'inverse'), quadrics.py:131
+        const double a6[6] = {a00, a01, a02, a11, a12, a22}, bb[3] = {b0, b1, b2}, mid[3] = {x0, x1, x2};
+        double t[3];
+        mf_optimal_position(a6, bb, mid, t);
+        x0 = t[0]; x1 = t[1]; x2 = t[2];
+    }
     double quad = 0.0;
     quad = quad + (x0 * a00) * x0;
     quad = quad + (x0 * a01) * x1;
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
                                                                 int* __restrict__ adj_eid,
                                                                 int* __restrict__ mate,
                                                                 int* __restrict__ minrep, int* __restrict__ absorbed,
-                                                                int order) {
+                                                                int order, int placement) {
     if (*abort_flag) return;
     const int g = threadIdx.x >> 3;  // 8 lanes per vertex (typical degree ~6)
     const int l = threadIdx.x & 7;
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
                 eid = eb + (j - nlow);
                 Q10 qu;
                 q_load(vq, u, qu);
-                double c = pair_cost(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
+                double c = pair_cost(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order, placement);
                 e0[eid] = v;
                 e1[eid] = u;
                 cost[eid] = c;
@@ -1404,7 +1411,8 @@ __global__ void __launch_bounds__(256) k_seg_sort_heavy(const int* __restrict__ 
 __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const int* __restrict__ coff,
                            const int* __restrict__ members, const int* __restrict__ vmesh,
                            const int* __restrict__ act, const double* __restrict__ P, const double* __restrict__ X,
-                           int C, double* __restrict__ Pout, double* __restrict__ Xout) {
+                           int C, double* __restrict__ Pout, double* __restrict__ Xout,
+                           const double* __restrict__ vq, int placement) {
     if (*abort_flag) return;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < Nout; r += gridDim.x * blockDim.x) {
         int s = coff[r], d = coff[r + 1] - s;
@@ -1425,9 +1433,21 @@ __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const i
             sz = sz + P[3 * v + 2];
         }
         double cnt = (double)d;
-        Pout[3 * r] = sx / cnt;
-        Pout[3 * r + 1] = sy / cnt;
-        Pout[3 * r + 2] = sz / cnt;
+        double avg[3] = {sx / cnt, sy / cnt, sz / cnt};
+        if (placement) {  // accumulate_quadrics + optimal_positions(..., 'inverse'), decimate.py:284-286
+            double acc[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int i = 0; i < d; i++) {
+                const double* q = vq + 10 * (size_t)members[s + i];
+#pragma unroll
+                for (int k = 0; k < 10; k++) acc[k] = acc[k] + q[k];
+            }
+            double t[3];
+            mf_optimal_position(acc, acc + 6, avg, t);
+            avg[0] = t[0]; avg[1] = t[1]; avg[2] = t[2];
+        }
+        Pout[3 * r] = avg[0];
+        Pout[3 * r + 1] = avg[1];
+        Pout[3 * r + 2] = avg[2];
         if (X) {
             for (int k = 0; k < C; k++) {
                 double acc = 0.0;

@@ -88,6 +88,8 @@ MF_DEV float narrow(double a) {
     }
     return (float)a;
 }
+MF_DEV double to_f64(double a) { return a; }
+MF_DEV double to_f64(float a) { return widen(a); }
 MF_DEV double avg_div(double acc, int cnt) { return x86_div(acc, (double)cnt); }
 MF_DEV float avg_div(float acc, int cnt) { return narrow(x86_div(widen(acc), (double)cnt)); }
 
@@ -128,6 +130,63 @@ __global__ void k_pool(int64_t n_out, int C, const int* __restrict__ off, const 
             if (mode == MF_POOL_AVERAGE) acc = avg_div(acc, e - s);
         }
         out[idx] = acc;
+    }
+}
+
+// ---- adjoints (pooling.py:80-102) ----
+// sum: grad_in[v] = g[replace[v]];  average: g[replace[v]] / count (numpy promotes to float64);
+// weighted: g[replace[v]] * (w[v] / denom[replace[v]]) with w, denom in the feature dtype.
+template <typename TG, typename TF, typename TO>
+__global__ void k_pool_bwd_gather(int64_t n, int C, const int* __restrict__ rep, const int* __restrict__ off,
+                                  const int* __restrict__ members, const TG* __restrict__ g,
+                                  const TF* __restrict__ w, int mode, TO* __restrict__ out) {
+    const int64_t total = n * (int64_t)C;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = idx / C;
+        const int k = (int)(idx - v * C);
+        const int r = rep[v];
+        const TG gv = g[(int64_t)r * C + k];
+        if (mode == MF_POOL_SUM) {
+            out[idx] = (TO)gv;
+        } else if (mode == MF_POOL_AVERAGE) {
+            out[idx] = (TO)x86_div(to_f64(gv), (double)(off[r + 1] - off[r]));
+        } else {  // weighted
+            TF den = (TF)0;
+            for (int i = off[r]; i < off[r + 1]; i++) den = x86_add(den, w[members[i]]);
+            TF q = x86_div(w[v], den);
+            out[idx] = (TO)x86_mul((TO)gv, (TO)q);
+        }
+    }
+}
+
+// max: the winner of (cluster, channel) is the lowest member whose value equals the
+// forward maximum (== : signed zeros tie, NaN never wins); it receives g, others 0.
+template <typename TG, typename TF>
+__global__ void k_pool_bwd_max(int64_t n_out, int C, const int* __restrict__ off, const int* __restrict__ members,
+                               const TF* __restrict__ X, const TG* __restrict__ g, TF* __restrict__ out,
+                               int* __restrict__ no_winner) {
+    const int64_t total = n_out * (int64_t)C;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / C;
+        const int k = (int)(idx - r * C);
+        TF acc = -INFINITY;
+        for (int i = off[r]; i < off[r + 1]; i++) {
+            TF v = X[(int64_t)members[i] * C + k];
+            acc = (acc != acc || acc > v) ? acc : v;
+        }
+        int win = -1;
+        for (int i = off[r]; i < off[r + 1]; i++)
+            if (X[(int64_t)members[i] * C + k] == acc) {
+                win = members[i];
+                break;
+            }
+        if (win < 0) {
+            atomicExch(no_winner, 1);
+            continue;
+        }
+        out[(int64_t)win * C + k] = x86_add((TF)0, (TF)g[idx]);  // np.add.at into zeros: -0.0 -> +0.0
     }
 }
 
@@ -245,6 +304,70 @@ int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c
     if (h_flag) {
         st->code = MF_ERR_VALUE;
         snprintf(st->message, sizeof(st->message), "weighted pooling: some cluster has zero total weight");
+        return st->code;
+    }
+    return MF_OK;
+}
+
+// out dtype: average -> f64; sum -> grad dtype; weighted -> promote(grad, features); max -> features dtype
+int pool_backward_run(Context* ctx, const void* grad, int gdtype, const void* features, int fdtype, int64_t n,
+                      int64_t c, const int* d_replace, const int* d_off, const int* d_members, int64_t n_out, int mode,
+                      const void* weights, void* out, int odtype, cudaStream_t stream, mf_status* st) {
+    auto es = [](int d) { return d == MF_DTYPE_F32 ? (size_t)4 : (size_t)8; };
+    size_t gb = (size_t)(n_out * c) * es(gdtype), xb = (mode == MF_POOL_MAX) ? (size_t)(n * c) * es(fdtype) : 0,
+           wb = (mode == MF_POOL_WEIGHTED) ? (size_t)n * es(fdtype) : 0, ob = (size_t)(n * c) * es(odtype);
+    bool hg = !is_device_ptr(grad), hx = xb && !is_device_ptr(features), hw = wb && !is_device_ptr(weights),
+         ho = !is_device_ptr(out);
+    void* tmp = nullptr;
+    MF_CUDA_TRY(cudaMallocAsync(&tmp, 1024 + (hg ? gb : 0) + (hx ? xb : 0) + (hw ? wb : 0) + (ho ? ob : 0), stream));
+    char* p = (char*)tmp;
+    int* flag = (int*)p;
+    p += 256;
+    auto stage = [&](bool host, const void* src, size_t bytes) -> const void* {
+        if (!host) return src;
+        cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, stream);
+        const void* r = p;
+        p += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    const void* dG = stage(hg, grad, gb);
+    const void* dX = xb ? stage(hx, features, xb) : nullptr;
+    const void* dW = wb ? stage(hw, weights, wb) : nullptr;
+    void* dO = ho ? (void*)p : out;
+    MF_CUDA_TRY(cudaMemsetAsync(flag, 0, 4, stream));
+    const bool f32g = gdtype == MF_DTYPE_F32, f32f = fdtype == MF_DTYPE_F32, f32o = odtype == MF_DTYPE_F32;
+    if (n * c > 0) {
+        if (mode == MF_POOL_MAX) {
+            MF_CUDA_TRY(cudaMemsetAsync(dO, 0, ob, stream));
+#define MFBWD_MAX(TG, TF) \
+    LAUNCH((k_pool_bwd_max<TG, TF>), grid_of(ctx, n_out * c), 256, 0, stream, n_out, (int)c, d_off, d_members, \
+           (const TF*)dX, (const TG*)dG, (TF*)dO, flag)
+            if (f32g && f32f) MFBWD_MAX(float, float);
+            else if (f32g) MFBWD_MAX(float, double);
+            else if (f32f) MFBWD_MAX(double, float);
+            else MFBWD_MAX(double, double);
+#undef MFBWD_MAX
+        } else {
+#define MFBWD_G(TG, TF, TO) \
+    LAUNCH((k_pool_bwd_gather<TG, TF, TO>), grid_of(ctx, n * c), 256, 0, stream, n, (int)c, d_replace, d_off, \
+           d_members, (const TG*)dG, (const TF*)dW, mode, (TO*)dO)
+            if (f32g && f32f && f32o) MFBWD_G(float, float, float);
+            else if (f32g && f32f) MFBWD_G(float, float, double);
+            else if (f32g && !f32f) MFBWD_G(float, double, double);
+            else if (!f32g && f32f) MFBWD_G(double, float, double);
+            else MFBWD_G(double, double, double);
+#undef MFBWD_G
+        }
+    }
+    if (ho) MF_CUDA_TRY(cudaMemcpyAsync(out, dO, ob, cudaMemcpyDeviceToHost, stream));
+    int h_flag = 0;
+    MF_CUDA_TRY(cudaMemcpyAsync(&h_flag, flag, 4, cudaMemcpyDeviceToHost, stream));
+    MF_CUDA_TRY(cudaFreeAsync(tmp, stream));
+    MF_CUDA_TRY(cudaStreamSynchronize(stream));
+    MF_CUDA_TRY(cudaGetLastError());
+    if (h_flag) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "max pooling backward: a cluster's maximum is NaN (no winner row)");
         return st->code;
     }
     return MF_OK;

@@ -75,3 +75,58 @@ def unpool(coarse_features, result) -> np.ndarray:
     )
     _native.raise_for(st)
     return out
+
+
+def _dtype_code(dt) -> int:
+    return _native.DTYPE_F32 if dt == np.float32 else _native.DTYPE_F64
+
+
+def pool_backward(grad_output, features, result, mode: str = "average", weights=None) -> np.ndarray:
+    """Gradient of pool() w.r.t. the input features (pooling.py:80-97).
+
+    sum: grad_output[replace]; average: grad_output[replace] / count (float64, numpy's
+    promotion); weighted: grad_output[replace] * w / sum(w); max: routed to the lowest
+    input row achieving the maximum, zeros elsewhere (features dtype).
+    """
+    if mode not in POOL_MODES:
+        raise ValueError(f"mode must be one of {POOL_MODES}, got {mode!r}")
+    replace = np.ascontiguousarray(result.replace, dtype=np.int64)
+    X = as_feature_matrix(features, len(replace))
+    n_out = result.n_vertices_out
+    if np.bincount(replace, minlength=n_out).min() == 0:
+        raise RuntimeError("replace tensor does not cover every output vertex")
+    W = None
+    if mode == "weighted":
+        if weights is None:
+            raise ValueError("weighted pooling requires per-input-vertex weights")
+        W = np.ascontiguousarray(np.asarray(weights, dtype=X.dtype))
+        if W.shape != (len(replace),):
+            raise ValueError(f"weights must have shape ({len(replace)},)")
+    G = as_feature_matrix(grad_output, n_out, "grad_output")
+    if mode == "average":
+        odt = np.float64
+    elif mode == "sum":
+        odt = G.dtype
+    elif mode == "weighted":
+        odt = np.result_type(G.dtype, X.dtype)
+    else:
+        odt = X.dtype
+    c = G.shape[1]
+    out = np.empty((len(replace), c), dtype=odt)
+    dec = _handle_for(result)
+    device = dec.device if dec is not None else _native.default_device()
+    st = _native.Status()
+    _native.lib().mf_pool_backward(
+        _native.context(device), dec.handle if dec is not None else None,
+        replace.ctypes.data if replace.size else None, len(replace), n_out,
+        G.ctypes.data if G.size else None, _dtype_code(G.dtype), X.ctypes.data if X.size else None,
+        _dtype_code(X.dtype), c, POOL_MODES.index(mode), None if W is None else W.ctypes.data,
+        out.ctypes.data if out.size else None, _dtype_code(odt), None, ctypes.byref(st),
+    )
+    _native.raise_for(st)
+    return out
+
+
+def unpool_backward(grad_output, result) -> np.ndarray:
+    """Gradient of unpool(): sum pooling of the fine-level gradient (pooling.py:100-102)."""
+    return pool(grad_output, result, mode="sum")

@@ -106,11 +106,18 @@ DECIMATE_CASES = [
      dict(target=42), [None, 3], True),
     ("batch_mixed", {"batch": [T(n, n) for n in (60, 120, 250, 60, 90)]}, dict(target=60), [9], True),
     ("batch16_cfg4lite", {"batch": [T(2500, b, 0.02) for b in range(16)]}, dict(target=1250), [None, 5], False),
+    # placement='inverse' (quadrics.py:89-114): LAPACK eigvalsh/solve -> tolerance-only parity;
+    # small meshes whose rank order is not decided by rounding noise
+    ("inv_toy", {"inline": [TOY_P, TOY_F]}, dict(target=2, rounds=1, placement="inverse"), [None], True),
+    ("inv_terrain300", T(300, 5), dict(target=150, placement="inverse"), [None], True),
+    ("inv_terrain1000", T(1000, 6), dict(target=130, placement="inverse"), [None, 3], True),
+    ("inv_batch", {"batch": [T(120 + 31 * b, 20 + b) for b in range(3)]}, dict(target=50, placement="inverse"),
+     [None], True),
 ]
 
 
-def run_decimate(mesh, target, rounds, seed):
-    cfg = mf.DecimationConfig(target_vertices=target, shuffle_seed=seed, rounds=rounds)
+def run_decimate(mesh, target, rounds, seed, placement="average"):
+    cfg = mf.DecimationConfig(target_vertices=target, shuffle_seed=seed, rounds=rounds, placement=placement)
     try:
         r = mf.decimate_parallel(mesh, cfg)
     except mf.InfeasibleTargetError as e:
@@ -137,10 +144,12 @@ def main():
         mesh = build_mesh(spec)
         for seed in seeds:
             t = time.time()
-            out, arrays = run_decimate(mesh, conf["target"], conf.get("rounds", "auto"), seed)
+            placement = conf.get("placement", "average")
+            out, arrays = run_decimate(mesh, conf["target"], conf.get("rounds", "auto"), seed, placement)
             key = f"{name}|seed={seed}"
             case = {"key": key, "name": name, "spec": spec, "target": conf["target"],
-                    "rounds": conf.get("rounds", "auto"), "seed": seed, "input": input_digest(mesh),
+                    "rounds": conf.get("rounds", "auto"), "seed": seed, "placement": placement,
+                    "input": input_digest(mesh),
                     "expect": out, "ref_seconds": round(time.time() - t, 3)}
             if keep_arrays and arrays is not None:
                 for k, v in arrays.items():
@@ -173,6 +182,17 @@ def main():
             entry["modes"][mode] = sha(out)
         up = mpool.unpool(small[f"{key}|max"], res)
         entry["unpool_max"] = sha(up)
+        # adjoints (pooling.py:80-102), grad of the pooled shape, same dtype and float64
+        for gdt in (dt, "float64"):
+            G = rng.standard_normal((n_out, c)).astype(gdt)
+            G[0, 0] = -0.0
+            small[f"{key}|G_{gdt}"] = G
+            for mode in mpool.POOL_MODES:
+                Xb = X.copy()
+                if mode == "max":
+                    Xb[np.isnan(Xb)] = 0.25  # a NaN maximum has no winner row in the reference (IndexError)
+                small[f"{key}|bwd_{mode}_{gdt}"] = mpool.pool_backward(G, Xb, res, mode=mode, weights=w)
+            small[f"{key}|unpool_bwd_{gdt}"] = mpool.unpool_backward(np.asarray(up, dtype=gdt), res)
         manifest["pool"].append(entry)
     # cfg3-lite hierarchy: terrain 20k, C=64 float32 features, max-pool down / unpool up
     mesh = msyn.delaunay_terrain(20_000, 0.02, 3)

@@ -14,7 +14,7 @@ import paper_2103_15076_b200 as mfg
 from paper_2103_15076_b200 import synthetic as S
 from paper_2103_15076_b200.numerics import forced_order
 
-from test_oracle_golden import build_mesh, input_digest, sha
+from test_oracle_golden import build_mesh, check_inverse, input_digest, sha
 
 pytestmark = pytest.mark.gpu
 
@@ -28,7 +28,8 @@ CASES = MANIFEST["decimate"]
 def test_gpu_decimate_matches_reference(case):
     mesh = build_mesh(case["spec"])
     assert input_digest(mesh) == case["input"]
-    cfg = mfg.DecimationConfig(target_vertices=case["target"], shuffle_seed=case["seed"], rounds=case["rounds"])
+    cfg = mfg.DecimationConfig(target_vertices=case["target"], shuffle_seed=case["seed"], rounds=case["rounds"],
+                               placement=case.get("placement", "average"))
     exp = case["expect"]
     with forced_order(ORDER):
         if "error" in exp:
@@ -40,6 +41,10 @@ def test_gpu_decimate_matches_reference(case):
         res = mfg.decimate_parallel(mesh, cfg)
     out = res.mesh.mesh if isinstance(res.mesh, mfg.BatchedMesh) else res.mesh
     assert out.n_vertices == exp["n_out"] and out.n_facets == exp["m_out"]
+    if case.get("placement") == "inverse":
+        check_inverse(dict(replace=res.replace, mapping=res.mapping, facets=out.facets, positions=out.positions,
+                           features=out.features), case)
+        return
     assert sha(res.replace) == exp["replace"]
     assert sha(res.mapping) == exp["mapping"]
     assert sha(out.facets) == exp["facets"]

@@ -191,3 +191,18 @@ def test_forced_ld_small(oracle, seed, monkeypatch):
     run_both(oracle, S.flat_grid(60), 1_800, seed=seed)
     meshes = [S.delaunay_terrain(300 + 40 * b, seed=b) for b in range(6)]
     run_both(oracle, mfg.concat_batch(meshes), 150, seed=seed)
+
+
+@pytest.mark.parametrize("mesh_fn,target,seed", [
+    (lambda: S.delaunay_terrain(20_000, noise=0.02, seed=1), 5_000, None),
+    (lambda: S.icosphere(4), 900, None),
+    (lambda: S.perturbed_grid(60, noise=0.02, seed=0), 900, 3),
+    (lambda: S.flat_grid(40), 800, None),
+])
+def test_inverse_placement_matches_oracle(oracle, mesh_fn, target, seed):
+    # same scalar algorithm on both sides (Jacobi |eig| range + partial-pivot LU, no FMA): bitwise
+    mesh = mesh_fn()
+    res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target, shuffle_seed=seed, placement="inverse"))
+    ref = oracle.decimate(mesh.positions, mesh.facets, mesh.features, target=target, seed=seed,
+                          order=einsum_order(), placement="inverse")
+    assert_same(res, ref)

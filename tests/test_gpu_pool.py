@@ -2,6 +2,8 @@
 signed zeros, NaN payloads, exact ties, clusters from 1 to 100k members
 (thread tier and heavy tier of the member sort), host and device buffers."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -87,3 +89,47 @@ def test_tensor_api_pool_unpool(oracle):
     assert bits_equal(pooled.cpu().numpy(), oracle.pool(X.cpu().numpy(), ref["replace"], 1200, "max"))
     up = T.unpool(pooled, dd)
     assert torch.equal(up, pooled[dd.replace])
+
+
+GOLDEN = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "small.npz"))
+
+
+@pytest.mark.parametrize("dt", ["float64", "float32"])
+def test_pool_backward_matches_reference(dt):
+    key = f"pool_handmade|{dt}"
+    rep, X, w = GOLDEN[f"{key}|replace"], GOLDEN[f"{key}|X"], GOLDEN[f"{key}|w"]
+    res = hand_result(rep, 60)
+    for gdt in (dt, "float64"):
+        G = GOLDEN[f"{key}|G_{gdt}"]
+        for mode in mfg.POOL_MODES:
+            Xb = X.copy()
+            if mode == "max":
+                Xb[np.isnan(Xb)] = 0.25
+            got = mfg.pool_backward(G, Xb, res, mode=mode, weights=w)
+            assert bits_equal(got, GOLDEN[f"{key}|bwd_{mode}_{gdt}"]), (mode, gdt)
+        up = mfg.unpool(GOLDEN[f"{key}|max"], res).astype(gdt)
+        assert bits_equal(mfg.unpool_backward(up, res), GOLDEN[f"{key}|unpool_bwd_{gdt}"])
+
+
+def test_pool_backward_large_vs_oracle(oracle):
+    mesh = S.delaunay_terrain(3000, noise=0.02, seed=9)
+    res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=800))
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((3000, 6)).astype(np.float32)
+    X[::7, 2] = 0.5  # exact ties inside clusters
+    G = rng.standard_normal((800, 6)).astype(np.float32)
+    w = (0.5 + rng.random(3000)).astype(np.float32)
+    for mode in mfg.POOL_MODES:
+        got = mfg.pool_backward(G, X, res, mode=mode, weights=w)
+        exp = oracle.pool_backward(G, X, res.replace, 800, mode, w)
+        assert bits_equal(got, exp), mode
+
+
+def test_adjoint_identities_gpu():
+    mesh = S.delaunay_terrain(30, seed=4)
+    res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=15))
+    rng = np.random.default_rng(3)
+    x, y = rng.standard_normal((30, 2)), rng.standard_normal((15, 2))
+    assert (mfg.pool(x, res, "sum") * y).sum() == pytest.approx((x * mfg.unpool(y, res)).sum(), rel=1e-12)
+    g = mfg.pool_backward(y, x, res, mode="average")
+    assert (mfg.pool(x, res, "average") * y).sum() == pytest.approx((x * g).sum(), rel=1e-12)

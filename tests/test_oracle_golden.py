@@ -57,10 +57,23 @@ def input_digest(mesh):
 
 def run_oracle(oracle, mesh, case):
     base = mesh.mesh if isinstance(mesh, mfg.BatchedMesh) else mesh
-    kw = dict(target=case["target"], rounds=case["rounds"], seed=case["seed"], order=ORDER)
+    kw = dict(target=case["target"], rounds=case["rounds"], seed=case["seed"], order=ORDER,
+              placement=case.get("placement", "average"))
     if isinstance(mesh, mfg.BatchedMesh):
         kw.update(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets)
     return oracle.decimate(base.positions, base.facets, base.features, **kw)
+
+
+INV_RTOL = 1e-9  # positions: LAPACK solve vs LU (observed ~1e-13); the north-star bar is 1e-5
+
+
+def check_inverse(out, case):
+    """placement='inverse': topology exact, positions within INV_RTOL of the reference."""
+    key = case["key"]
+    for k in ("replace", "mapping", "facets"):
+        np.testing.assert_array_equal(out[k], SMALL[f"{key}|{k}"], err_msg=k)
+    np.testing.assert_allclose(out["positions"], SMALL[f"{key}|positions"], rtol=INV_RTOL, atol=1e-12)
+    np.testing.assert_array_equal(out["features"], SMALL[f"{key}|features"])
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c["key"] for c in CASES])
@@ -75,6 +88,9 @@ def test_decimate_golden(oracle, case):
         return
     out = run_oracle(oracle, mesh, case)
     assert len(out["positions"]) == exp["n_out"] and len(out["facets"]) == exp["m_out"]
+    if case.get("placement") == "inverse":
+        check_inverse(out, case)
+        return
     for k in ("replace", "mapping", "facets", "positions"):
         assert sha(out[k]) == exp[k], k
     feats = out["features"]
@@ -127,3 +143,19 @@ def test_pcg64_matches_numpy(oracle):
 def test_host_einsum_order_recorded():
     # the fixtures pin numpy's lane-split einsum order of the generating host
     assert ORDER in (0, 1)
+
+
+@pytest.mark.parametrize("entry", MANIFEST["pool"], ids=[e["key"] for e in MANIFEST["pool"]])
+def test_pool_backward_golden(oracle, entry):
+    key = entry["key"]
+    rep, X, w = SMALL[f"{key}|replace"], SMALL[f"{key}|X"], SMALL[f"{key}|w"]
+    dt = key.split("|")[1]
+    for gdt in (dt, "float64"):
+        G = SMALL[f"{key}|G_{gdt}"]
+        for mode in ("average", "max", "weighted", "sum"):
+            Xb = X.copy()
+            if mode == "max":
+                Xb[np.isnan(Xb)] = 0.25
+            out = oracle.pool_backward(G, Xb, rep, entry["n_out"], mode, w)
+            exp = SMALL[f"{key}|bwd_{mode}_{gdt}"]
+            assert out.dtype == exp.dtype and np.array_equal(out.view(np.uint8), exp.view(np.uint8)), (mode, gdt)
