@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _native
+from . import _native, hostmem
 from .mesh import BatchedMesh, TriMesh
 from .numerics import einsum_order
 
@@ -134,7 +134,7 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     P = np.ascontiguousarray(base.positions, dtype=np.float64)
     F = np.ascontiguousarray(base.facets, dtype=np.int64)
     X = base.features
-    same = X.dtype == np.float64 and X.shape == P.shape and np.array_equal(X.view(np.uint64), P.view(np.uint64))
+    same = X.dtype == np.float64 and X.shape == P.shape and X.flags.c_contiguous and hostmem.same_bytes(X, P)
     Xc = None if same else np.ascontiguousarray(X)
     view = _native.MeshView()
     view.positions = P.ctypes.data
@@ -157,15 +157,15 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     _native.raise_for(st)
     dec = _native.Decimation(handle, device)
     n_out, m_out, c = dec.n_out, dec.m_out, view.c
-    pos = np.empty((n_out, 3))
-    fac = np.empty((m_out, 3), dtype=np.int64)
+    pos = hostmem.empty((n_out, 3), np.float64)
+    fac = hostmem.empty((m_out, 3), np.int64)
     feats_dtype = np.float64
     # the identity result keeps the input feature dtype (decimate.py:172-174); any real round folds into float64
     if Xc is not None and Xc.dtype == np.float32 and _all_identity(mesh, config):
         feats_dtype = np.float32
-    feats = np.empty((n_out, c), dtype=feats_dtype)
-    rep = np.empty(dec.n_in, dtype=np.int64)
-    mp = np.empty(dec.n_in, dtype=np.int64)
+    feats = hostmem.empty((n_out, c), feats_dtype)
+    rep = hostmem.empty((dec.n_in,), np.int64)
+    mp = hostmem.empty((dec.n_in,), np.int64)
     B = dec.n_meshes
     vo_out = np.empty(B + 1, dtype=np.int64)
     fo_out = np.empty(B + 1, dtype=np.int64)

@@ -13,7 +13,7 @@ import ctypes
 
 import numpy as np
 
-from . import _native
+from . import _native, hostmem
 from .validation import as_feature_matrix
 
 POOL_MODES = ("average", "max", "weighted", "sum")
@@ -43,7 +43,7 @@ def pool(features, result, mode: str = "average", weights=None) -> np.ndarray:
             if np.bincount(replace, minlength=n_out).min() == 0:
                 raise RuntimeError("replace tensor does not cover every output vertex")
             raise ValueError(f"weights must have shape ({len(replace)},)")
-    out = np.empty((n_out, X.shape[1]), dtype=X.dtype)
+    out = hostmem.empty((n_out, X.shape[1]), X.dtype)
     dec = _handle_for(result)
     device = dec.device if dec is not None else _native.default_device()
     st = _native.Status()
@@ -62,7 +62,7 @@ def unpool(coarse_features, result) -> np.ndarray:
     """Broadcast every output vertex's row to its whole cluster (pooling.py:74-77)."""
     coarse = as_feature_matrix(coarse_features, result.n_vertices_out, "coarse_features")
     replace = np.ascontiguousarray(result.replace, dtype=np.int64)
-    out = np.empty((len(replace), coarse.shape[1]), dtype=coarse.dtype)
+    out = hostmem.empty((len(replace), coarse.shape[1]), coarse.dtype)
     dec = _handle_for(result)
     device = dec.device if dec is not None else _native.default_device()
     st = _native.Status()
@@ -112,7 +112,7 @@ def pool_backward(grad_output, features, result, mode: str = "average", weights=
     else:
         odt = X.dtype
     c = G.shape[1]
-    out = np.empty((len(replace), c), dtype=odt)
+    out = hostmem.empty((len(replace), c), odt)
     dec = _handle_for(result)
     device = dec.device if dec is not None else _native.default_device()
     st = _native.Status()
