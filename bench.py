@@ -292,15 +292,30 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_setup()
+    ngpu = torch.cuda.device_count()
+    gloo = None
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local % ngpu)
+        backend = os.environ.get("MF_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local % ngpu))
+        else:
+            dist.init_process_group(backend)
+        # timing reductions: host floats over a gloo side group (works under either backend)
+        gloo = dist.new_group(backend="gloo")
     else:
         dist = None
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
+        return float(t.item())
 
     import paper_2103_15076_b200 as mfg
     from paper_2103_15076_b200 import _native
@@ -359,13 +374,13 @@ def run_ours(args):
 
     # ---------------- timed region: device-resident inputs
     if dist:
-        dist.barrier()
+        dist.barrier(group=gloo)
     torch.cuda.synchronize()
     _native.launch_count(reset=True)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    phys = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
-        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    phys = int(cvd.split(",")[local % ngpu]) if cvd else local % ngpu
     with ClockSampler(phys) as clk:
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
@@ -377,12 +392,9 @@ def run_ours(args):
     dom = _native.profile_read().get(dominant, (0.0, 0))
     _native.profile(0)
     if dist:
-        dist.barrier()
+        dist.barrier(group=gloo)
     step_ms = float(np.sum([s.elapsed_time(e) for s, e in zip(starts, ends)])) / args.steps
-    t = torch.tensor([step_ms], device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms_max = float(t.item())
+    step_ms_max = max_over_ranks(step_ms)
     value = world * m_in / (step_ms_max / 1e3)
 
     # ---------------- e2e: public numpy API, pinned host inputs, H2D + D2H inside
@@ -422,11 +434,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         e2e_step()
         e2e_t.append(time.perf_counter() - t0)
-    e2e_ms = 1e3 * float(np.mean(e2e_t))
-    t = torch.tensor([e2e_ms], device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(1e3 * float(np.mean(e2e_t)))
     h2d = Pp.nbytes + Fp.nbytes + (Xp.nbytes if Xp is not None else 0)
 
     if rank != 0:

@@ -99,10 +99,16 @@ constexpr int kScanTile = kScanBlock * kScanItems;
 constexpr unsigned long long kFlagAgg = 1ull << 32;
 constexpr unsigned long long kFlagPre = 2ull << 32;
 
-template <typename LoadOp>
+struct EpiNone {
+    MF_DEV void operator()(int, int, int) const {}
+};
+
+// `epi(i, exclusive_prefix, value)` runs for every element after its prefix is known
+// (lets a compaction write its payload in the same pass).
+template <typename LoadOp, typename Epi = EpiNone>
 __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, int* __restrict__ out,
                                                           unsigned long long* status, int* ticket,
-                                                          const int* __restrict__ abort_flag) {
+                                                          const int* __restrict__ abort_flag, Epi epi = Epi()) {
     if (abort_flag && *abort_flag) return;  // a failed round: every later stage is skipped
     __shared__ int s_tile;
     __shared__ int s_warp[kScanBlock / 32];
@@ -162,7 +168,10 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, in
 #pragma unroll
     for (int i = 0; i < kScanItems; i++) {
         long long idx = base + i;
-        if (idx < n) out[idx] = run;
+        if (idx < n) {
+            out[idx] = run;
+            epi((int)idx, run, v[i]);
+        }
         run += v[i];
         if (idx == n - 1) out[n] = run;
     }

@@ -149,14 +149,14 @@ struct ScanBuf {
     unsigned long long* status = nullptr;
 };
 
-template <typename LoadOp>
+template <typename LoadOp, typename Epi = EpiNone>
 static void run_scan(ScanBuf& sb, LoadOp op, int* out, int n, cudaStream_t s, const char* name,
-                     const int* abort_flag) {
+                     const int* abort_flag, Epi epi = Epi()) {
     int tiles = std::max(1, (n + kScanTile - 1) / kScanTile);
     RC(cudaMemsetAsync(sb.status, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), s));
     prof_pre(name, s);
-    k_scan_excl<LoadOp><<<tiles, kScanBlock, 0, s>>>(op, n, out, sb.status, reinterpret_cast<int*>(sb.status + tiles),
-                                                     abort_flag);
+    k_scan_excl<LoadOp, Epi><<<tiles, kScanBlock, 0, s>>>(op, n, out, sb.status,
+                                                          reinterpret_cast<int*>(sb.status + tiles), abort_flag, epi);
     RCK();
     prof_post(name, s);
     g_launches++;
@@ -321,7 +321,7 @@ struct WS {
     uint64_t *chi, *clo;
     int *cpay, *caux, *ksel, *mode;
     uint64_t *p_hi, *p_lo;
-    int *segA, *segB, *removed, *absorbed, *minrep, *anchor, *outidx, *rstep, *ccount, *coff, *cmem;
+    int *segA, *segB, *removed, *absorbed, *minrep, *anchor, *outidx, *rstep, *ccount, *coff, *cmem, *repv, *abshead, *absnext;
     unsigned char* has_live;
     int* mapped;
     int4* canon;
@@ -412,6 +412,9 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.ccount = A.take<int>((size_t)N0 + 1);
     W.coff = A.take<int>((size_t)N0 + 1);
     W.cmem = A.take<int>((size_t)N0);
+    W.repv = A.take<int>((size_t)N0);
+    W.abshead = A.take<int>((size_t)N0);
+    W.absnext = A.take<int>((size_t)N0);
     W.has_live = A.take<unsigned char>((size_t)N0);
     W.mapped = A.take<int>((size_t)Mcap * 3);
     W.canon = A.take<int4>((size_t)Mcap);
@@ -462,6 +465,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     int* d_heavy_n = W.counters + 4;
     int* d_heavy_c = W.counters + 12;
     int* d_mid_n = W.counters + 20;
+    int* d_scratch_used = W.counters + 24;
     for (int r = 0; r < R; r++) {
         const int N = p.h_N[r];
         const int Nn = p.h_N[r + 1];
@@ -496,8 +500,14 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
         // lexicographic edges + pair costs + rank keys
         run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
-        LAUNCH(k_edges, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.eoff, W.vq, Pc,
-               W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed, order, p.placement);
+        if (p.placement)
+            LAUNCH(k_edges<1>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt,
+                   W.upcnt, W.eoff, W.vq, Pc, W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed,
+                   W.abshead, order);
+        else
+            LAUNCH(k_edges<0>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt,
+                   W.upcnt, W.eoff, W.vq, Pc, W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed,
+                   W.abshead, order);
         const int* dE = W.eoff + N;
         if (seeded) {
             RC(cudaMemsetAsync(W.mlo, 0xFF, (size_t)B * sizeof(unsigned long long), stream));
@@ -508,7 +518,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         }
         // greedy matching (Suitor proposals) -> mutual proposals are the matched pairs
         LAUNCH(k_adj_keys, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.adj_eid,
-               W.key_hi, W.adj_k32);
+               W.key_hi, W.adj_k32, B, W.segA);
         // large meshes: locally-dominant rounds (persistent) first, then Suitor proposals on the
         // residual frontier; small meshes: Suitor only (the grid barriers would dominate)
         const bool use_ld = N >= p.ld_min;
@@ -532,7 +542,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                          use_ld ? W.front0 : nullptr, W.front1, W.ldc};
             LAUNCH(k_suitor, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, ma);
         }
-        LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, B, W.segA);
+        LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, W.key_hi,
+               seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay);
         // per-mesh selection; one big mesh first narrows its rank prefix with multi-block passes
         const bool big = (B == 1 && N > (1 << 16));
         auto select = [&](const int* seg_cnt, const int* removed_in) {
@@ -549,8 +560,6 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelSmem, stream, sa);
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
-        LAUNCH(k_trunc_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.mate, W.e0, W.key_hi,
-               seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay);
         select(W.segA, nullptr);
         LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, voff_r, W.segA, W.chi, W.clo,
                W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB);
@@ -562,31 +571,28 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, voff_r, W.segB, W.chi, W.clo, W.caux,
                W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.eoff, rf, r);
         // relabel: output index = rank of the cluster's lowest member
-        LAUNCH(k_relabel1, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.mate, W.e0, W.absorbed, W.anchor,
-               W.minrep);
-        run_scan(W.scan, LoadIsRep{W.anchor, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
-        RC(cudaMemsetAsync(W.ccount, 0, (size_t)(Nn + 1) * sizeof(int), stream));
-        LAUNCH(k_relabel3, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.anchor, W.minrep, W.outidx, W.rstep,
-               W.ccount);
-        // cluster CSR + contraction
-        run_scan(W.scan, LoadArr{W.ccount}, W.coff, Nn, stream, "k_scan<clusters>", d_abort);
-        RC(cudaMemsetAsync(W.cursor, 0, (size_t)(Nn + 1) * sizeof(int), stream));
-        LAUNCH(k_csr_scatter, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.rstep, W.coff, W.cursor, W.cmem);
-        LAUNCH(k_seg_sort_small, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.coff, W.cmem, W.heavy, d_heavy_c);
-        LAUNCH(k_seg_sort_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.coff, W.cmem, W.best, W.heavy,
-               d_heavy_c);
-        LAUNCH(k_contract, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.coff, W.cmem, vmesh, act, Pc, Xc,
-               (int)C, Pn, Xn, W.vq, p.placement);
+        run_scan(W.scan, LoadIsRep{W.mate, W.e0, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
+        LAUNCH(k_relabel3, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.mate, W.e0, W.absorbed, W.minrep, W.outidx,
+               W.rstep, W.repv, W.abshead, W.absnext);
+        // contraction over member lists (no cluster CSR needed)
+        if (p.placement)
+            LAUNCH(k_contract<1>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.e0, W.e1,
+                   W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c);
+        else
+            LAUNCH(k_contract<0>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.e0, W.e1,
+                   W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c);
+        LAUNCH(k_contract_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_c, W.repv, W.mate, W.e0,
+               W.e1, W.absorbed, W.abshead, W.absnext, Pc, Xc, (int)C, Pn, Xn, W.vq, p.placement, W.cmem, W.best,
+               d_scratch_used);
         // output facets: remap, drop degenerate, drop later duplicates (hash, min facet id wins)
         RC(cudaMemsetAsync(W.table, 0xFF, (size_t)W.tsize * sizeof(int), stream));
         RC(cudaMemsetAsync(W.has_live, 0, (size_t)N, stream));
         LAUNCH(k_facet_remap, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh, act, W.mapped,
                W.canon, W.slot, W.has_live, W.table, W.tsize - 1, std::max(1u, W.tsize / (unsigned)std::max(Nn, 1)));
-        run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort);
-        LAUNCH(k_facet_write, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, W.kout, W.mapped, Fn, B, foff_c,
-               foff_n);
+        run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort,
+                 EpiFacetWrite{W.mapped, Fn});
         LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
-               W.rt, W.mt, r == 0);
+               W.rt, W.mt, r == 0, B, W.kout, foff_c, foff_n);
         RC(cudaMemcpyAsync(d_stats + 4 * r + 0, foff_c + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));
         RC(cudaMemcpyAsync(d_stats + 4 * r + 1, W.eoff + N, sizeof(int), cudaMemcpyDeviceToDevice, stream));
         RC(cudaMemcpyAsync(d_stats + 4 * r + 2, foff_n + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));

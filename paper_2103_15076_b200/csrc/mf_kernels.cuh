@@ -214,13 +214,14 @@ MF_DEV void other_two(const int* __restrict__ F, int f, int corner, int& a, int&
 
 
 // Pair cost (quadrics.py:117-132 + evaluate 53-58) for 'average' placement.
+template <int PLACEMENT>
 MF_DEV double pair_cost(const Q10& qi, const Q10& qj, double pix, double piy, double piz, double pjx, double pjy,
-                        double pjz, int order, int placement) {
+                        double pjz, int order) {
     double a00 = qi.a00 + qj.a00, a01 = qi.a01 + qj.a01, a02 = qi.a02 + qj.a02;
     double a11 = qi.a11 + qj.a11, a12 = qi.a12 + qj.a12, a22 = qi.a22 + qj.a22;
     double b0 = qi.b0 + qj.b0, b1 = qi.b1 + qj.b1, b2 = qi.b2 + qj.b2, c = qi.c + qj.c;
     double x0 = 0.5 * (pix + pjx), x1 = 0.5 * (piy + pjy), x2 = 0.5 * (piz + pjz);
-    if (placement) {  // optimal_positions(q, midpoints, 'inverse'), quadrics.py:131
+    if (PLACEMENT) {  // optimal_positions(q, midpoints, 'inverse'), quadrics.py:131
         const double a6[6] = {a00, a01, a02, a11, a12, a22}, bb[3] = {b0, b1, b2}, mid[3] = {x0, x1, x2};
         double t[3];
         mf_optimal_position(a6, bb, mid, t);
@@ -430,6 +431,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __re
 // is exactly np.unique(axis=0)'s lexicographic order (mesh.py:131-134).
 // One lane per neighbour of v.  Lower-indexed neighbours
 // resolve their edge id by binary search in the neighbour's upper list.
+template <int PLACEMENT>
 __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __restrict__ abort_flag, int N,
                                                                 const int* __restrict__ inc_off,
                                                                 const int* __restrict__ nbr,
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
                                                                 int* __restrict__ adj_eid,
                                                                 int* __restrict__ mate,
                                                                 int* __restrict__ minrep, int* __restrict__ absorbed,
-                                                                int order, int placement) {
+                                                                int* __restrict__ abshead, int order) {
     if (*abort_flag) return;
     const int g = threadIdx.x >> 3;  // 8 lanes per vertex (typical degree ~6)
     const int l = threadIdx.x & 7;
@@ -453,6 +455,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
             mate[v] = -1;
             minrep[v] = v;
             absorbed[v] = -1;
+            abshead[v] = -1;
         }
         const int nu = ucnt[v];
         if (nu == 0) continue;
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
                 eid = eb + (j - nlow);
                 Q10 qu;
                 q_load(vq, u, qu);
-                double c = pair_cost(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order, placement);
+                double c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
                 e0[eid] = v;
                 e1[eid] = u;
                 cost[eid] = c;
@@ -901,8 +904,10 @@ __global__ void __launch_bounds__(256) k_ld_match(LDArgs a, int round) {
 __global__ void __launch_bounds__(256) k_adj_keys(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ ucnt,
                                                   const int* __restrict__ adj_eid, const uint64_t* __restrict__ key_hi,
-                                                  unsigned* __restrict__ adj_k32) {
+                                                  unsigned* __restrict__ adj_k32, int B, int* __restrict__ seg_cnt) {
     if (*abort_flag) return;
+    // zero the truncation-candidate segment counters k_mates appends to
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) seg_cnt[b] = 0;
     const int l = threadIdx.x & 7;
     const int groups = gridDim.x * (blockDim.x >> 3);
     for (int v = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); v < N; v += groups) {
@@ -913,21 +918,34 @@ __global__ void __launch_bounds__(256) k_adj_keys(const int* __restrict__ abort_
 }
 
 // mate = the suitor edge when the proposal is mutual.
+MF_DEV int seg_slot(const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt, int v,
+                    int& b);
+
+// mate = the suitor edge when the proposal is mutual (or the LD match); every
+// matched pair is also appended once (from its e0 end) as a budget-truncation
+// candidate keyed by its rank (decimate.py:256-258).
 __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigned long long* __restrict__ suitor,
-                        const int* __restrict__ e0,
-                        const int* __restrict__ e1, int* __restrict__ mate, int B, int* __restrict__ seg_cnt) {
+                        const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate,
+                        const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
+                        const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt,
+                        uint64_t* __restrict__ chi, uint64_t* __restrict__ clo, int* __restrict__ cpay) {
     if (*abort_flag) return;
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) seg_cnt[b] = 0;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int m = mate[v];
-        if (m >= 0) continue;  // matched by the LD rounds
-        unsigned long long w = suitor[v];
+        unsigned long long w = m >= 0 ? ~0ull : suitor[v];  // m >= 0: matched by the LD rounds
         if (w != ~0ull) {
             int e = (int)(unsigned)w;
             int u = e0[e] == v ? e1[e] : e0[e];
             if ((int)(unsigned)suitor[u] == e && suitor[u] != ~0ull) m = e;
         }
         mate[v] = m;
+        if (m >= 0 && e0[m] == v) {
+            int b;
+            int slot = seg_slot(vmesh, voff, seg_cnt, v, b);
+            chi[slot] = key_hi[m];
+            clo[slot] = key_lo ? key_lo[m] : (uint64_t)m;
+            cpay[slot] = m;
+        }
     }
 }
 
@@ -1178,10 +1196,30 @@ __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* _
 }
 
 // ---- flag producers fused into the decoupled look-back scan (LoadOp functors)
+// cluster anchor of v: lower end of its matched pair, the pair it was absorbed into, or itself
+MF_DEV int cluster_anchor(int v, const int* __restrict__ mate, const int* __restrict__ e0,
+                          const int* __restrict__ absorbed) {
+    const int m = mate[v];
+    if (m >= 0) return e0[m];
+    const int a = absorbed[v];
+    return a >= 0 ? a : v;
+}
 struct LoadIsRep {  // v is the lowest member of its cluster
-    const int* anchor;
+    const int* mate;
+    const int* e0;
+    const int* absorbed;
     const int* minrep;
-    MF_DEV int operator()(int v) const { return minrep[anchor[v]] == v; }
+    MF_DEV int operator()(int v) const { return minrep[cluster_anchor(v, mate, e0, absorbed)] == v; }
+};
+struct EpiFacetWrite {  // kept facet f -> output row prefix (order preserving compaction)
+    const int* mapped;
+    int* Fout;
+    MF_DEV void operator()(int f, int pos, int keep) const {
+        if (!keep) return;
+        Fout[3 * pos] = mapped[3 * f];
+        Fout[3 * pos + 1] = mapped[3 * f + 1];
+        Fout[3 * pos + 2] = mapped[3 * f + 2];
+    }
 };
 struct LoadKeep {  // facet survives: bypassed, or first occurrence of its non-degenerate triple
     const int* dM;
@@ -1342,25 +1380,20 @@ __global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* 
 // ------------------------------------------------------------------------
 // K7: relabel (decimate.py:130-137, 275-278).  Cluster anchor = lower end of
 // the matched pair; output index = rank of the cluster's lowest member.
-__global__ void k_relabel1(int N, const int* __restrict__ abort_flag, const int* __restrict__ mate,
-                           const int* __restrict__ e0, const int* __restrict__ absorbed, int* __restrict__ anchor,
-                           int* __restrict__ minrep) {
-    if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int m = mate[v], a = v;
-        if (m >= 0) a = e0[m];
-        else if (absorbed[v] >= 0) a = absorbed[v];
-        anchor[v] = a;
-    }
-}
-__global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int* __restrict__ anchor,
+// rstep = output index; the lowest member of output r is recorded (repv) and
+// absorbed vertices are linked into their anchor's list (order fixed later).
+__global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int* __restrict__ mate,
+                           const int* __restrict__ e0, const int* __restrict__ absorbed,
                            const int* __restrict__ minrep, const int* __restrict__ outidx, int* __restrict__ rstep,
-                           int* __restrict__ ccount) {
+                           int* __restrict__ repv, int* __restrict__ abshead, int* __restrict__ absnext) {
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int r = outidx[minrep[anchor[v]]];
+        const int anc = cluster_anchor(v, mate, e0, absorbed);
+        const int rep = minrep[anc];
+        const int r = outidx[rep];
         rstep[v] = r;
-        atomicAdd(ccount + r, 1);
+        if (rep == v) repv[r] = v;
+        if (mate[v] < 0 && absorbed[v] >= 0) absnext[v] = atomicExch(abshead + anc, v);
     }
 }
 
@@ -1408,15 +1441,57 @@ __global__ void __launch_bounds__(256) k_seg_sort_heavy(const int* __restrict__ 
 // K8: contraction by member mean (decimate.py:280-283) and feature mean
 // (decimate.py:142-145): fold from +0.0 in ascending member order, then
 // divide by the count.  Inactive (bypassed) meshes copy rows verbatim.
-__global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const int* __restrict__ coff,
-                           const int* __restrict__ members, const int* __restrict__ vmesh,
+template <int PLACEMENT>
+MF_DEV void fold_members(const int* m, int d, const double* __restrict__ P, const double* __restrict__ X, int C,
+                         const double* __restrict__ vq, int r, double* __restrict__ Pout, double* __restrict__ Xout) {
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    for (int i = 0; i < d; i++) {
+        const int v = m[i];
+        sx = sx + P[3 * v];
+        sy = sy + P[3 * v + 1];
+        sz = sz + P[3 * v + 2];
+    }
+    const double cnt = (double)d;
+    double avg[3] = {sx / cnt, sy / cnt, sz / cnt};
+    if (PLACEMENT) {  // accumulate_quadrics + optimal_positions(..., 'inverse'), decimate.py:284-286
+        double acc[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < d; i++) {
+            const double* q = vq + 10 * (size_t)m[i];
+#pragma unroll
+            for (int k = 0; k < 10; k++) acc[k] = acc[k] + q[k];
+        }
+        double t[3];
+        mf_optimal_position(acc, acc + 6, avg, t);
+        avg[0] = t[0]; avg[1] = t[1]; avg[2] = t[2];
+    }
+    Pout[3 * r] = avg[0];
+    Pout[3 * r + 1] = avg[1];
+    Pout[3 * r + 2] = avg[2];
+    if (X) {
+        for (int k = 0; k < C; k++) {
+            double acc = 0.0;
+            for (int i = 0; i < d; i++) acc = acc + X[(size_t)m[i] * C + k];
+            Xout[(size_t)r * C + k] = acc / cnt;
+        }
+    }
+}
+
+// K8: contraction by member mean (decimate.py:280-283) and feature mean
+// (decimate.py:142-145): members = anchor, its matched partner and the
+// vertices absorbed into it, folded from +0.0 in ascending order, then / count.
+// Inactive (bypassed) meshes copy rows verbatim; clusters of more than
+// kSmallDeg members go to the block tier.
+template <int PLACEMENT>
+__global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const int* __restrict__ repv,
+                           const int* __restrict__ mate, const int* __restrict__ e0, const int* __restrict__ e1,
+                           const int* __restrict__ absorbed, const int* __restrict__ abshead,
+                           const int* __restrict__ absnext, const int* __restrict__ vmesh,
                            const int* __restrict__ act, const double* __restrict__ P, const double* __restrict__ X,
                            int C, double* __restrict__ Pout, double* __restrict__ Xout,
-                           const double* __restrict__ vq, int placement) {
+                           const double* __restrict__ vq, int* __restrict__ heavy, int* __restrict__ heavy_count) {
     if (*abort_flag) return;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < Nout; r += gridDim.x * blockDim.x) {
-        int s = coff[r], d = coff[r + 1] - s;
-        int v0 = members[s];
+        const int v0 = repv[r];
         if (!act[mesh_of(vmesh, v0)]) {
             Pout[3 * r] = P[3 * v0];
             Pout[3 * r + 1] = P[3 * v0 + 1];
@@ -1425,36 +1500,69 @@ __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const i
                 for (int k = 0; k < C; k++) Xout[(size_t)r * C + k] = X[(size_t)v0 * C + k];
             continue;
         }
-        double sx = 0.0, sy = 0.0, sz = 0.0;
-        for (int i = 0; i < d; i++) {
-            int v = members[s + i];
-            sx = sx + P[3 * v];
-            sy = sy + P[3 * v + 1];
-            sz = sz + P[3 * v + 2];
-        }
-        double cnt = (double)d;
-        double avg[3] = {sx / cnt, sy / cnt, sz / cnt};
-        if (placement) {  // accumulate_quadrics + optimal_positions(..., 'inverse'), decimate.py:284-286
-            double acc[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int i = 0; i < d; i++) {
-                const double* q = vq + 10 * (size_t)members[s + i];
-#pragma unroll
-                for (int k = 0; k < 10; k++) acc[k] = acc[k] + q[k];
+        const int anc = cluster_anchor(v0, mate, e0, absorbed);
+        int m[kSmallDeg];
+        int d = 0;
+        m[d++] = anc;
+        if (mate[anc] >= 0) m[d++] = e1[mate[anc]];
+        bool big = false;
+        for (int a = abshead[anc]; a >= 0; a = absnext[a]) {
+            if (d == kSmallDeg) {
+                big = true;
+                break;
             }
-            double t[3];
-            mf_optimal_position(acc, acc + 6, avg, t);
-            avg[0] = t[0]; avg[1] = t[1]; avg[2] = t[2];
+            m[d++] = a;
         }
-        Pout[3 * r] = avg[0];
-        Pout[3 * r + 1] = avg[1];
-        Pout[3 * r + 2] = avg[2];
-        if (X) {
-            for (int k = 0; k < C; k++) {
-                double acc = 0.0;
-                for (int i = 0; i < d; i++) acc = acc + X[(size_t)members[s + i] * C + k];
-                Xout[(size_t)r * C + k] = acc / cnt;
-            }
+        if (big) {
+            heavy[atomicAdd(heavy_count, 1)] = r;
+            continue;
         }
+        isort<kSmallDeg>(m, d);
+        fold_members<PLACEMENT>(m, d, P, X, C, vq, r, Pout, Xout);
+    }
+}
+
+// block tier: collect the member list into scratch, sort it, fold on thread 0
+__global__ void __launch_bounds__(256) k_contract_heavy(const int* __restrict__ abort_flag,
+                                                        const int* __restrict__ heavy,
+                                                        const int* __restrict__ heavy_count,
+                                                        const int* __restrict__ repv, const int* __restrict__ mate,
+                                                        const int* __restrict__ e0, const int* __restrict__ e1,
+                                                        const int* __restrict__ absorbed,
+                                                        const int* __restrict__ abshead,
+                                                        const int* __restrict__ absnext, const double* __restrict__ P,
+                                                        const double* __restrict__ X, int C,
+                                                        double* __restrict__ Pout, double* __restrict__ Xout,
+                                                        const double* __restrict__ vq, int placement,
+                                                        int* __restrict__ scratch, int* __restrict__ tmp,
+                                                        int* __restrict__ scratch_used) {
+    __shared__ int smem[kChunk];
+    __shared__ int s_d, s_base;
+    if (*abort_flag) return;
+    const int H = *heavy_count;
+    for (int h = blockIdx.x; h < H; h += gridDim.x) {
+        const int r = heavy[h];
+        const int anc = cluster_anchor(repv[r], mate, e0, absorbed);
+        if (threadIdx.x == 0) {  // clusters are disjoint: their member lists fit in N slots in total
+            int d = 1 + (mate[anc] >= 0);
+            for (int a = abshead[anc]; a >= 0; a = absnext[a]) d++;
+            s_d = d;
+            s_base = atomicAdd(scratch_used, d);
+            int* m = scratch + s_base;
+            int i = 0;
+            m[i++] = anc;
+            if (mate[anc] >= 0) m[i++] = e1[mate[anc]];
+            for (int a = abshead[anc]; a >= 0; a = absnext[a]) m[i++] = a;
+        }
+        __syncthreads();
+        const int d = s_d;
+        int* m = scratch + s_base;
+        block_sort_ints(m, tmp + s_base, d, smem);
+        if (threadIdx.x == 0) {
+            if (placement) fold_members<1>(m, d, P, X, C, vq, r, Pout, Xout);
+            else fold_members<0>(m, d, P, X, C, vq, r, Pout, Xout);
+        }
+        __syncthreads();
     }
 }
 
@@ -1526,30 +1634,18 @@ __global__ void k_identity_index(int n, int* __restrict__ a, int* __restrict__ b
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = b[i] = i;
 }
 
-__global__ void k_facet_write(const int* __restrict__ dM, const int* __restrict__ abort_flag,
-                              const int* __restrict__ kout,
-                              const int* __restrict__ mapped, int* __restrict__ Fout, int B,
-                              const int* __restrict__ foff_in, int* __restrict__ foff_out) {
-    if (*abort_flag) return;
-    const int M = *dM;
-    int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    for (int b = tid; b <= B; b += nth) foff_out[b] = kout[foff_in[b]];
-    for (int f = tid; f < M; f += nth) {
-        int o = kout[f];
-        if (kout[f + 1] == o) continue;
-        Fout[3 * o] = mapped[3 * f];
-        Fout[3 * o + 1] = mapped[3 * f + 1];
-        Fout[3 * o + 2] = mapped[3 * f + 2];
-    }
-}
 
 // K10: chain replace / mapping across rounds (decimate.py:380-381); the
 // round's mapping (decimate.py:159-167) is formed on the fly.
 __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int* __restrict__ rstep,
                           const int* __restrict__ inc_off, const unsigned char* __restrict__ has_live,
                           const int* __restrict__ vmesh, const int* __restrict__ act, int* __restrict__ rt,
-                          int* __restrict__ mt, int first_round) {
+                          int* __restrict__ mt, int first_round, int B, const int* __restrict__ kout,
+                          const int* __restrict__ foff_in, int* __restrict__ foff_out) {
     if (*abort_flag) return;
+    // per-mesh output facet offsets = keep-scan prefix at each mesh's first input facet
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= B; b += gridDim.x * blockDim.x)
+        foff_out[b] = kout[foff_in[b]];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N0; i += gridDim.x * blockDim.x) {
         int r = first_round ? i : rt[i];
         rt[i] = rstep[r];
