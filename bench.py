@@ -154,6 +154,7 @@ class ClockSampler:
 # (N, M, E vertices/facets/edges in, Nn/Mn out; int32 indices, float64 values).
 # Each byte a kernel must move at least once -- see DESIGN.md "Kernels".
 def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
+    name = name.split("<")[0]  # template instances (k_edges<0>) share the model
     N, M, E, Nn, Mn = r["N"], r["M"], r["E"], r["N_out"], r["M_out"]
     table = {
         "k_facet_plane": 12 * M + 24 * N + 32 * M + 4 * N,
@@ -170,6 +171,7 @@ def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
         "k_adj_keys": 16 * E + 8 * E,
         "k_contract": 4 * N + 4 * Nn + 24 * N + 24 * Nn,
         "k_facet_remap": 12 * M + 4 * N + 12 * M + 16 * M + 4 * M + N,
+        "k_inc_scatter": 12 * M + 4 * N + 12 * M,
         "k_compose": 8 * r.get("N0", N) + 4 * N,
     }
     v = table.get(name)

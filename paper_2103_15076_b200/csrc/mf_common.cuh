@@ -11,6 +11,16 @@
 
 #define MF_DEV __device__ __forceinline__
 
+// Programmatic dependent launch: every kernel first waits for its
+// predecessor grid (griddepcontrol.wait is a no-op without a programmatic
+// edge) and then lets its own dependents start launching, so a graph node's
+// launch and prologue overlap the previous node's tail.
+#define MF_PDL_ENTRY                                              \
+    do {                                                          \
+        asm volatile("griddepcontrol.wait;" ::: "memory");        \
+        asm volatile("griddepcontrol.launch_dependents;" :::);    \
+    } while (0)
+
 namespace mf {
 
 constexpr int kWarp = 32;
@@ -108,7 +118,12 @@ struct EpiNone {
 template <typename LoadOp, typename Epi = EpiNone>
 __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, int* __restrict__ out,
                                                           unsigned long long* status, int* ticket,
-                                                          const int* __restrict__ abort_flag, Epi epi = Epi()) {
+                                                          const int* __restrict__ abort_flag, Epi epi = Epi(),
+                                                          unsigned long long* __restrict__ clear = nullptr,
+                                                          int clear_words = 0) {
+    MF_PDL_ENTRY;
+    // double-buffered look-back state: clear the buffer the NEXT scan will use
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < clear_words; i += gridDim.x * blockDim.x) clear[i] = 0ull;
     if (abort_flag && *abort_flag) return;  // a failed round: every later stage is skipped
     __shared__ int s_tile;
     __shared__ int s_warp[kScanBlock / 32];

@@ -98,14 +98,42 @@ static void rec_check(cudaError_t e, int line) {
 #define RC(expr) rec_check((expr), __LINE__)
 #define RCK() rec_check(cudaGetLastError(), __LINE__)
 
+// Launch through cudaLaunchKernelEx; while the round chain is being recorded
+// every launch carries the programmatic-stream-serialization attribute, so the
+// captured graph's kernel->kernel edges are programmatic (PDL) edges.
+thread_local bool g_pdl = false;
+static bool pdl_enabled() {  // measured a few % slower at cfg2 on B200, so opt-in (MF_PDL=1)
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_PDL");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (g_pdl && pdl_enabled()) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 #ifndef LAUNCH
-#define LAUNCH(kernel, grid, block, smem, stream, ...)                 \
-    do {                                                               \
-        prof_pre(#kernel, stream);                                     \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);    \
-        rec_check(cudaGetLastError(), __LINE__);                       \
-        prof_post(#kernel, stream);                                    \
-        g_launches++;                                                  \
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                                            \
+    do {                                                                                          \
+        prof_pre(#kernel, stream);                                                                \
+        rec_check(launch_ex(kernel, dim3(grid), dim3(block), (smem), (stream), __VA_ARGS__),      \
+                  __LINE__);                                                                      \
+        prof_post(#kernel, stream);                                                               \
+        g_launches++;                                                                             \
     } while (0)
 #endif
 
@@ -145,21 +173,26 @@ int64_t round_targets(int64_t n_in, int64_t target, int rounds, std::vector<int6
     return (int64_t)chain.size();
 }
 
+// two look-back state buffers: each scan uses one and clears the other for the next
 struct ScanBuf {
-    unsigned long long* status = nullptr;
+    unsigned long long* buf[2] = {nullptr, nullptr};
+    int words = 0;
+    int cur = 0;
 };
 
 template <typename LoadOp, typename Epi = EpiNone>
 static void run_scan(ScanBuf& sb, LoadOp op, int* out, int n, cudaStream_t s, const char* name,
                      const int* abort_flag, Epi epi = Epi()) {
     int tiles = std::max(1, (n + kScanTile - 1) / kScanTile);
-    RC(cudaMemsetAsync(sb.status, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), s));
+    unsigned long long* st = sb.buf[sb.cur];
+    unsigned long long* other = sb.buf[sb.cur ^ 1];
     prof_pre(name, s);
-    k_scan_excl<LoadOp, Epi><<<tiles, kScanBlock, 0, s>>>(op, n, out, sb.status,
-                                                          reinterpret_cast<int*>(sb.status + tiles), abort_flag, epi);
-    RCK();
+    rec_check(launch_ex(k_scan_excl<LoadOp, Epi>, dim3(tiles), dim3(kScanBlock), 0, s, op, n, out, st,
+                        reinterpret_cast<int*>(st + tiles), abort_flag, epi, other, sb.words),
+              __LINE__);
     prof_post(name, s);
     g_launches++;
+    sb.cur ^= 1;
 }
 
 // ------------------------------------------------------------------------
@@ -328,6 +361,7 @@ struct WS {
     int *slot, *kout;
     unsigned tsize;
     int* table;
+    unsigned long long* tkey;
     ScanBuf scan;
     int* status;  // [8] flags | foff_final[B+1] | fail[3B] | stats[4R]
     size_t status_words;
@@ -423,8 +457,12 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.tsize = 1u;
     while (W.tsize < (unsigned)(2 * Mcap)) W.tsize <<= 1;
     W.table = A.take<int>((size_t)W.tsize);
+    W.tkey = A.take<unsigned long long>((size_t)W.tsize);
     size_t maxn = (size_t)std::max(N0, Mcap) + 1;
-    W.scan.status = A.take<unsigned long long>(maxn / kScanTile + 4);
+    W.scan.words = (int)(maxn / kScanTile + 4);
+    W.scan.buf[0] = A.take<unsigned long long>((size_t)W.scan.words);
+    W.scan.buf[1] = A.take<unsigned long long>((size_t)W.scan.words);
+    W.scan.cur = 0;
     W.status_words = 8 + (size_t)(B + 1) + 3 * (size_t)B + 4 * (size_t)std::max(R, 1);
     W.status = A.take<int>(W.status_words);
 }
@@ -447,14 +485,14 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     int* d_voff = d_nin + (size_t)(R + 1) * B;
     int* d_foff0 = d_voff + (size_t)(R + 1) * (B + 1);
 
-    RC(cudaMemsetAsync(W.status, 0, W.status_words * sizeof(int), stream));
-    RC(cudaMemsetAsync(d_fail, 0xFF, (size_t)B * 3 * sizeof(int), stream));
-    RC(cudaMemsetAsync(d_badf, 0x7f, sizeof(int), stream));
-    RC(cudaMemsetAsync(W.ghist, 0, kSelBins * sizeof(int), stream));
+    g_pdl = true;
+    LAUNCH(k_graph_init, grid_for(ctx, std::max<int64_t>({(int64_t)N0 + 1, (int64_t)W.scan.words, (int64_t)W.status_words})),
+           256, 0, stream, W.status, (int)W.status_words, (int)(d_fail - W.status), (int)(d_fail - W.status) + 3 * B,
+           W.foff_a, d_foff0, B, W.deg, W.cursor, N0 + 1, W.counters, W.scan.buf[0], W.scan.buf[1], W.scan.words,
+           W.ghist, kSelBins);
     if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, W.F0, B, W.vo64, W.fo64, d_badf);
     if (n > 0) LAUNCH(k_check_finite, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, W.P0, d_badp);
     if (W.Xf32 && n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, W.X0);
-    RC(cudaMemcpyAsync(W.foff_a, d_foff0, (B + 1) * sizeof(int), cudaMemcpyDeviceToDevice, stream));
 
     const double* Pc = W.P0;
     const double* Xc = p.alias ? nullptr : W.X0;
@@ -483,9 +521,6 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             vmesh = W.vmesh;
             LAUNCH(k_vmesh, grid_for(ctx, N), 256, 0, stream, d_abort, N, voff_r, B, vmesh);
         }
-        RC(cudaMemsetAsync(W.deg, 0, (size_t)(N + 1) * sizeof(int), stream));
-        RC(cudaMemsetAsync(W.cursor, 0, (size_t)(N + 1) * sizeof(int), stream));
-        RC(cudaMemsetAsync(W.counters, 0, 64 * sizeof(int), stream));
         // facet planes + incidence CSR (corner-major order)
         LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, Pc, dM, vmesh, act, W.plane, W.deg, order);
         run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", d_abort);
@@ -503,30 +538,24 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         if (p.placement)
             LAUNCH(k_edges<1>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt,
                    W.upcnt, W.eoff, W.vq, Pc, W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed,
-                   W.abshead, order);
+                   W.abshead, order, B, W.mlo, W.mhi);
         else
             LAUNCH(k_edges<0>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt,
                    W.upcnt, W.eoff, W.vq, Pc, W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed,
-                   W.abshead, order);
+                   W.abshead, order, B, W.mlo, W.mhi);
         const int* dE = W.eoff + N;
         if (seeded) {
-            RC(cudaMemsetAsync(W.mlo, 0xFF, (size_t)B * sizeof(unsigned long long), stream));
-            RC(cudaMemsetAsync(W.mhi, 0, (size_t)B * sizeof(unsigned long long), stream));
             LAUNCH(k_cost_minmax, grid_for(ctx, Ecap), 256, 0, stream, d_abort, dE, W.cost, W.e0, vmesh, W.mlo, W.mhi);
             LAUNCH(k_seed_keys, grid_for(ctx, (Ecap + kSeedRun - 1) / kSeedRun), 256, 0, stream, d_abort, dE, W.cost, W.e0,
                    vmesh, W.eoff, voff_r, W.mlo, W.mhi, p.pcg[0], p.pcg[1], p.pcg[2], p.pcg[3], W.key_hi, W.key_lo);
         }
         // greedy matching (Suitor proposals) -> mutual proposals are the matched pairs
         LAUNCH(k_adj_keys, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.adj_eid,
-               W.key_hi, W.adj_k32, B, W.segA);
+               W.key_hi, W.adj_k32, B, W.segA, W.ldc, W.suitor);
         // large meshes: locally-dominant rounds (persistent) first, then Suitor proposals on the
         // residual frontier; small meshes: Suitor only (the grid barriers would dominate)
         const bool use_ld = N >= p.ld_min;
-        RC(cudaMemsetAsync(W.ldc, 0, 8 * sizeof(int), stream));
-        RC(cudaMemsetAsync(W.bar, 0, 8 * sizeof(unsigned), stream));
-        if (!use_ld) {
-            RC(cudaMemsetAsync(W.mate, 0xFF, (size_t)N * sizeof(int), stream));
-        } else {
+        if (use_ld) {
             LDArgs la{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
                       W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, kLDRounds, d_abort};
             LAUNCH(k_ld_init, grid_for(ctx, N), 256, 0, stream, la);
@@ -535,7 +564,6 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                 LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, round);
             }
         }
-        RC(cudaMemsetAsync(W.suitor, 0xFF, (size_t)N * sizeof(unsigned long long), stream));
         {
             MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.adj_k32, W.e0, W.e1, W.key_hi,
                          seeded ? W.key_lo : nullptr, W.suitor, d_abort, use_ld ? W.mate : nullptr,
@@ -572,8 +600,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.eoff, rf, r);
         // relabel: output index = rank of the cluster's lowest member
         run_scan(W.scan, LoadIsRep{W.mate, W.e0, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
-        LAUNCH(k_relabel3, grid_for(ctx, N), 256, 0, stream, N, d_abort, W.mate, W.e0, W.absorbed, W.minrep, W.outidx,
-               W.rstep, W.repv, W.abshead, W.absnext);
+        const bool packed = Nn < (1 << 21);
+        LAUNCH(k_relabel3, grid_for(ctx, std::max<int64_t>(N, W.tsize)), 256, 0, stream, N, d_abort, W.mate, W.e0,
+               W.absorbed, W.minrep, W.outidx, W.rstep, W.repv, W.abshead, W.absnext, W.table,
+               packed ? W.tkey : nullptr, (int)W.tsize, packed ? 0x7f7f7f7f : -1, W.has_live);
         // contraction over member lists (no cluster CSR needed)
         if (p.placement)
             LAUNCH(k_contract<1>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.e0, W.e1,
@@ -585,24 +615,26 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                W.e1, W.absorbed, W.abshead, W.absnext, Pc, Xc, (int)C, Pn, Xn, W.vq, p.placement, W.cmem, W.best,
                d_scratch_used);
         // output facets: remap, drop degenerate, drop later duplicates (hash, min facet id wins)
-        RC(cudaMemsetAsync(W.table, 0xFF, (size_t)W.tsize * sizeof(int), stream));
-        RC(cudaMemsetAsync(W.has_live, 0, (size_t)N, stream));
-        LAUNCH(k_facet_remap, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh, act, W.mapped,
-               W.canon, W.slot, W.has_live, W.table, W.tsize - 1, std::max(1u, W.tsize / (unsigned)std::max(Nn, 1)));
+        {
+            const unsigned per_vertex = std::max(1u, W.tsize / (unsigned)std::max(Nn, 1));
+            if (packed)
+                LAUNCH(k_facet_remap<true>, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh, act,
+                       W.mapped, W.canon, W.slot, W.has_live, W.table, W.tkey, W.tsize - 1, per_vertex);
+            else
+                LAUNCH(k_facet_remap<false>, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh,
+                       act, W.mapped, W.canon, W.slot, W.has_live, W.table, W.tkey, W.tsize - 1, per_vertex);
+        }
         run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort,
                  EpiFacetWrite{W.mapped, Fn});
         LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
-               W.rt, W.mt, r == 0, B, W.kout, foff_c, foff_n);
-        RC(cudaMemcpyAsync(d_stats + 4 * r + 0, foff_c + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));
-        RC(cudaMemcpyAsync(d_stats + 4 * r + 1, W.eoff + N, sizeof(int), cudaMemcpyDeviceToDevice, stream));
-        RC(cudaMemcpyAsync(d_stats + 4 * r + 2, foff_n + B, sizeof(int), cudaMemcpyDeviceToDevice, stream));
-        RC(cudaMemcpyAsync(d_stats + 4 * r + 3, W.ldc + 2, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+               W.rt, W.mt, r == 0, B, W.kout, foff_c, foff_n, last ? d_foff_fin : nullptr, d_stats + 4 * r,
+               W.eoff + N, W.ldc + 2, W.deg, W.cursor, last ? 0 : Nn + 1, W.counters);
         Pc = Pn;
         Xc = Xn;
         Fc = Fn;
         std::swap(foff_c, foff_n);
     }
-    RC(cudaMemcpyAsync(d_foff_fin, foff_c, (B + 1) * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+    g_pdl = false;
 }
 
 // ------------------------------------------------------------------------

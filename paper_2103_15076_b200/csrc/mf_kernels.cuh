@@ -118,6 +118,7 @@ MF_DEV int mesh_of(const int* __restrict__ vmesh, int v) { return vmesh ? vmesh[
 // ------------------------------------------------------------------------
 // K0: batch bookkeeping -- owning mesh of every vertex of this round.
 __global__ void k_vmesh(const int* __restrict__ abort_flag, int N, const int* __restrict__ voff, int B, int* __restrict__ vmesh) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int lo = 0, hi = B;  // find b with voff[b] <= v < voff[b+1]
@@ -133,6 +134,7 @@ __global__ void k_vmesh(const int* __restrict__ abort_flag, int N, const int* __
 __global__ void k_facet_plane(const int* __restrict__ abort_flag, const int* __restrict__ F, const double* __restrict__ P, const int* __restrict__ dM,
                               const int* __restrict__ vmesh, const int* __restrict__ act, Plane* __restrict__ plane,
                               int* __restrict__ deg, int order) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     const int M = *dM;
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
@@ -164,6 +166,7 @@ __global__ void k_facet_plane(const int* __restrict__ abort_flag, const int* __r
 __global__ void k_inc_scatter(const int* __restrict__ abort_flag, const int* __restrict__ F, const int* __restrict__ dM, int Mcap,
                               const int* __restrict__ vmesh, const int* __restrict__ act,
                               const int* __restrict__ inc_off, int* __restrict__ cursor, int* __restrict__ inc) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     const int M = *dM;
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
                                                   int* __restrict__ ucnt, int* __restrict__ upcnt,
                                                   int* __restrict__ mid, int* __restrict__ mid_count,
                                                   int* __restrict__ heavy, int* __restrict__ heavy_count) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         const int s = inc_off[v], d = inc_off[v + 1] - s;
@@ -360,6 +364,7 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __re
                                                                  int* __restrict__ ucnt, int* __restrict__ upcnt,
                                                                  int* __restrict__ heavy,
                                                                  int* __restrict__ heavy_count) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     __shared__ double s_q[2 * kGrpWarps][kGrp][10];
     __shared__ int s_c[2 * kGrpWarps][2 * kGrp];
@@ -445,8 +450,15 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __res
                                                                 int* __restrict__ adj_eid,
                                                                 int* __restrict__ mate,
                                                                 int* __restrict__ minrep, int* __restrict__ absorbed,
-                                                                int* __restrict__ abshead, int order) {
+                                                                int* __restrict__ abshead, int order, int B,
+                                                                unsigned long long* __restrict__ mlo,
+                                                                unsigned long long* __restrict__ mhi) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+        mlo[b] = ~0ull;
+        mhi[b] = 0ull;
+    }
     const int g = threadIdx.x >> 3;  // 8 lanes per vertex (typical degree ~6)
     const int l = threadIdx.x & 7;
     const int groups = gridDim.x * (blockDim.x >> 3);
@@ -499,6 +511,7 @@ __global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ ab
                                                       const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
                                                       int* __restrict__ nbr, int* __restrict__ nbr_tmp,
                                                       int* __restrict__ ucnt, int* __restrict__ upcnt) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     __shared__ int smem[kChunk];
     __shared__ Plane s_pl[256];
@@ -571,6 +584,7 @@ __global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ ab
 __global__ void k_cost_minmax(const int* __restrict__ abort_flag, const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
                               const int* __restrict__ vmesh, unsigned long long* __restrict__ mlo,
                               unsigned long long* __restrict__ mhi) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     const int E = *dE;
     uint64_t lo = ~0ull, hi = 0ull;
@@ -629,6 +643,7 @@ __global__ void k_seed_keys(const int* __restrict__ abort_flag, const int* __res
                             const unsigned long long* __restrict__ mlo, const unsigned long long* __restrict__ mhi,
                             uint64_t s_hi, uint64_t s_lo, uint64_t i_hi,
                             uint64_t i_lo, uint64_t* __restrict__ key_hi, uint64_t* __restrict__ key_lo) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     const int E = *dE;
     const u128 s0 = ((u128)s_hi << 64) | s_lo, inc = ((u128)i_hi << 64) | i_lo;
@@ -703,6 +718,7 @@ MF_DEV bool edge_lt(const MatchArgs& a, unsigned ke, int e, unsigned kf, int f) 
 }
 
 __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
+    MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     // 8 lanes per proposer: the adjacency of `cur` is scanned in parallel
     // (one neighbour per lane), the best winnable edge is an argmin over the
@@ -820,6 +836,7 @@ MF_DEV void block_append(bool keep, int v, int* __restrict__ out, int* __restric
 
 // initial frontier: every vertex with an edge (mate reset)
 __global__ void __launch_bounds__(256) k_ld_init(LDArgs a) {
+    MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     const int nb = (a.N + blockDim.x - 1) / blockDim.x;
     for (int b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -835,6 +852,7 @@ __global__ void __launch_bounds__(256) k_ld_init(LDArgs a) {
 
 // phase A of round `round`: each frontier vertex picks its best live edge
 __global__ void __launch_bounds__(256) k_ld_pick(LDArgs a, int round) {
+    MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     const int cur = round & 1;
     const int n = a.counters[cur];
@@ -872,6 +890,7 @@ __global__ void __launch_bounds__(256) k_ld_pick(LDArgs a, int round) {
 
 // phase B: mutual picks are matched; the rest (with a live edge) survive
 __global__ void __launch_bounds__(256) k_ld_match(LDArgs a, int round) {
+    MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     const int cur = round & 1;
     const int n = a.counters[cur];
@@ -904,10 +923,15 @@ __global__ void __launch_bounds__(256) k_ld_match(LDArgs a, int round) {
 __global__ void __launch_bounds__(256) k_adj_keys(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ ucnt,
                                                   const int* __restrict__ adj_eid, const uint64_t* __restrict__ key_hi,
-                                                  unsigned* __restrict__ adj_k32, int B, int* __restrict__ seg_cnt) {
+                                                  unsigned* __restrict__ adj_k32, int B, int* __restrict__ seg_cnt,
+                                                  int* __restrict__ ldc, unsigned long long* __restrict__ suitor) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
-    // zero the truncation-candidate segment counters k_mates appends to
+    // zero the truncation-candidate segment counters k_mates appends to, the LD
+    // round counters, and the suitor words
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) seg_cnt[b] = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 8; i += gridDim.x * blockDim.x) ldc[i] = 0;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) suitor[v] = ~0ull;
     const int l = threadIdx.x & 7;
     const int groups = gridDim.x * (blockDim.x >> 3);
     for (int v = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); v < N; v += groups) {
@@ -929,6 +953,7 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigne
                         const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
                         const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt,
                         uint64_t* __restrict__ chi, uint64_t* __restrict__ clo, int* __restrict__ cpay) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int m = mate[v];
@@ -995,6 +1020,7 @@ struct SelectArgs {
 };
 
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
+    MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     extern __shared__ unsigned char s_raw[];
     int* hist = reinterpret_cast<int*>(s_raw);                          // kSelBins
@@ -1111,6 +1137,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
 // shared memory and flushes non-zero bins; one block then picks the digit.
 // The single-CTA k_select resumes from the resulting state.
 __global__ void __launch_bounds__(512) k_sel_hist(SelectArgs a, int* __restrict__ ghist, int pass) {
+    MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     __shared__ int h[kSelBins];
     if (pass > 0 && a.mode[0] != 0) return;
@@ -1131,6 +1158,7 @@ __global__ void __launch_bounds__(512) k_sel_hist(SelectArgs a, int* __restrict_
 }
 
 __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* __restrict__ ghist, int pass) {
+    MF_PDL_ENTRY;
     __shared__ int s_scan[33];
     __shared__ int s_sel[3];
     if (*a.abort_flag) return;
@@ -1257,6 +1285,7 @@ __global__ void k_trunc_cand(const int* __restrict__ abort_flag, int N, const in
                              const uint64_t* __restrict__ key_lo, const int* __restrict__ vmesh,
                              const int* __restrict__ voff, int* __restrict__ seg_cnt, uint64_t* __restrict__ chi,
                              uint64_t* __restrict__ clo, int* __restrict__ cpay) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int e = mate[v];
@@ -1283,6 +1312,7 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
                               const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
                               const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate, int B,
                               const int* __restrict__ ksel, int* __restrict__ removed, int* __restrict__ seg_cnt2) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int b = tid; b < B; b += nth) {
@@ -1310,6 +1340,7 @@ __global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const i
                               const int* __restrict__ budget, const int* __restrict__ removed,
                               int* __restrict__ seg_cnt, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
                               int* __restrict__ caux) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         int nu = ucnt[v];
@@ -1351,6 +1382,7 @@ __global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* 
                                const int* __restrict__ budget, const int* __restrict__ nin,
                                const int* __restrict__ ksel, int* __restrict__ removed, const int* __restrict__ eoff,
                                RoundFail fail, int round) {
+    MF_PDL_ENTRY;
     if (*fail.abort) return;
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int i = tid; i < N; i += nth) {
@@ -1385,8 +1417,17 @@ __global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* 
 __global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int* __restrict__ mate,
                            const int* __restrict__ e0, const int* __restrict__ absorbed,
                            const int* __restrict__ minrep, const int* __restrict__ outidx, int* __restrict__ rstep,
-                           int* __restrict__ repv, int* __restrict__ abshead, int* __restrict__ absnext) {
+                           int* __restrict__ repv, int* __restrict__ abshead, int* __restrict__ absnext,
+                           int* __restrict__ table, unsigned long long* __restrict__ tkey, int tsize, int table_init,
+                           unsigned char* __restrict__ has_live) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
+    // reset the facet dedupe table and the live-facet flags for k_facet_remap
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tsize; i += gridDim.x * blockDim.x) {
+        table[i] = table_init;
+        if (tkey) tkey[i] = ~0ull;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) has_live[i] = 0;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         const int anc = cluster_anchor(v, mate, e0, absorbed);
         const int rep = minrep[anc];
@@ -1400,6 +1441,7 @@ __global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int*
 // Generic CSR scatter of items by key (order fixed afterwards by the segment sort).
 __global__ void k_csr_scatter(int n, const int* __restrict__ abort_flag, const int* __restrict__ key,
                               const int* __restrict__ off, int* __restrict__ cursor, int* __restrict__ members) {
+    MF_PDL_ENTRY;
     if (abort_flag && *abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         int r = key[v];
@@ -1410,6 +1452,7 @@ __global__ void k_csr_scatter(int n, const int* __restrict__ abort_flag, const i
 // Thread tier of the member sort; longer segments go to the heavy list.
 __global__ void k_seg_sort_small(int nseg, const int* __restrict__ abort_flag, const int* __restrict__ off,
                                  int* __restrict__ members, int* __restrict__ heavy, int* __restrict__ heavy_count) {
+    MF_PDL_ENTRY;
     if (abort_flag && *abort_flag) return;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nseg; r += gridDim.x * blockDim.x) {
         int s = off[r], d = off[r + 1] - s;
@@ -1428,6 +1471,7 @@ __global__ void __launch_bounds__(256) k_seg_sort_heavy(const int* __restrict__ 
                                                         const int* __restrict__ off, int* __restrict__ members,
                                                         int* __restrict__ tmp, const int* __restrict__ heavy,
                                                         const int* __restrict__ heavy_count) {
+    MF_PDL_ENTRY;
     __shared__ int smem[kChunk];
     if (abort_flag && *abort_flag) return;
     const int H = *heavy_count;
@@ -1489,6 +1533,7 @@ __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const i
                            const int* __restrict__ act, const double* __restrict__ P, const double* __restrict__ X,
                            int C, double* __restrict__ Pout, double* __restrict__ Xout,
                            const double* __restrict__ vq, int* __restrict__ heavy, int* __restrict__ heavy_count) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < Nout; r += gridDim.x * blockDim.x) {
         const int v0 = repv[r];
@@ -1536,6 +1581,7 @@ __global__ void __launch_bounds__(256) k_contract_heavy(const int* __restrict__ 
                                                         const double* __restrict__ vq, int placement,
                                                         int* __restrict__ scratch, int* __restrict__ tmp,
                                                         int* __restrict__ scratch_used) {
+    MF_PDL_ENTRY;
     __shared__ int smem[kChunk];
     __shared__ int s_d, s_base;
     if (*abort_flag) return;
@@ -1583,11 +1629,18 @@ MF_DEV uint32_t tri_hash(int a, int b, int c) {
 // Base slot = min vertex * (slots per output vertex) + a small hash of the
 // other two: facets sharing their lowest vertex land in one short run of the
 // table, and consecutive facets (spatially coherent) probe neighbouring lines.
+// PACKED (output vertex ids < 2^21): the sorted triple is the 64-bit table key
+// itself -- CAS on the key, atomicMin on the parallel id word, no fences.
+// Otherwise the key is the facet id and the triple lives in `canon` (a fence
+// orders its store before the publishing CAS).
+constexpr unsigned long long kEmptyKey = ~0ull;
+template <bool PACKED>
 __global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict__ abort_flag,
                               const int* __restrict__ F, const int* __restrict__ rstep, const int* __restrict__ vmesh,
                               const int* __restrict__ act, int* __restrict__ mapped, int4* __restrict__ canon,
                               int* __restrict__ slot, unsigned char* __restrict__ has_live, int* __restrict__ table,
-                              unsigned tmask, unsigned per_vertex) {
+                              unsigned long long* __restrict__ tkey, unsigned tmask, unsigned per_vertex) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
     const int M = *dM;
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
@@ -1608,22 +1661,38 @@ __global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict_
         has_live[ib] = 1;
         has_live[ic] = 1;
         int lo = min(a, min(b, c)), hi = max(a, max(b, c)), mid = a + b + c - lo - hi;
-        canon[f] = make_int4(lo, mid, hi, 0);
-        __threadfence();
         unsigned h = ((unsigned)lo * per_vertex + (tri_hash(lo, mid, hi) & 7u)) & tmask;
-        while (true) {
-            int cur = __ldcg(table + h);
-            if (cur < 0) {
-                int prev = atomicCAS(table + h, -1, f);
-                if (prev < 0) break;
-                cur = prev;
+        if (PACKED) {
+            const unsigned long long key = ((unsigned long long)lo << 42) | ((unsigned long long)mid << 21) | hi;
+            while (true) {
+                unsigned long long cur = __ldcg(tkey + h);
+                if (cur == kEmptyKey) {
+                    cur = atomicCAS(tkey + h, kEmptyKey, key);
+                    if (cur == kEmptyKey) cur = key;
+                }
+                if (cur == key) {
+                    atomicMin(table + h, f);
+                    break;
+                }
+                h = (h + 1) & tmask;
             }
-            int4 oc = __ldcg(canon + cur);
-            if (oc.x == lo && oc.y == mid && oc.z == hi) {
-                atomicMin(table + h, f);
-                break;
+        } else {
+            canon[f] = make_int4(lo, mid, hi, 0);
+            __threadfence();
+            while (true) {
+                int cur = __ldcg(table + h);
+                if (cur < 0) {
+                    int prev = atomicCAS(table + h, -1, f);
+                    if (prev < 0) break;
+                    cur = prev;
+                }
+                int4 oc = __ldcg(canon + cur);
+                if (oc.x == lo && oc.y == mid && oc.z == hi) {
+                    atomicMin(table + h, f);
+                    break;
+                }
+                h = (h + 1) & tmask;
             }
-            h = (h + 1) & tmask;
         }
         slot[f] = (int)h;
     }
@@ -1631,6 +1700,7 @@ __global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict_
 
 
 __global__ void k_identity_index(int n, int* __restrict__ a, int* __restrict__ b) {
+    MF_PDL_ENTRY;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = b[i] = i;
 }
 
@@ -1641,11 +1711,29 @@ __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int*
                           const int* __restrict__ inc_off, const unsigned char* __restrict__ has_live,
                           const int* __restrict__ vmesh, const int* __restrict__ act, int* __restrict__ rt,
                           int* __restrict__ mt, int first_round, int B, const int* __restrict__ kout,
-                          const int* __restrict__ foff_in, int* __restrict__ foff_out) {
+                          const int* __restrict__ foff_in, int* __restrict__ foff_out, int* __restrict__ foff_fin,
+                          int* __restrict__ stats, const int* __restrict__ n_edges, const int* __restrict__ ld_rounds,
+                          int* __restrict__ deg, int* __restrict__ cursor, int n1_next, int* __restrict__ counters) {
+    MF_PDL_ENTRY;
     if (*abort_flag) return;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     // per-mesh output facet offsets = keep-scan prefix at each mesh's first input facet
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= B; b += gridDim.x * blockDim.x)
+    for (int b = tid; b <= B; b += nth) {
         foff_out[b] = kout[foff_in[b]];
+        if (foff_fin) foff_fin[b] = kout[foff_in[b]];
+    }
+    if (tid == 0) {  // per-round counts for the host (one readback at the end)
+        stats[0] = foff_in[B];
+        stats[1] = *n_edges;
+        stats[2] = kout[foff_in[B]];
+        stats[3] = *ld_rounds;
+    }
+    // clear the next round's degree / cursor arrays and counters
+    for (int i = tid; i < n1_next; i += nth) {
+        deg[i] = 0;
+        cursor[i] = 0;
+    }
+    for (int i = tid; i < 64; i += nth) counters[i] = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N0; i += gridDim.x * blockDim.x) {
         int r = first_round ? i : rt[i];
         rt[i] = rstep[r];
@@ -1661,10 +1749,37 @@ __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int*
 }
 
 // ------------------------------------------------------------------------
+// One kernel instead of a run of memset / memcpy nodes at the start of the
+// graph (keeps the whole round chain a sequence of kernel nodes, so every
+// edge can be a programmatic-dependent-launch edge).
+__global__ void k_graph_init(int* __restrict__ status, int status_words, int fail_lo, int fail_hi,
+                             int* __restrict__ foff_a, const int* __restrict__ foff0, int B, int* __restrict__ deg,
+                             int* __restrict__ cursor, int n1, int* __restrict__ counters,
+                             unsigned long long* __restrict__ scan_a, unsigned long long* __restrict__ scan_b,
+                             int scan_words, int* __restrict__ ghist, int nghist) {
+    MF_PDL_ENTRY;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int i = tid; i < status_words; i += nth)
+        status[i] = (i == 1) ? 0x7f7f7f7f : ((i >= fail_lo && i < fail_hi) ? -1 : 0);
+    for (int b = tid; b <= B; b += nth) foff_a[b] = foff0[b];
+    for (int i = tid; i < n1; i += nth) {
+        deg[i] = 0;
+        cursor[i] = 0;
+    }
+    for (int i = tid; i < 64; i += nth) counters[i] = 0;
+    for (int i = tid; i < scan_words; i += nth) {
+        scan_a[i] = 0ull;
+        scan_b[i] = 0ull;
+    }
+    for (int i = tid; i < nghist; i += nth) ghist[i] = 0;
+}
+
+// ------------------------------------------------------------------------
 // boundary conversion / validation
 __global__ void k_facets_in(int64_t M, const int64_t* __restrict__ F64, int* __restrict__ F32, int B,
                             const int64_t* __restrict__ voff, const int64_t* __restrict__ foff,
                             int* __restrict__ bad) {
+    MF_PDL_ENTRY;
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < M; f += (int64_t)gridDim.x * blockDim.x) {
         int lo = 0, hi = B;
         while (hi - lo > 1) {
@@ -1681,18 +1796,22 @@ __global__ void k_facets_in(int64_t M, const int64_t* __restrict__ F64, int* __r
     }
 }
 __global__ void k_check_finite(int64_t n, const double* __restrict__ P, int* __restrict__ bad) {
+    MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (!isfinite(P[i])) atomicExch(bad, 1);
 }
 __global__ void k_f32_to_f64(int64_t n, const float* __restrict__ a, double* __restrict__ b) {
+    MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = (double)a[i];
 }
 __global__ void k_i32_to_i64(int64_t n, const int* __restrict__ a, int64_t* __restrict__ b, int64_t add) {
+    MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = (int64_t)a[i] + add;
 }
 __global__ void k_f64_to_f32(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+    MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = (float)a[i];
 }

@@ -25,6 +25,7 @@ static int grid_of(const Context* ctx, int64_t n, int block = 256) {
 
 __global__ void k_replace_in(int64_t n, const int64_t* __restrict__ r64, int64_t n_out, int* __restrict__ r32,
                              int* __restrict__ count, int* __restrict__ bad) {
+    MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = r64[i];
         if (r < 0 || r >= n_out) {
@@ -37,10 +38,12 @@ __global__ void k_replace_in(int64_t n, const int64_t* __restrict__ r64, int64_t
     }
 }
 __global__ void k_count_keys(int64_t n, const int* __restrict__ key, int* __restrict__ count) {
+    MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(count + key[i], 1);
 }
 __global__ void k_check_cover(int64_t n_out, const int* __restrict__ count, int* __restrict__ empty) {
+    MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_out; i += (int64_t)gridDim.x * blockDim.x)
         if (count[i] == 0) atomicExch(empty, 1);
 }
@@ -101,6 +104,7 @@ template <typename T>
 __global__ void k_pool(int64_t n_out, int C, const int* __restrict__ off, const int* __restrict__ members,
                        const T* __restrict__ X, const T* __restrict__ w, int mode, T* __restrict__ out,
                        int* __restrict__ zero_weight) {
+    MF_PDL_ENTRY;
     const int64_t total = n_out * (int64_t)C;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -140,6 +144,7 @@ template <typename TG, typename TF, typename TO>
 __global__ void k_pool_bwd_gather(int64_t n, int C, const int* __restrict__ rep, const int* __restrict__ off,
                                   const int* __restrict__ members, const TG* __restrict__ g,
                                   const TF* __restrict__ w, int mode, TO* __restrict__ out) {
+    MF_PDL_ENTRY;
     const int64_t total = n * (int64_t)C;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -166,6 +171,7 @@ template <typename TG, typename TF>
 __global__ void k_pool_bwd_max(int64_t n_out, int C, const int* __restrict__ off, const int* __restrict__ members,
                                const TF* __restrict__ X, const TG* __restrict__ g, TF* __restrict__ out,
                                int* __restrict__ no_winner) {
+    MF_PDL_ENTRY;
     const int64_t total = n_out * (int64_t)C;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -192,6 +198,7 @@ __global__ void k_pool_bwd_max(int64_t n_out, int C, const int* __restrict__ off
 
 __global__ void k_unpool_vec(int64_t n, int64_t row16, const int* __restrict__ rep, const int4* __restrict__ coarse,
                              int4* __restrict__ out) {
+    MF_PDL_ENTRY;
     const int64_t total = n * row16;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -202,6 +209,7 @@ __global__ void k_unpool_vec(int64_t n, int64_t row16, const int* __restrict__ r
 template <typename T>
 __global__ void k_unpool(int64_t n, int C, const int* __restrict__ rep, const T* __restrict__ coarse,
                          T* __restrict__ out) {
+    MF_PDL_ENTRY;
     const int64_t total = n * (int64_t)C;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -216,7 +224,7 @@ static void scan_into(const Context* ctx, unsigned long long* status, const int*
     int tiles = std::max(1, (n + kScanTile - 1) / kScanTile);
     cudaMemsetAsync(status, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), s);
     LAUNCH(k_scan_excl<LoadArr>, tiles, kScanBlock, 0, s, LoadArr{in}, n, out, status,
-           reinterpret_cast<int*>(status + tiles), nullptr);
+           reinterpret_cast<int*>(status + tiles), (const int*)nullptr, EpiNone(), (unsigned long long*)nullptr, 0);
     (void)ctx;
 }
 
