@@ -297,9 +297,10 @@ MF_DEV void reg_sort(int (&a)[L]) {
 
 // K3 thread tier (deg <= 8): one thread per vertex, incidences and the 16
 // neighbour candidates sorted by register networks, every plane / facet gather
-// issued before the ordered fold.  Degree 9..16 goes to the 16-lane group
+// issued before the ordered fold.  Degree 9..32 goes to the warp-per-vertex
 // kernel (list `mid`), larger to the block tier (list `heavy`).
 constexpr int kThreadDeg = 8;
+constexpr int kMid = 32;
 __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ inc,
                                                   const int* __restrict__ F, const Plane* __restrict__ plane,
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         const int s = inc_off[v], d = inc_off[v + 1] - s;
         if (d > kThreadDeg) {
-            if (d <= kGrp) mid[append_slot(mid_count)] = v;
+            if (d <= kMid) mid[append_slot(mid_count)] = v;
             else heavy[append_slot(heavy_count)] = v;
             continue;
         }
@@ -353,31 +354,36 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
     }
 }
 
-__global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __restrict__ abort_flag,
-                                                                 const int* __restrict__ list,
-                                                                 const int* __restrict__ list_count,
-                                                                 const int* __restrict__ inc_off,
-                                                                 const int* __restrict__ inc,
-                                                                 const int* __restrict__ F,
-                                                                 const Plane* __restrict__ plane, int Mcap,
-                                                                 double* __restrict__ vq, int* __restrict__ nbr,
-                                                                 int* __restrict__ ucnt, int* __restrict__ upcnt,
-                                                                 int* __restrict__ heavy,
-                                                                 int* __restrict__ heavy_count) {
+// Mid tier (degree 9..32): one full warp per vertex, one incidence per lane.
+__global__ void __launch_bounds__(256) k_vertex(const int* __restrict__ abort_flag, const int* __restrict__ list,
+                                                const int* __restrict__ list_count, const int* __restrict__ inc_off,
+                                                const int* __restrict__ inc, const int* __restrict__ F,
+                                                const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
+                                                int* __restrict__ nbr, int* __restrict__ ucnt,
+                                                int* __restrict__ upcnt, int* __restrict__ heavy,
+                                                int* __restrict__ heavy_count) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    __shared__ double s_q[2 * kGrpWarps][kGrp][10];
-    __shared__ int s_c[2 * kGrpWarps][2 * kGrp];
-    const int g = threadIdx.x >> 4;  // group within block
-    const int l = threadIdx.x & 15;
-    const unsigned mask = grp_mask();
-    const int groups = gridDim.x * (blockDim.x >> 4);
+    __shared__ double s_q[8][kMid][10];
+    __shared__ int s_c[8][2 * kMid];
+    const int g = threadIdx.x >> 5;  // warp within block
+    const int l = threadIdx.x & 31;
+    const unsigned mask = 0xffffffffu;
+    const int groups = gridDim.x * (blockDim.x >> 5);
     const int N = *list_count;
-    for (int vi = blockIdx.x * (blockDim.x >> 4) + g; vi < N; vi += groups) {
+    for (int vi = blockIdx.x * (blockDim.x >> 5) + g; vi < N; vi += groups) {
         const int v = list[vi];
         const int s = inc_off[v], d = inc_off[v + 1] - s;
         int k = (l < d) ? inc[s + l] : 0x7fffffff;
-        k = grp_bitonic16(k, mask);
+#pragma unroll
+        for (int kk = 2; kk <= kMid; kk <<= 1) {
+#pragma unroll
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                int y = __shfl_xor_sync(mask, k, j);
+                bool up = ((l & kk) == 0), lower = ((l & j) == 0);
+                k = (lower == up) ? min(k, y) : max(k, y);
+            }
+        }
         int a = 0x7fffffff, b = 0x7fffffff;
         if (l < d) {
             int corner, f;
@@ -398,9 +404,9 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __re
             for (int i = 0; i < d; i++) acc = acc + s_q[g][i][l];
             vq[10 * (size_t)v + l] = acc;
         }
-        // bitonic sort of the 32 candidates (16 lanes, one compare-exchange each per stage)
+        // bitonic sort of the 64 candidates (32 lanes, one compare-exchange each per stage)
         int* c = s_c[g];
-        for (int kk = 2; kk <= 32; kk <<= 1) {
+        for (int kk = 2; kk <= 2 * kMid; kk <<= 1) {
             for (int j = kk >> 1; j > 0; j >>= 1) {
                 int i = ((l & ~(j - 1)) << 1) | (l & (j - 1));  // l-th pair (i, i + j)
                 int x = c[i], y = c[i + j];
@@ -416,8 +422,6 @@ __global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_vertex(const int* __re
         bool k1 = (2 * l + 1 < 2 * d) && x1 != x0;
         unsigned b0 = __ballot_sync(mask, k0), b1 = __ballot_sync(mask, k1);
         unsigned u0 = __ballot_sync(mask, k0 && x0 > v), u1 = __ballot_sync(mask, k1 && x1 > v);
-        const unsigned sh = threadIdx.x & 16;
-        b0 >>= sh; b1 >>= sh; u0 >>= sh; u1 >>= sh;
         unsigned below = (1u << l) - 1u;
         int pos = __popc(b0 & below) + __popc(b1 & below);
         int* out = nbr + 2 * (size_t)s;
