@@ -160,7 +160,11 @@ def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
         "k_facet_plane": 12 * M + 24 * N + 32 * M + 4 * N,
         "k_inc_scatter": 12 * M + 4 * N + 12 * M,
         "k_vertex": 4 * N + 12 * M + 32 * M + 12 * M + 80 * N + 8 * E + 8 * N,
-        "k_edges": 8 * E + 16 * N + 80 * N + 24 * N + 8 * E + 8 * E + 8 * E + 8 * E + 12 * N,
+        # per-vertex counts/offsets + quadric + position in, upper neighbours in, edge (e0, e1, key)
+        # out, both adjacency slots (neighbour, edge id, key) out, per-vertex matching state init
+        "k_edges": 16 * N + 80 * N + 24 * N + 4 * E + 16 * E + 32 * E + 24 * N,
+        # slots (neighbour, edge id, key) in, rank-ordered (neighbour, edge id, key prefix) out, cursor
+        "k_adj_rank": 12 * N + 32 * E + 24 * E,
         # adjacency (nbr + edge id) + rank key per slot, suitor word per vertex
         "k_suitor": 8 * E + 8 * E + 16 * E + 8 * N,
         "k_select": 16 * Nn,
@@ -168,7 +172,6 @@ def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
         # must read every incidence at least once; all LD-round launches of the round share it
         "k_ld_pick": 24 * E + 12 * N,
         "k_vertex_t": 4 * N + 12 * M + 32 * M + 12 * M + 80 * N + 8 * E + 8 * N,
-        "k_adj_keys": 16 * E + 8 * E,
         "k_contract": 4 * N + 4 * Nn + 24 * N + 24 * Nn,
         "k_facet_remap": 12 * M + 4 * N + 12 * M + 16 * M + 4 * M + N,
         "k_inc_scatter": 12 * M + 4 * N + 12 * M,
@@ -489,7 +492,7 @@ def run_ours(args):
         "roofline": roof,
         "cpu_baseline": cpu,
         "kernels": {k: {"ms": round(v[0], 4), "share": round(v[0] / total_ms, 4), "launches": v[1]}
-                    for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:10]},
+                    for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:16]},
         "round_stats": rounds,
     }
     if vs is not None:

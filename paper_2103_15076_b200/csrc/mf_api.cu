@@ -92,6 +92,7 @@ int mf_context_create(int device, mf_context** out) {
     }
     c->c.sm_count = prop.multiProcessorCount;
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmem);
+    cudaFuncSetAttribute(k_select_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem);
     // keep freed stream-ordered allocations cached in the device pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

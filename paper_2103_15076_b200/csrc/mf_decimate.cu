@@ -137,6 +137,31 @@ static cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
     } while (0)
 #endif
 
+// Suitor variant per round size: 8 lanes per proposer below 2^18 vertices (more warps to hide
+// the slot scans: cfg2 78 vs 119 us), one thread per proposer above (one wave of proposers:
+// cfg4 136 vs 218 us, cfg3 326 vs 369 us).  MF_SUITOR=1 / 8 forces one (A/B runs).
+static int suitor_lanes(int N) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SUITOR");
+        v = (e && e[0] == '1') ? 1 : ((e && e[0] == '8') ? 8 : 0);
+    }
+    if (v) return v;
+    return N >= (1 << 18) ? 1 : 8;
+}
+
+// MF_SELECT_CL=1: 8-CTA cluster selection (DSMEM histogram merge) for mid-size meshes.  Measured
+// no faster than the single CTA at cfg2 (75 vs 75 us) and slower at cfg1 (95 vs 53 us): the pass
+// count, not the per-pass bandwidth, bounds these sizes -- so it is opt-in.
+static bool select_cluster() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SELECT_CL");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static int grid_for(const Context* ctx, int64_t n, int block = 256) {
     int64_t g = (n + block - 1) / block;
     int64_t cap = (int64_t)ctx->sm_count * 16;
@@ -224,7 +249,7 @@ static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan
         return st->code;
     }
     p.placement = cfg->placement;
-    if (p.n < 0 || p.m < 0 || p.n >= (int64_t)INT32_MAX - 1 || 3 * p.m >= (int64_t)INT32_MAX - 1) {
+    if (p.n < 0 || p.m < 0 || p.n >= (int64_t)INT32_MAX - 1 || 6 * p.m >= (int64_t)INT32_MAX - 1) {  // edge ids: adjacency slots < 6m
         st->code = MF_ERR_LIMIT;
         snprintf(st->message, sizeof(st->message), "mesh too large for 32-bit device indices (n=%lld, m=%lld)",
                  (long long)p.n, (long long)p.m);
@@ -341,12 +366,16 @@ struct WS {
     int *deg, *inc_off, *cursor, *inc, *inc_tmp;
     double* vq;
     unsigned* adj_k32;
+    int* acur;
+    int* snbr;  // adjacency slots, rank order after k_adj_rank (nbr keeps neighbour order)
+    uint64_t* skey;
+    int* lowfill;
     unsigned long long* suitor;
     int *bestu, *front0, *front1, *ldc;
     unsigned* bar;
     int* selstate;
     int* ghist;
-    int *nbr, *nbr_tmp, *adj_eid, *ucnt, *upcnt, *eoff, *heavy, *mid, *counters, *e0, *e1;
+    int *nbr, *nbr_tmp, *adj_eid, *ucnt, *upcnt, *eoff, *aoff, *heavy, *mid, *counters, *e0, *e1;
     double* cost;
     uint64_t *key_hi, *key_lo;
     unsigned long long *mlo, *mhi;
@@ -404,6 +433,10 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.nbr_tmp = A.take<int>((size_t)2 * Ecap);
     W.adj_eid = A.take<int>((size_t)2 * Ecap);
     W.adj_k32 = A.take<unsigned>((size_t)2 * Ecap);
+    W.acur = A.take<int>((size_t)N0);
+    W.snbr = A.take<int>((size_t)2 * Ecap);
+    W.skey = p.seeded ? nullptr : A.take<uint64_t>((size_t)2 * Ecap);
+    W.lowfill = A.take<int>((size_t)N0 + 1);
     W.suitor = A.take<unsigned long long>((size_t)N0);
     W.bestu = A.take<int>((size_t)N0);
     W.front0 = A.take<int>((size_t)N0);
@@ -411,17 +444,19 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.ldc = A.take<int>(8);
     W.bar = A.take<unsigned>(8);
     W.selstate = A.take<int>((size_t)2 * B);
-    W.ghist = A.take<int>(kSelBins);
+    W.ghist = A.take<int>(kSelScratch);
     W.ucnt = A.take<int>((size_t)N0);
     W.upcnt = A.take<int>((size_t)N0);
     W.eoff = A.take<int>((size_t)N0 + 1);
+    W.aoff = A.take<int>((size_t)N0 + 1);
     W.heavy = A.take<int>((size_t)N0);
     W.mid = A.take<int>((size_t)N0);
     W.counters = A.take<int>(64);
-    W.e0 = A.take<int>((size_t)Ecap);
-    W.e1 = A.take<int>((size_t)Ecap);
+    // unseeded edge ids are adjacency slot indices (sparse in [0, 2E)), seeded ones dense
+    W.e0 = A.take<int>((size_t)2 * Ecap);
+    W.e1 = A.take<int>((size_t)2 * Ecap);
     W.cost = A.take<double>((size_t)Ecap);
-    W.key_hi = A.take<uint64_t>((size_t)Ecap);
+    W.key_hi = A.take<uint64_t>((size_t)2 * Ecap);
     W.key_lo = p.seeded ? A.take<uint64_t>((size_t)Ecap) : nullptr;
     W.mlo = A.take<unsigned long long>((size_t)B);
     W.mhi = A.take<unsigned long long>((size_t)B);
@@ -488,8 +523,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     g_pdl = true;
     LAUNCH(k_graph_init, grid_for(ctx, std::max<int64_t>({(int64_t)N0 + 1, (int64_t)W.scan.words, (int64_t)W.status_words})),
            256, 0, stream, W.status, (int)W.status_words, (int)(d_fail - W.status), (int)(d_fail - W.status) + 3 * B,
-           W.foff_a, d_foff0, B, W.deg, W.cursor, N0 + 1, W.counters, W.scan.buf[0], W.scan.buf[1], W.scan.words,
-           W.ghist, kSelBins);
+           W.foff_a, d_foff0, B, W.deg, W.cursor, W.lowfill, N0 + 1, W.counters, W.scan.buf[0], W.scan.buf[1], W.scan.words,
+           W.ghist, kSelScratch);
     if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, W.F0, B, W.vo64, W.fo64, d_badf);
     if (n > 0) LAUNCH(k_check_finite, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, W.P0, d_badp);
     if (W.Xf32 && n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, W.X0);
@@ -534,41 +569,52 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
                W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
         // lexicographic edges + pair costs + rank keys
-        run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
-        if (p.placement)
-            LAUNCH(k_edges<1>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt,
-                   W.upcnt, W.eoff, W.vq, Pc, W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed,
-                   W.abshead, order, B, W.mlo, W.mhi);
-        else
-            LAUNCH(k_edges<0>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt,
-                   W.upcnt, W.eoff, W.vq, Pc, W.e0, W.e1, W.cost, W.key_hi, W.adj_eid, W.mate, W.minrep, W.absorbed,
-                   W.abshead, order, B, W.mlo, W.mhi);
+        // compact adjacency offsets (2 slots per edge); seeded rounds also need the dense
+        // lexicographic edge index (the PCG64 key-stream position, decimate.py:190)
+        run_scan(W.scan, LoadArr{W.ucnt}, W.aoff, N, stream, "k_scan<adj>", d_abort);
+        if (seeded) run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
+        {
+            EdgeOut eo{W.e0,     W.e1,     seeded ? W.cost : nullptr, W.key_hi, W.snbr,   W.adj_eid, W.skey,
+                       W.lowfill, W.mate,  W.minrep, W.absorbed, W.abshead, W.suitor, W.mlo, W.mhi,
+                       W.segA,   W.ldc};
+            const int eg = grid_for(ctx, (int64_t)N * kEdgeLanes);
+            if (p.placement)
+                LAUNCH(k_edges<1>, eg, 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.aoff, W.eoff, W.vq,
+                       Pc, eo, order, B);
+            else
+                LAUNCH(k_edges<0>, eg, 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.aoff, W.eoff, W.vq,
+                       Pc, eo, order, B);
+        }
         const int* dE = W.eoff + N;
         if (seeded) {
             LAUNCH(k_cost_minmax, grid_for(ctx, Ecap), 256, 0, stream, d_abort, dE, W.cost, W.e0, vmesh, W.mlo, W.mhi);
             LAUNCH(k_seed_keys, grid_for(ctx, (Ecap + kSeedRun - 1) / kSeedRun), 256, 0, stream, d_abort, dE, W.cost, W.e0,
                    vmesh, W.eoff, voff_r, W.mlo, W.mhi, p.pcg[0], p.pcg[1], p.pcg[2], p.pcg[3], W.key_hi, W.key_lo);
         }
-        // greedy matching (Suitor proposals) -> mutual proposals are the matched pairs
-        LAUNCH(k_adj_keys, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.adj_eid,
-               W.key_hi, W.adj_k32, B, W.segA, W.ldc, W.suitor);
+        if (seeded)
+            LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
+                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur);
+        else
+            LAUNCH(k_adj_rank<false>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
+                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur);
         // large meshes: locally-dominant rounds (persistent) first, then Suitor proposals on the
         // residual frontier; small meshes: Suitor only (the grid barriers would dominate)
         const bool use_ld = N >= p.ld_min;
         if (use_ld) {
-            LDArgs la{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
-                      W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, kLDRounds, d_abort};
+            LDArgs la{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
+                      W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, kLDRounds, d_abort, W.acur};
             LAUNCH(k_ld_init, grid_for(ctx, N), 256, 0, stream, la);
             for (int round = 0; round < kLDRounds; round++) {
-                LAUNCH(k_ld_pick, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, la, round);
+                LAUNCH(k_ld_pick, grid_for(ctx, N), 256, 0, stream, la, round);
                 LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, round);
             }
         }
         {
-            MatchArgs ma{N, W.inc_off, W.ucnt, W.nbr, W.adj_eid, W.adj_k32, W.e0, W.e1, W.key_hi,
+            MatchArgs ma{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.e0, W.e1, W.key_hi,
                          seeded ? W.key_lo : nullptr, W.suitor, d_abort, use_ld ? W.mate : nullptr,
-                         use_ld ? W.front0 : nullptr, W.front1, W.ldc};
-            LAUNCH(k_suitor, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, ma);
+                         use_ld ? W.front0 : nullptr, W.front1, W.ldc, W.acur};
+            if (suitor_lanes(N) == 8) LAUNCH(k_suitor, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, ma);
+            else LAUNCH(k_suitor1, grid_for(ctx, N), 256, 0, stream, ma);
         }
         LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, W.key_hi,
                seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay);
@@ -576,28 +622,30 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const bool big = (B == 1 && N >= (1 << 18));  // below: one CTA (latency-bound sizes)
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
-                          d_abort, W.selstate, W.selstate + B, 0};
+                          d_abort, W.selstate, W.selstate + B, 0, W.ghist};
             if (big) {
-                for (int pass = 0; pass < 2; pass++) {
+                for (int pass = 0; pass < kSelPasses; pass++) {
                     LAUNCH(k_sel_hist, std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2), 512, 0, stream, sa,
                            W.ghist, pass);
                     LAUNCH(k_sel_decide, 1, kSelThreads, 0, stream, sa, W.ghist, pass);
                 }
                 sa.resume = 1;
             }
-            LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelSmem, stream, sa);
+            if (B == 1 && !big && select_cluster()) LAUNCH(k_select_cl, kClCTAs, kClThreads, kClSmem, stream, sa);
+            else LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelSmem, stream, sa);
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
         select(W.segA, nullptr);
         LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, voff_r, W.segA, W.chi, W.clo,
                W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB);
         // absorb leftovers (one pass is exact: the matching is maximal when the budget is unmet)
-        LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.inc_off, W.ucnt, W.nbr, W.adj_eid,
-               W.cost, W.mate, W.e0, vmesh, voff_r, act, budget, W.removed, W.segB, W.chi, W.clo, W.caux);
+        LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
+               seeded ? W.cost : nullptr, W.key_hi, W.mate, W.e0, vmesh, voff_r, act, budget, W.removed, W.segB,
+               W.chi, W.clo, W.caux);
         select(W.segB, W.removed);
         RoundFail rf{d_abort, d_fail, d_fail + B, d_fail + 2 * B};
         LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, voff_r, W.segB, W.chi, W.clo, W.caux,
-               W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.eoff, rf, r);
+               W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.aoff, rf, r);
         // relabel: output index = rank of the cluster's lowest member
         run_scan(W.scan, LoadIsRep{W.mate, W.e0, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
         const bool packed = Nn < (1 << 21);
@@ -628,7 +676,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                  EpiFacetWrite{W.mapped, Fn});
         LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
                W.rt, W.mt, r == 0, B, W.kout, foff_c, foff_n, last ? d_foff_fin : nullptr, d_stats + 4 * r,
-               W.eoff + N, W.ldc + 2, W.deg, W.cursor, last ? 0 : Nn + 1, W.counters);
+               W.aoff + N, W.ldc + 2, W.deg, W.cursor, W.lowfill, last ? 0 : Nn + 1, W.counters);
         Pc = Pn;
         Xc = Xn;
         Fc = Fn;

@@ -20,6 +20,9 @@
 // topology parity.
 #pragma once
 
+#include <cooperative_groups.h>
+#include <type_traits>
+
 #include "mf_common.cuh"
 #include "mf_inverse.cuh"
 
@@ -435,76 +438,194 @@ __global__ void __launch_bounds__(256) k_vertex(const int* __restrict__ abort_fl
     }
 }
 
-// K4: lexicographic edge list + pair cost + rank key + adjacency edge ids.
+// K4: lexicographic edge list + pair cost + rank key + adjacency slots.
 // Edge id of (v, u>v) = eoff[v] + rank of u among v's upper neighbours, which
-// is exactly np.unique(axis=0)'s lexicographic order (mesh.py:131-134).
-// One lane per neighbour of v.  Lower-indexed neighbours
-// resolve their edge id by binary search in the neighbour's upper list.
+// is exactly np.unique(axis=0)'s lexicographic order (mesh.py:131-134).  Only
+// the upper end evaluates an edge (4 lanes per vertex, one upper neighbour
+// per lane): it stores the edge (e0, e1, key or cost), fills its own slot and
+// appends the edge into a free lower slot of the other end (one atomic per
+// edge on that vertex's fill counter) -- slot order inside a vertex is free,
+// k_adj_rank orders every vertex's slots by rank afterwards, so no lane ever
+// searches another vertex's list.
+MF_DEV void sort8_by_key(uint64_t& h, uint64_t& lo, int& u, int& e, unsigned mask) {
+    const int l = threadIdx.x & 7;
+#pragma unroll
+    for (int k = 2; k <= 8; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t ph = __shfl_xor_sync(mask, h, j, 8), pl = __shfl_xor_sync(mask, lo, j, 8);
+            const int pu = __shfl_xor_sync(mask, u, j, 8), pe = __shfl_xor_sync(mask, e, j, 8);
+            const bool want_min = (((l & k) == 0) == ((l & j) == 0));
+            const bool take = want_min ? key_lt(ph, pl, h, lo) : key_lt(h, lo, ph, pl);
+            if (take) { h = ph; lo = pl; u = pu; e = pe; }
+        }
+    }
+}
+
+struct EdgeOut {
+    int* e0;
+    int* e1;
+    double* cost;        // seeded rounds only (else nullptr)
+    uint64_t* key_hi;    // unseeded: f64_key(cost)
+    int* snbr;           // adjacency slots: neighbour, edge id, rank key (unseeded)
+    int* seid;
+    uint64_t* skey;
+    int* lowfill;        // per vertex: lower slots filled so far (zeroed by k_vertex_t)
+    int* mate;
+    int* minrep;
+    int* absorbed;
+    int* abshead;
+    unsigned long long* suitor;
+    unsigned long long* mlo;
+    unsigned long long* mhi;
+    int* seg_cnt;
+    int* ldc;
+};
+
+constexpr int kEdgeLanes = 4;
 template <int PLACEMENT>
-__global__ void __launch_bounds__(kGrp * 2 * kGrpWarps) k_edges(const int* __restrict__ abort_flag, int N,
-                                                                const int* __restrict__ inc_off,
-                                                                const int* __restrict__ nbr,
-                                                                const int* __restrict__ ucnt,
-                                                                const int* __restrict__ upcnt,
-                                                                const int* __restrict__ eoff,
-                                                                const double* __restrict__ vq,
-                                                                const double* __restrict__ P, int* __restrict__ e0,
-                                                                int* __restrict__ e1, double* __restrict__ cost,
-                                                                uint64_t* __restrict__ key_hi,
-                                                                int* __restrict__ adj_eid,
-                                                                int* __restrict__ mate,
-                                                                int* __restrict__ minrep, int* __restrict__ absorbed,
-                                                                int* __restrict__ abshead, int order, int B,
-                                                                unsigned long long* __restrict__ mlo,
-                                                                unsigned long long* __restrict__ mhi) {
+__global__ void __launch_bounds__(256) k_edges(const int* __restrict__ abort_flag, int N,
+                                               const int* __restrict__ inc_off, const int* __restrict__ nbr,
+                                               const int* __restrict__ ucnt, const int* __restrict__ upcnt,
+                                               const int* __restrict__ aoff, const int* __restrict__ eoff,
+                                               const double* __restrict__ vq, const double* __restrict__ P, EdgeOut o,
+                                               int order, int B) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
+    const bool seeded = o.cost != nullptr;
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
-        mlo[b] = ~0ull;
-        mhi[b] = 0ull;
+        o.mlo[b] = ~0ull;
+        o.mhi[b] = 0ull;
+        o.seg_cnt[b] = 0;  // truncation-candidate segments (k_mates appends)
     }
-    const int g = threadIdx.x >> 3;  // 8 lanes per vertex (typical degree ~6)
-    const int l = threadIdx.x & 7;
-    const int groups = gridDim.x * (blockDim.x >> 3);
-    for (int v = blockIdx.x * (blockDim.x >> 3) + g; v < N; v += groups) {
+    if (blockIdx.x == 0 && threadIdx.x < 8) o.ldc[threadIdx.x] = 0;  // LD round counters
+    const int l = threadIdx.x % kEdgeLanes;
+    const int groups = gridDim.x * (blockDim.x / kEdgeLanes);
+    for (int v = blockIdx.x * (blockDim.x / kEdgeLanes) + threadIdx.x / kEdgeLanes; v < N; v += groups) {
         if (l == 0) {
-            mate[v] = -1;
-            minrep[v] = v;
-            absorbed[v] = -1;
-            abshead[v] = -1;
+            o.mate[v] = -1;
+            o.minrep[v] = v;
+            o.absorbed[v] = -1;
+            o.abshead[v] = -1;
+            o.suitor[v] = ~0ull;
         }
-        const int nu = ucnt[v];
-        if (nu == 0) continue;
-        const size_t s2 = 2 * (size_t)inc_off[v];
-        const int nlow = nu - upcnt[v];
-        const int eb = eoff[v];
+        const int nu = ucnt[v], nup = upcnt[v];
+        if (l >= nup) continue;
+        const size_t sn = 2 * (size_t)inc_off[v];  // neighbour list (k_vertex layout)
+        const size_t s2 = (size_t)aoff[v];          // compact adjacency slots
+        const int nlow = nu - nup;
+        // unseeded: edge id = slot index of the upper end (aoff[v] + j), which orders edges
+        // lexicographically like the dense index; seeded: the dense index (PCG stream position)
+        const int eb = seeded ? eoff[v] : aoff[v] + nlow;
         Q10 qv;
         q_load(vq, v, qv);
         const double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
-        for (int j = l; j < nu; j += 8) {
-            int u = nbr[s2 + j];
-            int eid;
-            if (u > v) {
-                eid = eb + (j - nlow);
-                Q10 qu;
-                q_load(vq, u, qu);
-                double c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
-                e0[eid] = v;
-                e1[eid] = u;
-                cost[eid] = c;
-                key_hi[eid] = f64_key(c);
-            } else {
-                size_t su = 2 * (size_t)inc_off[u];
-                int nuu = ucnt[u];
-                int lo = nuu - upcnt[u], hi = nuu;
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (nbr[su + mid] < v) lo = mid + 1; else hi = mid;
-                }
-                eid = eoff[u] + (lo - (nuu - upcnt[u]));
+        for (int k = l; k < nup; k += kEdgeLanes) {
+            const int j = nlow + k;
+            const int u = nbr[sn + j];
+            const int eid = eb + k;
+            Q10 qu;
+            q_load(vq, u, qu);
+            const double c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
+            o.e0[eid] = v;
+            o.e1[eid] = u;
+            // unseeded: the rank key IS the order-preserving cost (f64_key is invertible, so no
+            // cost array); seeded: the cost feeds the bucket keys (k_seed_keys)
+            const uint64_t key = f64_key(c);
+            if (seeded) o.cost[eid] = c;
+            else o.key_hi[eid] = key;
+            const size_t su = (size_t)aoff[u] + atomicAdd(o.lowfill + u, 1);
+            o.snbr[s2 + j] = u;
+            o.seid[s2 + j] = eid;
+            o.snbr[su] = v;
+            o.seid[su] = eid;
+            if (!seeded) {
+                o.skey[s2 + j] = key;
+                o.skey[su] = key;
             }
-            adj_eid[s2 + j] = eid;
         }
+    }
+}
+
+// K4b: rank-ordered adjacency.  Every vertex of degree <= 8 has its slots
+// sorted in place by the full rank key of their edge -- one thread per vertex,
+// register bitonic network on (key_hi, key_lo | edge id) -- so the matching
+// kernels find a vertex's best live edge as the FIRST live slot from a
+// per-vertex cursor that only moves forward: a slot whose neighbour is
+// matched, or whose neighbour already holds a better proposal, stays dead.
+// Higher degrees keep their order (acur = -1) and are scanned in full.  The
+// 32-bit rank-key prefix of every slot is stored beside it (adj_k32) so the
+// scans compare prefixes and gather the full keys only on prefix ties.
+// Unseeded keys come from the slots (skey, secondary = edge id); seeded keys
+// are gathered once k_seed_keys has run.
+template <bool SEEDED>
+__global__ void __launch_bounds__(256) k_adj_rank(const int* __restrict__ abort_flag, int N,
+                                                  const int* __restrict__ aoff, const int* __restrict__ ucnt,
+                                                  int* __restrict__ snbr, int* __restrict__ seid,
+                                                  const uint64_t* __restrict__ skey,
+                                                  const uint64_t* __restrict__ key_hi,
+                                                  const uint64_t* __restrict__ key_lo, unsigned* __restrict__ adj_k32,
+                                                  int* __restrict__ acur) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    typedef typename std::conditional<SEEDED, uint64_t, unsigned>::type Lo;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        const size_t s = (size_t)aoff[v];
+        const int nu = ucnt[v];
+        if (nu > 8) {
+            for (int j = 0; j < nu; j++)
+                adj_k32[s + j] = (unsigned)((SEEDED ? key_hi[seid[s + j]] : skey[s + j]) >> 32);
+            acur[v] = -1;
+            continue;
+        }
+        uint64_t h[8];
+        Lo lo[8];
+        int u[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            h[i] = ~0ull;
+            lo[i] = (Lo)~0ull;
+            u[i] = -1;
+            if (i < nu) {
+                u[i] = snbr[s + i];
+                const int e = seid[s + i];
+                if (SEEDED) {
+                    h[i] = key_hi[e];
+                    lo[i] = (Lo)key_lo[e];
+                } else {
+                    h[i] = skey[s + i];
+                    lo[i] = (Lo)(unsigned)e;
+                }
+            }
+        }
+        // bitonic network over 8 register entries (keys are unique; padding sorts last)
+#pragma unroll
+        for (int k = 2; k <= 8; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const bool up = ((i & k) == 0);
+                        const bool gt = h[i] > h[ixj] || (h[i] == h[ixj] && lo[i] > lo[ixj]);
+                        if (gt == up) {
+                            uint64_t th = h[i]; h[i] = h[ixj]; h[ixj] = th;
+                            Lo tl = lo[i]; lo[i] = lo[ixj]; lo[ixj] = tl;
+                            int tu = u[i]; u[i] = u[ixj]; u[ixj] = tu;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (i < nu) {
+                snbr[s + i] = u[i];
+                seid[s + i] = (int)(unsigned)lo[i];  // seeded key_lo carries the edge id in its low bits
+                adj_k32[s + i] = (unsigned)(h[i] >> 32);
+            }
+        acur[v] = 0;
     }
 }
 
@@ -690,7 +811,7 @@ __global__ void k_seed_keys(const int* __restrict__ abort_flag, const int* __res
 // decimate.py:256-263 run to exhaustion -- with no grid-wide barrier.
 struct MatchArgs {
     int N;
-    const int* inc_off;
+    const int* aoff;      // compact adjacency offsets
     const int* ucnt;
     const int* nbr;
     const int* adj_eid;
@@ -705,6 +826,7 @@ struct MatchArgs {
     const int* front0;     // nullable: proposers = residual LD frontier, else all vertices
     const int* front1;
     const int* counters;
+    int* acur;             // rank-ordered adjacency cursors (k_adj_sort), -1 = unsorted vertex
 };
 
 MF_DEV void edge_key(const MatchArgs& a, int e, uint64_t& h, uint64_t& l) {
@@ -743,25 +865,59 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
         int cur = list ? __ldcg(list + ui) : ui;
         if (a.mate && __ldcg(a.mate + cur) >= 0) continue;
         while (cur >= 0) {
-            const size_t s = 2 * (size_t)a.inc_off[cur];
+            const size_t s = (size_t)a.aoff[cur];
             const int nu = a.ucnt[cur];
             int be = -1, bv = -1;
             unsigned bk = 0xffffffffu;
-            for (int j = l; j < nu; j += 8) {
-                const int e = a.adj_eid[s + j];
-                const unsigned ke = a.adj_k32[s + j];
-                if (be >= 0 && !edge_lt(a, ke, e, bk, be)) continue;
-                const int v = a.nbr[s + j];
-                if (a.mate && __ldcg(a.mate + v) >= 0) continue;
-                const unsigned long long sw = ld_volatile(a.suitor + v);
-                if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
-                bk = ke; be = e; bv = v;
-            }
+            const int c0 = a.acur[cur];
+            if (c0 >= 0) {
+                // rank-ordered adjacency: the best winnable edge is the first winnable slot.
+                // A slot is dead for good once its neighbour is LD-matched or holds a better
+                // proposal (suitor words only improve), so the cursor moves past dead slots.
+                int c = c0;
+                for (; c < nu; c += 8) {
+                    const int j = c + l;
+                    bool ok = false;
+                    unsigned ke = 0;
+                    int e = -1, v = -1;
+                    if (j < nu) {
+                        e = a.adj_eid[s + j];
+                        ke = a.adj_k32[s + j];
+                        v = a.nbr[s + j];
+                        ok = !(a.mate && __ldcg(a.mate + v) >= 0);
+                        if (ok) {
+                            const unsigned long long sw = ld_volatile(a.suitor + v);
+                            ok = sw == ~0ull || edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw);
+                        }
+                    }
+                    const unsigned bal = (__ballot_sync(mask, ok) >> (threadIdx.x & 24)) & 0xFFu;
+                    if (bal) {
+                        const int f = __ffs(bal) - 1;
+                        bk = __shfl_sync(mask, ke, f, 8);
+                        be = __shfl_sync(mask, e, f, 8);
+                        bv = __shfl_sync(mask, v, f, 8);
+                        c += f;
+                        break;
+                    }
+                }
+                if (l == 0) a.acur[cur] = c < nu ? c : nu;
+            } else {
+                for (int j = l; j < nu; j += 8) {
+                    const int e = a.adj_eid[s + j];
+                    const unsigned ke = a.adj_k32[s + j];
+                    if (be >= 0 && !edge_lt(a, ke, e, bk, be)) continue;
+                    const int v = a.nbr[s + j];
+                    if (a.mate && __ldcg(a.mate + v) >= 0) continue;
+                    const unsigned long long sw = ld_volatile(a.suitor + v);
+                    if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
+                    bk = ke; be = e; bv = v;
+                }
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) {
-                unsigned ok = __shfl_xor_sync(mask, bk, o, 8);
-                int oe = __shfl_xor_sync(mask, be, o, 8), ov = __shfl_xor_sync(mask, bv, o, 8);
-                if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bv = ov; }
+                for (int o = 4; o > 0; o >>= 1) {
+                    unsigned ok = __shfl_xor_sync(mask, bk, o, 8);
+                    int oe = __shfl_xor_sync(mask, be, o, 8), ov = __shfl_xor_sync(mask, bv, o, 8);
+                    if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bv = ov; }
+                }
             }
             if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
             int next = -2;      // -2: lost a race, re-scan cur
@@ -788,6 +944,77 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
     }
 }
 
+// Thread-per-proposer Suitor over the rank-ordered adjacency: a proposer walks
+// its slots from the cursor and proposes at the first winnable one (the best,
+// by the slot order); every proposer is in flight at once (one wave), which
+// is what bounds the displacement chains at latency-bound sizes.  Unsorted
+// (high-degree) vertices take the full argmin scan.
+__global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
+    MF_PDL_ENTRY;
+    if (*a.abort_flag) return;
+    const int* list = nullptr;
+    int nprop = a.N;
+    if (a.front0) {
+        const int which = __ldcg(a.counters + 3);
+        list = which ? a.front1 : a.front0;
+        nprop = __ldcg(a.counters + which);
+    }
+    for (int ui = blockIdx.x * blockDim.x + threadIdx.x; ui < nprop; ui += gridDim.x * blockDim.x) {
+        int cur = list ? __ldcg(list + ui) : ui;
+        if (a.mate && __ldcg(a.mate + cur) >= 0) continue;
+        while (cur >= 0) {
+            const size_t s = (size_t)a.aoff[cur];
+            const int nu = a.ucnt[cur];
+            int be = -1, bv = -1;
+            unsigned bk = 0xffffffffu;
+            int c = a.acur[cur];
+            if (c >= 0) {
+                for (; c < nu; c++) {
+                    const int v = a.nbr[s + c];
+                    if (a.mate && __ldcg(a.mate + v) >= 0) continue;
+                    const int e = a.adj_eid[s + c];
+                    const unsigned ke = a.adj_k32[s + c];
+                    const unsigned long long sw = ld_volatile(a.suitor + v);
+                    if (sw == ~0ull || edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) {
+                        bk = ke; be = e; bv = v;
+                        break;
+                    }
+                }
+                a.acur[cur] = c;
+            } else {
+                for (int j = 0; j < nu; j++) {
+                    const int e = a.adj_eid[s + j];
+                    const unsigned ke = a.adj_k32[s + j];
+                    if (be >= 0 && !edge_lt(a, ke, e, bk, be)) continue;
+                    const int v = a.nbr[s + j];
+                    if (a.mate && __ldcg(a.mate + v) >= 0) continue;
+                    const unsigned long long sw = ld_volatile(a.suitor + v);
+                    if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
+                    bk = ke; be = e; bv = v;
+                }
+            }
+            if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
+            const unsigned long long mine = ((unsigned long long)bk << 32) | (unsigned)be;
+            unsigned long long sw = ld_volatile(a.suitor + bv);
+            int next = -2;  // -2: lost a race, re-scan cur (the lost slot is dead now)
+            while (true) {
+                if (sw != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw >> 32), (int)(unsigned)sw)) break;
+                const unsigned long long old = atomicCAS(a.suitor + bv, sw, mine);
+                if (old == sw) {
+                    if (sw == ~0ull) next = -1;
+                    else {
+                        const int se = (int)(unsigned)sw;
+                        next = (a.e0[se] == bv) ? a.e1[se] : a.e0[se];
+                    }
+                    break;
+                }
+                sw = old;
+            }
+            if (next != -2) cur = next;
+        }
+    }
+}
+
 // Locally-dominant rounds (persistent, cooperative launch, grid barrier).
 // Each round every frontier vertex (8 lanes) picks its best live incident
 // edge (lowest rank among edges to unmatched neighbours); an edge that is the
@@ -796,10 +1023,10 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
 // Matched / exhausted vertices leave the frontier.  After `max_rounds` the
 // remaining frontier is finished by k_suitor on the residual graph.
 constexpr int kLDRounds = 12;  // fixed in the graph; rounds after convergence exit at once
-constexpr int kLDMinVertices = 1 << 19;
+constexpr int kLDMinVertices = 1 << 21;  // measured: Suitor alone wins at 640k (cfg4), LD at 10M (cfg5)
 struct LDArgs {
     int N;
-    const int* inc_off;
+    const int* aoff;
     const int* ucnt;
     const int* nbr;
     const int* adj_eid;
@@ -815,6 +1042,7 @@ struct LDArgs {
     unsigned* bar;
     int max_rounds;
     const int* abort_flag;
+    int* acur;      // per vertex: first possibly-live slot of its rank-ordered adjacency (-1 = unsorted)
 };
 
 MF_DEV bool ld_lt(const LDArgs& a, unsigned ke, int e, unsigned kf, int f) {
@@ -854,40 +1082,44 @@ __global__ void __launch_bounds__(256) k_ld_init(LDArgs a) {
     }
 }
 
-// phase A of round `round`: each frontier vertex picks its best live edge
-__global__ void __launch_bounds__(256) k_ld_pick(LDArgs a, int round) {
+// phase A of round `round`: each frontier vertex picks its best live edge --
+// the first slot from its cursor whose neighbour is unmatched (rank-ordered
+// adjacency, k_adj_sort); unsorted (high-degree) vertices scan every slot.
+__global__ void __maxnreg__(48) k_ld_pick(LDArgs a, int round) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     const int cur = round & 1;
     const int n = a.counters[cur];
     if (n == 0) return;
     const int* Fc = cur ? a.front1 : a.front0;
-    const int l = threadIdx.x & 7;
-    const unsigned mask = 0xFFu << (threadIdx.x & 24);
-    const int ngroups = (gridDim.x * blockDim.x) >> 3;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 3; i < n; i += ngroups) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int v = Fc[i];
-        const size_t s = 2 * (size_t)a.inc_off[v];
+        const size_t s = (size_t)a.aoff[v];
         const int nu = a.ucnt[v];
         int be = -1, bu = -1;
-        unsigned bk = 0xffffffffu;
-        for (int j = l; j < nu; j += 8) {
-            const int u = a.nbr[s + j];
-            if (a.mate[u] >= 0) continue;
-            const int e = a.adj_eid[s + j];
-            const unsigned ke = a.adj_k32[s + j];
-            if (be < 0 || ld_lt(a, ke, e, bk, be)) { bk = ke; be = e; bu = u; }
+        int c = a.acur[v];
+        if (c >= 0) {
+            for (; c < nu; c++) {
+                const int u = a.nbr[s + c];
+                if (a.mate[u] < 0) {
+                    be = a.adj_eid[s + c];
+                    bu = u;
+                    break;
+                }
+            }
+            a.acur[v] = c;
+        } else {
+            unsigned bk = 0xffffffffu;
+            for (int j = 0; j < nu; j++) {
+                const int u = a.nbr[s + j];
+                if (a.mate[u] >= 0) continue;
+                const int e = a.adj_eid[s + j];
+                const unsigned ke = a.adj_k32[s + j];
+                if (be < 0 || ld_lt(a, ke, e, bk, be)) { bk = ke; be = e; bu = u; }
+            }
         }
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-            unsigned ok = __shfl_xor_sync(mask, bk, o, 8);
-            int oe = __shfl_xor_sync(mask, be, o, 8), ou = __shfl_xor_sync(mask, bu, o, 8);
-            if (oe >= 0 && (be < 0 || ld_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bu = ou; }
-        }
-        if (l == 0) {
-            a.best[v] = be;
-            a.bestu[v] = bu;
-        }
+        a.best[v] = be;
+        a.bestu[v] = bu;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[cur ^ 1] = 0;
 }
@@ -922,32 +1154,28 @@ __global__ void __launch_bounds__(256) k_ld_match(LDArgs a, int round) {
     }
 }
 
-// 32-bit rank-key prefix per adjacency slot (after the keys are final), so the
-// matching scans contiguous prefixes instead of gathering 8-byte keys.
-__global__ void __launch_bounds__(256) k_adj_keys(const int* __restrict__ abort_flag, int N,
-                                                  const int* __restrict__ inc_off, const int* __restrict__ ucnt,
-                                                  const int* __restrict__ adj_eid, const uint64_t* __restrict__ key_hi,
-                                                  unsigned* __restrict__ adj_k32, int B, int* __restrict__ seg_cnt,
-                                                  int* __restrict__ ldc, unsigned long long* __restrict__ suitor) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
-    // zero the truncation-candidate segment counters k_mates appends to, the LD
-    // round counters, and the suitor words
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) seg_cnt[b] = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 8; i += gridDim.x * blockDim.x) ldc[i] = 0;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) suitor[v] = ~0ull;
-    const int l = threadIdx.x & 7;
-    const int groups = gridDim.x * (blockDim.x >> 3);
-    for (int v = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); v < N; v += groups) {
-        const size_t s = 2 * (size_t)inc_off[v];
-        const int nu = ucnt[v];
-        for (int j = l; j < nu; j += 8) adj_k32[s + j] = (unsigned)(key_hi[adj_eid[s + j]] >> 32);
-    }
+// Append slot in the candidate segment of v's mesh.  Must be reached by every
+// thread of the block (block-uniform loop): one mesh -> one atomic per block
+// (a per-warp atomic on a single counter serialises millions of appends);
+// batches -> per-mesh counters.
+MF_DEV int block_slot(bool keep, int* __restrict__ counter) {
+    __shared__ int s_scan[33];
+    __shared__ int s_base;
+    int tot;
+    const int pos = block_excl_scan(keep ? 1 : 0, s_scan, &tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(counter, tot) : 0;
+    __syncthreads();
+    const int r = s_base + pos;
+    __syncthreads();
+    return keep ? r : -1;
 }
-
-// mate = the suitor edge when the proposal is mutual.
-MF_DEV int seg_slot(const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt, int v,
-                    int& b);
+MF_DEV int seg_slot_uniform(bool keep, const int* __restrict__ vmesh, const int* __restrict__ voff,
+                            int* __restrict__ seg_cnt, int v) {
+    if (!vmesh) return block_slot(keep, seg_cnt);
+    if (!keep) return -1;
+    const int b = vmesh[v];
+    return voff[b] + atomicAdd(seg_cnt + b, 1);
+}
 
 // mate = the suitor edge when the proposal is mutual (or the LD match); every
 // matched pair is also appended once (from its e0 end) as a budget-truncation
@@ -959,18 +1187,24 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigne
                         uint64_t* __restrict__ chi, uint64_t* __restrict__ clo, int* __restrict__ cpay) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int m = mate[v];
-        unsigned long long w = m >= 0 ? ~0ull : suitor[v];  // m >= 0: matched by the LD rounds
-        if (w != ~0ull) {
-            int e = (int)(unsigned)w;
-            int u = e0[e] == v ? e1[e] : e0[e];
-            if ((int)(unsigned)suitor[u] == e && suitor[u] != ~0ull) m = e;
+    // block-uniform trip count: the single-mesh append is aggregated per block
+    for (int base = blockIdx.x * blockDim.x; base < N; base += gridDim.x * blockDim.x) {
+        const int v = base + threadIdx.x;
+        int m = -1;
+        bool cand = false;
+        if (v < N) {
+            m = mate[v];
+            unsigned long long w = m >= 0 ? ~0ull : suitor[v];  // m >= 0: matched by the LD rounds
+            if (w != ~0ull) {
+                int e = (int)(unsigned)w;
+                int u = e0[e] == v ? e1[e] : e0[e];
+                if ((int)(unsigned)suitor[u] == e && suitor[u] != ~0ull) m = e;
+            }
+            mate[v] = m;
+            cand = m >= 0 && e0[m] == v;
         }
-        mate[v] = m;
-        if (m >= 0 && e0[m] == v) {
-            int b;
-            int slot = seg_slot(vmesh, voff, seg_cnt, v, b);
+        const int slot = seg_slot_uniform(cand, vmesh, voff, seg_cnt, v);
+        if (cand) {
             chi[slot] = key_hi[m];
             clo[slot] = key_lo ? key_lo[m] : (uint64_t)m;
             cpay[slot] = m;
@@ -1004,6 +1238,38 @@ MF_DEV bool sel_prefix(uint64_t hi, uint64_t lo, uint64_t phi, uint64_t plo, int
     return (k >> top) == (p >> top);
 }
 
+// Common-prefix skip.  `o` / `n` are the OR / AND of every key of the bucket
+// that was just histogrammed; the surviving sub-bucket agrees on every bit
+// below `top` on which the whole bucket agreed, so those bits are copied into
+// the prefix and the next digit starts at the highest bit that still differs.
+// (Keys built from float64 costs share their sign / exponent bits, and the
+// secondary halves share their high zero bits: without the skip each such run
+// costs a full pass over the candidates.)
+MF_DEV void sel_skip(unsigned __int128& p, int& top, uint64_t oh, uint64_t ol, uint64_t ah, uint64_t al) {
+    unsigned __int128 diff = (((unsigned __int128)(oh ^ ah)) << 64) | (ol ^ al);
+    if (top < 128) diff &= ((((unsigned __int128)1) << top) - 1);
+    if (diff == 0) return;
+    const uint64_t dh = (uint64_t)(diff >> 64), dl = (uint64_t)diff;
+    const int D = dh ? 127 - __clzll((long long)dh) : 63 - __clzll((long long)dl);
+    if (D + 1 >= top) return;
+    unsigned __int128 m = ((top < 128) ? ((((unsigned __int128)1) << top) - 1) : ~(unsigned __int128)0) &
+                          ~((((unsigned __int128)1) << (D + 1)) - 1);
+    unsigned __int128 andv = (((unsigned __int128)ah) << 64) | al;
+    p = (p & ~m) | (andv & m);
+    top = D + 1;
+}
+
+// warp OR / AND reduction of a 128-bit key range summary
+MF_DEV void warp_orand(uint64_t& oh, uint64_t& ol, uint64_t& ah, uint64_t& al) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        oh |= __shfl_xor_sync(0xffffffffu, oh, o);
+        ol |= __shfl_xor_sync(0xffffffffu, ol, o);
+        ah &= __shfl_xor_sync(0xffffffffu, ah, o);
+        al &= __shfl_xor_sync(0xffffffffu, al, o);
+    }
+}
+
 struct SelectArgs {
     const uint64_t* chi;
     const uint64_t* clo;
@@ -1021,7 +1287,22 @@ struct SelectArgs {
     int* krem;          // resumable state (after the multi-block passes)
     int* top;
     int resume;
+    int* gscr;          // multi-block scratch (resume: bucket buffer)
 };
+
+// Multi-block pass scratch (ints): histogram | OR (2 u64), AND (2 u64) | stop |
+// compact | count | bucket buffer (kSelCap (hi, lo) pairs).  Once a decide
+// leaves a bucket that fits the shared-memory stage, the next histogram pass
+// also copies that bucket into the buffer, and k_select resumes from it
+// instead of streaming the whole segment again.
+constexpr int kSelScrHdr = kSelBins + 16;
+constexpr int kSelScratch = kSelScrHdr + 4 * kSelCap;  // ints
+constexpr int kSelPasses = 5;                            // multi-block passes before the single-CTA stage
+MF_DEV unsigned long long* sel_orand(int* g) { return reinterpret_cast<unsigned long long*>(g + kSelBins); }
+MF_DEV int* sel_stop(int* g) { return g + kSelBins + 8; }
+MF_DEV int* sel_compact(int* g) { return g + kSelBins + 9; }
+MF_DEV int* sel_count(int* g) { return g + kSelBins + 10; }
+MF_DEV uint64_t* sel_buf(int* g) { return reinterpret_cast<uint64_t*>(g + kSelScrHdr); }
 
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     MF_PDL_ENTRY;
@@ -1033,6 +1314,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     __shared__ int s_scan[33];
     __shared__ int s_sel[4];
     __shared__ int s_ncomp;
+    __shared__ unsigned long long s_oa[4];
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         const int c0 = a.voff[b], c1 = c0 + a.seg_cnt[b];
         const int cnt = c1 - c0;
@@ -1061,20 +1343,43 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
         bool in_smem = false;
         int n_s = 0;
         bool done = false;
+        if (a.resume && *sel_stop(a.gscr)) {  // the multi-block passes left the bucket in the buffer
+            n_s = *sel_count(a.gscr);
+            const uint64_t* buf = sel_buf(a.gscr);
+            for (int i = threadIdx.x; i < n_s; i += blockDim.x) {
+                sh[i] = buf[2 * i];
+                sl[i] = buf[2 * i + 1];
+            }
+            in_smem = true;
+            __syncthreads();
+        }
         while (!done) {
             int width = top >= kSelBits ? kSelBits : top;
             int shift = top - width;
             for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
+            if (threadIdx.x < 4) s_oa[threadIdx.x] = (threadIdx.x < 2) ? 0ull : ~0ull;
             __syncthreads();
+            uint64_t oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
             if (in_smem) {
                 for (int i = threadIdx.x; i < n_s; i += blockDim.x)
-                    if (sel_prefix(sh[i], sl[i], phi, plo, top)) atomicAdd(hist + sel_digit(sh[i], sl[i], shift, width), 1);
+                    if (sel_prefix(sh[i], sl[i], phi, plo, top)) {
+                        atomicAdd(hist + sel_digit(sh[i], sl[i], shift, width), 1);
+                        oh |= sh[i]; ol |= sl[i]; ah &= sh[i]; al &= sl[i];
+                    }
             } else {
 #pragma unroll 4
                 for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
                     uint64_t h = a.chi[i], l = a.clo[i];
-                    if (sel_prefix(h, l, phi, plo, top)) atomicAdd(hist + sel_digit(h, l, shift, width), 1);
+                    if (sel_prefix(h, l, phi, plo, top)) {
+                        atomicAdd(hist + sel_digit(h, l, shift, width), 1);
+                        oh |= h; ol |= l; ah &= h; al &= l;
+                    }
                 }
+            }
+            warp_orand(oh, ol, ah, al);
+            if ((threadIdx.x & 31) == 0) {
+                atomicOr(s_oa, oh); atomicOr(s_oa + 1, ol);
+                atomicAnd(s_oa + 2, ah); atomicAnd(s_oa + 3, al);
             }
             __syncthreads();
             // block scan over the bins: find digit d with cum(d) < kr <= cum(d) + hist[d]
@@ -1102,8 +1407,6 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
             const int hd = s_sel[2];
             unsigned __int128 p = ((unsigned __int128)phi << 64) | plo;
             p |= ((unsigned __int128)d) << shift;
-            phi = (uint64_t)(p >> 64);
-            plo = (uint64_t)p;
             top = shift;
             if (hd == kr) {
                 unsigned __int128 ones = (shift == 0) ? 0 : ((((unsigned __int128)1) << shift) - 1);
@@ -1115,50 +1418,243 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
                     a.ksel[b] = k;
                 }
                 done = true;
-            } else if (!in_smem && hd <= kSelCap) {
-                // compact the surviving bucket into shared memory
-                if (threadIdx.x == 0) s_ncomp = 0;
-                __syncthreads();
-                for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-                    uint64_t h = a.chi[i], l = a.clo[i];
-                    if (sel_prefix(h, l, phi, plo, top)) {
-                        int slot = atomicAdd(&s_ncomp, 1);
-                        sh[slot] = h;
-                        sl[slot] = l;
+            } else {
+                sel_skip(p, top, s_oa[0], s_oa[1], s_oa[2], s_oa[3]);
+                phi = (uint64_t)(p >> 64);
+                plo = (uint64_t)p;
+                if (!in_smem && hd <= kSelCap) {
+                    // compact the surviving bucket into shared memory
+                    if (threadIdx.x == 0) s_ncomp = 0;
+                    __syncthreads();
+                    for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+                        uint64_t h = a.chi[i], l = a.clo[i];
+                        if (sel_prefix(h, l, phi, plo, top)) {
+                            int slot = atomicAdd(&s_ncomp, 1);
+                            sh[slot] = h;
+                            sl[slot] = l;
+                        }
                     }
+                    __syncthreads();
+                    n_s = s_ncomp;
+                    in_smem = true;
                 }
-                __syncthreads();
-                n_s = s_ncomp;
-                in_smem = true;
             }
             __syncthreads();
         }
     }
 }
 
+// Cluster selection for one mid-size segment (a single mesh below the
+// multi-block threshold): kClCTAs CTAs of one thread-block cluster split the
+// candidates; each pass every CTA histograms its slice in its own shared
+// memory, rank 0 pulls the slices' histograms (and the bucket's OR / AND)
+// through distributed shared memory with plain loads, picks the digit and
+// writes the decision into every rank's shared memory, and all ranks carry
+// the same selection state (two cluster barriers per pass).  Once the bucket fits, every rank keeps its share
+// of it in shared memory, so later passes touch no global memory.
+constexpr int kClCTAs = 8;
+constexpr int kClThreads = 512;
+constexpr int kClSmem = kSelBins * 4 + 2 * kSelCap * 8;
+__global__ void __cluster_dims__(kClCTAs, 1, 1) __launch_bounds__(kClThreads) k_select_cl(SelectArgs a) {
+    MF_PDL_ENTRY;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    extern __shared__ unsigned char s_raw[];
+    int* hist = reinterpret_cast<int*>(s_raw);
+    uint64_t* sh = reinterpret_cast<uint64_t*>(s_raw + kSelBins * 4);
+    uint64_t* sl = sh + kSelCap;
+    __shared__ unsigned long long s_oa[4];
+    __shared__ int s_scan[33];
+    __shared__ int s_sel[3];
+    __shared__ int s_dec[3];                 // decision broadcast by rank 0: digit, count below, bucket size
+    __shared__ unsigned long long s_moa[4];  // merged OR / AND broadcast by rank 0
+    __shared__ int s_ncomp;
+    if (*a.abort_flag) return;  // the same word for every rank: the whole cluster leaves together
+    const int c0 = a.voff[0], c1 = c0 + a.seg_cnt[0];
+    const int cnt = c1 - c0;
+    const int want = a.act[0] ? a.budget[0] - (a.removed ? a.removed[0] : 0) : 0;
+    int k = want < cnt ? want : cnt;
+    if (k < 0) k = 0;
+    if (k == 0 || k >= cnt) {
+        if (rank == 0 && threadIdx.x == 0) {
+            a.ksel[0] = k;
+            a.mode[0] = (k == 0) ? 2 : 1;
+        }
+        return;
+    }
+    const int per = (cnt + kClCTAs - 1) / kClCTAs;
+    const int lo = c0 + min(cnt, (int)rank * per), hi = c0 + min(cnt, ((int)rank + 1) * per);
+    uint64_t phi = 0, plo = 0;
+    int top = 128, kr = k, n_s = 0;
+    bool in_smem = false;
+    while (true) {
+        const int width = top >= kSelBits ? kSelBits : top;
+        const int shift = top - width;
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
+        if (threadIdx.x < 4) s_oa[threadIdx.x] = (threadIdx.x < 2) ? 0ull : ~0ull;
+        __syncthreads();
+        uint64_t oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+        if (in_smem) {
+            for (int i = threadIdx.x; i < n_s; i += blockDim.x)
+                if (sel_prefix(sh[i], sl[i], phi, plo, top)) {
+                    atomicAdd(hist + sel_digit(sh[i], sl[i], shift, width), 1);
+                    oh |= sh[i]; ol |= sl[i]; ah &= sh[i]; al &= sl[i];
+                }
+        } else {
+            for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                const uint64_t h = a.chi[i], l = a.clo[i];
+                if (sel_prefix(h, l, phi, plo, top)) {
+                    atomicAdd(hist + sel_digit(h, l, shift, width), 1);
+                    oh |= h; ol |= l; ah &= h; al &= l;
+                }
+            }
+        }
+        warp_orand(oh, ol, ah, al);
+        if ((threadIdx.x & 31) == 0) {
+            atomicOr(s_oa, oh); atomicOr(s_oa + 1, ol);
+            atomicAnd(s_oa + 2, ah); atomicAnd(s_oa + 3, al);
+        }
+        cl.sync();  // every slice histogrammed
+        if (rank == 0) {
+            // pull the slices' histograms and OR / AND words through DSMEM (plain loads)
+            const int pb = kSelBins / kClThreads;
+            int hb[kSelBins / kClThreads];
+            int loc = 0;
+#pragma unroll
+            for (int j = 0; j < pb; j++) hb[j] = hist[threadIdx.x * pb + j];
+            for (int r = 1; r < kClCTAs; r++) {
+                const int* hr = cl.map_shared_rank(hist, r);
+#pragma unroll
+                for (int j = 0; j < pb; j++) hb[j] += hr[threadIdx.x * pb + j];
+            }
+#pragma unroll
+            for (int j = 0; j < pb; j++) loc += hb[j];
+            if (threadIdx.x < 4) {
+                unsigned long long w = s_oa[threadIdx.x];
+                for (int r = 1; r < kClCTAs; r++) {
+                    const unsigned long long x = cl.map_shared_rank(s_oa, r)[threadIdx.x];
+                    w = (threadIdx.x < 2) ? (w | x) : (w & x);
+                }
+                s_moa[threadIdx.x] = w;
+            }
+            int tot;
+            const int ex = block_excl_scan(loc, s_scan, &tot);
+            if (ex < kr && kr <= ex + loc) {
+                int cum = ex;
+#pragma unroll
+                for (int j = 0; j < pb; j++) {
+                    if (cum < kr && cum + hb[j] >= kr) {
+                        s_sel[0] = threadIdx.x * pb + j;
+                        s_sel[1] = cum;
+                        s_sel[2] = hb[j];
+                    }
+                    cum += hb[j];
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < kClCTAs) {
+                int* dec = cl.map_shared_rank(s_dec, threadIdx.x);
+                unsigned long long* moa = cl.map_shared_rank(s_moa, threadIdx.x);
+                dec[0] = s_sel[0];
+                dec[1] = s_sel[1];
+                dec[2] = s_sel[2];
+                if (threadIdx.x) {
+                    moa[0] = s_moa[0]; moa[1] = s_moa[1]; moa[2] = s_moa[2]; moa[3] = s_moa[3];
+                }
+            }
+        }
+        cl.sync();  // the decision is in every rank
+        const int d = s_dec[0];
+        kr -= s_dec[1];
+        const int hd = s_dec[2];
+        unsigned __int128 p = ((unsigned __int128)phi << 64) | plo;
+        p |= ((unsigned __int128)d) << shift;
+        top = shift;
+        if (hd == kr) {
+            const unsigned __int128 ones = (shift == 0) ? 0 : ((((unsigned __int128)1) << shift) - 1);
+            p |= ones;
+            if (rank == 0 && threadIdx.x == 0) {
+                a.thr_hi[0] = (uint64_t)(p >> 64);
+                a.thr_lo[0] = (uint64_t)p;
+                a.mode[0] = 3;
+                a.ksel[0] = k;
+            }
+            break;
+        }
+        sel_skip(p, top, s_moa[0], s_moa[1], s_moa[2], s_moa[3]);
+        phi = (uint64_t)(p >> 64);
+        plo = (uint64_t)p;
+        if (!in_smem && hd <= kSelCap) {  // this rank's share of the bucket -> shared memory
+            if (threadIdx.x == 0) s_ncomp = 0;
+            __syncthreads();
+            for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                const uint64_t h = a.chi[i], l = a.clo[i];
+                if (sel_prefix(h, l, phi, plo, top)) {
+                    const int slot = atomicAdd(&s_ncomp, 1);
+                    sh[slot] = h;
+                    sl[slot] = l;
+                }
+            }
+            __syncthreads();
+            n_s = s_ncomp;
+            in_smem = true;
+        }
+        __syncthreads();
+    }
+    cl.sync();  // no rank leaves while another may still read its shared memory
+}
+
 // Multi-block MSD passes for one large segment (a single big mesh): every
 // block histograms its slice of the candidates under the current prefix in
-// shared memory and flushes non-zero bins; one block then picks the digit.
-// The single-CTA k_select resumes from the resulting state.
+// shared memory and flushes non-zero bins (plus the bucket's OR / AND); one
+// block then picks the digit and skips the bits the bucket shares.  Passes
+// stop once the surviving bucket fits the shared-memory stage of k_select,
+// which resumes from the resulting state.
 __global__ void __launch_bounds__(512) k_sel_hist(SelectArgs a, int* __restrict__ ghist, int pass) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     __shared__ int h[kSelBins];
-    if (pass > 0 && a.mode[0] != 0) return;
-    const int top = 128 - kSelBits * pass;
+    __shared__ unsigned long long s_oa[4];
+    if (pass > 0 && (a.mode[0] != 0 || *sel_stop(ghist))) return;
+    const int top = pass ? a.top[0] : 128;
     const int width = top >= kSelBits ? kSelBits : top;
     const int shift = top - width;
     const uint64_t phi = pass ? a.thr_hi[0] : 0, plo = pass ? a.thr_lo[0] : 0;
     for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+    if (threadIdx.x < 4) s_oa[threadIdx.x] = (threadIdx.x < 2) ? 0ull : ~0ull;
     __syncthreads();
+    uint64_t oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
     const int c0 = a.voff[0], c1 = c0 + a.seg_cnt[0];
+    const bool compact = pass > 0 && *sel_compact(ghist);  // bucket <= kSelCap: copy it out too
+    uint64_t* buf = sel_buf(ghist);
     for (int i = c0 + blockIdx.x * blockDim.x + threadIdx.x; i < c1; i += gridDim.x * blockDim.x) {
         uint64_t hh = a.chi[i], ll = a.clo[i];
-        if (sel_prefix(hh, ll, phi, plo, top)) atomicAdd(h + sel_digit(hh, ll, shift, width), 1);
+        if (sel_prefix(hh, ll, phi, plo, top)) {
+            atomicAdd(h + sel_digit(hh, ll, shift, width), 1);
+            oh |= hh; ol |= ll; ah &= hh; al &= ll;
+            if (compact) {
+                const int slot = atomicAdd(sel_count(ghist), 1);
+                buf[2 * slot] = hh;
+                buf[2 * slot + 1] = ll;
+            }
+        }
+    }
+    warp_orand(oh, ol, ah, al);
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(s_oa, oh); atomicOr(s_oa + 1, ol);
+        atomicAnd(s_oa + 2, ah); atomicAnd(s_oa + 3, al);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
         if (h[i]) atomicAdd(ghist + i, h[i]);
+    unsigned long long* g = sel_orand(ghist);
+    if (threadIdx.x == 0) {
+        if (s_oa[0]) atomicOr(g, s_oa[0]);
+        if (s_oa[1]) atomicOr(g + 1, s_oa[1]);
+        if (~s_oa[2]) atomicAnd(g + 2, s_oa[2]);
+        if (~s_oa[3]) atomicAnd(g + 3, s_oa[3]);
+    }
 }
 
 __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* __restrict__ ghist, int pass) {
@@ -1166,27 +1662,38 @@ __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* _
     __shared__ int s_scan[33];
     __shared__ int s_sel[3];
     if (*a.abort_flag) return;
+    unsigned long long* g = sel_orand(ghist);
     const int cnt = a.seg_cnt[0];
     int kr;
     uint64_t phi = 0, plo = 0;
+    int top = 128;
+    auto reset = [&]() {  // scratch back to its neutral state for the next pass / next selection
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) ghist[i] = 0;
+        if (threadIdx.x < 4) g[threadIdx.x] = (threadIdx.x < 2) ? 0ull : ~0ull;
+    };
     if (pass == 0) {
         int want = a.act[0] ? a.budget[0] - (a.removed ? a.removed[0] : 0) : 0;
         int k = want < cnt ? want : cnt;
         if (k < 0) k = 0;
-        if (threadIdx.x == 0) a.ksel[0] = k;
+        if (threadIdx.x == 0) {
+            a.ksel[0] = k;
+            *sel_stop(ghist) = 0;
+            *sel_compact(ghist) = 0;
+            *sel_count(ghist) = 0;
+        }
         if (k == 0 || k >= cnt) {
             if (threadIdx.x == 0) a.mode[0] = (k == 0) ? 2 : 1;
-            for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) ghist[i] = 0;
+            reset();
             return;
         }
         kr = k;
     } else {
-        if (a.mode[0] != 0) return;
+        if (a.mode[0] != 0 || *sel_stop(ghist)) return;
         kr = a.krem[0];
         phi = a.thr_hi[0];
         plo = a.thr_lo[0];
+        top = a.top[0];
     }
-    const int top = 128 - kSelBits * pass;
     const int width = top >= kSelBits ? kSelBits : top;
     const int shift = top - width;
     const int per = kSelBins / kSelThreads;
@@ -1208,23 +1715,29 @@ __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* _
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) ghist[i] = 0;
+    const uint64_t oh = g[0], ol = g[1], ah = g[2], al = g[3];
+    __syncthreads();
+    reset();
     if (threadIdx.x != 0) return;
     const int d = s_sel[0];
     kr -= s_sel[1];
     unsigned __int128 p = ((unsigned __int128)phi << 64) | plo;
     p |= ((unsigned __int128)d) << shift;
+    int ntop = shift;
     if (s_sel[2] == kr) {
         unsigned __int128 ones = (shift == 0) ? 0 : ((((unsigned __int128)1) << shift) - 1);
         p |= ones;
         a.mode[0] = 3;
     } else {
         a.mode[0] = 0;
+        sel_skip(p, ntop, oh, ol, ah, al);
+        if (*sel_compact(ghist)) *sel_stop(ghist) = 1;       // this pass copied the bucket: hand over
+        else if (s_sel[2] <= kSelCap) *sel_compact(ghist) = 1;  // next pass copies it
     }
     a.thr_hi[0] = (uint64_t)(p >> 64);
     a.thr_lo[0] = (uint64_t)p;
     a.krem[0] = kr;
-    a.top[0] = shift;
+    a.top[0] = ntop;
 }
 
 // ---- flag producers fused into the decoupled look-back scan (LoadOp functors)
@@ -1268,40 +1781,6 @@ MF_DEV bool is_selected(int mode, uint64_t h, uint64_t l, uint64_t th, uint64_t 
     return mode == 1 || (mode == 3 && !key_lt(th, tl, h, l));
 }
 
-// Candidate flags (pass 1) and ordered writes (pass 2) for budget truncation:
-// the matched edges, one per pair from its e0 end.
-// Candidates are appended into their mesh's own vertex-index range, so each
-// segment is contiguous without a scan (order inside a segment is irrelevant:
-// the selection is by unique key).
-MF_DEV int seg_slot(const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt, int v,
-                    int& b) {
-    if (!vmesh) {
-        b = 0;
-        return append_slot(seg_cnt);
-    }
-    b = vmesh[v];
-    return voff[b] + atomicAdd(seg_cnt + b, 1);
-}
-
-// Budget truncation candidates: the matched edges, one per pair from its e0 end.
-__global__ void k_trunc_cand(const int* __restrict__ abort_flag, int N, const int* __restrict__ mate,
-                             const int* __restrict__ e0, const uint64_t* __restrict__ key_hi,
-                             const uint64_t* __restrict__ key_lo, const int* __restrict__ vmesh,
-                             const int* __restrict__ voff, int* __restrict__ seg_cnt, uint64_t* __restrict__ chi,
-                             uint64_t* __restrict__ clo, int* __restrict__ cpay) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int e = mate[v];
-        if (e < 0 || e0[e] != v) continue;
-        int b;
-        int slot = seg_slot(vmesh, voff, seg_cnt, v, b);
-        chi[slot] = key_hi[e];
-        clo[slot] = key_lo ? key_lo[e] : (uint64_t)e;
-        cpay[slot] = e;
-    }
-}
-
 MF_DEV bool seg_valid(const int* __restrict__ vmesh, const int* __restrict__ voff, const int* __restrict__ seg_cnt,
                       int i, int& b) {
     b = vmesh ? vmesh[i] : 0;
@@ -1336,9 +1815,10 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
 // Absorb candidates (decimate.py:207-221): every unmatched vertex with edges
 // picks its lowest (cost, rep) incident edge; the matching is maximal here so
 // every neighbour is clustered and one pass suffices.
-__global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const int* __restrict__ inc_off,
+__global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const int* __restrict__ aoff,
                               const int* __restrict__ ucnt, const int* __restrict__ nbr,
                               const int* __restrict__ adj_eid, const double* __restrict__ cost,
+                              const uint64_t* __restrict__ ckey,
                               const int* __restrict__ mate, const int* __restrict__ e0, const int* __restrict__ vmesh,
                               const int* __restrict__ voff, const int* __restrict__ act,
                               const int* __restrict__ budget, const int* __restrict__ removed,
@@ -1346,27 +1826,37 @@ __global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const i
                               int* __restrict__ caux) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        int nu = ucnt[v];
-        if (nu == 0 || mate[v] >= 0) continue;
-        int bm = mesh_of(vmesh, v);
-        if (!act[bm] || removed[bm] >= budget[bm]) continue;
-        size_t s = 2 * (size_t)inc_off[v];
+    if (!vmesh && (!act[0] || removed[0] >= budget[0])) return;  // budget met: no absorption this round
+    for (int base = blockIdx.x * blockDim.x; base < N; base += gridDim.x * blockDim.x) {
+        const int v = base + threadIdx.x;
+        bool cand = false;
         uint64_t bk = ~0ull;
         int brep = 0x7fffffff;
-        for (int j = 0; j < nu; j++) {
-            int mu = mate[nbr[s + j]];
-            if (mu < 0) continue;  // cannot happen for a maximal matching
-            int rep = e0[mu];
-            uint64_t k = f64_key(cost[adj_eid[s + j]]);
-            if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
+        int nu = 0;
+        if (v < N) {
+            nu = ucnt[v];
+            if (nu > 0 && mate[v] < 0) {
+                int bm = mesh_of(vmesh, v);
+                if (act[bm] && removed[bm] < budget[bm]) {
+                    size_t s = (size_t)aoff[v];
+                    for (int j = 0; j < nu; j++) {
+                        int mu = mate[nbr[s + j]];
+                        if (mu < 0) continue;  // cannot happen for a maximal matching
+                        int rep = e0[mu];
+                        const int e = adj_eid[s + j];
+                        uint64_t k = cost ? f64_key(cost[e]) : ckey[e];  // unseeded: ckey == f64_key(cost)
+                        if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
+                    }
+                    cand = brep != 0x7fffffff;
+                }
+            }
         }
-        if (brep == 0x7fffffff) continue;
-        int b;
-        int slot = seg_slot(vmesh, voff, seg_cnt, v, b);
-        chi[slot] = bk;
-        clo[slot] = ((uint64_t)(unsigned)brep << 32) | (unsigned)v;
-        caux[slot] = brep;
+        const int slot = seg_slot_uniform(cand, vmesh, voff, seg_cnt, v);
+        if (cand) {
+            chi[slot] = bk;
+            clo[slot] = ((uint64_t)(unsigned)brep << 32) | (unsigned)v;
+            caux[slot] = brep;
+        }
     }
 }
 
@@ -1384,7 +1874,7 @@ __global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* 
                                const uint64_t* __restrict__ tlo, int* __restrict__ absorbed,
                                int* __restrict__ minrep, int B, const int* __restrict__ act,
                                const int* __restrict__ budget, const int* __restrict__ nin,
-                               const int* __restrict__ ksel, int* __restrict__ removed, const int* __restrict__ eoff,
+                               const int* __restrict__ ksel, int* __restrict__ removed, const int* __restrict__ aoff,
                                RoundFail fail, int round) {
     MF_PDL_ENTRY;
     if (*fail.abort) return;
@@ -1406,7 +1896,7 @@ __global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* 
             if (fail.fail_ach[b] < 0) {
                 fail.fail_ach[b] = nin[b] - r;
                 fail.fail_round[b] = round;
-                fail.fail_noedge[b] = (eoff[voff[b + 1]] == eoff[voff[b]]);
+                fail.fail_noedge[b] = (aoff[voff[b + 1]] == aoff[voff[b]]);
             }
             atomicExch(fail.abort, 1);
         }
@@ -1717,7 +2207,8 @@ __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int*
                           int* __restrict__ mt, int first_round, int B, const int* __restrict__ kout,
                           const int* __restrict__ foff_in, int* __restrict__ foff_out, int* __restrict__ foff_fin,
                           int* __restrict__ stats, const int* __restrict__ n_edges, const int* __restrict__ ld_rounds,
-                          int* __restrict__ deg, int* __restrict__ cursor, int n1_next, int* __restrict__ counters) {
+                          int* __restrict__ deg, int* __restrict__ cursor, int* __restrict__ lowfill, int n1_next,
+                          int* __restrict__ counters) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
@@ -1728,14 +2219,15 @@ __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int*
     }
     if (tid == 0) {  // per-round counts for the host (one readback at the end)
         stats[0] = foff_in[B];
-        stats[1] = *n_edges;
+        stats[1] = *n_edges >> 1;  // adjacency slots = 2 per edge
         stats[2] = kout[foff_in[B]];
         stats[3] = *ld_rounds;
     }
-    // clear the next round's degree / cursor arrays and counters
+    // clear the next round's degree / cursor / lower-slot fill arrays and counters
     for (int i = tid; i < n1_next; i += nth) {
         deg[i] = 0;
         cursor[i] = 0;
+        lowfill[i] = 0;
     }
     for (int i = tid; i < 64; i += nth) counters[i] = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N0; i += gridDim.x * blockDim.x) {
@@ -1758,7 +2250,7 @@ __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int*
 // edge can be a programmatic-dependent-launch edge).
 __global__ void k_graph_init(int* __restrict__ status, int status_words, int fail_lo, int fail_hi,
                              int* __restrict__ foff_a, const int* __restrict__ foff0, int B, int* __restrict__ deg,
-                             int* __restrict__ cursor, int n1, int* __restrict__ counters,
+                             int* __restrict__ cursor, int* __restrict__ lowfill, int n1, int* __restrict__ counters,
                              unsigned long long* __restrict__ scan_a, unsigned long long* __restrict__ scan_b,
                              int scan_words, int* __restrict__ ghist, int nghist) {
     MF_PDL_ENTRY;
@@ -1769,13 +2261,15 @@ __global__ void k_graph_init(int* __restrict__ status, int status_words, int fai
     for (int i = tid; i < n1; i += nth) {
         deg[i] = 0;
         cursor[i] = 0;
+        lowfill[i] = 0;
     }
     for (int i = tid; i < 64; i += nth) counters[i] = 0;
     for (int i = tid; i < scan_words; i += nth) {
         scan_a[i] = 0ull;
         scan_b[i] = 0ull;
     }
-    for (int i = tid; i < nghist; i += nth) ghist[i] = 0;
+    // selection scratch: histogram + OR words zero, AND words all-ones (see kSelScratch)
+    for (int i = tid; i < nghist; i += nth) ghist[i] = (i >= kSelBins + 4 && i < kSelBins + 8) ? -1 : 0;
 }
 
 // ------------------------------------------------------------------------

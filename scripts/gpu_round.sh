@@ -12,7 +12,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv
 python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1 || echo "build failed"
 
 if [[ $PARTS == *tests* ]]; then
-  timeout 1200 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest gpu rc=$?"
+  timeout 1200 python -m pytest tests -m gpu -x -q --timeout=120 > "$OUT/pytest_gpu.log" 2>&1; echo "pytest gpu rc=$?"
   tail -3 "$OUT/pytest_gpu.log"
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?"
   tail -1 "$OUT/smoke.log"
