@@ -125,6 +125,17 @@ int mf_unpool(mf_context *ctx, const mf_decimation *res, const int64_t *replace,
 
 int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t *chain, int64_t cap);
 
+/* quality_report's per-output-vertex error (replaces decimate.py:580-602 up to the
+ * numpy reductions): cluster quadric of the ORIGINAL mesh's vertex quadrics (summed in
+ * ascending member order, accumulate_quadrics quadrics.py:80-86) evaluated at the output
+ * positions (Quadric.evaluate, quadrics.py:53-58).  `original`: the input mesh (host or
+ * device pointers, offsets ignored); replace: host/device int64[n] or taken from `res`;
+ * positions_out: float64[n_out, 3]; errors: float64[n_out] (host or device).  The caller
+ * takes mean / max / bincount exactly like the reference (decimate.py:594-602). */
+int mf_quality_errors(mf_context *ctx, const mf_mesh_view *original, const mf_decimation *res,
+                      const int64_t *replace, int64_t n_out, const double *positions_out, int32_t einsum_order,
+                      double *errors, void *stream, mf_status *status);
+
 /* Per-kernel CUDA-event timing on the launching stream (mode 0 off, 1 all, 2 only `only`). */
 void mf_profile(int32_t mode, const char *only);
 int32_t mf_profile_read(char *names, int32_t name_cap, double *total_ms, int64_t *launches, int32_t cap);

@@ -613,6 +613,29 @@ void mfo_vertex_quadrics(const double *P, int64_t n, const int64_t *F, int64_t m
     omesh g = {n, m, 0, (double *)P, (int64_t *)F, NULL};
     vertex_quadrics(&g, order, Q13);
 }
+/* quality_report (decimate.py:580-602) up to the numpy reductions: the original
+ * vertex quadrics (quadrics.py:69-77) summed per cluster in vertex order from +0.0
+ * (accumulate_quadrics, quadrics.py:80-86), evaluated at the output positions
+ * (Quadric.evaluate, quadrics.py:53-58). */
+int mfo_quality_errors(const double *P, int64_t n, const int64_t *F, int64_t m, const int64_t *replace,
+                       int64_t n_out, const double *Pout, int order, double *errors) {
+    double *Q = (double *)xmalloc((size_t)(n ? n : 1) * QW * sizeof(double));
+    double *acc = (double *)xcalloc((size_t)(n_out ? n_out : 1) * QW, sizeof(double));
+    omesh g = {n, m, 0, (double *)P, (int64_t *)F, NULL};
+    vertex_quadrics(&g, order, Q);
+    for (int64_t v = 0; v < n; v++) {
+        int64_t r = replace[v];
+        if (r < 0 || r >= n_out) { free(Q); free(acc); return 2; }
+        for (int k = 0; k < QW; k++) acc[QW * r + k] += Q[QW * v + k];
+    }
+    for (int64_t r = 0; r < n_out; r++) {
+        const double *q = acc + QW * r;
+        errors[r] = q_evaluate(q, q + 9, q[12], Pout + 3 * r, order);
+    }
+    free(Q); free(acc);
+    return 0;
+}
+
 int64_t mfo_edge_costs(const double *P, int64_t n, const int64_t *F, int64_t m, int order, int64_t *edges_out,
                        double *cost_out) {
     omesh g = {n, m, 0, (double *)P, (int64_t *)F, NULL};

@@ -24,6 +24,8 @@ void mfo_result_copy(const mfo_result *r, double *positions, int64_t *facets, do
                      int64_t *mapping);
 void mfo_result_free(mfo_result *r);
 void mfo_vertex_quadrics(const double *P, int64_t n, const int64_t *F, int64_t m, int order, double *Q13);
+int mfo_quality_errors(const double *P, int64_t n, const int64_t *F, int64_t m, const int64_t *replace,
+                       int64_t n_out, const double *Pout, int order, double *errors);
 int64_t mfo_edge_costs(const double *P, int64_t n, const int64_t *F, int64_t m, int order, int64_t *edges_out,
                        double *cost_out);
 void mfo_pcg64_random(const uint64_t pcg[4], int64_t n, double *out);

@@ -68,6 +68,9 @@ def lib():
         L.mfo_result_copy.argtypes = [ctypes.c_void_p, _f64p, _i64p, _f64p, _i64p, _i64p]
         L.mfo_result_free.argtypes = [ctypes.c_void_p]
         L.mfo_vertex_quadrics.argtypes = [_f64p, ctypes.c_int64, _i64p, ctypes.c_int64, ctypes.c_int, _f64p]
+        L.mfo_quality_errors.argtypes = [_f64p, ctypes.c_int64, _i64p, ctypes.c_int64, _i64p, ctypes.c_int64, _f64p,
+                                         ctypes.c_int, _f64p]
+        L.mfo_quality_errors.restype = ctypes.c_int
         L.mfo_edge_costs.restype = ctypes.c_int64
         L.mfo_edge_costs.argtypes = [_f64p, ctypes.c_int64, _i64p, ctypes.c_int64, ctypes.c_int, _i64p, _f64p]
         L.mfo_pcg64_random.argtypes = [_u64p, ctypes.c_int64, _f64p]
@@ -107,6 +110,20 @@ def vertex_quadrics(positions, facets, order=0) -> np.ndarray:
     Q = np.zeros((len(P), 13))
     lib().mfo_vertex_quadrics(_p(P, _f64p), len(P), _p(F, _i64p), len(F), order, _p(Q, _f64p))
     return Q
+
+
+def quality_errors(positions, facets, replace, positions_out, order=0) -> np.ndarray:
+    """quality_report's per-output-vertex errors (decimate.py:580-602 before the numpy reductions)."""
+    P = np.ascontiguousarray(positions, dtype=np.float64)
+    F = np.ascontiguousarray(facets, dtype=np.int64).reshape(-1, 3)
+    R = np.ascontiguousarray(replace, dtype=np.int64)
+    Po = np.ascontiguousarray(positions_out, dtype=np.float64).reshape(-1, 3)
+    err = np.zeros(len(Po))
+    rc = lib().mfo_quality_errors(_p(P, _f64p), len(P), _p(F, _i64p), len(F), _p(R, _i64p), len(Po), _p(Po, _f64p),
+                                  order, _p(err, _f64p))
+    if rc:
+        raise ValueError("replace holds indices outside [0, n_out)")
+    return err
 
 
 def edge_costs(positions, facets, order=0):

@@ -17,6 +17,7 @@ from .decimate import (
 from .errors import InfeasibleTargetError, MeshError, NativeError, StructuralError
 from .mesh import BatchedMesh, TriMesh, concat_batch
 from .pooling import POOL_MODES, pool, pool_backward, unpool, unpool_backward
+from .quality import QualityReport, quality_report
 
 __version__ = "0.1.0"
 
@@ -28,6 +29,7 @@ __all__ = [
     "MeshError",
     "NativeError",
     "POOL_MODES",
+    "QualityReport",
     "StructuralError",
     "TriMesh",
     "VertexCluster",
@@ -36,6 +38,7 @@ __all__ = [
     "decimate_parallel",
     "pool",
     "pool_backward",
+    "quality_report",
     "representative_vertices",
     "round_targets",
     "unpool",

@@ -99,6 +99,9 @@ def lib():
         L.mf_unpool.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _i32, _i64, _vp, _vp, ctypes.POINTER(Status)]
         L.mf_unpool.restype = ctypes.c_int
         L.mf_round_targets.argtypes = [_i64, _i64, _i32, ctypes.POINTER(_i64), _i64]
+        L.mf_quality_errors.argtypes = [_vp, ctypes.POINTER(MeshView), _vp, _vp, _i64, _vp, _i32, _vp, _vp,
+                                        ctypes.POINTER(Status)]
+        L.mf_quality_errors.restype = ctypes.c_int
         L.mf_round_targets.restype = _i64
         L.mf_kernel_launch_count.argtypes = [_i32]
         L.mf_kernel_launch_count.restype = _i64

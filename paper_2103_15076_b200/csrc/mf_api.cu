@@ -310,6 +310,58 @@ int mf_unpool(mf_context* ctx, const mf_decimation* res, const int64_t* replace,
     return rc;
 }
 
+/* quality_report errors (decimate.py:580-602) */
+int mf_quality_errors(mf_context* ctx, const mf_mesh_view* original, const mf_decimation* res, const int64_t* replace,
+                      int64_t n_out, const double* positions_out, int32_t einsum_order, double* errors, void* stream,
+                      mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || !original) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "context and original mesh are required");
+        return st->code;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    const int64_t n = original->n;
+    const int* d_off = nullptr;
+    const int* d_mem = nullptr;
+    void* blk_r = nullptr;
+    void* blk_csr = nullptr;
+    int rc = MF_OK;
+    if (res) {
+        Result& r = const_cast<mf_decimation*>(res)->r;
+        if (r.n_in != n || r.n_out != n_out) {
+            st->code = MF_ERR_VALUE;
+            snprintf(st->message, sizeof(st->message), "result does not belong to this mesh (%lld -> %lld vertices)",
+                     (long long)r.n_in, (long long)r.n_out);
+            return st->code;
+        }
+        if (!r.csr_block) {
+            int *o, *mm;
+            if ((rc = build_cluster_csr(&ctx->c, r.replace, r.n_in, r.n_out, &o, &mm, &r.csr_block, s, st)))
+                return rc;
+            r.csr_off = o;
+            r.csr_members = mm;
+        }
+        d_off = r.csr_off;
+        d_mem = r.csr_members;
+    } else {
+        int *r32, *cnt;
+        if ((rc = upload_replace(&ctx->c, replace, n, n_out, 1, &r32, &cnt, &blk_r, s, st))) goto done;
+        int *o, *mm;
+        if ((rc = build_cluster_csr(&ctx->c, r32, n, n_out, &o, &mm, &blk_csr, s, st))) goto done;
+        d_off = o;
+        d_mem = mm;
+    }
+    rc = quality_run(&ctx->c, original, d_off, d_mem, n_out, positions_out, einsum_order, errors, s, st);
+done:
+    if (blk_r) cudaFreeAsync(blk_r, s);
+    if (blk_csr) cudaFreeAsync(blk_csr, s);
+    return rc;
+}
+
 int32_t mf_decimation_round_stats(const mf_decimation* res, int64_t* out, int32_t cap_rounds) {
     if (!res) return -1;
     int32_t R = (int32_t)(res->r.round_stats.size() / 6);

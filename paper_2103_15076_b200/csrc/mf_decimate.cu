@@ -536,8 +536,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     int* foff_n = W.foff_b;
     const int order = p.order;
     int* d_heavy_n = W.counters + 4;
-    int* d_heavy_c = W.counters + 12;
     int* d_mid_n = W.counters + 20;
+    int* d_heavy_c = W.counters + 12;
     int* d_scratch_used = W.counters + 24;
     for (int r = 0; r < R; r++) {
         const int N = p.h_N[r];
@@ -591,21 +591,21 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_seed_keys, grid_for(ctx, (Ecap + kSeedRun - 1) / kSeedRun), 256, 0, stream, d_abort, dE, W.cost, W.e0,
                    vmesh, W.eoff, voff_r, W.mlo, W.mhi, p.pcg[0], p.pcg[1], p.pcg[2], p.pcg[3], W.key_hi, W.key_lo);
         }
+        // large meshes: locally-dominant rounds first (round 0's picks written by k_adj_rank),
+        // then Suitor proposals on the residual frontier; smaller meshes: Suitor only
+        const bool use_ld = N >= p.ld_min;
         if (seeded)
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
-                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur);
+                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         else
             LAUNCH(k_adj_rank<false>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
-                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur);
-        // large meshes: locally-dominant rounds (persistent) first, then Suitor proposals on the
-        // residual frontier; small meshes: Suitor only (the grid barriers would dominate)
-        const bool use_ld = N >= p.ld_min;
+                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         if (use_ld) {
             LDArgs la{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
                       W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, kLDRounds, d_abort, W.acur};
             LAUNCH(k_ld_init, grid_for(ctx, N), 256, 0, stream, la);
             for (int round = 0; round < kLDRounds; round++) {
-                LAUNCH(k_ld_pick, grid_for(ctx, N), 256, 0, stream, la, round);
+                if (round > 0) LAUNCH(k_ld_pick, grid_for(ctx, N), 256, 0, stream, la, round);
                 LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, round);
             }
         }
@@ -732,6 +732,117 @@ static bool use_graphs() {
         v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
+}
+
+// ------------------------------------------------------------------------
+// quality_report errors (decimate.py:580-602): the ORIGINAL mesh's vertex
+// quadrics through the round kernels (facet planes, corner-major incidence
+// CSR, ordered fold), then the cluster fold + evaluation (k_quality).
+// d_off / d_mem: cluster CSR of replace over the original vertices.
+int quality_run(Context* ctx, const mf_mesh_view* mv, const int* d_off, const int* d_mem, int64_t n_out,
+                const double* positions_out, int order, double* errors, cudaStream_t stream, mf_status* st) {
+    const int64_t n = mv->n, m = mv->m;
+    if (n >= (int64_t)INT32_MAX - 1 || 6 * m >= (int64_t)INT32_MAX - 1) {
+        st->code = MF_ERR_LIMIT;
+        snprintf(st->message, sizeof(st->message), "mesh too large for 32-bit device indices");
+        return st->code;
+    }
+    const int N = (int)n, Mc = (int)std::max<int64_t>(m, 1);
+    const int scan_words = (int)((std::max<int64_t>(n, 1) + 1) / kScanTile + 4);
+    Arena me;
+    me.measuring = true;
+    auto lay = [&](Arena& A, WS& W, int64_t*& vo, double*& Pin, double*& Pout, double*& err, int*& misc) {
+        misc = A.take<int>(64);  // [0] abort [1] bad facet [2] m [3] act [8..] counters
+        vo = A.take<int64_t>(4);
+        W.F64 = A.take<int64_t>((size_t)Mc * 3);
+        W.F0 = A.take<int>((size_t)Mc * 3);
+        Pin = A.take<double>((size_t)std::max<int64_t>(n, 1) * 3);
+        Pout = A.take<double>((size_t)std::max<int64_t>(n_out, 1) * 3);
+        err = A.take<double>((size_t)std::max<int64_t>(n_out, 1));
+        W.plane = A.take<Plane>((size_t)Mc);
+        W.deg = A.take<int>((size_t)N + 1);
+        W.inc_off = A.take<int>((size_t)N + 1);
+        W.cursor = A.take<int>((size_t)N + 1);
+        W.inc = A.take<int>((size_t)Mc * 3);
+        W.inc_tmp = A.take<int>((size_t)Mc * 3);
+        W.vq = A.take<double>((size_t)std::max(N, 1) * 10);
+        W.nbr = A.take<int>((size_t)Mc * 6);
+        W.nbr_tmp = A.take<int>((size_t)Mc * 6);
+        W.ucnt = A.take<int>((size_t)N + 1);
+        W.upcnt = A.take<int>((size_t)N + 1);
+        W.heavy = A.take<int>((size_t)N + 1);
+        W.mid = A.take<int>((size_t)N + 1);
+        W.scan.words = scan_words;
+        W.scan.buf[0] = A.take<unsigned long long>((size_t)scan_words);
+        W.scan.buf[1] = A.take<unsigned long long>((size_t)scan_words);
+    };
+    WS W;
+    int64_t* d_vo;
+    double *d_P, *d_Pout, *d_err;
+    int* misc;
+    lay(me, W, d_vo, d_P, d_Pout, d_err, misc);
+    void* block = nullptr;
+    MF_CUDA_TRY(cudaMallocAsync(&block, me.off, stream));
+    Arena A;
+    A.base = (char*)block;
+    A.cap = me.off;
+    lay(A, W, d_vo, d_P, d_Pout, d_err, misc);
+    int rc = MF_OK;
+    int h_misc[4] = {0, 0x7f7f7f7f, (int)m, 1};
+    int64_t h_vo[4] = {0, n, 0, m};
+    auto fail = [&](cudaError_t e) {
+        st->code = rc = MF_ERR_CUDA;
+        snprintf(st->message, sizeof(st->message), "%s", cudaGetErrorString(e));
+    };
+    cudaError_t e = cudaSuccess;
+#define QTRY(x)                               \
+    do {                                      \
+        if ((e = (x)) != cudaSuccess) {       \
+            fail(e);                          \
+            goto done;                        \
+        }                                     \
+    } while (0)
+    QTRY(cudaMemsetAsync(misc, 0, 64 * sizeof(int), stream));
+    QTRY(cudaMemcpyAsync(misc, h_misc, sizeof(h_misc), cudaMemcpyHostToDevice, stream));
+    QTRY(cudaMemcpyAsync(d_vo, h_vo, sizeof(h_vo), cudaMemcpyHostToDevice, stream));
+    QTRY(cudaMemsetAsync(W.deg, 0, ((size_t)N + 1) * 4, stream));
+    QTRY(cudaMemsetAsync(W.cursor, 0, ((size_t)N + 1) * 4, stream));
+    QTRY(cudaMemsetAsync(W.scan.buf[0], 0, (size_t)scan_words * 8, stream));
+    QTRY(cudaMemsetAsync(W.scan.buf[1], 0, (size_t)scan_words * 8, stream));
+    if (n) QTRY(cudaMemcpyAsync(d_P, mv->positions, (size_t)n * 24, cudaMemcpyDefault, stream));
+    if (n_out) QTRY(cudaMemcpyAsync(d_Pout, positions_out, (size_t)n_out * 24, cudaMemcpyDefault, stream));
+    if (m) {
+        QTRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 24, cudaMemcpyDefault, stream));
+        LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, W.F0, 1, d_vo, d_vo + 2, misc + 1);
+        LAUNCH(k_facet_plane, grid_for(ctx, m), 256, 0, stream, misc, W.F0, d_P, misc + 2, (const int*)nullptr,
+               misc + 3, W.plane, W.deg, order);
+    }
+    if (n) {
+        run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", misc);
+        if (m) LAUNCH(k_inc_scatter, grid_for(ctx, m), 256, 0, stream, misc, W.F0, misc + 2, Mc, (const int*)nullptr,
+                      misc + 3, W.inc_off, W.cursor, W.inc);
+        LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, misc, N, W.inc_off, W.inc, W.F0, W.plane, Mc, W.vq,
+               W.nbr, W.ucnt, W.upcnt, W.mid, misc + 12, W.heavy, misc + 8);
+        LAUNCH(k_vertex, ctx->sm_count * 8, 256, 0, stream, misc, W.mid, misc + 12, W.inc_off, W.inc, W.F0, W.plane,
+               Mc, W.vq, W.nbr, W.ucnt, W.upcnt, W.heavy, misc + 8);
+        LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, misc, W.heavy, misc + 8, W.inc_off, W.inc, W.inc_tmp,
+               W.F0, W.plane, Mc, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
+    }
+    if (n_out) LAUNCH(k_quality, grid_for(ctx, n_out), 256, 0, stream, (int)n_out, d_off, d_mem, W.vq, d_Pout, order,
+                      d_err);
+    QTRY(cudaGetLastError());
+    if (n_out) QTRY(cudaMemcpyAsync(errors, d_err, (size_t)n_out * 8, cudaMemcpyDefault, stream));
+    QTRY(cudaMemcpyAsync(h_misc, misc, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    QTRY(cudaStreamSynchronize(stream));
+    if (m && h_misc[1] != 0x7f7f7f7f) {
+        st->code = rc = MF_ERR_STRUCTURAL;
+        snprintf(st->message, sizeof(st->message), "facet %d references an out-of-range vertex or repeats a vertex",
+                 h_misc[1]);
+    }
+done:
+#undef QTRY
+    cudaFreeAsync(block, stream);
+    return rc;
 }
 
 int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,

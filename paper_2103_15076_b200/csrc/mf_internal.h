@@ -74,6 +74,8 @@ int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c
              cudaStream_t stream, mf_status* st);
 int build_cluster_csr(Context* ctx, const int* d_replace, int64_t n, int64_t n_out, int** d_off, int** d_members,
                       void** block, cudaStream_t stream, mf_status* st);
+int quality_run(Context* ctx, const mf_mesh_view* mv, const int* d_off, const int* d_mem, int64_t n_out,
+                const double* positions_out, int order, double* errors, cudaStream_t stream, mf_status* st);
 
 // memory-space helper: true when p is device (or managed) memory on any device
 bool is_device_ptr(const void* p);

@@ -565,17 +565,31 @@ __global__ void __launch_bounds__(256) k_adj_rank(const int* __restrict__ abort_
                                                   const uint64_t* __restrict__ skey,
                                                   const uint64_t* __restrict__ key_hi,
                                                   const uint64_t* __restrict__ key_lo, unsigned* __restrict__ adj_k32,
-                                                  int* __restrict__ acur) {
+                                                  int* __restrict__ acur, int* __restrict__ best,
+                                                  int* __restrict__ bestu) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
     typedef typename std::conditional<SEEDED, uint64_t, unsigned>::type Lo;
+    // best / bestu (locally-dominant rounds only): every vertex's round-0 pick, i.e. its
+    // lowest-ranked edge -- nothing is matched yet, so the first LD pick pass is not needed
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         const size_t s = (size_t)aoff[v];
         const int nu = ucnt[v];
         if (nu > 8) {
-            for (int j = 0; j < nu; j++)
-                adj_k32[s + j] = (unsigned)((SEEDED ? key_hi[seid[s + j]] : skey[s + j]) >> 32);
+            uint64_t bh = ~0ull, bl = ~0ull;
+            int be = -1, bu = -1;
+            for (int j = 0; j < nu; j++) {
+                const int e = seid[s + j];
+                const uint64_t h = SEEDED ? key_hi[e] : skey[s + j];
+                const uint64_t l = SEEDED ? key_lo[e] : (uint64_t)(unsigned)e;
+                adj_k32[s + j] = (unsigned)(h >> 32);
+                if (key_lt(h, l, bh, bl)) { bh = h; bl = l; be = e; bu = snbr[s + j]; }
+            }
             acur[v] = -1;
+            if (best) {
+                best[v] = be;
+                bestu[v] = bu;
+            }
             continue;
         }
         uint64_t h[8];
@@ -626,6 +640,10 @@ __global__ void __launch_bounds__(256) k_adj_rank(const int* __restrict__ abort_
                 adj_k32[s + i] = (unsigned)(h[i] >> 32);
             }
         acur[v] = 0;
+        if (best) {
+            best[v] = nu ? (int)(unsigned)lo[0] : -1;
+            bestu[v] = nu ? u[0] : -1;
+        }
     }
 }
 
@@ -1082,9 +1100,10 @@ __global__ void __launch_bounds__(256) k_ld_init(LDArgs a) {
     }
 }
 
-// phase A of round `round`: each frontier vertex picks its best live edge --
-// the first slot from its cursor whose neighbour is unmatched (rank-ordered
-// adjacency, k_adj_sort); unsorted (high-degree) vertices scan every slot.
+// phase A of round `round` >= 1 (round 0's picks come from k_adj_rank): each
+// frontier vertex whose previous pick died picks its best live edge -- the
+// first slot from its cursor whose neighbour is unmatched (rank-ordered
+// adjacency); unsorted (high-degree) vertices scan every slot.
 __global__ void __maxnreg__(48) k_ld_pick(LDArgs a, int round) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
@@ -1094,6 +1113,10 @@ __global__ void __maxnreg__(48) k_ld_pick(LDArgs a, int round) {
     const int* Fc = cur ? a.front1 : a.front0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int v = Fc[i];
+        // the previous pick stays the best live edge while its other end is unmatched
+        // (edges only die): no adjacency reads for those frontier vertices
+        const int pu = a.bestu[v];
+        if (pu >= 0 && a.mate[pu] < 0) continue;
         const size_t s = (size_t)a.aoff[v];
         const int nu = a.ucnt[v];
         int be = -1, bu = -1;
@@ -1222,7 +1245,7 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigne
 // Output per segment: mode 1 = all, 2 = none, 3 = keys <= (thr_hi, thr_lo).
 constexpr int kSelBits = 11;
 constexpr int kSelBins = 1 << kSelBits;
-constexpr int kSelCap = 4096;  // keys held in shared memory (64 KiB)
+constexpr int kSelCap = 4096;  // keys held in shared memory (64 KiB; a larger carve-out measured slower)
 constexpr int kSelThreads = 1024;
 constexpr int kSelSmem = kSelBins * 4 + 2 * kSelCap * 8;
 
@@ -1269,6 +1292,10 @@ MF_DEV void warp_orand(uint64_t& oh, uint64_t& ol, uint64_t& ah, uint64_t& al) {
         al &= __shfl_xor_sync(0xffffffffu, al, o);
     }
 }
+
+// Histogram increment (plain shared-memory atomic: warp-aggregating the
+// contended leading digits measured slower than the conflicts it saves).
+MF_DEV void hist_add(int* hist, int d) { atomicAdd(hist + d, 1); }
 
 struct SelectArgs {
     const uint64_t* chi;
@@ -1343,6 +1370,32 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
         bool in_smem = false;
         int n_s = 0;
         bool done = false;
+        if (!a.resume && cnt <= kSelCap) {
+            // the whole segment fits: one coalesced load, and the bits every key shares are
+            // skipped before the first pass
+            uint64_t oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+            if (threadIdx.x < 4) s_oa[threadIdx.x] = (threadIdx.x < 2) ? 0ull : ~0ull;
+            for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+                const uint64_t h = a.chi[c0 + i], l = a.clo[c0 + i];
+                sh[i] = h;
+                sl[i] = l;
+                oh |= h; ol |= l; ah &= h; al &= l;
+            }
+            __syncthreads();
+            warp_orand(oh, ol, ah, al);
+            if ((threadIdx.x & 31) == 0) {
+                atomicOr(s_oa, oh); atomicOr(s_oa + 1, ol);
+                atomicAnd(s_oa + 2, ah); atomicAnd(s_oa + 3, al);
+            }
+            __syncthreads();
+            unsigned __int128 p0 = 0;
+            sel_skip(p0, top, s_oa[0], s_oa[1], s_oa[2], s_oa[3]);
+            phi = (uint64_t)(p0 >> 64);
+            plo = (uint64_t)p0;
+            n_s = cnt;
+            in_smem = true;
+            __syncthreads();
+        }
         if (a.resume && *sel_stop(a.gscr)) {  // the multi-block passes left the bucket in the buffer
             n_s = *sel_count(a.gscr);
             const uint64_t* buf = sel_buf(a.gscr);
@@ -1363,7 +1416,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
             if (in_smem) {
                 for (int i = threadIdx.x; i < n_s; i += blockDim.x)
                     if (sel_prefix(sh[i], sl[i], phi, plo, top)) {
-                        atomicAdd(hist + sel_digit(sh[i], sl[i], shift, width), 1);
+                        hist_add(hist, sel_digit(sh[i], sl[i], shift, width));
                         oh |= sh[i]; ol |= sl[i]; ah &= sh[i]; al &= sl[i];
                     }
             } else {
@@ -1371,7 +1424,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
                 for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
                     uint64_t h = a.chi[i], l = a.clo[i];
                     if (sel_prefix(h, l, phi, plo, top)) {
-                        atomicAdd(hist + sel_digit(h, l, shift, width), 1);
+                        hist_add(hist, sel_digit(h, l, shift, width));
                         oh |= h; ol |= l; ah &= h; al &= l;
                     }
                 }
@@ -1498,14 +1551,14 @@ __global__ void __cluster_dims__(kClCTAs, 1, 1) __launch_bounds__(kClThreads) k_
         if (in_smem) {
             for (int i = threadIdx.x; i < n_s; i += blockDim.x)
                 if (sel_prefix(sh[i], sl[i], phi, plo, top)) {
-                    atomicAdd(hist + sel_digit(sh[i], sl[i], shift, width), 1);
+                    hist_add(hist, sel_digit(sh[i], sl[i], shift, width));
                     oh |= sh[i]; ol |= sl[i]; ah &= sh[i]; al &= sl[i];
                 }
         } else {
             for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
                 const uint64_t h = a.chi[i], l = a.clo[i];
                 if (sel_prefix(h, l, phi, plo, top)) {
-                    atomicAdd(hist + sel_digit(h, l, shift, width), 1);
+                    hist_add(hist, sel_digit(h, l, shift, width));
                     oh |= h; ol |= l; ah &= h; al &= l;
                 }
             }
@@ -1631,7 +1684,7 @@ __global__ void __launch_bounds__(512) k_sel_hist(SelectArgs a, int* __restrict_
     for (int i = c0 + blockIdx.x * blockDim.x + threadIdx.x; i < c1; i += gridDim.x * blockDim.x) {
         uint64_t hh = a.chi[i], ll = a.clo[i];
         if (sel_prefix(hh, ll, phi, plo, top)) {
-            atomicAdd(h + sel_digit(hh, ll, shift, width), 1);
+            hist_add(h, sel_digit(hh, ll, shift, width));
             oh |= hh; ol |= ll; ah &= hh; al &= ll;
             if (compact) {
                 const int slot = atomicAdd(sel_count(ghist), 1);
@@ -2103,6 +2156,40 @@ __global__ void __launch_bounds__(256) k_contract_heavy(const int* __restrict__ 
             else fold_members<0>(m, d, P, X, C, vq, r, Pout, Xout);
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------
+// quality_report (decimate.py:580-602): cluster quadric = sum of the members'
+// original vertex quadrics in ascending member order from +0.0
+// (accumulate_quadrics, quadrics.py:80-86), evaluated at the output position
+// (Quadric.evaluate, quadrics.py:53-58: row-major quadratic form, einsum-order
+// linear term).  One thread per output vertex over the cluster CSR.
+__global__ void k_quality(int n_out, const int* __restrict__ off, const int* __restrict__ members,
+                          const double* __restrict__ vq, const double* __restrict__ Pout, int order,
+                          double* __restrict__ err) {
+    MF_PDL_ENTRY;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_out; r += gridDim.x * blockDim.x) {
+        double acc[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int i = off[r]; i < off[r + 1]; i++) {
+            const double* q = vq + 10 * (size_t)members[i];
+#pragma unroll
+            for (int k = 0; k < 10; k++) acc[k] = acc[k] + q[k];
+        }
+        const double x0 = Pout[3 * (size_t)r], x1 = Pout[3 * (size_t)r + 1], x2 = Pout[3 * (size_t)r + 2];
+        const double a00 = acc[0], a01 = acc[1], a02 = acc[2], a11 = acc[3], a12 = acc[4], a22 = acc[5];
+        double quad = 0.0;
+        quad = quad + (x0 * a00) * x0;
+        quad = quad + (x0 * a01) * x1;
+        quad = quad + (x0 * a02) * x2;
+        quad = quad + (x1 * a01) * x0;
+        quad = quad + (x1 * a11) * x1;
+        quad = quad + (x1 * a12) * x2;
+        quad = quad + (x2 * a02) * x0;
+        quad = quad + (x2 * a12) * x1;
+        quad = quad + (x2 * a22) * x2;
+        const double lin = 2.0 * dot3(acc[6], acc[7], acc[8], x0, x1, x2, order);
+        err[r] = (quad + lin) + acc[9];
     }
 }
 
