@@ -125,6 +125,44 @@ int mf_unpool(mf_context *ctx, const mf_decimation *res, const int64_t *replace,
 
 int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t *chain, int64_t cap);
 
+/* Binary little-endian PLY bodies (io.py:226-431), decoded / encoded on the device.
+ * Field types: MF_PLY_I1 .. MF_PLY_F8 = PLY char, uchar, short, ushort, int, uint, float, double. */
+enum { MF_PLY_I1 = 0, MF_PLY_U1 = 1, MF_PLY_I2 = 2, MF_PLY_U2 = 3, MF_PLY_I4 = 4, MF_PLY_U4 = 5, MF_PLY_F4 = 6,
+       MF_PLY_F8 = 7 };
+typedef struct mf_ply_vertex_spec {
+    int32_t record_size;  /* bytes per vertex record */
+    int32_t offset[6];    /* byte offsets of x y z red green blue in a record (-1: absent) */
+    int32_t type[6];      /* MF_PLY_* of each field */
+} mf_ply_vertex_spec;
+/* body: bytes after end_header (host or device).  Vertex records start at byte 0,
+ * uniform-arity face records (uchar count + arity indices of index_type) at face_offset.
+ * Outputs: positions float64[nv, 3]; features float64[nv, n_channels] (3 = copy of the
+ * positions, 6 = + colours c / 255 * 2 - 1, io.py:390-392); facets int64[n_faces *
+ * (arity - 2), 3] fan-triangulated (io.py:92-93).  Replaces io.py:277-306 + 329-344. */
+int mf_ply_decode(mf_context *ctx, const uint8_t *body, int64_t body_len, int64_t n_vertices,
+                  const mf_ply_vertex_spec *vertex_spec, int64_t face_offset, int64_t n_faces, int32_t arity,
+                  int32_t index_type, double *positions, double *features, int32_t n_channels, int64_t *facets,
+                  void *stream, mf_status *status);
+/* _save_ply body (io.py:404-431): n vertex records (float32 xyz, + uchar rgb when
+ * features has >= 6 channels) then m records (uchar 3, int32 x3); body must hold
+ * n * (12 or 15) + m * 13 bytes (host or device). */
+int mf_ply_encode(mf_context *ctx, const double *positions, int64_t n, const double *features, int64_t c,
+                  const int64_t *facets, int64_t m, uint8_t *body, void *stream, mf_status *status);
+
+/* vertex_facet_adjacency (mesh.py:114-122): offsets int64[n+1], facet_ids int64[3m]
+ * (each vertex's facets ascending).  facets: int64[m, 3]; host or device pointers. */
+int mf_vertex_facet_adjacency(mf_context *ctx, const int64_t *facets, int64_t m, int64_t n, int64_t *offsets,
+                              int64_t *facet_ids, void *stream, mf_status *status);
+/* facet2vertex_forward (conv.py:222-250), strided when vertex_ids != NULL (rows = len,
+ * e.g. representative_vertices(result), decimate.py:118-123): out[rows, C*L] in the
+ * features' dtype.  offsets / facet_ids: the adjacency over n vertices; features
+ * [m, C] (MF_DTYPE_F32/F64); weights float64[T, C, L] already rounded to the features'
+ * dtype (kernel.weights.astype(dtype), conv.py:241); coeff float64[m, T]. */
+int mf_facet2vertex(mf_context *ctx, const int64_t *offsets, int64_t n, const int64_t *facet_ids,
+                    const void *features, int32_t dtype, int64_t m, int64_t c, const double *weights, int64_t t,
+                    int64_t multiplier, const double *coeff, const int64_t *vertex_ids, int64_t rows, void *out,
+                    void *stream, mf_status *status);
+
 /* quality_report's per-output-vertex error (replaces decimate.py:580-602 up to the
  * numpy reductions): cluster quadric of the ORIGINAL mesh's vertex quadrics (summed in
  * ascending member order, accumulate_quadrics quadrics.py:80-86) evaluated at the output

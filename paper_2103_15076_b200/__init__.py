@@ -14,8 +14,10 @@ from .decimate import (
     representative_vertices,
     round_targets,
 )
-from .errors import InfeasibleTargetError, MeshError, NativeError, StructuralError
+from .conv import ConvKernel, VertexFacetAdjacency, facet2vertex_forward, vertex_facet_adjacency
+from .errors import InfeasibleTargetError, MeshError, MeshFormatError, NativeError, StructuralError
 from .mesh import BatchedMesh, TriMesh, concat_batch
+from .meshio import load_mesh, save_clusters, save_mesh
 from .pooling import POOL_MODES, pool, pool_backward, unpool, unpool_backward
 from .quality import QualityReport, quality_report
 
@@ -23,24 +25,32 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BatchedMesh",
+    "ConvKernel",
     "DecimationConfig",
     "DecimationResult",
     "InfeasibleTargetError",
     "MeshError",
+    "MeshFormatError",
     "NativeError",
     "POOL_MODES",
     "QualityReport",
     "StructuralError",
     "TriMesh",
+    "VertexFacetAdjacency",
     "VertexCluster",
     "clusters",
     "concat_batch",
     "decimate_parallel",
+    "facet2vertex_forward",
+    "load_mesh",
     "pool",
     "pool_backward",
     "quality_report",
     "representative_vertices",
     "round_targets",
+    "save_clusters",
+    "save_mesh",
     "unpool",
     "unpool_backward",
+    "vertex_facet_adjacency",
 ]

@@ -102,6 +102,16 @@ def lib():
         L.mf_quality_errors.argtypes = [_vp, ctypes.POINTER(MeshView), _vp, _vp, _i64, _vp, _i32, _vp, _vp,
                                         ctypes.POINTER(Status)]
         L.mf_quality_errors.restype = ctypes.c_int
+        L.mf_ply_decode.argtypes = [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
+                                    ctypes.POINTER(Status)]
+        L.mf_ply_decode.restype = ctypes.c_int
+        L.mf_ply_encode.argtypes = [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, ctypes.POINTER(Status)]
+        L.mf_ply_encode.restype = ctypes.c_int
+        L.mf_vertex_facet_adjacency.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(Status)]
+        L.mf_vertex_facet_adjacency.restype = ctypes.c_int
+        L.mf_facet2vertex.argtypes = [_vp, _vp, _i64, _vp, _vp, _i32, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _i64,
+                                      _vp, _vp, ctypes.POINTER(Status)]
+        L.mf_facet2vertex.restype = ctypes.c_int
         L.mf_round_targets.restype = _i64
         L.mf_kernel_launch_count.argtypes = [_i32]
         L.mf_kernel_launch_count.restype = _i64

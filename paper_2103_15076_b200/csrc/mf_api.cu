@@ -310,6 +310,91 @@ int mf_unpool(mf_context* ctx, const mf_decimation* res, const int64_t* replace,
     return rc;
 }
 
+/* binary PLY bodies (io.py:226-431) */
+int mf_ply_decode(mf_context* ctx, const uint8_t* body, int64_t body_len, int64_t n_vertices,
+                  const mf_ply_vertex_spec* vspec, int64_t face_offset, int64_t n_faces, int32_t arity,
+                  int32_t index_type, double* positions, double* features, int32_t n_channels, int64_t* facets,
+                  void* stream, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    bool ok = ctx && vspec && n_vertices >= 0 && n_faces >= 0 && body_len >= 0 && (n_channels == 3 || n_channels == 6);
+    if (ok && n_vertices) ok = vspec->record_size > 0 && (int64_t)vspec->record_size * n_vertices <= body_len;
+    if (ok && n_faces) {
+        const int isz = index_type <= MF_PLY_U1 ? 1 : (index_type <= MF_PLY_U2 ? 2 : (index_type <= MF_PLY_U4 ? 4 : 8));
+        ok = arity >= 3 && index_type >= MF_PLY_I1 && index_type <= MF_PLY_U4 && face_offset >= 0 &&
+             face_offset + (int64_t)(1 + arity * isz) * n_faces <= body_len;
+    }
+    if (ok)
+        for (int k = 0; k < 6; k++) {
+            const int o = vspec->offset[k], t = vspec->type[k];
+            if ((k < 3 || n_channels == 6) && (o < 0 || t < MF_PLY_I1 || t > MF_PLY_F8 || o >= vspec->record_size)) ok = false;
+        }
+    if (!ok) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "invalid PLY layout (record sizes / offsets exceed the body)");
+        return st->code;
+    }
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    PlyVertexSpec vs;
+    vs.record = vspec->record_size;
+    for (int k = 0; k < 6; k++) {
+        vs.off[k] = (k < 3 || n_channels == 6) ? vspec->offset[k] : -1;
+        vs.type[k] = vspec->type[k];
+    }
+    return ply_decode_run(&ctx->c, body, body_len, n_vertices, vs, face_offset, n_faces, arity, index_type,
+                          positions, features, n_channels, facets, (cudaStream_t)stream, st);
+}
+
+int mf_ply_encode(mf_context* ctx, const double* positions, int64_t n, const double* features, int64_t c,
+                  const int64_t* facets, int64_t m, uint8_t* body, void* stream, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || n < 0 || m < 0 || (n && !positions) || (m && !facets) || (n + m && !body)) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "invalid PLY encode arguments");
+        return st->code;
+    }
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    return ply_encode_run(&ctx->c, positions, n, c >= 6 ? features : nullptr, c, facets, m, body,
+                          (cudaStream_t)stream, st);
+}
+
+/* vertex_facet_adjacency (mesh.py:114-122) */
+int mf_vertex_facet_adjacency(mf_context* ctx, const int64_t* facets, int64_t m, int64_t n, int64_t* offsets,
+                              int64_t* facet_ids, void* stream, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || m < 0 || n < 0 || (m && !facets) || !offsets || (m && !facet_ids)) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "invalid adjacency arguments");
+        return st->code;
+    }
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    return adjacency_run(&ctx->c, facets, m, n, offsets, facet_ids, (cudaStream_t)stream, st);
+}
+
+/* facet2vertex_forward (conv.py:222-250) */
+int mf_facet2vertex(mf_context* ctx, const int64_t* offsets, int64_t n, const int64_t* facet_ids, const void* features,
+                    int32_t dtype, int64_t m, int64_t c, const double* weights, int64_t t, int64_t multiplier,
+                    const double* coeff, const int64_t* vertex_ids, int64_t rows, void* out, void* stream,
+                    mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || n < 0 || m < 0 || c < 0 || t < 0 || multiplier < 0 || rows < 0 ||
+        (dtype != MF_DTYPE_F32 && dtype != MF_DTYPE_F64)) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "invalid facet2vertex arguments");
+        return st->code;
+    }
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    return f2v_run(&ctx->c, offsets, n, facet_ids, features, dtype, m, c, weights, t, multiplier, coeff, vertex_ids,
+                   rows, out, (cudaStream_t)stream, st);
+}
+
 /* quality_report errors (decimate.py:580-602) */
 int mf_quality_errors(mf_context* ctx, const mf_mesh_view* original, const mf_decimation* res, const int64_t* replace,
                       int64_t n_out, const double* positions_out, int32_t einsum_order, double* errors, void* stream,

@@ -74,6 +74,17 @@ int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c
              cudaStream_t stream, mf_status* st);
 int build_cluster_csr(Context* ctx, const int* d_replace, int64_t n, int64_t n_out, int** d_off, int** d_members,
                       void** block, cudaStream_t stream, mf_status* st);
+struct PlyVertexSpec;
+int ply_decode_run(Context* ctx, const unsigned char* body, int64_t body_len, int64_t nv, const PlyVertexSpec& vs,
+                   int64_t face_off, int64_t nf, int arity, int itype, double* P, double* X, int C, int64_t* F,
+                   cudaStream_t stream, mf_status* st);
+int ply_encode_run(Context* ctx, const double* P, int64_t n, const double* X, int64_t C, const int64_t* F, int64_t m,
+                   unsigned char* out, cudaStream_t stream, mf_status* st);
+int adjacency_run(Context* ctx, const int64_t* facets, int64_t m, int64_t n, int64_t* offsets, int64_t* facet_ids,
+                  cudaStream_t stream, mf_status* st);
+int f2v_run(Context* ctx, const int64_t* offsets, int64_t n, const int64_t* facet_ids, const void* X, int dtype,
+            int64_t m, int64_t C, const double* W, int64_t nt, int64_t L, const double* coeff,
+            const int64_t* vertex_ids, int64_t rows, void* out, cudaStream_t stream, mf_status* st);
 int quality_run(Context* ctx, const mf_mesh_view* mv, const int* d_off, const int* d_mem, int64_t n_out,
                 const double* positions_out, int order, double* errors, cudaStream_t stream, mf_status* st);
 

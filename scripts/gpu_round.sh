@@ -37,9 +37,13 @@ if [[ $PARTS == *ncu* ]]; then
   done
   for c in cfg2 cfg5; do
     timeout 1500 ncu --set full --clock-control none --import-source on \
-      -k regex:'k_suitor|k_vertex$|k_edges|k_facet_remap|k_select|k_inc_scatter|k_facet_plane' \
-      -s 40 -c 12 -f -o "$OUT/full_$c" \
-      python scripts/one_step.py --config $c --warmup 6 > "$OUT/full_$c.log" 2>&1
+      -k regex:'k_suitor|k_vertex_t|k_edges|k_adj_rank|k_ld_pick|k_facet_remap|k_select|k_inc_scatter|k_facet_plane|k_scan_excl' \
+      -s 0 -c 24 -f -o "$OUT/full_$c" \
+      python scripts/one_step.py --config $c --warmup 1 > "$OUT/full_$c.log" 2>&1
     echo "ncu full $c rc=$?"
+    # keep the merge-back small: CSV / text exports, the report itself only when small
+    ncu -i "$OUT/full_$c.ncu-rep" --page raw --csv > "$OUT/full_${c}_raw.csv" 2>/dev/null
+    ncu -i "$OUT/full_$c.ncu-rep" --page details > "$OUT/full_${c}_details.txt" 2>/dev/null
+    if [ $(stat -c %s "$OUT/full_$c.ncu-rep") -gt 20000000 ]; then rm -f "$OUT/full_$c.ncu-rep"; fi
   done
 fi

@@ -38,7 +38,11 @@ def kname(raw: str) -> str:
 
 
 def read(rep: str):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):  # a `--page raw --csv` export made next to the capture
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
     recs = []
