@@ -598,8 +598,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
                    W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         else
-            LAUNCH(k_adj_rank<false>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
-                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
+            LAUNCH(k_adj_rank_tiled, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
+                   W.skey, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         if (use_ld) {
             LDArgs la{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
                       W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, kLDRounds, d_abort, W.acur};
@@ -856,6 +856,43 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     const int B = p.B, R = p.R;
     const int64_t n = p.n, m = p.m, C = p.C;
     MF_CUDA_TRY(cudaSetDevice(ctx->device));
+    // Features that are a bitwise copy of the positions (the default, mesh.py:28-29) fold like
+    // the positions, so they need not be carried: decide on the device (one extra upload of the
+    // features instead of a host memcmp), then stage both from the device copies.
+    const void* P_src = mv->positions;
+    const void* X_src = mv->features;
+    void* alias_tmp = nullptr;
+    struct TmpFree {
+        void*& p;
+        cudaStream_t s;
+        ~TmpFree() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } tmp_free{alias_tmp, stream};
+    if (!p.alias && mv->features && p.fdtype == MF_DTYPE_F64 && C == 3 && p.placement == 0 && n > 0) {
+        const size_t b = (size_t)n * 24, ab = (b + 255) & ~size_t(255);
+        const bool pd = is_device_ptr(mv->positions), xd = is_device_ptr(mv->features);
+        MF_CUDA_TRY(cudaMallocAsync(&alias_tmp, (pd ? 0 : ab) + (xd ? 0 : ab) + 256, stream));
+        char* q = (char*)alias_tmp;
+        int* d_diff = (int*)q;
+        q += 256;
+        MF_CUDA_TRY(cudaMemsetAsync(d_diff, 0, 4, stream));
+        if (!pd) {
+            MF_CUDA_TRY(cudaMemcpyAsync(q, mv->positions, b, cudaMemcpyHostToDevice, stream));
+            P_src = q;
+            q += ab;
+        }
+        if (!xd) {
+            MF_CUDA_TRY(cudaMemcpyAsync(q, mv->features, b, cudaMemcpyHostToDevice, stream));
+            X_src = q;
+        }
+        LAUNCH(k_words_differ, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, (const unsigned long long*)P_src,
+               (const unsigned long long*)X_src, d_diff);
+        int h_diff = 1;
+        MF_CUDA_TRY(cudaMemcpyAsync(&h_diff, d_diff, 4, cudaMemcpyDeviceToHost, stream));
+        MF_CUDA_TRY(cudaStreamSynchronize(stream));
+        if (!h_diff) p.alias = true;
+    }
 
     // ---- workspace (grown on demand; cached graphs are tied to the arena address)
     WS W;
@@ -905,13 +942,13 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     // ---- stage params + inputs (outside the graph: host pointers / caller buffers change per call)
     MF_CUDA_TRY(cudaMemcpyAsync(W.params, hp, p.params_words * 4, cudaMemcpyHostToDevice, stream));
     MF_CUDA_TRY(cudaMemcpyAsync(W.vo64, h_o64, 2 * (size_t)(B + 1) * 8, cudaMemcpyHostToDevice, stream));
-    if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, mv->positions, (size_t)n * 24, cudaMemcpyDefault, stream));
+    if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, P_src, (size_t)n * 24, cudaMemcpyDefault, stream));
     if (m) MF_CUDA_TRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 24, cudaMemcpyDefault, stream));
     if (!p.alias && n * C > 0) {
         if (!mv->features)
-            MF_CUDA_TRY(cudaMemcpyAsync(W.X0, mv->positions, (size_t)n * 24, cudaMemcpyDefault, stream));
+            MF_CUDA_TRY(cudaMemcpyAsync(W.X0, P_src, (size_t)n * 24, cudaMemcpyDefault, stream));
         else if (p.fdtype == MF_DTYPE_F64)
-            MF_CUDA_TRY(cudaMemcpyAsync(W.X0, mv->features, (size_t)(n * C) * 8, cudaMemcpyDefault, stream));
+            MF_CUDA_TRY(cudaMemcpyAsync(W.X0, X_src, (size_t)(n * C) * 8, cudaMemcpyDefault, stream));
         else
             MF_CUDA_TRY(cudaMemcpyAsync(W.Xf32, mv->features, (size_t)(n * C) * 4, cudaMemcpyDefault, stream));
     }

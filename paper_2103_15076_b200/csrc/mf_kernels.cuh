@@ -558,6 +558,85 @@ __global__ void __launch_bounds__(256) k_edges(const int* __restrict__ abort_fla
 // scans compare prefixes and gather the full keys only on prefix ties.
 // Unseeded keys come from the slots (skey, secondary = edge id); seeded keys
 // are gathered once k_seed_keys has run.
+// Slots of one vertex at sn / se / sk / k32 (global or shared memory).
+template <bool SEEDED>
+MF_DEV void rank_one(int v, int nu, int* sn, int* se, const uint64_t* sk, const uint64_t* __restrict__ key_hi,
+                     const uint64_t* __restrict__ key_lo, unsigned* k32, int* __restrict__ acur,
+                     int* __restrict__ best, int* __restrict__ bestu) {
+    typedef typename std::conditional<SEEDED, uint64_t, unsigned>::type Lo;
+    if (nu > 8) {
+        uint64_t bh = ~0ull, bl = ~0ull;
+        int be = -1, bu = -1;
+        for (int j = 0; j < nu; j++) {
+            const int e = se[j];
+            const uint64_t h = SEEDED ? key_hi[e] : sk[j];
+            const uint64_t l = SEEDED ? key_lo[e] : (uint64_t)(unsigned)e;
+            k32[j] = (unsigned)(h >> 32);
+            if (key_lt(h, l, bh, bl)) { bh = h; bl = l; be = e; bu = sn[j]; }
+        }
+        acur[v] = -1;
+        if (best) {
+            best[v] = be;
+            bestu[v] = bu;
+        }
+        return;
+    }
+    uint64_t h[8];
+    Lo lo[8];
+    int u[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        h[i] = ~0ull;
+        lo[i] = (Lo)~0ull;
+        u[i] = -1;
+        if (i < nu) {
+            u[i] = sn[i];
+            const int e = se[i];
+            if (SEEDED) {
+                h[i] = key_hi[e];
+                lo[i] = (Lo)key_lo[e];
+            } else {
+                h[i] = sk[i];
+                lo[i] = (Lo)(unsigned)e;
+            }
+        }
+    }
+    // bitonic network over 8 register entries (keys are unique; padding sorts last)
+#pragma unroll
+    for (int k = 2; k <= 8; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = ((i & k) == 0);
+                    const bool gt = h[i] > h[ixj] || (h[i] == h[ixj] && lo[i] > lo[ixj]);
+                    if (gt == up) {
+                        uint64_t th = h[i]; h[i] = h[ixj]; h[ixj] = th;
+                        Lo tl = lo[i]; lo[i] = lo[ixj]; lo[ixj] = tl;
+                        int tu = u[i]; u[i] = u[ixj]; u[ixj] = tu;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+        if (i < nu) {
+            sn[i] = u[i];
+            se[i] = (int)(unsigned)lo[i];  // seeded key_lo carries the edge id in its low bits
+            k32[i] = (unsigned)(h[i] >> 32);
+        }
+    acur[v] = 0;
+    if (best) {
+        best[v] = nu ? (int)(unsigned)lo[0] : -1;
+        bestu[v] = nu ? u[0] : -1;
+    }
+}
+
+// best / bestu (locally-dominant rounds only): every vertex's round-0 pick, i.e. its
+// lowest-ranked edge -- nothing is matched yet, so the first LD pick pass is not needed.
 template <bool SEEDED>
 __global__ void __launch_bounds__(256) k_adj_rank(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ aoff, const int* __restrict__ ucnt,
@@ -569,81 +648,58 @@ __global__ void __launch_bounds__(256) k_adj_rank(const int* __restrict__ abort_
                                                   int* __restrict__ bestu) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    typedef typename std::conditional<SEEDED, uint64_t, unsigned>::type Lo;
-    // best / bestu (locally-dominant rounds only): every vertex's round-0 pick, i.e. its
-    // lowest-ranked edge -- nothing is matched yet, so the first LD pick pass is not needed
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         const size_t s = (size_t)aoff[v];
-        const int nu = ucnt[v];
-        if (nu > 8) {
-            uint64_t bh = ~0ull, bl = ~0ull;
-            int be = -1, bu = -1;
-            for (int j = 0; j < nu; j++) {
-                const int e = seid[s + j];
-                const uint64_t h = SEEDED ? key_hi[e] : skey[s + j];
-                const uint64_t l = SEEDED ? key_lo[e] : (uint64_t)(unsigned)e;
-                adj_k32[s + j] = (unsigned)(h >> 32);
-                if (key_lt(h, l, bh, bl)) { bh = h; bl = l; be = e; bu = snbr[s + j]; }
+        rank_one<SEEDED>(v, ucnt[v], snbr + s, seid + s, SEEDED ? nullptr : skey + s, key_hi, key_lo, adj_k32 + s,
+                         acur, best, bestu);
+    }
+}
+
+// Unseeded rounds: the same sort with the slots of 256 consecutive vertices (one
+// contiguous range of the compact adjacency) staged through shared memory, so
+// every global load / store is coalesced; a tile whose range exceeds the stage
+// (high-degree vertices) sorts in place in global memory.
+constexpr int kRankCap = 2048;
+__global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ abort_flag, int N,
+                                                        const int* __restrict__ aoff, const int* __restrict__ ucnt,
+                                                        int* __restrict__ snbr, int* __restrict__ seid,
+                                                        const uint64_t* __restrict__ skey,
+                                                        unsigned* __restrict__ adj_k32, int* __restrict__ acur,
+                                                        int* __restrict__ best, int* __restrict__ bestu) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    __shared__ int s_n[kRankCap], s_e[kRankCap];
+    __shared__ uint64_t s_k[kRankCap];
+    __shared__ unsigned s_32[kRankCap];
+    for (int v0 = blockIdx.x * blockDim.x; v0 < N; v0 += gridDim.x * blockDim.x) {
+        const int v1 = min(N, v0 + (int)blockDim.x);
+        const int base = aoff[v0], cnt = aoff[v1] - base;
+        const int v = v0 + threadIdx.x;
+        if (cnt > kRankCap) {
+            if (v < v1) {
+                const size_t s = (size_t)aoff[v];
+                rank_one<false>(v, ucnt[v], snbr + s, seid + s, skey + s, nullptr, nullptr, adj_k32 + s, acur, best,
+                                bestu);
             }
-            acur[v] = -1;
-            if (best) {
-                best[v] = be;
-                bestu[v] = bu;
-            }
-            continue;
+            continue;  // block-uniform
         }
-        uint64_t h[8];
-        Lo lo[8];
-        int u[8];
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            h[i] = ~0ull;
-            lo[i] = (Lo)~0ull;
-            u[i] = -1;
-            if (i < nu) {
-                u[i] = snbr[s + i];
-                const int e = seid[s + i];
-                if (SEEDED) {
-                    h[i] = key_hi[e];
-                    lo[i] = (Lo)key_lo[e];
-                } else {
-                    h[i] = skey[s + i];
-                    lo[i] = (Lo)(unsigned)e;
-                }
-            }
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            s_n[i] = snbr[base + i];
+            s_e[i] = seid[base + i];
+            s_k[i] = skey[base + i];
         }
-        // bitonic network over 8 register entries (keys are unique; padding sorts last)
-#pragma unroll
-        for (int k = 2; k <= 8; k <<= 1) {
-#pragma unroll
-            for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    const int ixj = i ^ j;
-                    if (ixj > i) {
-                        const bool up = ((i & k) == 0);
-                        const bool gt = h[i] > h[ixj] || (h[i] == h[ixj] && lo[i] > lo[ixj]);
-                        if (gt == up) {
-                            uint64_t th = h[i]; h[i] = h[ixj]; h[ixj] = th;
-                            Lo tl = lo[i]; lo[i] = lo[ixj]; lo[ixj] = tl;
-                            int tu = u[i]; u[i] = u[ixj]; u[ixj] = tu;
-                        }
-                    }
-                }
-            }
+        __syncthreads();
+        if (v < v1) {
+            const int o = aoff[v] - base;
+            rank_one<false>(v, ucnt[v], s_n + o, s_e + o, s_k + o, nullptr, nullptr, s_32 + o, acur, best, bestu);
         }
-#pragma unroll
-        for (int i = 0; i < 8; i++)
-            if (i < nu) {
-                snbr[s + i] = u[i];
-                seid[s + i] = (int)(unsigned)lo[i];  // seeded key_lo carries the edge id in its low bits
-                adj_k32[s + i] = (unsigned)(h[i] >> 32);
-            }
-        acur[v] = 0;
-        if (best) {
-            best[v] = nu ? (int)(unsigned)lo[0] : -1;
-            bestu[v] = nu ? u[0] : -1;
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            snbr[base + i] = s_n[i];
+            seid[base + i] = s_e[i];
+            adj_k32[base + i] = s_32[i];
         }
+        __syncthreads();
     }
 }
 
@@ -2394,6 +2450,15 @@ __global__ void k_i32_to_i64(int64_t n, const int* __restrict__ a, int64_t* __re
     MF_PDL_ENTRY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = (int64_t)a[i] + add;
+}
+// any differing 64-bit word -> *diff = 1 (features-are-positions check, mesh.py:28-29)
+__global__ void k_words_differ(int64_t n, const unsigned long long* __restrict__ a,
+                               const unsigned long long* __restrict__ b, int* __restrict__ diff) {
+    MF_PDL_ENTRY;
+    bool d = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d |= a[i] != b[i];
+    if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) *diff = 1;
 }
 __global__ void k_f64_to_f32(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
     MF_PDL_ENTRY;

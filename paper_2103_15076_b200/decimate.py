@@ -134,8 +134,9 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     P = np.ascontiguousarray(base.positions, dtype=np.float64)
     F = np.ascontiguousarray(base.facets, dtype=np.int64)
     X = base.features
-    same = X.dtype == np.float64 and X.shape == P.shape and X.flags.c_contiguous and hostmem.same_bytes(X, P)
-    Xc = None if same else np.ascontiguousarray(X)
+    # features that are a bitwise copy of the positions (mesh.py:28-29) are detected on the
+    # device (mf_decimate), so they are always handed over
+    Xc = None if X is P else np.ascontiguousarray(X)
     view = _native.MeshView()
     view.positions = P.ctypes.data
     view.facets = F.ctypes.data if F.size else None
