@@ -15,11 +15,20 @@
 // predecessor grid (griddepcontrol.wait is a no-op without a programmatic
 // edge) and then lets its own dependents start launching, so a graph node's
 // launch and prologue overlap the previous node's tail.
+#ifdef MF_PDL_EARLY_TRIGGER
 #define MF_PDL_ENTRY                                              \
     do {                                                          \
         asm volatile("griddepcontrol.wait;" ::: "memory");        \
         asm volatile("griddepcontrol.launch_dependents;" :::);    \
     } while (0)
+#else
+// no explicit trigger: a block triggers its dependents when it exits, so a
+// dependent grid's CTAs never compete with the primary's unlaunched CTAs
+#define MF_PDL_ENTRY                                              \
+    do {                                                          \
+        asm volatile("griddepcontrol.wait;" ::: "memory");        \
+    } while (0)
+#endif
 
 namespace mf {
 
@@ -103,8 +112,19 @@ MF_DEV void grid_sync(unsigned* bar) {
 // out[i] = sum(in[0..i)), out[n] = total.  `status` must hold ceil(n/TILE)
 // zeroed words and `ticket` one zeroed int (both reset with one memset).
 constexpr int kScanBlock = 256;
-constexpr int kScanItems = 8;
+constexpr int kScanItems = 8;                      // items per thread for plain array loads
 constexpr int kScanTile = kScanBlock * kScanItems;
+constexpr int kScanTileMin = kScanBlock * 2;       // smallest tile (gathering load functors): sizes the state
+// items per thread of a load functor: LoadOp::items when it declares one (functors whose
+// load is a chain of dependent gathers use short tiles -- more CTAs in flight), else 8
+template <typename T, typename = void>
+struct ScanItems {
+    static constexpr int value = kScanItems;
+};
+template <typename T>
+struct ScanItems<T, decltype((void)T::items, void())> {
+    static constexpr int value = T::items;
+};
 
 constexpr unsigned long long kFlagAgg = 1ull << 32;
 constexpr unsigned long long kFlagPre = 2ull << 32;
@@ -131,11 +151,12 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, in
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
     const int tile = s_tile;
-    const long long base = (long long)tile * kScanTile + (long long)threadIdx.x * kScanItems;
-    int v[kScanItems];
+    constexpr int kItems = ScanItems<LoadOp>::value;
+    const long long base = (long long)tile * (kScanBlock * kItems) + (long long)threadIdx.x * kItems;
+    int v[kItems];
     int tsum = 0;
 #pragma unroll
-    for (int i = 0; i < kScanItems; i++) {
+    for (int i = 0; i < kItems; i++) {
         long long idx = base + i;
         v[i] = (idx < n) ? load((int)idx) : 0;
         tsum += v[i];
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, in
     __syncthreads();
     int run = s_prefix + s_warp[warp] + (incl - tsum);
 #pragma unroll
-    for (int i = 0; i < kScanItems; i++) {
+    for (int i = 0; i < kItems; i++) {
         long long idx = base + i;
         if (idx < n) {
             out[idx] = run;

@@ -162,6 +162,15 @@ static bool select_cluster() {
     return v == 1;
 }
 
+static int select_cap() {  // MF_SEL_CAP: keys in k_select's shared-memory stage (A/B runs)
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SEL_CAP");
+        v = e ? std::max(kSelCap, std::min(kSelCapMax, atoi(e))) : kSelCap;
+    }
+    return v;
+}
+
 static int grid_for(const Context* ctx, int64_t n, int block = 256) {
     int64_t g = (n + block - 1) / block;
     int64_t cap = (int64_t)ctx->sm_count * 16;
@@ -208,7 +217,8 @@ struct ScanBuf {
 template <typename LoadOp, typename Epi = EpiNone>
 static void run_scan(ScanBuf& sb, LoadOp op, int* out, int n, cudaStream_t s, const char* name,
                      const int* abort_flag, Epi epi = Epi()) {
-    int tiles = std::max(1, (n + kScanTile - 1) / kScanTile);
+    const int tile = kScanBlock * ScanItems<LoadOp>::value;
+    int tiles = std::max(1, (n + tile - 1) / tile);
     unsigned long long* st = sb.buf[sb.cur];
     unsigned long long* other = sb.buf[sb.cur ^ 1];
     prof_pre(name, s);
@@ -237,6 +247,7 @@ struct Plan {
     uint64_t pcg[4] = {0, 0, 0, 0};
     size_t params_words = 0;
     int ld_min = kLDMinVertices;  // rounds with at least this many vertices start with LD rounds
+    int ld1_min = 1 << 30;        // ... and from this many, with one LD round (MF_LD1_MIN, A/B)
     int placement = 0;            // 0 = average, 1 = inverse (quadrics.py:89-114)
 };
 
@@ -345,6 +356,7 @@ static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan
     p.seeded = cfg->seeded != 0;
     p.order = cfg->einsum_order;
     if (const char* e = getenv("MF_LD_MIN")) p.ld_min = atoi(e);
+    if (const char* e = getenv("MF_LD1_MIN")) p.ld1_min = atoi(e);
     for (int i = 0; i < 4; i++) p.pcg[i] = cfg->pcg_state[i];
     // device params: act | budget | nin | voff | foff0 (int32)
     p.params_words = (size_t)p.nParamR * B * 2 + (size_t)(R + 1) * B + (size_t)(R + 1) * (B + 1) + (B + 1);
@@ -494,7 +506,7 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.table = A.take<int>((size_t)W.tsize);
     W.tkey = A.take<unsigned long long>((size_t)W.tsize);
     size_t maxn = (size_t)std::max(N0, Mcap) + 1;
-    W.scan.words = (int)(maxn / kScanTile + 4);
+    W.scan.words = (int)(maxn / kScanTileMin + 4);
     W.scan.buf[0] = A.take<unsigned long long>((size_t)W.scan.words);
     W.scan.buf[1] = A.take<unsigned long long>((size_t)W.scan.words);
     W.scan.cur = 0;
@@ -536,8 +548,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     int* foff_n = W.foff_b;
     const int order = p.order;
     int* d_heavy_n = W.counters + 4;
-    int* d_mid_n = W.counters + 20;
     int* d_heavy_c = W.counters + 12;
+    int* d_mid_n = W.counters + 20;
     int* d_scratch_used = W.counters + 24;
     for (int r = 0; r < R; r++) {
         const int N = p.h_N[r];
@@ -593,7 +605,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         }
         // large meshes: locally-dominant rounds first (round 0's picks written by k_adj_rank),
         // then Suitor proposals on the residual frontier; smaller meshes: Suitor only
-        const bool use_ld = N >= p.ld_min;
+        // locally-dominant rounds: all 12 from ld_min vertices; below, from ld1_min, only round
+        // 0 (the mutual best edges, matched before the proposals start)
+        const int ld_rounds = N >= p.ld_min ? kLDRounds : (N >= p.ld1_min ? 1 : 0);
+        const bool use_ld = ld_rounds > 0;
         if (seeded)
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
                    W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
@@ -602,9 +617,9 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                    W.skey, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         if (use_ld) {
             LDArgs la{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
-                      W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, kLDRounds, d_abort, W.acur};
+                      W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, ld_rounds, d_abort, W.acur};
             LAUNCH(k_ld_init, grid_for(ctx, N), 256, 0, stream, la);
-            for (int round = 0; round < kLDRounds; round++) {
+            for (int round = 0; round < ld_rounds; round++) {
                 if (round > 0) LAUNCH(k_ld_pick, grid_for(ctx, N), 256, 0, stream, la, round);
                 LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, round);
             }
@@ -622,7 +637,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const bool big = (B == 1 && N >= (1 << 18));  // below: one CTA (latency-bound sizes)
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
-                          d_abort, W.selstate, W.selstate + B, 0, W.ghist};
+                          d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap()};
             if (big) {
                 for (int pass = 0; pass < kSelPasses; pass++) {
                     LAUNCH(k_sel_hist, std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2), 512, 0, stream, sa,
@@ -632,7 +647,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                 sa.resume = 1;
             }
             if (B == 1 && !big && select_cluster()) LAUNCH(k_select_cl, kClCTAs, kClThreads, kClSmem, stream, sa);
-            else LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelSmem, stream, sa);
+            else LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelBins * 4 + 2 * sa.cap * 8, stream, sa);
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
         select(W.segA, nullptr);
@@ -719,7 +734,7 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode, p.ld_min, p.placement};
+                              g_prof_mode, p.ld_min, p.ld1_min, p.placement};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
     return k;
@@ -748,7 +763,7 @@ int quality_run(Context* ctx, const mf_mesh_view* mv, const int* d_off, const in
         return st->code;
     }
     const int N = (int)n, Mc = (int)std::max<int64_t>(m, 1);
-    const int scan_words = (int)((std::max<int64_t>(n, 1) + 1) / kScanTile + 4);
+    const int scan_words = (int)((std::max<int64_t>(n, 1) + 1) / kScanTileMin + 4);
     Arena me;
     me.measuring = true;
     auto lay = [&](Arena& A, WS& W, int64_t*& vo, double*& Pin, double*& Pout, double*& err, int*& misc) {

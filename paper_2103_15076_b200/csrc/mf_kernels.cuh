@@ -943,6 +943,7 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
             const int nu = a.ucnt[cur];
             int be = -1, bv = -1;
             unsigned bk = 0xffffffffu;
+            unsigned long long bsw = ~0ull;  // the suitor word seen when the slot was judged winnable
             const int c0 = a.acur[cur];
             if (c0 >= 0) {
                 // rank-ordered adjacency: the best winnable edge is the first winnable slot.
@@ -954,13 +955,14 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                     bool ok = false;
                     unsigned ke = 0;
                     int e = -1, v = -1;
+                    unsigned long long sw = ~0ull;
                     if (j < nu) {
                         e = a.adj_eid[s + j];
                         ke = a.adj_k32[s + j];
                         v = a.nbr[s + j];
                         ok = !(a.mate && __ldcg(a.mate + v) >= 0);
                         if (ok) {
-                            const unsigned long long sw = ld_volatile(a.suitor + v);
+                            sw = ld_volatile(a.suitor + v);
                             ok = sw == ~0ull || edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw);
                         }
                     }
@@ -970,6 +972,7 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                         bk = __shfl_sync(mask, ke, f, 8);
                         be = __shfl_sync(mask, e, f, 8);
                         bv = __shfl_sync(mask, v, f, 8);
+                        bsw = __shfl_sync(mask, sw, f, 8);
                         c += f;
                         break;
                     }
@@ -984,20 +987,21 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                     if (a.mate && __ldcg(a.mate + v) >= 0) continue;
                     const unsigned long long sw = ld_volatile(a.suitor + v);
                     if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
-                    bk = ke; be = e; bv = v;
+                    bk = ke; be = e; bv = v; bsw = sw;
                 }
 #pragma unroll
                 for (int o = 4; o > 0; o >>= 1) {
                     unsigned ok = __shfl_xor_sync(mask, bk, o, 8);
                     int oe = __shfl_xor_sync(mask, be, o, 8), ov = __shfl_xor_sync(mask, bv, o, 8);
-                    if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bv = ov; }
+                    unsigned long long osw = __shfl_xor_sync(mask, bsw, o, 8);
+                    if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bv = ov; bsw = osw; }
                 }
             }
             if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
             int next = -2;      // -2: lost a race, re-scan cur
             if (l == 0) {
                 const unsigned long long mine = ((unsigned long long)bk << 32) | (unsigned)be;
-                unsigned long long sw = ld_volatile(a.suitor + bv);
+                unsigned long long sw = bsw;  // a stale expected value only costs one failed CAS
                 while (true) {
                     if (sw != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw >> 32), (int)(unsigned)sw)) break;
                     unsigned long long old = atomicCAS(a.suitor + bv, sw, mine);
@@ -1041,6 +1045,7 @@ __global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
             const int nu = a.ucnt[cur];
             int be = -1, bv = -1;
             unsigned bk = 0xffffffffu;
+            unsigned long long bsw = ~0ull;
             int c = a.acur[cur];
             if (c >= 0) {
                 for (; c < nu; c++) {
@@ -1050,7 +1055,7 @@ __global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
                     const unsigned ke = a.adj_k32[s + c];
                     const unsigned long long sw = ld_volatile(a.suitor + v);
                     if (sw == ~0ull || edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) {
-                        bk = ke; be = e; bv = v;
+                        bk = ke; be = e; bv = v; bsw = sw;
                         break;
                     }
                 }
@@ -1064,12 +1069,12 @@ __global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
                     if (a.mate && __ldcg(a.mate + v) >= 0) continue;
                     const unsigned long long sw = ld_volatile(a.suitor + v);
                     if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
-                    bk = ke; be = e; bv = v;
+                    bk = ke; be = e; bv = v; bsw = sw;
                 }
             }
             if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
             const unsigned long long mine = ((unsigned long long)bk << 32) | (unsigned)be;
-            unsigned long long sw = ld_volatile(a.suitor + bv);
+            unsigned long long sw = bsw;  // a stale expected value only costs one failed CAS
             int next = -2;  // -2: lost a race, re-scan cur (the lost slot is dead now)
             while (true) {
                 if (sw != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw >> 32), (int)(unsigned)sw)) break;
@@ -1304,6 +1309,7 @@ constexpr int kSelBins = 1 << kSelBits;
 constexpr int kSelCap = 4096;  // keys held in shared memory (64 KiB; a larger carve-out measured slower)
 constexpr int kSelThreads = 1024;
 constexpr int kSelSmem = kSelBins * 4 + 2 * kSelCap * 8;
+constexpr int kSelCapMax = 12288;  // largest stage k_select may be launched with (MF_SEL_CAP)
 
 MF_DEV int sel_digit(uint64_t hi, uint64_t lo, int shift, int width) {
     // bits [shift, shift+width) of the 128-bit key (may straddle the 64-bit boundary)
@@ -1371,6 +1377,7 @@ struct SelectArgs {
     int* top;
     int resume;
     int* gscr;          // multi-block scratch (resume: bucket buffer)
+    int cap;            // k_select: keys its shared-memory stage holds (>= kSelCap)
 };
 
 // Multi-block pass scratch (ints): histogram | OR (2 u64), AND (2 u64) | stop |
@@ -1393,7 +1400,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     extern __shared__ unsigned char s_raw[];
     int* hist = reinterpret_cast<int*>(s_raw);                          // kSelBins
     uint64_t* sh = reinterpret_cast<uint64_t*>(s_raw + kSelBins * 4);   // kSelCap
-    uint64_t* sl = sh + kSelCap;                                        // kSelCap
+    uint64_t* sl = sh + a.cap;                                          // a.cap
     __shared__ int s_scan[33];
     __shared__ int s_sel[4];
     __shared__ int s_ncomp;
@@ -1426,7 +1433,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
         bool in_smem = false;
         int n_s = 0;
         bool done = false;
-        if (!a.resume && cnt <= kSelCap) {
+        if (!a.resume && cnt <= a.cap) {
             // the whole segment fits: one coalesced load, and the bits every key shares are
             // skipped before the first pass
             uint64_t oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
@@ -1531,7 +1538,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
                 sel_skip(p, top, s_oa[0], s_oa[1], s_oa[2], s_oa[3]);
                 phi = (uint64_t)(p >> 64);
                 plo = (uint64_t)p;
-                if (!in_smem && hd <= kSelCap) {
+                if (!in_smem && hd <= a.cap) {
                     // compact the surviving bucket into shared memory
                     if (threadIdx.x == 0) s_ncomp = 0;
                     __syncthreads();
@@ -1859,6 +1866,7 @@ MF_DEV int cluster_anchor(int v, const int* __restrict__ mate, const int* __rest
     return a >= 0 ? a : v;
 }
 struct LoadIsRep {  // v is the lowest member of its cluster
+    static constexpr int items = 2;  // three dependent gathers per item: short tiles
     const int* mate;
     const int* e0;
     const int* absorbed;
@@ -1876,6 +1884,7 @@ struct EpiFacetWrite {  // kept facet f -> output row prefix (order preserving c
     }
 };
 struct LoadKeep {  // facet survives: bypassed, or first occurrence of its non-degenerate triple
+    static constexpr int items = 2;  // slot -> table gather per item: short tiles
     const int* dM;
     const int* slot;
     const int* table;
