@@ -247,7 +247,8 @@ struct Plan {
     uint64_t pcg[4] = {0, 0, 0, 0};
     size_t params_words = 0;
     int ld_min = kLDMinVertices;  // rounds with at least this many vertices start with LD rounds
-    int ld1_min = 1 << 30;        // ... and from this many, with one LD round (MF_LD1_MIN, A/B)
+    int ld1_min = 1 << 17;        // ... from this many, one LD round (measured: cfg4 1.07 -> 1.04 ms, cfg3
+                                  // 2.97 -> 2.92; at cfg2 (115k) the two extra launches outweigh it)
     int placement = 0;            // 0 = average, 1 = inverse (quadrics.py:89-114)
 };
 
