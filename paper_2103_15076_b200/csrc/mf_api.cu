@@ -48,6 +48,19 @@ static int copy_i32_as_i64(const int* src, int64_t n, int64_t* dst, cudaStream_t
     return MF_OK;
 }
 
+// Destination the device can write: device memory as is, pinned host memory through its
+// mapped device address; nullptr for pageable host memory.
+static void* device_writable(void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return p;
+    if (a.type == cudaMemoryTypeHost && a.devicePointer) return a.devicePointer;
+    return nullptr;
+}
+
 static int copy_f64_as(const double* src, int64_t n, void* dst, int dtype, cudaStream_t s, mf_status* st) {
     if (!dst || n <= 0) return MF_OK;
     if (dtype == MF_DTYPE_F64) {
@@ -110,6 +123,9 @@ void mf_context_destroy(mf_context* ctx) {
     drop_graphs(&ctx->c);
     if (ctx->c.arena) cudaFree(ctx->c.arena);
     if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+    if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
+    for (cudaEvent_t e : ctx->c.aux_ev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -155,16 +171,38 @@ int mf_decimation_copy(const mf_decimation* res, double* positions, int64_t* fac
     const Result& r = res->r;
     cudaStream_t s = (cudaStream_t)stream;
     MF_CUDA_TRY(cudaSetDevice(r.device));
-    if (positions && r.n_out)
+    // Every output whose destination the device can write (device memory, or pinned host
+    // memory through its mapped address) is emitted by ONE kernel: int32 -> int64 widening
+    // and float64 copies fused, host-bound bytes written over the bus directly -- no staging
+    // buffers, no per-array copies.  Pageable destinations take the staged path.
+    const double* fsrc = r.features_alias ? r.positions : r.features;
+    EmitJobs jobs;
+    auto add = [&](int kind, const void* src, void* dst, int64_t n) -> bool {
+        if (!dst || n <= 0) return true;
+        void* d = device_writable(dst);
+        if (!d) return false;
+        jobs.add(kind, src, d, n);
+        return true;
+    };
+    const bool pos_ok = add(kEmitF64, r.positions, positions, r.n_out * 3);
+    const bool fac_ok = add(kEmitI32, r.facets, facets, r.m_out * 3);
+    const bool fea_ok = features_dtype == MF_DTYPE_F64 ? add(kEmitF64, fsrc, features, r.n_out * r.c)
+                                                       : add(kEmitF32, fsrc, features, r.n_out * r.c);
+    const bool rep_ok = add(kEmitI32, r.replace, replace, r.n_in);
+    const bool map_ok = add(kEmitI32, r.mapping, mapping, r.n_in);
+    if (jobs.count) {
+        LAUNCH(k_emit, grid_n(jobs.total()), 256, 0, s, jobs);
+        MF_CUDA_TRY(cudaGetLastError());
+    }
+    if (!pos_ok && positions && r.n_out)
         MF_CUDA_TRY(cudaMemcpyAsync(positions, r.positions, (size_t)r.n_out * 24, cudaMemcpyDefault, s));
     int rc;
-    if ((rc = copy_i32_as_i64(r.facets, r.m_out * 3, facets, s, st))) return rc;
-    if (features) {
-        const double* src = r.features_alias ? r.positions : r.features;
-        if ((rc = copy_f64_as(src, r.n_out * r.c, features, features_dtype, s, st))) return rc;
+    if (!fac_ok && (rc = copy_i32_as_i64(r.facets, r.m_out * 3, facets, s, st))) return rc;
+    if (!fea_ok && features) {
+        if ((rc = copy_f64_as(fsrc, r.n_out * r.c, features, features_dtype, s, st))) return rc;
     }
-    if ((rc = copy_i32_as_i64(r.replace, r.n_in, replace, s, st))) return rc;
-    if ((rc = copy_i32_as_i64(r.mapping, r.n_in, mapping, s, st))) return rc;
+    if (!rep_ok && (rc = copy_i32_as_i64(r.replace, r.n_in, replace, s, st))) return rc;
+    if (!map_ok && (rc = copy_i32_as_i64(r.mapping, r.n_in, mapping, s, st))) return rc;
     for (int which = 0; which < 2; which++) {
         int64_t* dst = which ? facet_offsets : vertex_offsets;
         const std::vector<int64_t>& src = which ? r.facet_offsets : r.vertex_offsets;

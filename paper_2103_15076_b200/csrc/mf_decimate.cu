@@ -392,7 +392,7 @@ struct WS {
     double* cost;
     uint64_t *key_hi, *key_lo;
     unsigned long long *mlo, *mhi;
-    int *mate, *best;
+    int *mate, *best, *pairlo;
     uint64_t *chi, *clo;
     int *cpay, *caux, *ksel, *mode;
     uint64_t *p_hi, *p_lo;
@@ -474,6 +474,7 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.mlo = A.take<unsigned long long>((size_t)B);
     W.mhi = A.take<unsigned long long>((size_t)B);
     W.mate = A.take<int>((size_t)N0);
+    W.pairlo = A.take<int>((size_t)N0);
     W.best = A.take<int>((size_t)N0);
     W.chi = A.take<uint64_t>((size_t)N0);
     W.clo = A.take<uint64_t>((size_t)N0);
@@ -633,7 +634,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             else LAUNCH(k_suitor1, grid_for(ctx, N), 256, 0, stream, ma);
         }
         LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, W.key_hi,
-               seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay);
+               seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay, W.pairlo);
         // per-mesh selection; one big mesh first narrows its rank prefix with multi-block passes
         const bool big = (B == 1 && N >= (1 << 18));  // below: one CTA (latency-bound sizes)
         auto select = [&](const int* seg_cnt, const int* removed_in) {
@@ -653,29 +654,29 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
         select(W.segA, nullptr);
         LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, voff_r, W.segA, W.chi, W.clo,
-               W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB);
+               W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB, W.pairlo);
         // absorb leftovers (one pass is exact: the matching is maximal when the budget is unmet)
         LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
-               seeded ? W.cost : nullptr, W.key_hi, W.mate, W.e0, vmesh, voff_r, act, budget, W.removed, W.segB,
+               seeded ? W.cost : nullptr, W.key_hi, W.pairlo, vmesh, voff_r, act, budget, W.removed, W.segB,
                W.chi, W.clo, W.caux);
         select(W.segB, W.removed);
         RoundFail rf{d_abort, d_fail, d_fail + B, d_fail + 2 * B};
         LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, voff_r, W.segB, W.chi, W.clo, W.caux,
                W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.aoff, rf, r);
         // relabel: output index = rank of the cluster's lowest member
-        run_scan(W.scan, LoadIsRep{W.mate, W.e0, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
+        run_scan(W.scan, LoadIsRep{W.pairlo, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
         const bool packed = Nn < (1 << 21);
-        LAUNCH(k_relabel3, grid_for(ctx, std::max<int64_t>(N, W.tsize)), 256, 0, stream, N, d_abort, W.mate, W.e0,
+        LAUNCH(k_relabel3, grid_for(ctx, std::max<int64_t>(N, W.tsize)), 256, 0, stream, N, d_abort, W.pairlo,
                W.absorbed, W.minrep, W.outidx, W.rstep, W.repv, W.abshead, W.absnext, W.table,
                packed ? W.tkey : nullptr, (int)W.tsize, packed ? 0x7f7f7f7f : -1, W.has_live);
         // contraction over member lists (no cluster CSR needed)
         if (p.placement)
-            LAUNCH(k_contract<1>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.e0, W.e1,
+            LAUNCH(k_contract<1>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.pairlo, W.e1,
                    W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c);
         else
-            LAUNCH(k_contract<0>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.e0, W.e1,
+            LAUNCH(k_contract<0>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.pairlo, W.e1,
                    W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c);
-        LAUNCH(k_contract_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_c, W.repv, W.mate, W.e0,
+        LAUNCH(k_contract_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_c, W.repv, W.mate, W.pairlo,
                W.e1, W.absorbed, W.abshead, W.absnext, Pc, Xc, (int)C, Pn, Xn, W.vq, p.placement, W.cmem, W.best,
                d_scratch_used);
         // output facets: remap, drop degenerate, drop later duplicates (hash, min facet id wins)
@@ -862,7 +863,7 @@ done:
 }
 
 int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,
-                 Result** out, mf_status* st) {
+                 Result** out, mf_status* st, bool force_carry) {
     st->code = MF_OK;
     st->mesh_index = -1;
     st->achievable_vertices = 0;
@@ -873,8 +874,13 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     const int64_t n = p.n, m = p.m, C = p.C;
     MF_CUDA_TRY(cudaSetDevice(ctx->device));
     // Features that are a bitwise copy of the positions (the default, mesh.py:28-29) fold like
-    // the positions, so they need not be carried: decide on the device (one extra upload of the
-    // features instead of a host memcmp), then stage both from the device copies.
+    // the positions and need not be carried.  Optimistic: run as aliased and verify while the
+    // round chain runs -- a host memcmp for small host arrays, else an upload on a side stream
+    // plus a compare kernel after the chain; a mismatch (features of the right shape that are
+    // NOT the positions) reruns the call carrying them.
+    const bool verify = !force_carry && !p.alias && mv->features && p.fdtype == MF_DTYPE_F64 && C == 3 &&
+                        p.placement == 0 && n > 0;
+    if (verify) p.alias = true;
     const void* P_src = mv->positions;
     const void* X_src = mv->features;
     void* alias_tmp = nullptr;
@@ -885,29 +891,26 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             if (p) cudaFreeAsync(p, s);
         }
     } tmp_free{alias_tmp, stream};
-    if (!p.alias && mv->features && p.fdtype == MF_DTYPE_F64 && C == 3 && p.placement == 0 && n > 0) {
-        const size_t b = (size_t)n * 24, ab = (b + 255) & ~size_t(255);
-        const bool pd = is_device_ptr(mv->positions), xd = is_device_ptr(mv->features);
-        MF_CUDA_TRY(cudaMallocAsync(&alias_tmp, (pd ? 0 : ab) + (xd ? 0 : ab) + 256, stream));
-        char* q = (char*)alias_tmp;
-        int* d_diff = (int*)q;
-        q += 256;
+    const size_t pbytes = (size_t)n * 24;
+    const bool host_check = verify && !is_device_ptr(mv->positions) && !is_device_ptr(mv->features) &&
+                            pbytes <= ((size_t)16 << 20);
+    int* d_diff = nullptr;
+    if (verify && !host_check) {
+        const bool xd = is_device_ptr(mv->features);
+        MF_CUDA_TRY(cudaMallocAsync(&alias_tmp, 256 + (xd ? 0 : ((pbytes + 255) & ~size_t(255))), stream));
+        d_diff = (int*)alias_tmp;
         MF_CUDA_TRY(cudaMemsetAsync(d_diff, 0, 4, stream));
-        if (!pd) {
-            MF_CUDA_TRY(cudaMemcpyAsync(q, mv->positions, b, cudaMemcpyHostToDevice, stream));
-            P_src = q;
-            q += ab;
+        if (!xd) {  // upload on the side stream: overlaps the round chain, joined before the compare
+            if (!ctx->aux) {
+                MF_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+                for (cudaEvent_t& e : ctx->aux_ev) MF_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            MF_CUDA_TRY(cudaEventRecord(ctx->aux_ev[0], stream));  // alias_tmp allocated
+            MF_CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
+            X_src = (char*)alias_tmp + 256;
+            MF_CUDA_TRY(cudaMemcpyAsync((void*)X_src, mv->features, pbytes, cudaMemcpyHostToDevice, ctx->aux));
+            MF_CUDA_TRY(cudaEventRecord(ctx->aux_ev[1], ctx->aux));
         }
-        if (!xd) {
-            MF_CUDA_TRY(cudaMemcpyAsync(q, mv->features, b, cudaMemcpyHostToDevice, stream));
-            X_src = q;
-        }
-        LAUNCH(k_words_differ, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, (const unsigned long long*)P_src,
-               (const unsigned long long*)X_src, d_diff);
-        int h_diff = 1;
-        MF_CUDA_TRY(cudaMemcpyAsync(&h_diff, d_diff, 4, cudaMemcpyDeviceToHost, stream));
-        MF_CUDA_TRY(cudaStreamSynchronize(stream));
-        if (!h_diff) p.alias = true;
     }
 
     // ---- workspace (grown on demand; cached graphs are tied to the arena address)
@@ -1068,10 +1071,24 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         }
         if (n) LAUNCH(k_identity_index, grid_for(ctx, n), 256, 0, stream, (int)n, res->replace, res->mapping);
     }
+    // ---- verify the optimistic features alias (overlapped with the chain)
+    int h_diff = 0;
+    if (d_diff) {
+        if (X_src != mv->features) MF_CUDA_TRY(cudaStreamWaitEvent(stream, ctx->aux_ev[1], 0));
+        LAUNCH(k_words_differ, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, (const unsigned long long*)W.P0,
+               (const unsigned long long*)X_src, d_diff);
+        MF_CUDA_TRY(cudaMemcpyAsync(&h_diff, d_diff, 4, cudaMemcpyDeviceToHost, stream));
+    }
+    if (host_check) h_diff = memcmp(mv->positions, mv->features, pbytes) != 0;  // while the GPU works
     // ---- single readback
     MF_CUDA_TRY(cudaMemcpyAsync(h_status, W.status, W.status_words * 4, cudaMemcpyDeviceToHost, stream));
     MF_CUDA_TRY(cudaStreamSynchronize(stream));
     MF_CUDA_TRY(cudaGetLastError());
+    if (h_diff) {  // features of the positions' shape that differ from them: carry them
+        cudaFreeAsync(res->block, stream);
+        delete res;
+        return decimate_run(ctx, mv, cfg, stream, out, st, true);
+    }
     if (graph_prof) prof_collect(*graph_prof);
     prof_collect_pending();
     const int* h_fo = h_status + 8;

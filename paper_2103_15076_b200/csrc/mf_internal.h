@@ -29,6 +29,9 @@ struct Context {
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
     cudaEvent_t done_event = nullptr;
+    // side stream + events: uploads that overlap the round chain (features check)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t aux_ev[2] = {nullptr, nullptr};
     std::string last_error;
 };
 
@@ -68,7 +71,7 @@ struct Result {
 };
 
 int decimate_run(Context* ctx, const mf_mesh_view* mesh, const mf_decimate_config* cfg, cudaStream_t stream,
-                 Result** out, mf_status* st);
+                 Result** out, mf_status* st, bool force_carry = false);
 int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c, const int* d_replace,
              const int* d_off, const int* d_members, int64_t n_out, int mode, const void* weights, void* out,
              cudaStream_t stream, mf_status* st);

@@ -1268,7 +1268,8 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigne
                         const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate,
                         const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
                         const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt,
-                        uint64_t* __restrict__ chi, uint64_t* __restrict__ clo, int* __restrict__ cpay) {
+                        uint64_t* __restrict__ chi, uint64_t* __restrict__ clo, int* __restrict__ cpay,
+                        int* __restrict__ pairlo) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
     // block-uniform trip count: the single-mesh append is aggregated per block
@@ -1285,7 +1286,9 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigne
                 if ((int)(unsigned)suitor[u] == e && suitor[u] != ~0ull) m = e;
             }
             mate[v] = m;
-            cand = m >= 0 && e0[m] == v;
+            const int lo = m >= 0 ? e0[m] : -1;
+            pairlo[v] = lo;
+            cand = lo == v;
         }
         const int slot = seg_slot_uniform(cand, vmesh, voff, seg_cnt, v);
         if (cand) {
@@ -1858,20 +1861,19 @@ __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* _
 
 // ---- flag producers fused into the decoupled look-back scan (LoadOp functors)
 // cluster anchor of v: lower end of its matched pair, the pair it was absorbed into, or itself
-MF_DEV int cluster_anchor(int v, const int* __restrict__ mate, const int* __restrict__ e0,
-                          const int* __restrict__ absorbed) {
-    const int m = mate[v];
-    if (m >= 0) return e0[m];
+// (pairlo[v]: lower end of v's matched pair or -1, written with the final matching)
+MF_DEV int cluster_anchor(int v, const int* __restrict__ pairlo, const int* __restrict__ absorbed) {
+    const int p = pairlo[v];
+    if (p >= 0) return p;
     const int a = absorbed[v];
     return a >= 0 ? a : v;
 }
 struct LoadIsRep {  // v is the lowest member of its cluster
-    static constexpr int items = 2;  // three dependent gathers per item: short tiles
-    const int* mate;
-    const int* e0;
+    static constexpr int items = 2;  // two dependent gathers per item: short tiles
+    const int* pairlo;
     const int* absorbed;
     const int* minrep;
-    MF_DEV int operator()(int v) const { return minrep[cluster_anchor(v, mate, e0, absorbed)] == v; }
+    MF_DEV int operator()(int v) const { return minrep[cluster_anchor(v, pairlo, absorbed)] == v; }
 };
 struct EpiFacetWrite {  // kept facet f -> output row prefix (order preserving compaction)
     const int* mapped;
@@ -1912,7 +1914,8 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
                               const int* __restrict__ cpay, const int* __restrict__ mode,
                               const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
                               const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate, int B,
-                              const int* __restrict__ ksel, int* __restrict__ removed, int* __restrict__ seg_cnt2) {
+                              const int* __restrict__ ksel, int* __restrict__ removed, int* __restrict__ seg_cnt2,
+                              int* __restrict__ pairlo) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
@@ -1924,9 +1927,11 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
         int b;
         if (!seg_valid(vmesh, voff, seg_cnt, i, b)) continue;
         if (is_selected(mode[b], chi[i], clo[i], thi[b], tlo[b])) continue;
-        int e = cpay[i];
-        mate[e0[e]] = -1;
-        mate[e1[e]] = -1;
+        const int e = cpay[i], va = e0[e], vb = e1[e];
+        mate[va] = -1;
+        mate[vb] = -1;
+        pairlo[va] = -1;
+        pairlo[vb] = -1;
     }
 }
 
@@ -1936,8 +1941,8 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
 __global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const int* __restrict__ aoff,
                               const int* __restrict__ ucnt, const int* __restrict__ nbr,
                               const int* __restrict__ adj_eid, const double* __restrict__ cost,
-                              const uint64_t* __restrict__ ckey,
-                              const int* __restrict__ mate, const int* __restrict__ e0, const int* __restrict__ vmesh,
+                              const uint64_t* __restrict__ ckey, const int* __restrict__ pairlo,
+                              const int* __restrict__ vmesh,
                               const int* __restrict__ voff, const int* __restrict__ act,
                               const int* __restrict__ budget, const int* __restrict__ removed,
                               int* __restrict__ seg_cnt, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
@@ -1953,14 +1958,13 @@ __global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const i
         int nu = 0;
         if (v < N) {
             nu = ucnt[v];
-            if (nu > 0 && mate[v] < 0) {
+            if (nu > 0 && pairlo[v] < 0) {
                 int bm = mesh_of(vmesh, v);
                 if (act[bm] && removed[bm] < budget[bm]) {
                     size_t s = (size_t)aoff[v];
                     for (int j = 0; j < nu; j++) {
-                        int mu = mate[nbr[s + j]];
-                        if (mu < 0) continue;  // cannot happen for a maximal matching
-                        int rep = e0[mu];
+                        const int rep = pairlo[nbr[s + j]];  // the neighbour's cluster anchor
+                        if (rep < 0) continue;  // cannot happen for a maximal matching
                         const int e = adj_eid[s + j];
                         uint64_t k = cost ? f64_key(cost[e]) : ckey[e];  // unseeded: ckey == f64_key(cost)
                         if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
@@ -2026,8 +2030,8 @@ __global__ void k_absorb_apply(int N, const int* __restrict__ vmesh, const int* 
 // the matched pair; output index = rank of the cluster's lowest member.
 // rstep = output index; the lowest member of output r is recorded (repv) and
 // absorbed vertices are linked into their anchor's list (order fixed later).
-__global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int* __restrict__ mate,
-                           const int* __restrict__ e0, const int* __restrict__ absorbed,
+__global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int* __restrict__ pairlo,
+                           const int* __restrict__ absorbed,
                            const int* __restrict__ minrep, const int* __restrict__ outidx, int* __restrict__ rstep,
                            int* __restrict__ repv, int* __restrict__ abshead, int* __restrict__ absnext,
                            int* __restrict__ table, unsigned long long* __restrict__ tkey, int tsize, int table_init,
@@ -2041,12 +2045,14 @@ __global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int*
     }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) has_live[i] = 0;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        const int anc = cluster_anchor(v, mate, e0, absorbed);
+        const int p = pairlo[v];
+        const int ab = p >= 0 ? -1 : absorbed[v];
+        const int anc = p >= 0 ? p : (ab >= 0 ? ab : v);
         const int rep = minrep[anc];
         const int r = outidx[rep];
         rstep[v] = r;
         if (rep == v) repv[r] = v;
-        if (mate[v] < 0 && absorbed[v] >= 0) absnext[v] = atomicExch(abshead + anc, v);
+        if (ab >= 0) absnext[v] = atomicExch(abshead + anc, v);
     }
 }
 
@@ -2139,7 +2145,7 @@ MF_DEV void fold_members(const int* m, int d, const double* __restrict__ P, cons
 // kSmallDeg members go to the block tier.
 template <int PLACEMENT>
 __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const int* __restrict__ repv,
-                           const int* __restrict__ mate, const int* __restrict__ e0, const int* __restrict__ e1,
+                           const int* __restrict__ mate, const int* __restrict__ pairlo, const int* __restrict__ e1,
                            const int* __restrict__ absorbed, const int* __restrict__ abshead,
                            const int* __restrict__ absnext, const int* __restrict__ vmesh,
                            const int* __restrict__ act, const double* __restrict__ P, const double* __restrict__ X,
@@ -2157,7 +2163,7 @@ __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const i
                 for (int k = 0; k < C; k++) Xout[(size_t)r * C + k] = X[(size_t)v0 * C + k];
             continue;
         }
-        const int anc = cluster_anchor(v0, mate, e0, absorbed);
+        const int anc = cluster_anchor(v0, pairlo, absorbed);
         int m[kSmallDeg];
         int d = 0;
         m[d++] = anc;
@@ -2184,7 +2190,7 @@ __global__ void __launch_bounds__(256) k_contract_heavy(const int* __restrict__ 
                                                         const int* __restrict__ heavy,
                                                         const int* __restrict__ heavy_count,
                                                         const int* __restrict__ repv, const int* __restrict__ mate,
-                                                        const int* __restrict__ e0, const int* __restrict__ e1,
+                                                        const int* __restrict__ pairlo, const int* __restrict__ e1,
                                                         const int* __restrict__ absorbed,
                                                         const int* __restrict__ abshead,
                                                         const int* __restrict__ absnext, const double* __restrict__ P,
@@ -2200,7 +2206,7 @@ __global__ void __launch_bounds__(256) k_contract_heavy(const int* __restrict__ 
     const int H = *heavy_count;
     for (int h = blockIdx.x; h < H; h += gridDim.x) {
         const int r = heavy[h];
-        const int anc = cluster_anchor(repv[r], mate, e0, absorbed);
+        const int anc = cluster_anchor(repv[r], pairlo, absorbed);
         if (threadIdx.x == 0) {  // clusters are disjoint: their member lists fit in N slots in total
             int d = 1 + (mate[anc] >= 0);
             for (int a = abshead[anc]; a >= 0; a = absnext[a]) d++;
@@ -2468,6 +2474,39 @@ __global__ void k_words_differ(int64_t n, const unsigned long long* __restrict__
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         d |= a[i] != b[i];
     if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) *diff = 1;
+}
+// Fused result emission (mf_decimation_copy): up to 8 jobs, each widening int32 -> int64,
+// copying float64, or narrowing float64 -> float32 into a device-writable destination.
+constexpr int kEmitI32 = 0, kEmitF64 = 1, kEmitF32 = 2;
+struct EmitJobs {
+    const void* src[8];
+    void* dst[8];
+    int64_t n[8];
+    int kind[8];
+    int count = 0;
+    void add(int k, const void* s, void* d, int64_t cnt) {
+        src[count] = s;
+        dst[count] = d;
+        n[count] = cnt;
+        kind[count] = k;
+        count++;
+    }
+    int64_t total() const {
+        int64_t t = 0;
+        for (int i = 0; i < count; i++) t += n[i];
+        return t;
+    }
+};
+__global__ void k_emit(EmitJobs j) {
+    MF_PDL_ENTRY;
+    for (int q = 0; q < j.count; q++) {
+        const int64_t n = j.n[q];
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            if (j.kind[q] == kEmitI32) ((int64_t*)j.dst[q])[i] = ((const int*)j.src[q])[i];
+            else if (j.kind[q] == kEmitF64) ((double*)j.dst[q])[i] = ((const double*)j.src[q])[i];
+            else ((float*)j.dst[q])[i] = (float)((const double*)j.src[q])[i];
+        }
+    }
 }
 __global__ void k_f64_to_f32(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
     MF_PDL_ENTRY;

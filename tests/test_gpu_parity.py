@@ -116,6 +116,20 @@ def test_features_float32_and_channels(oracle):
     run_both(oracle, m2, 300, seed=2)
 
 
+@pytest.mark.parametrize("n,where", [(800, "head"), (800, "tail"), (800_000, "tail")])
+def test_features_like_positions_but_different(oracle, n, where):
+    """float64 (n, 3) features are first assumed to be the positions (the default) and
+    verified while the rounds run -- on the host for small meshes, on the device (side-stream
+    upload) for large ones; one differing word must make the call carry them."""
+    mesh = S.delaunay_terrain(n, seed=6)
+    feats = mesh.positions.copy()
+    feats[0 if where == "head" else -1, 2] += 0.5
+    m2 = mfg.TriMesh(mesh.positions, mesh.facets, feats)
+    run_both(oracle, m2, n // 3)
+    # and the exact copy (aliased) still matches
+    run_both(oracle, mfg.TriMesh(mesh.positions, mesh.facets, mesh.positions.copy()), n // 3)
+
+
 def fan_mesh(k, seed=0, lift=0.0):
     """One hub vertex of degree k (heavy tier when k > 32) inside a ring."""
     rng = np.random.default_rng(seed)
