@@ -683,10 +683,28 @@ __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ 
             }
             continue;  // block-uniform
         }
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-            s_n[i] = snbr[base + i];
-            s_e[i] = seid[base + i];
-            s_k[i] = skey[base + i];
+        // 4 strided elements per trip: their 12 loads are in flight together
+        for (int i0 = threadIdx.x; i0 < cnt; i0 += 4 * blockDim.x) {
+            int n4[4], e4[4];
+            uint64_t k4[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int i = i0 + q * blockDim.x;
+                if (i < cnt) {
+                    n4[q] = snbr[base + i];
+                    e4[q] = seid[base + i];
+                    k4[q] = skey[base + i];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int i = i0 + q * blockDim.x;
+                if (i < cnt) {
+                    s_n[i] = n4[q];
+                    s_e[i] = e4[q];
+                    s_k[i] = k4[q];
+                }
+            }
         }
         __syncthreads();
         if (v < v1) {
@@ -1961,13 +1979,28 @@ __global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const i
             if (nu > 0 && pairlo[v] < 0) {
                 int bm = mesh_of(vmesh, v);
                 if (act[bm] && removed[bm] < budget[bm]) {
-                    size_t s = (size_t)aoff[v];
-                    for (int j = 0; j < nu; j++) {
-                        const int rep = pairlo[nbr[s + j]];  // the neighbour's cluster anchor
-                        if (rep < 0) continue;  // cannot happen for a maximal matching
-                        const int e = adj_eid[s + j];
-                        uint64_t k = cost ? f64_key(cost[e]) : ckey[e];  // unseeded: ckey == f64_key(cost)
-                        if (k < bk || (k == bk && rep < brep)) { bk = k; brep = rep; }
+                    const size_t s = (size_t)aoff[v];
+                    // up to 8 slots at a time: neighbour / edge loads, then the anchor gathers,
+                    // then the key gathers, each batch in flight together (3 round trips)
+                    for (int j0 = 0; j0 < nu; j0 += 8) {
+                        int nb[8], ed[8], rp[8];
+                        uint64_t ky[8];
+#pragma unroll
+                        for (int q = 0; q < 8; q++)
+                            if (j0 + q < nu) {
+                                nb[q] = nbr[s + j0 + q];
+                                ed[q] = adj_eid[s + j0 + q];
+                            }
+#pragma unroll
+                        for (int q = 0; q < 8; q++) rp[q] = (j0 + q < nu) ? pairlo[nb[q]] : -1;  // the anchor
+#pragma unroll
+                        for (int q = 0; q < 8; q++)  // unseeded: ckey == f64_key(cost)
+                            ky[q] = rp[q] >= 0 ? (cost ? f64_key(cost[ed[q]]) : ckey[ed[q]]) : ~0ull;
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            if (rp[q] < 0) continue;  // cannot happen for a maximal matching
+                            if (ky[q] < bk || (ky[q] == bk && rp[q] < brep)) { bk = ky[q]; brep = rp[q]; }
+                        }
                     }
                     cand = brep != 0x7fffffff;
                 }

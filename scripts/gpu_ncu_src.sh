@@ -1,0 +1,16 @@
+#!/bin/bash
+# One kernel, full set + source-level stall sampling, exported as CSV on the box.
+#   gpurun -- 'bash scripts/gpu_ncu_src.sh <tag> <cfg> <kernel-regex>'
+set -u
+TAG=$1; CFG=$2; RX=$3
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$RX" -s 0 -c 1 -f -o "$OUT/src" \
+  python scripts/one_step.py --config $CFG --warmup 1 > "$OUT/ncu.log" 2>&1
+echo "ncu rc=$?"
+ncu -i "$OUT/src.ncu-rep" --page source --csv --print-source sass > "$OUT/src_sass.csv" 2>/dev/null
+ncu -i "$OUT/src.ncu-rep" --page source --csv --print-source cuda > "$OUT/src_cuda.csv" 2>/dev/null
+ncu -i "$OUT/src.ncu-rep" --page details > "$OUT/details.txt" 2>/dev/null
+rm -f "$OUT/src.ncu-rep"
+ls -la "$OUT"
