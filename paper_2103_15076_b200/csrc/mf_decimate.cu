@@ -171,6 +171,15 @@ static int select_cap() {  // MF_SEL_CAP: keys in k_select's shared-memory stage
     return v;
 }
 
+static bool use_cond() {  // MF_COND=0: fixed round / pass counts instead of conditional nodes (A/B)
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_COND");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static int grid_for(const Context* ctx, int64_t n, int block = 256) {
     int64_t g = (n + block - 1) / block;
     int64_t cap = (int64_t)ctx->sm_count * 16;
@@ -518,7 +527,62 @@ static void layout(Arena& A, WS& W, const Plan& p) {
 
 // ------------------------------------------------------------------------
 // the device sequence (captured into a graph); inputs already staged in W
-static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream) {
+// Device-driven control flow while capturing: stages whose work is decided on the
+// device become conditional graph nodes (WHILE for the locally-dominant rounds and the
+// multi-block selection passes, IF for the absorb stage), their bodies captured on
+// dedicated streams (nesting depth 2).  A kernel of the chain sets each condition
+// (cudaGraphSetConditional), so converged rounds, finished passes and unneeded stages
+// cost no launches.  Off (nullptr streams) when not capturing or when profiling.
+struct CondCapture {
+    cudaStream_t body[2] = {nullptr, nullptr};
+    cudaStream_t outer[2] = {nullptr, nullptr};
+    cudaGraphNode_t node[2] = {nullptr, nullptr};
+    int depth = 0;
+    bool on() const { return body[0] != nullptr; }
+    cudaGraphConditionalHandle handle(cudaStream_t s, unsigned dflt) {
+        cudaStreamCaptureStatus st;
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t* d = nullptr;
+        size_t nd = 0;
+        RC(cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &d, &nd));
+        cudaGraphConditionalHandle h = 0;
+        RC(cudaGraphConditionalHandleCreate(&h, g, dflt, cudaGraphCondAssignDefault));
+        return h;
+    }
+    // adds the conditional node after the capture frontier of `s`; returns the body stream
+    cudaStream_t begin(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+        cudaStreamCaptureStatus st;
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t* d = nullptr;
+        size_t nd = 0;
+        RC(cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &d, &nd));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = type;
+        cp.conditional.size = 1;
+        RC(cudaGraphAddNode(&node[depth], g, d, nd, &cp));
+        outer[depth] = s;
+        cudaStream_t b = body[depth];
+        RC(cudaStreamBeginCaptureToGraph(b, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+        depth++;
+        return b;
+    }
+    cudaStream_t end() {  // closes the innermost body; returns the stream that continues
+        depth--;
+        cudaGraph_t bg = nullptr;
+        RC(cudaStreamEndCapture(body[depth], &bg));
+        RC(cudaStreamUpdateCaptureDependencies(outer[depth], &node[depth], 1, cudaStreamSetCaptureDependencies));
+        return outer[depth];
+    }
+};
+
+static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream, cudaStream_t body0 = nullptr,
+                   cudaStream_t body1 = nullptr) {
+    CondCapture cc;
+    cc.body[0] = body0;
+    cc.body[1] = body1;
     const int B = p.B, R = p.R, N0 = p.N0, Mcap = p.Mcap, Ecap = p.Ecap;
     const int64_t n = p.n, m = p.m, C = p.C;
     const bool seeded = p.seeded;
@@ -619,11 +683,19 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                    W.skey, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         if (use_ld) {
             LDArgs la{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
-                      W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, ld_rounds, d_abort, W.acur};
+                      W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, ld_rounds, d_abort, W.acur, 0};
             LAUNCH(k_ld_init, grid_for(ctx, N), 256, 0, stream, la);
-            for (int round = 0; round < ld_rounds; round++) {
-                if (round > 0) LAUNCH(k_ld_pick, grid_for(ctx, N), 256, 0, stream, la, round);
-                LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, round);
+            if (cc.on() && ld_rounds > 1) {  // as many rounds as the frontier needs (WHILE node)
+                la.cond = cc.handle(stream, 1u);
+                stream = cc.begin(stream, la.cond, cudaGraphCondTypeWhile);
+                LAUNCH(k_ld_pick, grid_for(ctx, N), 256, 0, stream, la, -1);
+                LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, -1);
+                stream = cc.end();
+            } else {
+                for (int round = 0; round < ld_rounds; round++) {
+                    if (round > 0) LAUNCH(k_ld_pick, grid_for(ctx, N), 256, 0, stream, la, round);
+                    LAUNCH(k_ld_match, grid_for(ctx, N), 256, 0, stream, la, round);
+                }
             }
         }
         {
@@ -639,12 +711,21 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const bool big = (B == 1 && N >= (1 << 18));  // below: one CTA (latency-bound sizes)
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
-                          d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap()};
+                          d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap(), 0};
             if (big) {
-                for (int pass = 0; pass < kSelPasses; pass++) {
-                    LAUNCH(k_sel_hist, std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2), 512, 0, stream, sa,
-                           W.ghist, pass);
-                    LAUNCH(k_sel_decide, 1, kSelThreads, 0, stream, sa, W.ghist, pass);
+                const int hist_grid = std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2);
+                if (cc.on() && cc.depth < 2) {  // passes until decided / handed over (WHILE node)
+                    sa.cond = cc.handle(stream, 1u);
+                    stream = cc.begin(stream, sa.cond, cudaGraphCondTypeWhile);
+                    LAUNCH(k_sel_hist, hist_grid, 512, 0, stream, sa, W.ghist, -1);
+                    LAUNCH(k_sel_decide, 1, kSelThreads, 0, stream, sa, W.ghist, -1);
+                    stream = cc.end();
+                    sa.cond = 0;
+                } else {
+                    for (int pass = 0; pass < kSelPasses; pass++) {
+                        LAUNCH(k_sel_hist, hist_grid, 512, 0, stream, sa, W.ghist, pass);
+                        LAUNCH(k_sel_decide, 1, kSelThreads, 0, stream, sa, W.ghist, pass);
+                    }
                 }
                 sa.resume = 1;
             }
@@ -653,8 +734,13 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
         select(W.segA, nullptr);
+        // the absorb stage runs only when some mesh misses its budget after truncation (IF node,
+        // condition set by k_trunc_apply); skipping it leaves removed / absorbed as they are
+        const cudaGraphConditionalHandle absorb_cond = cc.on() ? cc.handle(stream, 1u) : 0;
         LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, voff_r, W.segA, W.chi, W.clo,
-               W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB, W.pairlo);
+               W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB, W.pairlo, act,
+               budget, absorb_cond);
+        if (absorb_cond) stream = cc.begin(stream, absorb_cond, cudaGraphCondTypeIf);
         // absorb leftovers (one pass is exact: the matching is maximal when the budget is unmet)
         LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
                seeded ? W.cost : nullptr, W.key_hi, W.pairlo, vmesh, voff_r, act, budget, W.removed, W.segB,
@@ -663,6 +749,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         RoundFail rf{d_abort, d_fail, d_fail + B, d_fail + 2 * B};
         LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, voff_r, W.segB, W.chi, W.clo, W.caux,
                W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.aoff, rf, r);
+        if (absorb_cond) stream = cc.end();
         // relabel: output index = rank of the cluster's lowest member
         run_scan(W.scan, LoadIsRep{W.pairlo, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
         const bool packed = Nn < (1 << 21);
@@ -713,6 +800,7 @@ struct GraphCache {
     std::map<std::vector<int64_t>, GraphEntry> entries;
     void* arena = nullptr;
     cudaStream_t capture = nullptr;
+    cudaStream_t body[2] = {nullptr, nullptr};  // conditional-node body captures
     ~GraphCache() { clear(); }
     void clear() {
         for (auto& kv : entries)
@@ -729,6 +817,8 @@ void drop_graphs(const Context* ctx) {
     auto it = c.find(ctx);
     if (it != c.end()) {
         if (it->second.capture) cudaStreamDestroy(it->second.capture);
+        for (cudaStream_t b : it->second.body)
+            if (b) cudaStreamDestroy(b);
         c.erase(it);
     }
 }
@@ -987,7 +1077,10 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             gc.clear();
             gc.arena = ctx->arena;
         }
-        if (!gc.capture) MF_CUDA_TRY(cudaStreamCreateWithFlags(&gc.capture, cudaStreamNonBlocking));
+        if (!gc.capture) {
+            MF_CUDA_TRY(cudaStreamCreateWithFlags(&gc.capture, cudaStreamNonBlocking));
+            for (cudaStream_t& b : gc.body) MF_CUDA_TRY(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+        }
         std::vector<int64_t> key = graph_key(p);
         auto it = gc.entries.find(key);
         if (it == gc.entries.end()) {
@@ -995,7 +1088,9 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             size_t rec0 = g_prof_recs.size();
             int64_t l0 = g_launches;
             MF_CUDA_TRY(cudaStreamBeginCapture(gc.capture, cudaStreamCaptureModeThreadLocal));
-            record(ctx, p, W, gc.capture);
+            // conditional nodes unless profiling (event nodes cannot live in bodies) or PDL edges
+            const bool cond = use_cond() && g_prof_mode == 0 && !pdl_enabled();
+            record(ctx, p, W, gc.capture, cond ? gc.body[0] : nullptr, cond ? gc.body[1] : nullptr);
             int64_t nk = g_launches - l0;
             g_launches = l0;
             cudaGraph_t g = nullptr;

@@ -1140,6 +1140,7 @@ struct LDArgs {
     int max_rounds;
     const int* abort_flag;
     int* acur;      // per vertex: first possibly-live slot of its rank-ordered adjacency (-1 = unsorted)
+    cudaGraphConditionalHandle cond;  // device-driven round loop (WHILE node), 0 = fixed rounds
 };
 
 MF_DEV bool ld_lt(const LDArgs& a, unsigned ke, int e, unsigned kf, int f) {
@@ -1183,9 +1184,14 @@ __global__ void __launch_bounds__(256) k_ld_init(LDArgs a) {
 // frontier vertex whose previous pick died picks its best live edge -- the
 // first slot from its cursor whose neighbour is unmatched (rank-ordered
 // adjacency); unsorted (high-degree) vertices scan every slot.
+// `round` < 0: inside the device-driven loop -- the round comes from counters[4]
 __global__ void __maxnreg__(48) k_ld_pick(LDArgs a, int round) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
+    if (round < 0) {
+        round = ld_volatile(a.counters + 4);
+        if (round == 0) return;  // round 0's picks come from k_adj_rank
+    }
     const int cur = round & 1;
     const int n = a.counters[cur];
     if (n == 0) return;
@@ -1229,14 +1235,18 @@ __global__ void __maxnreg__(48) k_ld_pick(LDArgs a, int round) {
 // phase B: mutual picks are matched; the rest (with a live edge) survive
 __global__ void __launch_bounds__(256) k_ld_match(LDArgs a, int round) {
     MF_PDL_ENTRY;
-    if (*a.abort_flag) return;
+    const bool loop = round < 0;  // device-driven rounds: this kernel decides whether another follows
+    if (*a.abort_flag) {
+        if (loop && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.cond, 0u);
+        return;
+    }
+    if (loop) round = ld_volatile(a.counters + 4);
     const int cur = round & 1;
     const int n = a.counters[cur];
     if (n && blockIdx.x == 0 && threadIdx.x == 0) {
         a.counters[3] = cur ^ 1;  // the residual frontier lives here after this round
         a.counters[2] = round + 1;
     }
-    if (n == 0) return;
     const int* Fc = cur ? a.front1 : a.front0;
     int* Fn = cur ? a.front0 : a.front1;
     const int nb = (n + blockDim.x - 1) / blockDim.x;
@@ -1253,6 +1263,22 @@ __global__ void __launch_bounds__(256) k_ld_match(LDArgs a, int round) {
             }
         }
         block_append(keep, v, Fn, a.counters + (cur ^ 1));
+    }
+    if (!loop) return;
+    // the last block to finish sees the complete next frontier and sets the loop condition
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.counters + 5, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        const int next = ld_volatile(a.counters + (cur ^ 1));
+        a.counters[5] = 0;
+        a.counters[4] = round + 1;
+        cudaGraphSetConditional(a.cond, (next > 0 && round + 1 < a.max_rounds) ? 1u : 0u);
     }
 }
 
@@ -1399,6 +1425,7 @@ struct SelectArgs {
     int resume;
     int* gscr;          // multi-block scratch (resume: bucket buffer)
     int cap;            // k_select: keys its shared-memory stage holds (>= kSelCap)
+    cudaGraphConditionalHandle cond;  // device-driven multi-block passes (WHILE node), 0 = fixed passes
 };
 
 // Multi-block pass scratch (ints): histogram | OR (2 u64), AND (2 u64) | stop |
@@ -1414,6 +1441,8 @@ MF_DEV int* sel_stop(int* g) { return g + kSelBins + 8; }
 MF_DEV int* sel_compact(int* g) { return g + kSelBins + 9; }
 MF_DEV int* sel_count(int* g) { return g + kSelBins + 10; }
 MF_DEV uint64_t* sel_buf(int* g) { return reinterpret_cast<uint64_t*>(g + kSelScrHdr); }
+MF_DEV int* sel_pass(int* g) { return g + kSelBins + 11; }  // pass of the device-driven loop
+constexpr int kSelPassesMax = 12;                          // loop cap (128-bit keys, 11-bit digits)
 
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     MF_PDL_ENTRY;
@@ -1751,6 +1780,7 @@ __global__ void __cluster_dims__(kClCTAs, 1, 1) __launch_bounds__(kClThreads) k_
 __global__ void __launch_bounds__(512) k_sel_hist(SelectArgs a, int* __restrict__ ghist, int pass) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
+    if (pass < 0) pass = ld_volatile(sel_pass(ghist));
     __shared__ int h[kSelBins];
     __shared__ unsigned long long s_oa[4];
     if (pass > 0 && (a.mode[0] != 0 || *sel_stop(ghist))) return;
@@ -1798,7 +1828,18 @@ __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* _
     MF_PDL_ENTRY;
     __shared__ int s_scan[33];
     __shared__ int s_sel[3];
-    if (*a.abort_flag) return;
+    const bool loop = pass < 0;  // device-driven passes: every exit decides whether another follows
+    auto stop_loop = [&]() {
+        if (loop && threadIdx.x == 0) {
+            *sel_pass(ghist) = 0;
+            cudaGraphSetConditional(a.cond, 0u);
+        }
+    };
+    if (*a.abort_flag) {
+        stop_loop();
+        return;
+    }
+    if (loop) pass = ld_volatile(sel_pass(ghist));
     unsigned long long* g = sel_orand(ghist);
     const int cnt = a.seg_cnt[0];
     int kr;
@@ -1821,11 +1862,15 @@ __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* _
         if (k == 0 || k >= cnt) {
             if (threadIdx.x == 0) a.mode[0] = (k == 0) ? 2 : 1;
             reset();
+            stop_loop();
             return;
         }
         kr = k;
     } else {
-        if (a.mode[0] != 0 || *sel_stop(ghist)) return;
+        if (a.mode[0] != 0 || *sel_stop(ghist)) {
+            stop_loop();
+            return;
+        }
         kr = a.krem[0];
         phi = a.thr_hi[0];
         plo = a.thr_lo[0];
@@ -1875,6 +1920,11 @@ __global__ void __launch_bounds__(kSelThreads) k_sel_decide(SelectArgs a, int* _
     a.thr_lo[0] = (uint64_t)p;
     a.krem[0] = kr;
     a.top[0] = ntop;
+    if (loop) {
+        const bool more = a.mode[0] == 0 && !*sel_stop(ghist) && pass + 1 < kSelPassesMax;
+        *sel_pass(ghist) = more ? pass + 1 : 0;
+        cudaGraphSetConditional(a.cond, more ? 1u : 0u);
+    }
 }
 
 // ---- flag producers fused into the decoupled look-back scan (LoadOp functors)
@@ -1933,9 +1983,16 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
                               const uint64_t* __restrict__ thi, const uint64_t* __restrict__ tlo,
                               const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate, int B,
                               const int* __restrict__ ksel, int* __restrict__ removed, int* __restrict__ seg_cnt2,
-                              int* __restrict__ pairlo) {
+                              int* __restrict__ pairlo, const int* __restrict__ act, const int* __restrict__ budget,
+                              cudaGraphConditionalHandle absorb_cond) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
+    if (absorb_cond && blockIdx.x == 0 && threadIdx.x == 0) {
+        // the absorb stage (an IF node) runs only if some mesh still misses its budget
+        bool need = false;
+        for (int b = 0; b < B && !need; b++) need = act[b] && ksel[b] < budget[b];
+        cudaGraphSetConditional(absorb_cond, need ? 1u : 0u);
+    }
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int b = tid; b < B; b += nth) {
         removed[b] = ksel[b];
