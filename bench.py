@@ -176,6 +176,9 @@ def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
         "k_facet_remap": 12 * M + 4 * N + 12 * M + 16 * M + 4 * M + N,
         "k_inc_scatter": 12 * M + 4 * N + 12 * M,
         "k_compose": 8 * r.get("N0", N) + 4 * N,
+        # one per call (after its last round): replace / mapping int32 -> int64, positions and
+        # facets out (features alias the positions in the bench workloads)
+        "k_emit": (12 * r.get("N0", N) * 2 + 24 * Nn + 8 * 3 * Mn + 4 * 3 * Mn + 24 * Nn) if r.get("last") else 0,
     }
     v = table.get(name)
     return None if v is None else float(v)
@@ -366,8 +369,10 @@ def run_ours(args):
     _native.profile(0)
     rounds = []
     for dd in dds:
-        for r in dd.round_stats():
+        rs = dd.round_stats()
+        for i, r in enumerate(rs):
             r["N0"] = dd._dec.n_in
+            r["last"] = i == len(rs) - 1  # the call's outputs are emitted after its last round
             rounds.append(r)
     total_ms = sum(v[0] for v in breakdown.values())
     dominant = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
