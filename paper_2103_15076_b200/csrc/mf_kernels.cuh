@@ -304,7 +304,7 @@ MF_DEV void reg_sort(int (&a)[L]) {
 // kernel (list `mid`), larger to the block tier (list `heavy`).
 constexpr int kThreadDeg = 8;
 constexpr int kMid = 32;
-__global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_flag, int N,
+__global__ void __launch_bounds__(128, 10) k_vertex_t(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ inc,
                                                   const int* __restrict__ F, const Plane* __restrict__ plane,
                                                   int Mcap, double* __restrict__ vq, int* __restrict__ nbr,
@@ -1300,9 +1300,17 @@ MF_DEV int block_slot(bool keep, int* __restrict__ counter) {
 MF_DEV int seg_slot_uniform(bool keep, const int* __restrict__ vmesh, const int* __restrict__ voff,
                             int* __restrict__ seg_cnt, int v) {
     if (!vmesh) return block_slot(keep, seg_cnt);
+    // batches: a warp's vertices are consecutive, so they span one or two meshes -- one
+    // atomic per (warp, mesh) group instead of one per candidate
+    const unsigned full = 0xffffffffu;
+    const int b = keep ? vmesh[v] : -1;
+    const unsigned peers = __match_any_sync(full, b);
     if (!keep) return -1;
-    const int b = vmesh[v];
-    return voff[b] + atomicAdd(seg_cnt + b, 1);
+    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(seg_cnt + b, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    return voff[b] + base + __popc(peers & ((1u << lane) - 1u));
 }
 
 // mate = the suitor edge when the proposal is mutual (or the LD match); every
