@@ -304,7 +304,7 @@ MF_DEV void reg_sort(int (&a)[L]) {
 // kernel (list `mid`), larger to the block tier (list `heavy`).
 constexpr int kThreadDeg = 8;
 constexpr int kMid = 32;
-__global__ void __launch_bounds__(128, 10) k_vertex_t(const int* __restrict__ abort_flag, int N,
+__global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ inc,
                                                   const int* __restrict__ F, const Plane* __restrict__ plane,
                                                   int Mcap, double* __restrict__ vq, int* __restrict__ nbr,
