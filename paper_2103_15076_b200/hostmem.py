@@ -1,24 +1,19 @@
 """Pinned host buffers for the numpy API.
 
 Results handed back as numpy arrays are allocated in page-locked memory
-(torch's caching host allocator, wrapped zero-copy as numpy) so the
-device->host copies run at full PCIe/C2C rate instead of being staged through
-a pageable bounce buffer; arrays passed back in (e.g. features pooled level by
-level) are then pinned too.  The allocator caches freed blocks, so repeated
+(torch's caching host allocator, wrapped zero-copy as numpy): the library's
+fused result-emission kernel writes them directly through their mapped device
+addresses, and the remaining copies run at full PCIe/C2C rate instead of being
+staged through a pageable bounce buffer; arrays passed back in (e.g. features
+pooled level by level) are then pinned too.  The allocator caches freed blocks, so repeated
 calls do not pay cudaHostAlloc.  Without a usable CUDA runtime this falls back
 to ordinary numpy allocations (the compute path itself still requires the GPU).
 """
-
-import ctypes
-import ctypes.util
 
 import numpy as np
 
 _TORCH_DT = None
 _ok = None
-_libc = ctypes.CDLL(ctypes.util.find_library("c"))
-_libc.memcmp.restype = ctypes.c_int
-_libc.memcmp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
 
 
 def _torch():
@@ -42,8 +37,3 @@ def empty(shape, dtype) -> np.ndarray:
 
         return torch.empty(tuple(shape), dtype=_TORCH_DT[dtype], pin_memory=True).numpy()
     return np.empty(shape, dtype=dtype)
-
-
-def same_bytes(a: np.ndarray, b: np.ndarray) -> bool:
-    """Bitwise equality of two C-contiguous arrays (memcmp, no temporaries)."""
-    return a.nbytes == b.nbytes and (a.nbytes == 0 or _libc.memcmp(a.ctypes.data, b.ctypes.data, a.nbytes) == 0)
