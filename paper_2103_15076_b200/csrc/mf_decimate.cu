@@ -171,11 +171,14 @@ static int select_cap() {  // MF_SEL_CAP: keys in k_select's shared-memory stage
     return v;
 }
 
-static bool use_cond() {  // MF_COND=0: fixed round / pass counts instead of conditional nodes (A/B)
+// MF_COND=1: conditional graph nodes (device-driven loop / skip).  Opt-in: measured neutral on
+// B200, and Nsight Compute cannot profile the kernel nodes of a graph that holds conditional
+// nodes -- the default graph stays fully profileable.
+static bool use_cond() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MF_COND");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = (e && e[0] == '1') ? 1 : 0;
     }
     return v == 1;
 }

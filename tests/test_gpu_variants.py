@@ -49,8 +49,8 @@ VARIANTS = [
     {"MF_SEL_CAP": "12288"},
     {"MF_GRAPHS": "0"},
     {"MF_PDL": "1"},
-    {"MF_COND": "0"},
-    {"MF_LD_MIN": "1", "MF_COND": "0"},
+    {"MF_COND": "1"},
+    {"MF_LD_MIN": "1", "MF_COND": "1"},
 ]
 
 
