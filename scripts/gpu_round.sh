@@ -44,6 +44,6 @@ if [[ $PARTS == *ncu* ]]; then
     # keep the merge-back small: CSV / text exports, the report itself only when small
     ncu -i "$OUT/full_$c.ncu-rep" --page raw --csv > "$OUT/full_${c}_raw.csv" 2>/dev/null
     ncu -i "$OUT/full_$c.ncu-rep" --page details > "$OUT/full_${c}_details.txt" 2>/dev/null
-    if [ $(stat -c %s "$OUT/full_$c.ncu-rep") -gt 20000000 ]; then rm -f "$OUT/full_$c.ncu-rep"; fi
+    if [ -f "$OUT/full_$c.ncu-rep" ] && [ $(stat -c %s "$OUT/full_$c.ncu-rep") -gt 20000000 ]; then rm -f "$OUT/full_$c.ncu-rep"; fi
   done
 fi
