@@ -104,7 +104,8 @@ int mf_context_create(int device, mf_context** out) {
         return MF_ERR_CUDA;
     }
     c->c.sm_count = prop.multiProcessorCount;
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelBins * 4 + 2 * kSelCapMax * 8);
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSelBins * 4 + 8 * std::max(2 * kSelCapMax, kSelChiCap));
     cudaFuncSetAttribute(k_select_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem);
     // keep freed stream-ordered allocations cached in the device pool
     cudaMemPool_t pool;

@@ -714,7 +714,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const bool big = (B == 1 && N >= (1 << 18));  // below: one CTA (latency-bound sizes)
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
-                          d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap(), 0};
+                          d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap(), 0,
+                          B == 1 ? kSelChiCap : 0};
             if (big) {
                 const int hist_grid = std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2);
                 if (cc.on() && cc.depth < 2) {  // passes until decided / handed over (WHILE node)
@@ -733,7 +734,9 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                 sa.resume = 1;
             }
             if (B == 1 && !big && select_cluster()) LAUNCH(k_select_cl, kClCTAs, kClThreads, kClSmem, stream, sa);
-            else LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads, kSelBins * 4 + 2 * sa.cap * 8, stream, sa);
+            else
+                LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads,
+                       kSelBins * 4 + 8 * std::max(2 * sa.cap, sa.chicap), stream, sa);
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh
         select(W.segA, nullptr);

@@ -1365,6 +1365,8 @@ constexpr int kSelCap = 4096;  // keys held in shared memory (64 KiB; a larger c
 constexpr int kSelThreads = 1024;
 constexpr int kSelSmem = kSelBins * 4 + 2 * kSelCap * 8;
 constexpr int kSelCapMax = 12288;  // largest stage k_select may be launched with (MF_SEL_CAP)
+constexpr int kSelChiCap = 27136;  // single-mesh two-phase path: primary keys + tie secondaries (212 KiB)
+constexpr int kSelBucket = 512;    // its compacted bucket (4 KiB static)
 
 MF_DEV int sel_digit(uint64_t hi, uint64_t lo, int shift, int width) {
     // bits [shift, shift+width) of the 128-bit key (may straddle the 64-bit boundary)
@@ -1434,6 +1436,7 @@ struct SelectArgs {
     int* gscr;          // multi-block scratch (resume: bucket buffer)
     int cap;            // k_select: keys its shared-memory stage holds (>= kSelCap)
     cudaGraphConditionalHandle cond;  // device-driven multi-block passes (WHILE node), 0 = fixed passes
+    int chicap;         // k_select: primary keys the stage holds for the two-phase path (0 = off)
 };
 
 // Multi-block pass scratch (ints): histogram | OR (2 u64), AND (2 u64) | stop |
@@ -1452,6 +1455,153 @@ MF_DEV uint64_t* sel_buf(int* g) { return reinterpret_cast<uint64_t*>(g + kSelSc
 MF_DEV int* sel_pass(int* g) { return g + kSelBins + 11; }  // pass of the device-driven loop
 constexpr int kSelPassesMax = 12;                          // loop cap (128-bit keys, 11-bit digits)
 
+// Block-wide k-th smallest (1-based kr) of vals[0..n) (u64, duplicates allowed) below
+// the prefix (p, top): MSD radix with 11-bit digits and the common-prefix skip.
+// Returns true when the kr-th is the last element of a digit bucket -- every value in
+// [p, p | ones(top)) is then selected -- and false when all 64 bits are fixed (p is the
+// exact value, kr its rank among the equal values).  Uniform across the block.
+// `scratch` (cap values): once a bucket fits, it is copied there and later passes walk
+// only the bucket instead of every value.
+MF_DEV bool radix_kth_u64(const uint64_t* vals, int n, int& kr, uint64_t& p, int& top, int* hist, int* s_scan,
+                          int* s_sel, unsigned long long* s_oa, uint64_t* scratch, int cap) {
+    bool compacted = false;
+    if (n <= 32 && top >= 64) {  // tiny input (typically the ties of phase two): one warp sorts it
+        if (threadIdx.x < 32) {
+            const int l = threadIdx.x;
+            uint64_t x = l < n ? vals[l] : ~0ull;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const uint64_t y = __shfl_xor_sync(0xffffffffu, x, j);
+                    const bool up = ((l & k) == 0), lower = ((l & j) == 0);
+                    x = (lower == up) ? (x < y ? x : y) : (x > y ? x : y);
+                }
+            const uint64_t v = __shfl_sync(0xffffffffu, x, kr - 1);
+            const int below = __popc(__ballot_sync(0xffffffffu, l < n && x < v));
+            if (l == 0) {
+                s_oa[2] = v;
+                s_sel[3] = kr - below;
+            }
+        }
+        __syncthreads();
+        p = s_oa[2];
+        kr = s_sel[3];
+        top = 0;
+        __syncthreads();
+        return false;
+    }
+    while (top > 0) {
+        const int width = top >= kSelBits ? kSelBits : top;
+        const int shift = top - width;
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0;
+        if (threadIdx.x < 2) s_oa[threadIdx.x] = threadIdx.x ? ~0ull : 0ull;
+        __syncthreads();
+        uint64_t o = 0, an = ~0ull;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t x = vals[i];
+            if (top >= 64 || (x >> top) == (p >> top)) {
+                hist_add(hist, (int)((x >> shift) & ((1u << width) - 1u)));
+                o |= x;
+                an &= x;
+            }
+        }
+#pragma unroll
+        for (int q = 16; q > 0; q >>= 1) {
+            o |= __shfl_xor_sync(0xffffffffu, o, q);
+            an &= __shfl_xor_sync(0xffffffffu, an, q);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicOr(s_oa, o);
+            atomicAnd(s_oa + 1, an);
+        }
+        __syncthreads();
+        const int per = kSelBins / blockDim.x;
+        int loc = 0;
+        for (int j = 0; j < per; j++) loc += hist[threadIdx.x * per + j];
+        int tot;
+        const int ex = block_excl_scan(loc, s_scan, &tot);
+        if (ex < kr && kr <= ex + loc) {
+            int cum = ex;
+            for (int j = 0; j < per; j++) {
+                const int h = hist[threadIdx.x * per + j];
+                if (cum + h >= kr) {
+                    s_sel[0] = threadIdx.x * per + j;
+                    s_sel[1] = cum;
+                    s_sel[2] = h;
+                    break;
+                }
+                cum += h;
+            }
+        }
+        __syncthreads();
+        const int d = s_sel[0], h = s_sel[2];
+        kr -= s_sel[1];
+        p |= (uint64_t)d << shift;
+        top = shift;
+        const uint64_t diff = (s_oa[0] ^ s_oa[1]) & (shift >= 64 ? ~0ull : ((1ull << shift) - 1ull));
+        const uint64_t common = s_oa[1];
+        __syncthreads();
+        if (h == kr) return true;
+        if (!compacted && h <= cap && h > 32 && h < n) {  // walk only the bucket from now on
+            if (threadIdx.x == 0) s_sel[3] = 0;
+            __syncthreads();
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint64_t x = vals[i];
+                if ((x >> top) == (p >> top)) scratch[atomicAdd(&s_sel[3], 1)] = x;
+            }
+            __syncthreads();
+            vals = scratch;
+            n = h;
+            compacted = true;
+        }
+        if (h <= 32 && top > 0) {
+            // a small bucket: one warp sorts it and reads the kr-th directly (no more passes)
+            uint64_t* small = reinterpret_cast<uint64_t*>(hist);  // the histogram is free now
+            if (threadIdx.x == 0) s_sel[3] = 0;
+            __syncthreads();
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint64_t x = vals[i];
+                if ((x >> top) == (p >> top)) small[atomicAdd(&s_sel[3], 1)] = x;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                const int l = threadIdx.x;
+                uint64_t x = l < h ? small[l] : ~0ull;
+#pragma unroll
+                for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        const uint64_t y = __shfl_xor_sync(0xffffffffu, x, j);
+                        const bool up = ((l & k) == 0), lower = ((l & j) == 0);
+                        x = (lower == up) ? (x < y ? x : y) : (x > y ? x : y);
+                    }
+                const uint64_t v = __shfl_sync(0xffffffffu, x, kr - 1);
+                const int below = __popc(__ballot_sync(0xffffffffu, l < h && x < v));
+                if (l == 0) {
+                    small[32] = v;
+                    s_sel[3] = kr - below;
+                }
+            }
+            __syncthreads();
+            p = small[32];
+            kr = s_sel[3];
+            top = 0;
+            __syncthreads();
+            return false;
+        }
+        if (diff) {  // skip the bits every value of the bucket shares
+            const int D = 63 - __clzll((long long)diff);
+            if (D + 1 < top) {
+                const uint64_t m = ((top >= 64) ? ~0ull : ((1ull << top) - 1ull)) & ~((1ull << (D + 1)) - 1ull);
+                p = (p & ~m) | (common & m);
+                top = D + 1;
+            }
+        }
+    }
+    return false;
+}
+
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
@@ -1463,6 +1613,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
     __shared__ int s_sel[4];
     __shared__ int s_ncomp;
     __shared__ unsigned long long s_oa[4];
+    __shared__ uint64_t s_bucket[kSelBucket];  // the two-phase path's compacted digit bucket
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         const int c0 = a.voff[b], c1 = c0 + a.seg_cnt[b];
         const int cnt = c1 - c0;
@@ -1488,6 +1639,62 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
             }
             kr = k;
         }
+        if (!a.resume && cnt > a.cap && cnt <= a.chicap) {
+            // mid-size segment: the 64-bit primary keys fit the stage -- select on them in
+            // shared memory (one coalesced load), then, only among the keys equal to the
+            // k-th primary key, on the secondary half gathered from global memory
+            uint64_t* sv = sh;  // a.chicap keys
+            for (int i0 = threadIdx.x; i0 < cnt; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+                uint64_t v8[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int i = i0 + q * blockDim.x;
+                    v8[q] = i < cnt ? __ldcg(a.chi + c0 + i) : 0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int i = i0 + q * blockDim.x;
+                    if (i < cnt) sv[i] = v8[q];
+                }
+            }
+            __syncthreads();
+            uint64_t t = 0, q = 0;
+            int topc = 64;
+            const bool whole = radix_kth_u64(sv, cnt, kr, t, topc, hist, s_scan, s_sel, s_oa, s_bucket, kSelBucket);
+            if (whole) {
+                t |= (topc >= 64) ? ~0ull : ((1ull << topc) - 1ull);
+                q = ~0ull;
+            } else {
+                if (threadIdx.x == 0) s_ncomp = 0;
+                __syncthreads();
+                uint64_t* sq = sv + cnt;  // secondary halves of the primary-key ties
+                const int room = a.chicap - cnt;
+                for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+                    if (sv[i] == t) {
+                        const int slot = atomicAdd(&s_ncomp, 1);
+                        if (slot < room) sq[slot] = a.clo[c0 + i];
+                    }
+                __syncthreads();
+                const int ne = s_ncomp;
+                if (ne > room) {  // more ties than room (pathological): the general path below
+                    kr = k;
+                    __syncthreads();
+                    goto general;
+                }
+                int topq = 64;
+                if (radix_kth_u64(sq, ne, kr, q, topq, hist, s_scan, s_sel, s_oa, s_bucket, kSelBucket))
+                    q |= (topq >= 64) ? ~0ull : ((1ull << topq) - 1ull);
+            }
+            if (threadIdx.x == 0) {
+                a.thr_hi[b] = t;
+                a.thr_lo[b] = q;
+                a.mode[b] = 3;
+                a.ksel[b] = k;
+            }
+            __syncthreads();
+            continue;
+        }
+    general:
         bool in_smem = false;
         int n_s = 0;
         bool done = false;
