@@ -140,14 +140,20 @@ static cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 // Suitor variant per round size: 8 lanes per proposer below 2^18 vertices (more warps to hide
 // the slot scans: cfg2 78 vs 119 us), one thread per proposer above (one wave of proposers:
 // cfg4 136 vs 218 us, cfg3 326 vs 369 us).  MF_SUITOR=1 / 8 forces one (A/B runs).
-static int suitor_lanes(int N) {
+// lanes per proposer: the rank-ordered adjacency makes the first winnable slot usually one of
+// the first few, so lanes only pay while they fill the machine; measured (r1h): 8 lanes at cfg1
+// (N*8 within one wave), 4 at both cfg2 rounds (0.569 -> 0.559 ms; 2 lanes 0.596; 8 lanes in
+// round 2 only: 0.578), a thread each at cfg4 (640k)
+static int suitor_lanes(int N, int sm_count) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MF_SUITOR");
-        v = (e && e[0] == '1') ? 1 : ((e && e[0] == '8') ? 8 : 0);
+        v = e ? atoi(e) : 0;
+        if (v != 1 && v != 2 && v != 4 && v != 8) v = 0;
     }
     if (v) return v;
-    return N >= (1 << 18) ? 1 : 8;
+    if (N >= (1 << 18)) return 1;
+    return (int64_t)N * 8 <= (int64_t)sm_count * 2048 ? 8 : 4;  // 8 lanes only within one wave
 }
 
 // MF_SELECT_CL=1: 8-CTA cluster selection (DSMEM histogram merge) for mid-size meshes.  Measured
@@ -392,8 +398,8 @@ struct WS {
     double* vq;
     unsigned* adj_k32;
     int* acur;
-    int* snbr;  // adjacency slots, rank order after k_adj_rank (nbr keeps neighbour order)
-    uint64_t* skey;
+    int* snbr;    // adjacency slots in rank order (k_adj_rank output; nbr keeps neighbour order)
+    int* seid_u;  // unseeded: edge ids of the unsorted slots (their neighbours / keys are e1 / key_hi)
     int* lowfill;
     unsigned long long* suitor;
     int *bestu, *front0, *front1, *ldc;
@@ -460,7 +466,7 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.adj_k32 = A.take<unsigned>((size_t)2 * Ecap);
     W.acur = A.take<int>((size_t)N0);
     W.snbr = A.take<int>((size_t)2 * Ecap);
-    W.skey = p.seeded ? nullptr : A.take<uint64_t>((size_t)2 * Ecap);
+    W.seid_u = p.seeded ? nullptr : A.take<int>((size_t)2 * Ecap);
     W.lowfill = A.take<int>((size_t)N0 + 1);
     W.suitor = A.take<unsigned long long>((size_t)N0);
     W.bestu = A.take<int>((size_t)N0);
@@ -477,7 +483,8 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.heavy = A.take<int>((size_t)N0);
     W.mid = A.take<int>((size_t)N0);
     W.counters = A.take<int>(64);
-    // unseeded edge ids are adjacency slot indices (sparse in [0, 2E)), seeded ones dense
+    // unseeded edge ids are adjacency slot indices (sparse in [0, 2E)) and e1 / key_hi are the
+    // unsorted slot arrays (neighbour, rank key) of k_edges, e0 the slot owner; seeded ids dense
     W.e0 = A.take<int>((size_t)2 * Ecap);
     W.e1 = A.take<int>((size_t)2 * Ecap);
     W.cost = A.take<double>((size_t)Ecap);
@@ -655,9 +662,12 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         run_scan(W.scan, LoadArr{W.ucnt}, W.aoff, N, stream, "k_scan<adj>", d_abort);
         if (seeded) run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
         {
-            EdgeOut eo{W.e0,     W.e1,     seeded ? W.cost : nullptr, W.key_hi, W.snbr,   W.adj_eid, W.skey,
-                       W.lowfill, W.mate,  W.minrep, W.absorbed, W.abshead, W.suitor, W.mlo, W.mhi,
-                       W.segA,   W.ldc};
+            // unseeded: the unsorted slots are written straight into e1 / key_hi (+ seid_u), and
+            // k_adj_rank_tiled sorts them out of place into snbr / adj_eid / adj_k32
+            EdgeOut eo{W.e0,      W.e1,   seeded ? W.cost : nullptr, nullptr, seeded ? W.snbr : W.e1,
+                       seeded ? W.adj_eid : W.seid_u, seeded ? nullptr : W.key_hi,
+                       W.lowfill, W.mate, W.minrep, W.absorbed, W.abshead, W.suitor, W.mlo, W.mhi,
+                       W.segA,    W.ldc};
             const int eg = grid_for(ctx, (int64_t)N * kEdgeLanes);
             if (p.placement)
                 LAUNCH(k_edges<1>, eg, 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.aoff, W.eoff, W.vq,
@@ -680,10 +690,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const bool use_ld = ld_rounds > 0;
         if (seeded)
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
-                   W.skey, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
+                   nullptr, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         else
-            LAUNCH(k_adj_rank_tiled, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
-                   W.skey, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
+            LAUNCH(k_adj_rank_tiled, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.e1, W.seid_u,
+                   W.key_hi, W.snbr, W.adj_eid, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         if (use_ld) {
             LDArgs la{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,
                       W.mate, W.best, W.bestu, W.front0, W.front1, W.ldc, W.bar, ld_rounds, d_abort, W.acur, 0};
@@ -705,7 +715,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             MatchArgs ma{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.e0, W.e1, W.key_hi,
                          seeded ? W.key_lo : nullptr, W.suitor, d_abort, use_ld ? W.mate : nullptr,
                          use_ld ? W.front0 : nullptr, W.front1, W.ldc, W.acur};
-            if (suitor_lanes(N) == 8) LAUNCH(k_suitor, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, ma);
+            const int sl = suitor_lanes(N, ctx->sm_count);
+            if (sl == 8) LAUNCH(k_suitor<8>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, ma);
+            else if (sl == 4) LAUNCH(k_suitor<4>, grid_for(ctx, (int64_t)N * 4), 256, 0, stream, ma);
+            else if (sl == 2) LAUNCH(k_suitor<2>, grid_for(ctx, (int64_t)N * 2), 256, 0, stream, ma);
             else LAUNCH(k_suitor1, grid_for(ctx, N), 256, 0, stream, ma);
         }
         LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, W.key_hi,

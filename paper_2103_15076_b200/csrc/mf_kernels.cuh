@@ -484,7 +484,7 @@ struct EdgeOut {
 
 constexpr int kEdgeLanes = 4;
 template <int PLACEMENT>
-__global__ void __launch_bounds__(256) k_edges(const int* __restrict__ abort_flag, int N,
+__global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __restrict__ abort_flag, int N,
                                                const int* __restrict__ inc_off, const int* __restrict__ nbr,
                                                const int* __restrict__ ucnt, const int* __restrict__ upcnt,
                                                const int* __restrict__ aoff, const int* __restrict__ eoff,
@@ -510,9 +510,13 @@ __global__ void __launch_bounds__(256) k_edges(const int* __restrict__ abort_fla
             o.suitor[v] = ~0ull;
         }
         const int nu = ucnt[v], nup = upcnt[v];
+        const size_t s2 = (size_t)aoff[v];  // compact adjacency slots
+        // unseeded: an edge's id is its lower end's slot, so e0 is the slot owner -- written
+        // for every slot of v (full sectors; only the lower end's slots are ever read as e0)
+        if (!seeded)
+            for (int j = l; j < nu; j += kEdgeLanes) o.e0[s2 + j] = v;
         if (l >= nup) continue;
         const size_t sn = 2 * (size_t)inc_off[v];  // neighbour list (k_vertex layout)
-        const size_t s2 = (size_t)aoff[v];          // compact adjacency slots
         const int nlow = nu - nup;
         // unseeded: edge id = slot index of the upper end (aoff[v] + j), which orders edges
         // lexicographically like the dense index; seeded: the dense index (PCG stream position)
@@ -527,13 +531,15 @@ __global__ void __launch_bounds__(256) k_edges(const int* __restrict__ abort_fla
             Q10 qu;
             q_load(vq, u, qu);
             const double c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
-            o.e0[eid] = v;
-            o.e1[eid] = u;
             // unseeded: the rank key IS the order-preserving cost (f64_key is invertible, so no
-            // cost array); seeded: the cost feeds the bucket keys (k_seed_keys)
+            // cost array), and the slot arrays double as e1 / key_hi (o.snbr = e1, o.skey = key_hi:
+            // the own slot s2 + j is the edge id); seeded: dense ids, the cost feeds k_seed_keys
             const uint64_t key = f64_key(c);
-            if (seeded) o.cost[eid] = c;
-            else o.key_hi[eid] = key;
+            if (seeded) {
+                o.e0[eid] = v;
+                o.e1[eid] = u;
+                o.cost[eid] = c;
+            }
             const size_t su = (size_t)aoff[u] + atomicAdd(o.lowfill + u, 1);
             o.snbr[s2 + j] = u;
             o.seid[s2 + j] = eid;
@@ -560,9 +566,9 @@ __global__ void __launch_bounds__(256) k_edges(const int* __restrict__ abort_fla
 // are gathered once k_seed_keys has run.
 // Slots of one vertex at sn / se / sk / k32 (global or shared memory).
 template <bool SEEDED>
-MF_DEV void rank_one(int v, int nu, int* sn, int* se, const uint64_t* sk, const uint64_t* __restrict__ key_hi,
-                     const uint64_t* __restrict__ key_lo, unsigned* k32, int* __restrict__ acur,
-                     int* __restrict__ best, int* __restrict__ bestu) {
+MF_DEV void rank_one(int v, int nu, const int* sn, const int* se, const uint64_t* sk, int* sn_out, int* se_out,
+                     const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo, unsigned* k32,
+                     int* __restrict__ acur, int* __restrict__ best, int* __restrict__ bestu) {
     typedef typename std::conditional<SEEDED, uint64_t, unsigned>::type Lo;
     if (nu > 8) {
         uint64_t bh = ~0ull, bl = ~0ull;
@@ -571,8 +577,11 @@ MF_DEV void rank_one(int v, int nu, int* sn, int* se, const uint64_t* sk, const 
             const int e = se[j];
             const uint64_t h = SEEDED ? key_hi[e] : sk[j];
             const uint64_t l = SEEDED ? key_lo[e] : (uint64_t)(unsigned)e;
+            const int u = sn[j];
             k32[j] = (unsigned)(h >> 32);
-            if (key_lt(h, l, bh, bl)) { bh = h; bl = l; be = e; bu = sn[j]; }
+            sn_out[j] = u;
+            se_out[j] = e;
+            if (key_lt(h, l, bh, bl)) { bh = h; bl = l; be = e; bu = u; }
         }
         acur[v] = -1;
         if (best) {
@@ -624,8 +633,8 @@ MF_DEV void rank_one(int v, int nu, int* sn, int* se, const uint64_t* sk, const 
 #pragma unroll
     for (int i = 0; i < 8; i++)
         if (i < nu) {
-            sn[i] = u[i];
-            se[i] = (int)(unsigned)lo[i];  // seeded key_lo carries the edge id in its low bits
+            sn_out[i] = u[i];
+            se_out[i] = (int)(unsigned)lo[i];  // seeded key_lo carries the edge id in its low bits
             k32[i] = (unsigned)(h[i] >> 32);
         }
     acur[v] = 0;
@@ -650,21 +659,24 @@ __global__ void __launch_bounds__(256) k_adj_rank(const int* __restrict__ abort_
     if (*abort_flag) return;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
         const size_t s = (size_t)aoff[v];
-        rank_one<SEEDED>(v, ucnt[v], snbr + s, seid + s, SEEDED ? nullptr : skey + s, key_hi, key_lo, adj_k32 + s,
-                         acur, best, bestu);
+        rank_one<SEEDED>(v, ucnt[v], snbr + s, seid + s, SEEDED ? nullptr : skey + s, snbr + s, seid + s, key_hi,
+                         key_lo, adj_k32 + s, acur, best, bestu);
     }
 }
 
 // Unseeded rounds: the same sort with the slots of 256 consecutive vertices (one
 // contiguous range of the compact adjacency) staged through shared memory, so
 // every global load / store is coalesced; a tile whose range exceeds the stage
-// (high-degree vertices) sorts in place in global memory.
+// (high-degree vertices) sorts straight from / to global memory.  Out of place:
+// the unsorted slots (in_nbr, in_eid, in_key) double as the edge arrays e1 /
+// key_hi (an edge's id is its lower end's slot), so they must survive.
 constexpr int kRankCap = 2048;
 __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ abort_flag, int N,
                                                         const int* __restrict__ aoff, const int* __restrict__ ucnt,
-                                                        int* __restrict__ snbr, int* __restrict__ seid,
-                                                        const uint64_t* __restrict__ skey,
-                                                        unsigned* __restrict__ adj_k32, int* __restrict__ acur,
+                                                        const int* __restrict__ in_nbr, const int* __restrict__ in_eid,
+                                                        const uint64_t* __restrict__ skey, int* __restrict__ snbr,
+                                                        int* __restrict__ seid, unsigned* __restrict__ adj_k32,
+                                                        int* __restrict__ acur,
                                                         int* __restrict__ best, int* __restrict__ bestu) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
@@ -678,8 +690,8 @@ __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ 
         if (cnt > kRankCap) {
             if (v < v1) {
                 const size_t s = (size_t)aoff[v];
-                rank_one<false>(v, ucnt[v], snbr + s, seid + s, skey + s, nullptr, nullptr, adj_k32 + s, acur, best,
-                                bestu);
+                rank_one<false>(v, ucnt[v], in_nbr + s, in_eid + s, skey + s, snbr + s, seid + s, nullptr, nullptr,
+                                adj_k32 + s, acur, best, bestu);
             }
             continue;  // block-uniform
         }
@@ -691,8 +703,8 @@ __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ 
             for (int q = 0; q < 4; q++) {
                 const int i = i0 + q * blockDim.x;
                 if (i < cnt) {
-                    n4[q] = snbr[base + i];
-                    e4[q] = seid[base + i];
+                    n4[q] = in_nbr[base + i];
+                    e4[q] = in_eid[base + i];
                     k4[q] = skey[base + i];
                 }
             }
@@ -709,7 +721,8 @@ __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ 
         __syncthreads();
         if (v < v1) {
             const int o = aoff[v] - base;
-            rank_one<false>(v, ucnt[v], s_n + o, s_e + o, s_k + o, nullptr, nullptr, s_32 + o, acur, best, bestu);
+            rank_one<false>(v, ucnt[v], s_n + o, s_e + o, s_k + o, s_n + o, s_e + o, nullptr, nullptr, s_32 + o, acur,
+                            best, bestu);
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
@@ -935,6 +948,7 @@ MF_DEV bool edge_lt(const MatchArgs& a, unsigned ke, int e, unsigned kf, int f) 
     return key_lt(h1, l1, h2, l2);
 }
 
+template <int L>
 __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
@@ -942,10 +956,12 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
     // (one neighbour per lane), the best winnable edge is an argmin over the
     // group, and lane 0 issues a 64-bit CAS of (key prefix | edge id) on the
     // neighbour's suitor word.  Control flow is uniform per group.
-    const int g = threadIdx.x >> 3;
-    const int l = threadIdx.x & 7;
-    const unsigned mask = 0xFFu << (threadIdx.x & 24);
-    const int groups = gridDim.x * (blockDim.x >> 3);
+    constexpr int LB = L == 8 ? 3 : (L == 4 ? 2 : 1);
+    const int g = threadIdx.x >> LB;
+    const int l = threadIdx.x & (L - 1);
+    const unsigned gmask = (1u << L) - 1u;
+    const unsigned mask = gmask << (threadIdx.x & (32 - L));
+    const int groups = gridDim.x * (blockDim.x >> LB);
     const int* list = nullptr;
     int nprop = a.N;
     if (a.front0) {
@@ -953,7 +969,7 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
         list = which ? a.front1 : a.front0;
         nprop = __ldcg(a.counters + which);
     }
-    for (int ui = blockIdx.x * (blockDim.x >> 3) + g; ui < nprop; ui += groups) {
+    for (int ui = blockIdx.x * (blockDim.x >> LB) + g; ui < nprop; ui += groups) {
         int cur = list ? __ldcg(list + ui) : ui;
         if (a.mate && __ldcg(a.mate + cur) >= 0) continue;
         while (cur >= 0) {
@@ -968,7 +984,7 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                 // A slot is dead for good once its neighbour is LD-matched or holds a better
                 // proposal (suitor words only improve), so the cursor moves past dead slots.
                 int c = c0;
-                for (; c < nu; c += 8) {
+                for (; c < nu; c += L) {
                     const int j = c + l;
                     bool ok = false;
                     unsigned ke = 0;
@@ -984,20 +1000,20 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                             ok = sw == ~0ull || edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw);
                         }
                     }
-                    const unsigned bal = (__ballot_sync(mask, ok) >> (threadIdx.x & 24)) & 0xFFu;
+                    const unsigned bal = (__ballot_sync(mask, ok) >> (threadIdx.x & (32 - L))) & gmask;
                     if (bal) {
                         const int f = __ffs(bal) - 1;
-                        bk = __shfl_sync(mask, ke, f, 8);
-                        be = __shfl_sync(mask, e, f, 8);
-                        bv = __shfl_sync(mask, v, f, 8);
-                        bsw = __shfl_sync(mask, sw, f, 8);
+                        bk = __shfl_sync(mask, ke, f, L);
+                        be = __shfl_sync(mask, e, f, L);
+                        bv = __shfl_sync(mask, v, f, L);
+                        bsw = __shfl_sync(mask, sw, f, L);
                         c += f;
                         break;
                     }
                 }
                 if (l == 0) a.acur[cur] = c < nu ? c : nu;
             } else {
-                for (int j = l; j < nu; j += 8) {
+                for (int j = l; j < nu; j += L) {
                     const int e = a.adj_eid[s + j];
                     const unsigned ke = a.adj_k32[s + j];
                     if (be >= 0 && !edge_lt(a, ke, e, bk, be)) continue;
@@ -1008,10 +1024,10 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                     bk = ke; be = e; bv = v; bsw = sw;
                 }
 #pragma unroll
-                for (int o = 4; o > 0; o >>= 1) {
-                    unsigned ok = __shfl_xor_sync(mask, bk, o, 8);
-                    int oe = __shfl_xor_sync(mask, be, o, 8), ov = __shfl_xor_sync(mask, bv, o, 8);
-                    unsigned long long osw = __shfl_xor_sync(mask, bsw, o, 8);
+                for (int o = L / 2; o > 0; o >>= 1) {
+                    unsigned ok = __shfl_xor_sync(mask, bk, o, L);
+                    int oe = __shfl_xor_sync(mask, be, o, L), ov = __shfl_xor_sync(mask, bv, o, L);
+                    unsigned long long osw = __shfl_xor_sync(mask, bsw, o, L);
                     if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bv = ov; bsw = osw; }
                 }
             }
@@ -1034,7 +1050,7 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                     sw = old;
                 }
             }
-            next = __shfl_sync(mask, next, 0, 8);
+            next = __shfl_sync(mask, next, 0, L);
             if (next != -2) cur = next;
         }
     }

@@ -43,6 +43,8 @@ print("VARIANT-OK")
 VARIANTS = [
     {"MF_SUITOR": "1"},
     {"MF_SUITOR": "8"},
+    {"MF_SUITOR": "4"},
+    {"MF_SUITOR": "2"},
     {"MF_LD1_MIN": "1"},
     {"MF_LD_MIN": "1", "MF_SUITOR": "1"},
     {"MF_SELECT_CL": "1"},
