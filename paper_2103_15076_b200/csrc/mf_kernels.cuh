@@ -509,14 +509,16 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
             o.abshead[v] = -1;
             o.suitor[v] = ~0ull;
         }
+        // every per-vertex word is loaded up front (one latency), the neighbour list's offset
+        // included -- loaded after the nup branch it cost a dependent round trip (ncu stalls)
         const int nu = ucnt[v], nup = upcnt[v];
         const size_t s2 = (size_t)aoff[v];  // compact adjacency slots
+        const size_t sn = 2 * (size_t)inc_off[v];  // neighbour list (k_vertex layout)
         // unseeded: an edge's id is its lower end's slot, so e0 is the slot owner -- written
         // for every slot of v (full sectors; only the lower end's slots are ever read as e0)
         if (!seeded)
             for (int j = l; j < nu; j += kEdgeLanes) o.e0[s2 + j] = v;
         if (l >= nup) continue;
-        const size_t sn = 2 * (size_t)inc_off[v];  // neighbour list (k_vertex layout)
         const int nlow = nu - nup;
         // unseeded: edge id = slot index of the upper end (aoff[v] + j), which orders edges
         // lexicographically like the dense index; seeded: the dense index (PCG stream position)
@@ -530,7 +532,15 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
             const int eid = eb + k;
             Q10 qu;
             q_load(vq, u, qu);
-            const double c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, P[3 * u], P[3 * u + 1], P[3 * u + 2], order);
+            const double ux = P[3 * u], uy = P[3 * u + 1], uz = P[3 * u + 2];
+            // the other end's slot: its atomic and the key-independent stores go out while the
+            // quadric gathers are in flight
+            const size_t su = (size_t)aoff[u] + atomicAdd(o.lowfill + u, 1);
+            o.snbr[s2 + j] = u;
+            o.seid[s2 + j] = eid;
+            o.snbr[su] = v;
+            o.seid[su] = eid;
+            const double c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, ux, uy, uz, order);
             // unseeded: the rank key IS the order-preserving cost (f64_key is invertible, so no
             // cost array), and the slot arrays double as e1 / key_hi (o.snbr = e1, o.skey = key_hi:
             // the own slot s2 + j is the edge id); seeded: dense ids, the cost feeds k_seed_keys
@@ -540,11 +550,6 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
                 o.e1[eid] = u;
                 o.cost[eid] = c;
             }
-            const size_t su = (size_t)aoff[u] + atomicAdd(o.lowfill + u, 1);
-            o.snbr[s2 + j] = u;
-            o.seid[s2 + j] = eid;
-            o.snbr[su] = v;
-            o.seid[su] = eid;
             if (!seeded) {
                 o.skey[s2 + j] = key;
                 o.skey[su] = key;
