@@ -104,6 +104,7 @@ int mf_context_create(int device, mf_context** out) {
         return MF_ERR_CUDA;
     }
     c->c.sm_count = prop.multiProcessorCount;
+    cudaFuncSetAttribute(k_adj_rank_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankSmem);
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSelBins * 4 + 8 * std::max(2 * kSelCapMax, kSelChiCap));
     cudaFuncSetAttribute(k_select_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem);

@@ -692,7 +692,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
                    nullptr, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         else
-            LAUNCH(k_adj_rank_tiled, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.e1, W.seid_u,
+            LAUNCH(k_adj_rank_tiled, std::min(grid_for(ctx, N), ctx->sm_count * 3), 256, kRankSmem, stream, d_abort, N, W.aoff, W.ucnt, W.e1, W.seid_u,
                    W.key_hi, W.snbr, W.adj_eid, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         if (use_ld) {
             LDArgs la{N, W.aoff, W.ucnt, W.snbr, W.adj_eid, W.adj_k32, W.key_hi, seeded ? W.key_lo : nullptr,

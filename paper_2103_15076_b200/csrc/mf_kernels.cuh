@@ -676,6 +676,17 @@ __global__ void __launch_bounds__(256) k_adj_rank(const int* __restrict__ abort_
 // the unsorted slots (in_nbr, in_eid, in_key) double as the edge arrays e1 /
 // key_hi (an edge's id is its lower end's slot), so they must survive.
 constexpr int kRankCap = 2048;
+constexpr int kRankSmem = 2 * kRankCap * (4 + 4 + 8) + kRankCap * 4;  // double-buffered inputs + k32 (72 KiB)
+MF_DEV void cp_async4(void* s, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
+}
+MF_DEV void cp_async8(void* s, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
+}
+MF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+MF_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+// The next tile's slots are fetched with cp.async into the other buffer while the
+// current tile sorts, so the load phase of one tile overlaps the compute of the last.
 __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ abort_flag, int N,
                                                         const int* __restrict__ aoff, const int* __restrict__ ucnt,
                                                         const int* __restrict__ in_nbr, const int* __restrict__ in_eid,
@@ -685,58 +696,66 @@ __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ 
                                                         int* __restrict__ best, int* __restrict__ bestu) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    __shared__ int s_n[kRankCap], s_e[kRankCap];
-    __shared__ uint64_t s_k[kRankCap];
-    __shared__ unsigned s_32[kRankCap];
-    for (int v0 = blockIdx.x * blockDim.x; v0 < N; v0 += gridDim.x * blockDim.x) {
-        const int v1 = min(N, v0 + (int)blockDim.x);
+    extern __shared__ __align__(16) unsigned char rank_smem[];
+    uint64_t* s_kb = reinterpret_cast<uint64_t*>(rank_smem);         // [2][cap]
+    int* s_nb = reinterpret_cast<int*>(s_kb + 2 * kRankCap);           // [2][cap]
+    int* s_eb = s_nb + 2 * kRankCap;                                   // [2][cap]
+    unsigned* s_32 = reinterpret_cast<unsigned*>(s_eb + 2 * kRankCap);  // [cap]
+    const int T = blockDim.x;
+    const int stride = gridDim.x * T;
+    // issue the cp.async group of the tile starting at v0 into buffer `buf` (empty group past the end)
+    auto prefetch = [&](int v0, int buf) {
+        if (v0 < N) {
+            const int v1 = min(N, v0 + T);
+            const int base = aoff[v0], cnt = aoff[v1] - base;
+            if (cnt <= kRankCap) {
+                int* dn = s_nb + buf * kRankCap;
+                int* de = s_eb + buf * kRankCap;
+                uint64_t* dk = s_kb + buf * kRankCap;
+                for (int i = threadIdx.x; i < cnt; i += T) {
+                    cp_async4(dn + i, in_nbr + base + i);
+                    cp_async4(de + i, in_eid + base + i);
+                    cp_async8(dk + i, skey + base + i);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    int buf = 0;
+    prefetch(blockIdx.x * T, 0);
+    for (int v0 = blockIdx.x * T; v0 < N; v0 += stride, buf ^= 1) {
+        prefetch(v0 + stride, buf ^ 1);
+        const int v1 = min(N, v0 + T);
         const int base = aoff[v0], cnt = aoff[v1] - base;
         const int v = v0 + threadIdx.x;
+        cp_async_wait1();  // this tile's group has landed (the next one may still fly)
+        __syncthreads();
         if (cnt > kRankCap) {
             if (v < v1) {
                 const size_t s = (size_t)aoff[v];
                 rank_one<false>(v, ucnt[v], in_nbr + s, in_eid + s, skey + s, snbr + s, seid + s, nullptr, nullptr,
                                 adj_k32 + s, acur, best, bestu);
             }
+            __syncthreads();
             continue;  // block-uniform
         }
-        // 4 strided elements per trip: their 12 loads are in flight together
-        for (int i0 = threadIdx.x; i0 < cnt; i0 += 4 * blockDim.x) {
-            int n4[4], e4[4];
-            uint64_t k4[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const int i = i0 + q * blockDim.x;
-                if (i < cnt) {
-                    n4[q] = in_nbr[base + i];
-                    e4[q] = in_eid[base + i];
-                    k4[q] = skey[base + i];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const int i = i0 + q * blockDim.x;
-                if (i < cnt) {
-                    s_n[i] = n4[q];
-                    s_e[i] = e4[q];
-                    s_k[i] = k4[q];
-                }
-            }
-        }
-        __syncthreads();
+        int* s_n = s_nb + buf * kRankCap;
+        int* s_e = s_eb + buf * kRankCap;
+        uint64_t* s_k = s_kb + buf * kRankCap;
         if (v < v1) {
             const int o = aoff[v] - base;
             rank_one<false>(v, ucnt[v], s_n + o, s_e + o, s_k + o, s_n + o, s_e + o, nullptr, nullptr, s_32 + o, acur,
                             best, bestu);
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        for (int i = threadIdx.x; i < cnt; i += T) {
             snbr[base + i] = s_n[i];
             seid[base + i] = s_e[i];
             adj_k32[base + i] = s_32[i];
         }
-        __syncthreads();
+        __syncthreads();  // buffers free before the next prefetch overwrites them
     }
+    asm volatile("cp.async.wait_all;\n" ::);
 }
 
 // K3h: heavy tier -- one block per high-degree vertex (any degree).
