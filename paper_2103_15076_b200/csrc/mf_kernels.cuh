@@ -1684,6 +1684,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
             // shared memory (one coalesced load), then, only among the keys equal to the
             // k-th primary key, on the secondary half gathered from global memory
             uint64_t* sv = sh;  // a.chicap keys
+            uint64_t o = 0, an = ~0ull;
+            if (threadIdx.x < 2) s_oa[threadIdx.x] = threadIdx.x ? ~0ull : 0ull;
             for (int i0 = threadIdx.x; i0 < cnt; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
                 uint64_t v8[8];
 #pragma unroll
@@ -1694,12 +1696,43 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     const int i = i0 + q * blockDim.x;
-                    if (i < cnt) sv[i] = v8[q];
+                    if (i < cnt) {
+                        sv[i] = v8[q];
+                        o |= v8[q];
+                        an &= v8[q];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 16; q > 0; q >>= 1) {
+                o |= __shfl_xor_sync(0xffffffffu, o, q);
+                an &= __shfl_xor_sync(0xffffffffu, an, q);
+            }
+            __syncthreads();
+            if ((threadIdx.x & 31) == 0) {
+                atomicOr(s_oa, o);
+                atomicAnd(s_oa + 1, an);
+            }
+            __syncthreads();
+            // the bits every primary key shares (sign / exponent of the float64 costs) are fixed
+            // before the first pass: histogramming them would pile every key into one or two
+            // bins, and those shared-memory atomics serialise
+            uint64_t t = 0, q = 0;
+            int topc = 64;
+            {
+                const uint64_t diff = s_oa[0] ^ s_oa[1];
+                if (diff) {
+                    const int D = 63 - __clzll((long long)diff);
+                    if (D < 63) {
+                        t = s_oa[1] & ~((1ull << (D + 1)) - 1ull);
+                        topc = D + 1;
+                    }
+                } else {
+                    t = s_oa[1];
+                    topc = 0;
                 }
             }
             __syncthreads();
-            uint64_t t = 0, q = 0;
-            int topc = 64;
             const bool whole = radix_kth_u64(sv, cnt, kr, t, topc, hist, s_scan, s_sel, s_oa, s_bucket, kSelBucket);
             if (whole) {
                 t |= (topc >= 64) ? ~0ull : ((1ull << topc) - 1ull);
