@@ -402,7 +402,7 @@ struct WS {
     int* seid_u;  // unseeded: edge ids of the unsorted slots (their neighbours / keys are e1 / key_hi)
     int* lowfill;
     unsigned long long* suitor;
-    int *bestu, *front0, *front1, *ldc;
+    int *bestu, *front0, *front1, *ldc, *loose;
     unsigned* bar;
     int* selstate;
     int* ghist;
@@ -472,7 +472,8 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.bestu = A.take<int>((size_t)N0);
     W.front0 = A.take<int>((size_t)N0);
     W.front1 = A.take<int>((size_t)N0);
-    W.ldc = A.take<int>(8);
+    W.loose = A.take<int>((size_t)N0);
+    W.ldc = A.take<int>(8);  // [0..5] LD rounds, [6] unmatched vertices listed by k_mates
     W.bar = A.take<unsigned>(8);
     W.selstate = A.take<int>((size_t)2 * B);
     W.ghist = A.take<int>(kSelScratch);
@@ -722,7 +723,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             else LAUNCH(k_suitor1, grid_for(ctx, N), 256, 0, stream, ma);
         }
         LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, W.key_hi,
-               seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay, W.pairlo);
+               seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay, W.pairlo, W.loose, W.ldc + 6);
         // per-mesh selection; one big mesh first narrows its rank prefix with multi-block passes
         const bool big = (B == 1 && N >= (1 << 18));  // below: one CTA (latency-bound sizes)
         auto select = [&](const int* seg_cnt, const int* removed_in) {
@@ -761,7 +762,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                budget, absorb_cond);
         if (absorb_cond) stream = cc.begin(stream, absorb_cond, cudaGraphCondTypeIf);
         // absorb leftovers (one pass is exact: the matching is maximal when the budget is unmet)
-        LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
+        LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, W.loose, W.ldc + 6, W.aoff, W.ucnt, W.snbr,
+               W.adj_eid,
                seeded ? W.cost : nullptr, W.key_hi, W.pairlo, vmesh, voff_r, act, budget, W.removed, W.segB,
                W.chi, W.clo, W.caux);
         select(W.segB, W.removed);

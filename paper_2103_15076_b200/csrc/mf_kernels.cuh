@@ -1337,6 +1337,22 @@ MF_DEV int block_slot(bool keep, int* __restrict__ counter) {
     __syncthreads();
     return keep ? r : -1;
 }
+// Two block-aggregated appends from one block scan (counts packed 16:16; blocks <= 1024 threads).
+MF_DEV void block_slot2(bool ka, int* __restrict__ ca, int& ra, bool kb, int* __restrict__ cb, int& rb) {
+    __shared__ int s_scan[33];
+    __shared__ int s_base[2];
+    int tot;
+    const int pos = block_excl_scan((ka ? 1 : 0) | (kb ? 0x10000 : 0), s_scan, &tot);
+    if (threadIdx.x == 0) {
+        const int ta = tot & 0xffff, tb = tot >> 16;
+        s_base[0] = ta ? atomicAdd(ca, ta) : 0;
+        s_base[1] = tb ? atomicAdd(cb, tb) : 0;
+    }
+    __syncthreads();
+    ra = ka ? s_base[0] + (pos & 0xffff) : -1;
+    rb = kb ? s_base[1] + (pos >> 16) : -1;
+    __syncthreads();
+}
 MF_DEV int seg_slot_uniform(bool keep, const int* __restrict__ vmesh, const int* __restrict__ voff,
                             int* __restrict__ seg_cnt, int v) {
     if (!vmesh) return block_slot(keep, seg_cnt);
@@ -1361,10 +1377,12 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigne
                         const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
                         const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt,
                         uint64_t* __restrict__ chi, uint64_t* __restrict__ clo, int* __restrict__ cpay,
-                        int* __restrict__ pairlo) {
+                        int* __restrict__ pairlo, int* __restrict__ loose, int* __restrict__ loose_cnt) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    // block-uniform trip count: the single-mesh append is aggregated per block
+    // block-uniform trip count: the single-mesh append is aggregated per block.  Unmatched
+    // vertices are listed for the absorb stage (the only loose vertices it can see: pairs
+    // dropped by the truncation exist only where the budget is met, and then it does not run)
     for (int base = blockIdx.x * blockDim.x; base < N; base += gridDim.x * blockDim.x) {
         const int v = base + threadIdx.x;
         int m = -1;
@@ -1382,7 +1400,15 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigne
             pairlo[v] = lo;
             cand = lo == v;
         }
-        const int slot = seg_slot_uniform(cand, vmesh, voff, seg_cnt, v);
+        const bool lz = v < N && m < 0;
+        int slot, lslot;
+        if (!vmesh) {
+            block_slot2(cand, seg_cnt, slot, lz, loose_cnt, lslot);
+        } else {
+            slot = seg_slot_uniform(cand, vmesh, voff, seg_cnt, v);
+            lslot = block_slot(lz, loose_cnt);
+        }
+        if (lz) loose[lslot] = v;
         if (cand) {
             chi[slot] = key_hi[m];
             clo[slot] = key_lo ? key_lo[m] : (uint64_t)m;
@@ -2301,7 +2327,8 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
 // Absorb candidates (decimate.py:207-221): every unmatched vertex with edges
 // picks its lowest (cost, rep) incident edge; the matching is maximal here so
 // every neighbour is clustered and one pass suffices.
-__global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const int* __restrict__ aoff,
+__global__ void k_absorb_cand(const int* __restrict__ abort_flag, const int* __restrict__ loose,
+                              const int* __restrict__ loose_cnt, const int* __restrict__ aoff,
                               const int* __restrict__ ucnt, const int* __restrict__ nbr,
                               const int* __restrict__ adj_eid, const double* __restrict__ cost,
                               const uint64_t* __restrict__ ckey, const int* __restrict__ pairlo,
@@ -2313,13 +2340,15 @@ __global__ void k_absorb_cand(const int* __restrict__ abort_flag, int N, const i
     MF_PDL_ENTRY;
     if (*abort_flag) return;
     if (!vmesh && (!act[0] || removed[0] >= budget[0])) return;  // budget met: no absorption this round
-    for (int base = blockIdx.x * blockDim.x; base < N; base += gridDim.x * blockDim.x) {
-        const int v = base + threadIdx.x;
+    const int L = *loose_cnt;  // the unmatched vertices k_mates listed (a thread each)
+    for (int base = blockIdx.x * blockDim.x; base < L; base += gridDim.x * blockDim.x) {
+        const int li = base + threadIdx.x;
+        const int v = li < L ? loose[li] : -1;
         bool cand = false;
         uint64_t bk = ~0ull;
         int brep = 0x7fffffff;
         int nu = 0;
-        if (v < N) {
+        if (v >= 0) {
             nu = ucnt[v];
             if (nu > 0 && pairlo[v] < 0) {
                 int bm = mesh_of(vmesh, v);
