@@ -1705,7 +1705,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
             }
             kr = k;
         }
-        if (!a.resume && cnt > a.cap && cnt <= a.chicap) {
+        if (!a.resume && cnt <= a.chicap) {
             // mid-size segment: the 64-bit primary keys fit the stage -- select on them in
             // shared memory (one coalesced load), then, only among the keys equal to the
             // k-th primary key, on the secondary half gathered from global memory
