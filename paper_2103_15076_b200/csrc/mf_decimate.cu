@@ -22,6 +22,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mf_internal.h"
@@ -426,6 +427,28 @@ struct WS {
     int* status;  // [8] flags | foff_final[B+1] | fail[3B] | stats[4R]
     size_t status_words;
 };
+
+// memcmp(a, b, bytes) != 0, split over host threads above 8 MB
+static bool host_differ(const void* a, const void* b, size_t bytes) {
+    const size_t chunk = (size_t)8 << 20;
+    unsigned hw = std::thread::hardware_concurrency();
+    size_t T = std::min<size_t>(std::min<unsigned>(hw ? hw : 1, 16), (bytes + chunk - 1) / chunk);
+    if (T <= 1) return memcmp(a, b, bytes) != 0;
+    std::vector<std::thread> th;
+    std::vector<char> diff(T, 0);
+    const size_t per = (bytes + T - 1) / T;
+    for (size_t t = 0; t < T; t++)
+        th.emplace_back([&, t]() {
+            const size_t o = t * per, e = std::min(bytes, o + per);
+            if (o < e) diff[t] = memcmp((const char*)a + o, (const char*)b + o, e - o) != 0;
+        });
+    bool d = false;
+    for (size_t t = 0; t < T; t++) {
+        th[t].join();
+        d = d || diff[t];
+    }
+    return d;
+}
 
 static void layout(Arena& A, WS& W, const Plan& p) {
     const int B = p.B, R = p.R, N0 = p.N0, N1 = p.N1, Mcap = p.Mcap, Ecap = p.Ecap, Nfin = p.Nfin;
@@ -1003,8 +1026,9 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         }
     } tmp_free{alias_tmp, stream};
     const size_t pbytes = (size_t)n * 24;
-    const bool host_check = verify && !is_device_ptr(mv->positions) && !is_device_ptr(mv->features) &&
-                            pbytes <= ((size_t)16 << 20);
+    // host arrays are compared in host memory (threads, while the GPU works): the PCIe link is
+    // what bounds a call with host arrays, so the features are never uploaded just to be compared
+    const bool host_check = verify && !is_device_ptr(mv->positions) && !is_device_ptr(mv->features);
     int* d_diff = nullptr;
     if (verify && !host_check) {
         const bool xd = is_device_ptr(mv->features);
@@ -1195,7 +1219,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
                (const unsigned long long*)X_src, d_diff);
         MF_CUDA_TRY(cudaMemcpyAsync(&h_diff, d_diff, 4, cudaMemcpyDeviceToHost, stream));
     }
-    if (host_check) h_diff = memcmp(mv->positions, mv->features, pbytes) != 0;  // while the GPU works
+    if (host_check) h_diff = host_differ(mv->positions, mv->features, pbytes);  // while the GPU works
     // ---- single readback
     MF_CUDA_TRY(cudaMemcpyAsync(h_status, W.status, W.status_words * 4, cudaMemcpyDeviceToHost, stream));
     MF_CUDA_TRY(cudaStreamSynchronize(stream));
