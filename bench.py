@@ -497,7 +497,7 @@ def run_ours(args):
         "roofline": roof,
         "cpu_baseline": cpu,
         "kernels": {k: {"ms": round(v[0], 4), "share": round(v[0] / total_ms, 4), "launches": v[1]}
-                    for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:16]},
+                    for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:40]},
         "round_stats": rounds,
     }
     if vs is not None:

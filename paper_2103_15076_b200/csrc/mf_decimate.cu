@@ -691,7 +691,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             EdgeOut eo{W.e0,      W.e1,   seeded ? W.cost : nullptr, nullptr, seeded ? W.snbr : W.e1,
                        seeded ? W.adj_eid : W.seid_u, seeded ? nullptr : W.key_hi,
                        W.lowfill, W.mate, W.minrep, W.absorbed, W.abshead, W.suitor, W.mlo, W.mhi,
-                       W.segA,    W.ldc};
+                       W.segA,    W.ldc,  W.segB};
             const int eg = grid_for(ctx, (int64_t)N * kEdgeLanes);
             if (p.placement)
                 LAUNCH(k_edges<1>, eg, 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.aoff, W.eoff, W.vq,
@@ -780,15 +780,17 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // the absorb stage runs only when some mesh misses its budget after truncation (IF node,
         // condition set by k_trunc_apply); skipping it leaves removed / absorbed as they are
         const cudaGraphConditionalHandle absorb_cond = cc.on() ? cc.handle(stream, 1u) : 0;
-        LAUNCH(k_trunc_apply, grid_for(ctx, N), 256, 0, stream, d_abort, N, vmesh, voff_r, W.segA, W.chi, W.clo,
-               W.cpay, W.mode, W.p_hi, W.p_lo, W.e0, W.e1, W.mate, B, W.ksel, W.removed, W.segB, W.pairlo, act,
-               budget, absorb_cond);
+        // truncation + absorb candidates (one pass is exact: the matching is maximal when the
+        // budget is unmet), one launch: they act on disjoint meshes
+        {
+            TruncArgs ta{N,    vmesh,  voff_r, W.segA,    W.chi,     W.clo,    W.cpay,   W.mode, W.p_hi, W.p_lo,
+                         W.e0, W.e1,   W.mate, B,         W.ksel,    W.removed, W.segB,  W.pairlo, act,  budget,
+                         absorb_cond};
+            AbsorbArgs aa{W.loose, W.ldc + 6, W.aoff, W.ucnt, W.snbr, W.adj_eid, seeded ? W.cost : nullptr, W.key_hi,
+                          W.pairlo, vmesh, voff_r, act, budget, W.ksel, W.segB, W.chi, W.clo, W.caux};
+            LAUNCH(k_trunc_absorb, grid_for(ctx, N), 256, 0, stream, d_abort, ta, aa);
+        }
         if (absorb_cond) stream = cc.begin(stream, absorb_cond, cudaGraphCondTypeIf);
-        // absorb leftovers (one pass is exact: the matching is maximal when the budget is unmet)
-        LAUNCH(k_absorb_cand, grid_for(ctx, N), 256, 0, stream, d_abort, W.loose, W.ldc + 6, W.aoff, W.ucnt, W.snbr,
-               W.adj_eid,
-               seeded ? W.cost : nullptr, W.key_hi, W.pairlo, vmesh, voff_r, act, budget, W.removed, W.segB,
-               W.chi, W.clo, W.caux);
         select(W.segB, W.removed);
         RoundFail rf{d_abort, d_fail, d_fail + B, d_fail + 2 * B};
         LAUNCH(k_absorb_apply, grid_for(ctx, N), 256, 0, stream, N, vmesh, voff_r, W.segB, W.chi, W.clo, W.caux,

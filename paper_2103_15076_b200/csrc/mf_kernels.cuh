@@ -480,6 +480,7 @@ struct EdgeOut {
     unsigned long long* mhi;
     int* seg_cnt;
     int* ldc;
+    int* seg_cnt2;  // absorb-candidate segments (appended while the truncation runs)
 };
 
 constexpr int kEdgeLanes = 4;
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
         o.mlo[b] = ~0ull;
         o.mhi[b] = 0ull;
         o.seg_cnt[b] = 0;  // truncation-candidate segments (k_mates appends)
+        o.seg_cnt2[b] = 0;
     }
     if (blockIdx.x == 0 && threadIdx.x < 8) o.ldc[threadIdx.x] = 0;  // LD round counters
     const int l = threadIdx.x % kEdgeLanes;
@@ -2290,7 +2292,7 @@ MF_DEV bool seg_valid(const int* __restrict__ vmesh, const int* __restrict__ vof
 }
 
 // Unmatch the pairs beyond the budget; removed = number kept.
-__global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const int* __restrict__ vmesh,
+MF_DEV void trunc_apply_body(const int* __restrict__ abort_flag, int N, const int* __restrict__ vmesh,
                               const int* __restrict__ voff, const int* __restrict__ seg_cnt,
                               const uint64_t* __restrict__ chi, const uint64_t* __restrict__ clo,
                               const int* __restrict__ cpay, const int* __restrict__ mode,
@@ -2299,8 +2301,6 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
                               const int* __restrict__ ksel, int* __restrict__ removed, int* __restrict__ seg_cnt2,
                               int* __restrict__ pairlo, const int* __restrict__ act, const int* __restrict__ budget,
                               cudaGraphConditionalHandle absorb_cond) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
     if (absorb_cond && blockIdx.x == 0 && threadIdx.x == 0) {
         // the absorb stage (an IF node) runs only if some mesh still misses its budget
         bool need = false;
@@ -2308,10 +2308,8 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
         cudaGraphSetConditional(absorb_cond, need ? 1u : 0u);
     }
     int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    for (int b = tid; b < B; b += nth) {
-        removed[b] = ksel[b];
-        seg_cnt2[b] = 0;
-    }
+    for (int b = tid; b < B; b += nth) removed[b] = ksel[b];
+    (void)seg_cnt2;  // zeroed by k_edges: the absorb phase appends concurrently
     for (int i = tid; i < N; i += nth) {
         int b;
         if (!seg_valid(vmesh, voff, seg_cnt, i, b)) continue;
@@ -2327,7 +2325,7 @@ __global__ void k_trunc_apply(const int* __restrict__ abort_flag, int N, const i
 // Absorb candidates (decimate.py:207-221): every unmatched vertex with edges
 // picks its lowest (cost, rep) incident edge; the matching is maximal here so
 // every neighbour is clustered and one pass suffices.
-__global__ void k_absorb_cand(const int* __restrict__ abort_flag, const int* __restrict__ loose,
+MF_DEV void absorb_cand_body(const int* __restrict__ loose,
                               const int* __restrict__ loose_cnt, const int* __restrict__ aoff,
                               const int* __restrict__ ucnt, const int* __restrict__ nbr,
                               const int* __restrict__ adj_eid, const double* __restrict__ cost,
@@ -2337,8 +2335,6 @@ __global__ void k_absorb_cand(const int* __restrict__ abort_flag, const int* __r
                               const int* __restrict__ budget, const int* __restrict__ removed,
                               int* __restrict__ seg_cnt, uint64_t* __restrict__ chi, uint64_t* __restrict__ clo,
                               int* __restrict__ caux) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
     if (!vmesh && (!act[0] || removed[0] >= budget[0])) return;  // budget met: no absorption this round
     const int L = *loose_cnt;  // the unmatched vertices k_mates listed (a thread each)
     for (int base = blockIdx.x * blockDim.x; base < L; base += gridDim.x * blockDim.x) {
@@ -2387,6 +2383,43 @@ __global__ void k_absorb_cand(const int* __restrict__ abort_flag, const int* __r
             caux[slot] = brep;
         }
     }
+}
+
+// Truncation and absorb candidates in one launch.  They touch disjoint meshes: the
+// truncation unmatches pairs only where the budget is met (the selection kept fewer
+// than all of them), and absorption runs only where it is not -- so the absorb phase
+// needs no barrier behind the truncation (it reads the kept count from `ksel`, which
+// is what the truncation stores into `removed`).
+struct TruncArgs {
+    int N;
+    const int *vmesh, *voff, *seg_cnt;
+    const uint64_t *chi, *clo;
+    const int *cpay, *mode;
+    const uint64_t *thi, *tlo;
+    const int *e0, *e1;
+    int* mate;
+    int B;
+    const int* ksel;
+    int *removed, *seg_cnt2, *pairlo;
+    const int *act, *budget;
+    cudaGraphConditionalHandle absorb_cond;
+};
+struct AbsorbArgs {
+    const int *loose, *loose_cnt, *aoff, *ucnt, *nbr, *adj_eid;
+    const double* cost;
+    const uint64_t* ckey;
+    const int *pairlo, *vmesh, *voff, *act, *budget, *kept;
+    int* seg_cnt;
+    uint64_t *chi, *clo;
+    int* caux;
+};
+__global__ void k_trunc_absorb(const int* __restrict__ abort_flag, TruncArgs t, AbsorbArgs a) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    trunc_apply_body(abort_flag, t.N, t.vmesh, t.voff, t.seg_cnt, t.chi, t.clo, t.cpay, t.mode, t.thi, t.tlo, t.e0,
+                     t.e1, t.mate, t.B, t.ksel, t.removed, t.seg_cnt2, t.pairlo, t.act, t.budget, t.absorb_cond);
+    absorb_cand_body(a.loose, a.loose_cnt, a.aoff, a.ucnt, a.nbr, a.adj_eid, a.cost, a.ckey, a.pairlo, a.vmesh, a.voff,
+                     a.act, a.budget, a.kept, a.seg_cnt, a.chi, a.clo, a.caux);
 }
 
 struct RoundFail {
