@@ -637,8 +637,9 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
            256, 0, stream, W.status, (int)W.status_words, (int)(d_fail - W.status), (int)(d_fail - W.status) + 3 * B,
            W.foff_a, d_foff0, B, W.deg, W.cursor, W.lowfill, N0 + 1, W.counters, W.scan.buf[0], W.scan.buf[1], W.scan.words,
            W.ghist, kSelScratch);
-    if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, W.F0, B, W.vo64, W.fo64, d_badf);
-    if (n > 0) LAUNCH(k_check_finite, grid_for(ctx, 3 * n), 256, 0, stream, 3 * n, W.P0, d_badp);
+    if (m > 0 || n > 0)
+        LAUNCH(k_inputs_in, grid_for(ctx, std::max<int64_t>(m, 3 * n)), 256, 0, stream, m, W.F64, W.F0, B, W.vo64,
+               W.fo64, d_badf, 3 * n, W.P0, d_badp);
     if (W.Xf32 && n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, W.X0);
 
     const double* Pc = W.P0;
@@ -676,10 +677,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // vertex quadrics + unique neighbour lists
         LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap,
                W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
-        LAUNCH(k_vertex, ctx->sm_count * 8, 256, 0, stream, d_abort, W.mid, d_mid_n, W.inc_off, W.inc, Fc, W.plane,
-               Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.heavy, d_heavy_n);
-        LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
-               W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
+        LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, d_abort, W.mid, d_mid_n, W.heavy, d_heavy_n,
+               W.inc_off, W.inc, W.inc_tmp, Fc, W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
         // lexicographic edges + pair costs + rank keys
         // compact adjacency offsets (2 slots per edge); seeded rounds also need the dense
         // lexicographic edge index (the PCG64 key-stream position, decimate.py:190)
@@ -976,10 +975,8 @@ int quality_run(Context* ctx, const mf_mesh_view* mv, const int* d_off, const in
                       misc + 3, W.inc_off, W.cursor, W.inc);
         LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, misc, N, W.inc_off, W.inc, W.F0, W.plane, Mc, W.vq,
                W.nbr, W.ucnt, W.upcnt, W.mid, misc + 12, W.heavy, misc + 8);
-        LAUNCH(k_vertex, ctx->sm_count * 8, 256, 0, stream, misc, W.mid, misc + 12, W.inc_off, W.inc, W.F0, W.plane,
-               Mc, W.vq, W.nbr, W.ucnt, W.upcnt, W.heavy, misc + 8);
-        LAUNCH(k_vertex_heavy, ctx->sm_count, 256, 0, stream, misc, W.heavy, misc + 8, W.inc_off, W.inc, W.inc_tmp,
-               W.F0, W.plane, Mc, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
+        LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, misc, W.mid, misc + 12, W.heavy, misc + 8,
+               W.inc_off, W.inc, W.inc_tmp, W.F0, W.plane, Mc, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
     }
     if (n_out) LAUNCH(k_quality, grid_for(ctx, n_out), 256, 0, stream, (int)n_out, d_off, d_mem, W.vq, d_Pout, order,
                       d_err);

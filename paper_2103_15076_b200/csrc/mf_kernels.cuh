@@ -2,14 +2,14 @@
 //
 // Kernel map (reference call site -> kernel), SURVEY.md §8(a):
 //   mesh.py:72-88 + quadrics.py:36-45    k_facet_plane        facet plane (n, d), incidence degrees
-//   quadrics.py:69-77 (np.add.at order)  k_inc_scatter + k_vertex{,_heavy}: corner-major incidence CSR,
+//   quadrics.py:69-77 (np.add.at order)  k_inc_scatter + k_vertex_t / k_vertex_tiers: incidence CSR,
 //                                         sequential per-vertex quadric fold, unique neighbour lists
 //   mesh.py:125-134 + quadrics.py:117-132 k_edges             lexicographic edge ids, pair cost, rank keys
 //   decimate.py:181-191 (seeded)         k_cost_minmax + k_seed_keys  PCG64 jump-ahead keys, buckets
 //   decimate.py:248-263 (greedy)         k_suitor + k_mates    proposal (Suitor) greedy matching, CAS only
-//   decimate.py:256-263 (budget stop)    k_trunc_* + k_select  per-mesh MSD radix select of the lowest ranks
-//   decimate.py:194-226 (absorb)         k_absorb_* + k_select one-pass absorption of the leftovers
-//   decimate.py:130-137, 275-278         k_relabel{1,2,3}      min-member flags + exclusive scan
+//   decimate.py:256-263 (budget stop)    k_select + k_trunc_absorb  per-mesh radix select of the lowest ranks
+//   decimate.py:194-226 (absorb)         k_trunc_absorb + k_select + k_absorb_apply  one-pass absorption
+//   decimate.py:130-137, 275-278         k_scan<rep> + k_relabel3  min-member flags + exclusive scan
 //   decimate.py:142-145, 280-283         k_contract{,_heavy}   ascending-member fold from +0.0, / count
 //   decimate.py:147-167                  k_facet_remap / keep / write   remap, degenerate drop, hash dedupe
 //   decimate.py:380-381                  k_compose             replace / mapping chaining (-1 sticky)
@@ -358,15 +358,13 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
 }
 
 // Mid tier (degree 9..32): one full warp per vertex, one incidence per lane.
-__global__ void __launch_bounds__(256) k_vertex(const int* __restrict__ abort_flag, const int* __restrict__ list,
+MF_DEV void vertex_mid_body(const int* __restrict__ list,
                                                 const int* __restrict__ list_count, const int* __restrict__ inc_off,
                                                 const int* __restrict__ inc, const int* __restrict__ F,
                                                 const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
                                                 int* __restrict__ nbr, int* __restrict__ ucnt,
                                                 int* __restrict__ upcnt, int* __restrict__ heavy,
                                                 int* __restrict__ heavy_count) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
     __shared__ double s_q[8][kMid][10];
     __shared__ int s_c[8][2 * kMid];
     const int g = threadIdx.x >> 5;  // warp within block
@@ -761,14 +759,12 @@ __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ 
 }
 
 // K3h: heavy tier -- one block per high-degree vertex (any degree).
-__global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ abort_flag, const int* __restrict__ heavy, const int* __restrict__ heavy_count,
+MF_DEV void vertex_heavy_body(const int* __restrict__ heavy, const int* __restrict__ heavy_count,
                                                       const int* __restrict__ inc_off, int* __restrict__ inc,
                                                       int* __restrict__ inc_tmp, const int* __restrict__ F,
                                                       const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
                                                       int* __restrict__ nbr, int* __restrict__ nbr_tmp,
                                                       int* __restrict__ ucnt, int* __restrict__ upcnt) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
     __shared__ int smem[kChunk];
     __shared__ Plane s_pl[256];
     __shared__ int s_scan[33];
@@ -834,6 +830,22 @@ __global__ void __launch_bounds__(256) k_vertex_heavy(const int* __restrict__ ab
 }
 
 
+
+// Mid (degree 9..32, a warp per vertex) and heavy (a block per vertex) tiers in one
+// launch: both lists are complete once k_vertex_t has run, and they are disjoint.
+__global__ void __launch_bounds__(256) k_vertex_tiers(const int* __restrict__ abort_flag, const int* __restrict__ mid,
+                                                      const int* __restrict__ mid_count, const int* __restrict__ heavy,
+                                                      const int* __restrict__ heavy_count,
+                                                      const int* __restrict__ inc_off, int* __restrict__ inc,
+                                                      int* __restrict__ inc_tmp, const int* __restrict__ F,
+                                                      const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
+                                                      int* __restrict__ nbr, int* __restrict__ nbr_tmp,
+                                                      int* __restrict__ ucnt, int* __restrict__ upcnt) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    vertex_heavy_body(heavy, heavy_count, inc_off, inc, inc_tmp, F, plane, Mcap, vq, nbr, nbr_tmp, ucnt, upcnt);
+    vertex_mid_body(mid, mid_count, inc_off, inc, F, plane, Mcap, vq, nbr, ucnt, upcnt, nullptr, nullptr);
+}
 
 // ------------------------------------------------------------------------
 // Seeded shuffle keys (decimate.py:184-191).
@@ -2891,10 +2903,29 @@ __global__ void k_facets_in(int64_t M, const int64_t* __restrict__ F64, int* __r
         F32[3 * f + 2] = (int)c;
     }
 }
-__global__ void k_check_finite(int64_t n, const double* __restrict__ P, int* __restrict__ bad) {
+// Both input checks in one launch: facets converted / validated (as k_facets_in) and
+// positions checked for NaN / inf.
+__global__ void k_inputs_in(int64_t M, const int64_t* __restrict__ F64, int* __restrict__ F32, int B,
+                            const int64_t* __restrict__ voff, const int64_t* __restrict__ foff, int* __restrict__ badf,
+                            int64_t n3, const double* __restrict__ P, int* __restrict__ badp) {
     MF_PDL_ENTRY;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        if (!isfinite(P[i])) atomicExch(bad, 1);
+    const int64_t T = M > n3 ? M : n3;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < T; f += (int64_t)gridDim.x * blockDim.x) {
+        if (f < n3 && !isfinite(P[f])) atomicExch(badp, 1);
+        if (f >= M) continue;
+        int lo = 0, hi = B;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (foff[mid] <= f) lo = mid; else hi = mid;
+        }
+        int64_t vlo = voff[lo], vhi = voff[lo + 1];
+        int64_t a = F64[3 * f], b = F64[3 * f + 1], c = F64[3 * f + 2];
+        bool ok = a >= vlo && a < vhi && b >= vlo && b < vhi && c >= vlo && c < vhi && a != b && b != c && a != c;
+        if (!ok) atomicMin(badf, (int)min(f, (int64_t)0x7ffffffe));
+        F32[3 * f] = (int)a;
+        F32[3 * f + 1] = (int)b;
+        F32[3 * f + 2] = (int)c;
+    }
 }
 __global__ void k_f32_to_f64(int64_t n, const float* __restrict__ a, double* __restrict__ b) {
     MF_PDL_ENTRY;
