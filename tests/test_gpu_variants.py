@@ -46,6 +46,7 @@ VARIANTS = [
     {"MF_SUITOR": "4"},
     {"MF_SUITOR": "2"},
     {"MF_LD1_MIN": "1"},
+    {"MF_LD1_MIN": "1", "MF_LD_MID": "5"},
     {"MF_LD_MIN": "1", "MF_SUITOR": "1"},
     {"MF_SELECT_CL": "1"},
     {"MF_SEL_CAP": "12288"},
