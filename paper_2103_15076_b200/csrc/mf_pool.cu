@@ -200,8 +200,19 @@ __global__ void k_unpool_vec(int64_t n, int64_t row16, const int* __restrict__ r
                              int4* __restrict__ out) {
     MF_PDL_ENTRY;
     const int64_t total = n * row16;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; idx + 3 * stride < total; idx += 4 * stride) {  // four rows' gathers in flight
+        int4 r[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int64_t i = idx + q * stride, v = i / row16, j = i - v * row16;
+            r[q] = __ldg(coarse + (int64_t)rep[v] * row16 + j);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) out[idx + q * stride] = r[q];
+    }
+    for (; idx < total; idx += stride) {
         int64_t v = idx / row16, j = idx - v * row16;
         out[idx] = __ldg(coarse + (int64_t)rep[v] * row16 + j);
     }
