@@ -196,9 +196,12 @@ MF_DEV void q_add_plane(Q10& q, const Plane& p) {
     q.c = q.c + p.d * p.d;  // degenerate facets: n = 0, d = -0*.. -> d*d == +0 == forced 0 (quadrics.py:65)
 }
 MF_DEV void q_store(double* __restrict__ vq, int v, const Q10& q) {
-    double* o = vq + 10 * (size_t)v;
-    o[0] = q.a00; o[1] = q.a01; o[2] = q.a02; o[3] = q.a11; o[4] = q.a12;
-    o[5] = q.a22; o[6] = q.b0; o[7] = q.b1; o[8] = q.b2; o[9] = q.c;
+    double2* o = reinterpret_cast<double2*>(vq + 10 * (size_t)v);  // 80-byte rows: 16-byte aligned
+    o[0] = make_double2(q.a00, q.a01);
+    o[1] = make_double2(q.a02, q.a11);
+    o[2] = make_double2(q.a12, q.a22);
+    o[3] = make_double2(q.b0, q.b1);
+    o[4] = make_double2(q.b2, q.c);
 }
 MF_DEV void q_load(const double* __restrict__ vq, int v, Q10& q) {
     const double2* o = reinterpret_cast<const double2*>(vq + 10 * (size_t)v);
