@@ -307,6 +307,7 @@ MF_DEV void reg_sort(int (&a)[L]) {
 // kernel (list `mid`), larger to the block tier (list `heavy`).
 constexpr int kThreadDeg = 8;
 constexpr int kMid = 32;
+constexpr int kVtStage = 4096;  // k_vertex_t neighbour-list stage (ints): 128 vertices of mean degree <= 16
 __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ inc,
                                                   const int* __restrict__ F, const Plane* __restrict__ plane,
@@ -316,47 +317,70 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
                                                   int* __restrict__ heavy, int* __restrict__ heavy_count) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
-        const int s = inc_off[v], d = inc_off[v + 1] - s;
-        if (d > kThreadDeg) {
-            if (d <= kMid) mid[append_slot(mid_count)] = v;
-            else heavy[append_slot(heavy_count)] = v;
-            continue;
-        }
-        int k[kThreadDeg];
-#pragma unroll
-        for (int i = 0; i < kThreadDeg; i++) k[i] = (i < d) ? inc[s + i] : 0x7fffffff;
-        reg_sort(k);
-        Q10 q;
-        q_zero(q);
-        int c[2 * kThreadDeg];
-#pragma unroll
-        for (int i = 0; i < kThreadDeg; i++) {
-            c[2 * i] = 0x7fffffff;
-            c[2 * i + 1] = 0x7fffffff;
-            if (i < d) {
-                int corner, f;
-                decode_inc(k[i], Mcap, corner, f);
-                Plane p = plane[f];
-                q_add_plane(q, p);
-                other_two(F, f, corner, c[2 * i], c[2 * i + 1]);
+    // The neighbour lists of a block's 128 consecutive vertices form one contiguous range
+    // (2 * inc_off layout); they are assembled in shared memory and written out coalesced
+    // (per-thread stores of a few ints at 2*deg strides touch a sector each).  Slots of
+    // mid / heavy vertices and the unused tail of each list get whatever the stage holds:
+    // k_vertex_tiers writes the former afterwards, nothing reads the latter.
+    __shared__ int s_nb[kVtStage];
+    for (int base = blockIdx.x * blockDim.x; base < N; base += gridDim.x * blockDim.x) {
+        const int v = base + threadIdx.x;
+        const int r0 = inc_off[base], r1 = inc_off[min(N, base + (int)blockDim.x)];
+        const bool staged = 2 * (r1 - r0) <= kVtStage;  // block-uniform
+        bool work = false;
+        int s = 0, d = 0;
+        if (v < N) {
+            s = inc_off[v];
+            d = inc_off[v + 1] - s;
+            if (d > kThreadDeg) {
+                if (d <= kMid) mid[append_slot(mid_count)] = v;
+                else heavy[append_slot(heavy_count)] = v;
+            } else {
+                work = true;
             }
         }
-        q_store(vq, v, q);
-        reg_sort(c);
-        int nu = 0, nup = 0;
-        int* out = nbr + 2 * (size_t)s;
+        if (work) {
+            int k[kThreadDeg];
 #pragma unroll
-        for (int i = 0; i < 2 * kThreadDeg; i++) {
-            const int x = c[i];
-            const bool keep = (x != 0x7fffffff) && (i == 0 || x != c[i > 0 ? i - 1 : 0]);
-            if (keep) {
-                out[nu++] = x;
-                nup += x > v;
+            for (int i = 0; i < kThreadDeg; i++) k[i] = (i < d) ? inc[s + i] : 0x7fffffff;
+            reg_sort(k);
+            Q10 q;
+            q_zero(q);
+            int c[2 * kThreadDeg];
+#pragma unroll
+            for (int i = 0; i < kThreadDeg; i++) {
+                c[2 * i] = 0x7fffffff;
+                c[2 * i + 1] = 0x7fffffff;
+                if (i < d) {
+                    int corner, f;
+                    decode_inc(k[i], Mcap, corner, f);
+                    Plane p = plane[f];
+                    q_add_plane(q, p);
+                    other_two(F, f, corner, c[2 * i], c[2 * i + 1]);
+                }
             }
+            q_store(vq, v, q);
+            reg_sort(c);
+            int nu = 0, nup = 0;
+            int* out = staged ? s_nb + 2 * (s - r0) : nbr + 2 * (size_t)s;
+#pragma unroll
+            for (int i = 0; i < 2 * kThreadDeg; i++) {
+                const int x = c[i];
+                const bool keep = (x != 0x7fffffff) && (i == 0 || x != c[i > 0 ? i - 1 : 0]);
+                if (keep) {
+                    out[nu++] = x;
+                    nup += x > v;
+                }
+            }
+            ucnt[v] = nu;
+            upcnt[v] = nup;
         }
-        ucnt[v] = nu;
-        upcnt[v] = nup;
+        if (staged) {
+            __syncthreads();
+            int* dst = nbr + 2 * (size_t)r0;
+            for (int i = threadIdx.x; i < 2 * (r1 - r0); i += blockDim.x) dst[i] = s_nb[i];
+            __syncthreads();
+        }
     }
 }
 
