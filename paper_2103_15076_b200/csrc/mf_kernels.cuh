@@ -2997,9 +2997,32 @@ struct EmitJobs {
 };
 __global__ void k_emit(EmitJobs j) {
     MF_PDL_ENTRY;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     for (int q = 0; q < j.count; q++) {
         const int64_t n = j.n[q];
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = j.kind[q];
+        // two elements per thread as one 16-byte store when both ends are 16-byte aligned
+        if (k != kEmitF32 && (((uintptr_t)j.dst[q] | (uintptr_t)j.src[q]) & 15) == 0) {
+            const int64_t h = n >> 1;
+            if (k == kEmitI32) {
+                const int2* sp = (const int2*)j.src[q];
+                longlong2* dp = (longlong2*)j.dst[q];
+                for (int64_t i = tid; i < h; i += nth) {
+                    const int2 x = sp[i];
+                    dp[i] = make_longlong2(x.x, x.y);
+                }
+            } else {
+                const double2* sp = (const double2*)j.src[q];
+                double2* dp = (double2*)j.dst[q];
+                for (int64_t i = tid; i < h; i += nth) dp[i] = sp[i];
+            }
+            if ((n & 1) && tid == 0) {
+                if (k == kEmitI32) ((int64_t*)j.dst[q])[n - 1] = ((const int*)j.src[q])[n - 1];
+                else ((double*)j.dst[q])[n - 1] = ((const double*)j.src[q])[n - 1];
+            }
+            continue;
+        }
+        for (int64_t i = tid; i < n; i += nth) {
             if (j.kind[q] == kEmitI32) ((int64_t*)j.dst[q])[i] = ((const int*)j.src[q])[i];
             else if (j.kind[q] == kEmitF64) ((double*)j.dst[q])[i] = ((const double*)j.src[q])[i];
             else ((float*)j.dst[q])[i] = (float)((const double*)j.src[q])[i];
