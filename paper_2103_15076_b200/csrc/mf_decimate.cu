@@ -268,6 +268,8 @@ struct Plan {
     int ld_min = kLDMinVertices;  // rounds with at least this many vertices start with LD rounds
     int ld1_min = 1 << 17;        // ... from this many, one LD round (measured: cfg4 1.07 -> 1.04 ms, cfg3
                                   // 2.97 -> 2.92; at cfg2 (115k) the two extra launches outweigh it)
+    int ld_big = 4;               // LD rounds from ld_min (MF_LD_BIG; cfg5 13.06 -> 12.85 ms vs 12: the
+                                  // frontier is small after 3-4 rounds and Suitor finishes it faster)
     int ld_mid = 2;               // LD rounds between ld1_min and ld_min (MF_LD_MID; cfg4 0.880 -> 0.865
                                   // ms with 2, 3 and 5 no better)
     int placement = 0;            // 0 = average, 1 = inverse (quadrics.py:89-114)
@@ -380,6 +382,7 @@ static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan
     if (const char* e = getenv("MF_LD_MIN")) p.ld_min = atoi(e);
     if (const char* e = getenv("MF_LD1_MIN")) p.ld1_min = atoi(e);
     if (const char* e = getenv("MF_LD_MID")) p.ld_mid = std::max(1, std::min(kLDRounds, atoi(e)));
+    if (const char* e = getenv("MF_LD_BIG")) p.ld_big = std::max(1, std::min(kLDRounds, atoi(e)));
     for (int i = 0; i < 4; i++) p.pcg[i] = cfg->pcg_state[i];
     // device params: act | budget | nin | voff | foff0 (int32)
     p.params_words = (size_t)p.nParamR * B * 2 + (size_t)(R + 1) * B + (size_t)(R + 1) * (B + 1) + (B + 1);
@@ -712,7 +715,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // then Suitor proposals on the residual frontier; smaller meshes: Suitor only
         // locally-dominant rounds: all 12 from ld_min vertices; below, from ld1_min, only round
         // 0 (the mutual best edges, matched before the proposals start)
-        const int ld_rounds = N >= p.ld_min ? kLDRounds : (N >= p.ld1_min ? p.ld_mid : 0);
+        const int ld_rounds = N >= p.ld_min ? p.ld_big : (N >= p.ld1_min ? p.ld_mid : 0);
         const bool use_ld = ld_rounds > 0;
         if (seeded)
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
@@ -874,7 +877,7 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.placement};
+                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
     return k;

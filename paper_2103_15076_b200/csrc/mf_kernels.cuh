@@ -1200,7 +1200,7 @@ __global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
 // neighbourhood in rank order, so the sequential greedy scan accepts it too.
 // Matched / exhausted vertices leave the frontier.  After `max_rounds` the
 // remaining frontier is finished by k_suitor on the residual graph.
-constexpr int kLDRounds = 12;  // fixed in the graph; rounds after convergence exit at once
+constexpr int kLDRounds = 12;  // most LD rounds a graph holds (default plan: 4 from 2^21, 2 from 2^17)
 constexpr int kLDMinVertices = 1 << 21;  // measured: Suitor alone wins at 640k (cfg4), LD at 10M (cfg5)
 struct LDArgs {
     int N;

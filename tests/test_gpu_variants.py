@@ -48,6 +48,7 @@ VARIANTS = [
     {"MF_LD1_MIN": "1"},
     {"MF_LD1_MIN": "1", "MF_LD_MID": "5"},
     {"MF_LD_MIN": "1", "MF_SUITOR": "1"},
+    {"MF_LD_MIN": "1", "MF_LD_BIG": "12"},
     {"MF_SELECT_CL": "1"},
     {"MF_SEL_CAP": "12288"},
     {"MF_GRAPHS": "0"},
