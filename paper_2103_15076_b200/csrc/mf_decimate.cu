@@ -802,7 +802,11 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.aoff, rf, r);
         if (absorb_cond) stream = cc.end();
         // relabel: output index = rank of the cluster's lowest member
-        run_scan(W.scan, LoadIsRep{W.pairlo, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
+        if (N >= (1 << 20))  // 4-item tiles for large rounds (cfg5 0.27 -> 0.20 ms)
+            run_scan(W.scan, LoadIsRepT<4>{W.pairlo, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>",
+                     d_abort);
+        else
+            run_scan(W.scan, LoadIsRep{W.pairlo, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
         const bool packed = Nn < (1 << 21);
         LAUNCH(k_relabel3, grid_for(ctx, std::max<int64_t>(N, W.tsize)), 256, 0, stream, N, d_abort, W.pairlo,
                W.absorbed, W.minrep, W.outidx, W.rstep, W.repv, W.abshead, W.absnext, W.table,
@@ -827,8 +831,13 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                 LAUNCH(k_facet_remap<false>, grid_for(ctx, Mcap), 256, 0, stream, dM, d_abort, Fc, W.rstep, vmesh,
                        act, W.mapped, W.canon, W.slot, W.has_live, W.table, W.tkey, W.tsize - 1, per_vertex);
         }
-        run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort,
-                 EpiFacetWrite{W.mapped, Fn});
+        // keep scan: 2-item tiles for latency-bound sizes, longer ones for large meshes (cfg5 0.64 -> 0.61 ms)
+        if (Mcap >= (1 << 20))  // (8-item tiles: 0.78 ms)
+            run_scan(W.scan, LoadKeepT<4>{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort,
+                     EpiFacetWrite{W.mapped, Fn});
+        else
+            run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort,
+                     EpiFacetWrite{W.mapped, Fn});
         LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
                W.rt, W.mt, r == 0, B, W.kout, foff_c, foff_n, last ? d_foff_fin : nullptr, d_stats + 4 * r,
                W.aoff + N, W.ldc + 2, W.deg, W.cursor, W.lowfill, last ? 0 : Nn + 1, W.counters);

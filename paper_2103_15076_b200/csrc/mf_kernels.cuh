@@ -2291,13 +2291,16 @@ MF_DEV int cluster_anchor(int v, const int* __restrict__ pairlo, const int* __re
     const int a = absorbed[v];
     return a >= 0 ? a : v;
 }
-struct LoadIsRep {  // v is the lowest member of its cluster
-    static constexpr int items = 2;  // two dependent gathers per item: short tiles
+template <int ITEMS>
+struct LoadIsRepT {  // v is the lowest member of its cluster
+    static constexpr int items = ITEMS;  // two dependent gathers per item: short tiles
     const int* pairlo;
     const int* absorbed;
     const int* minrep;
     MF_DEV int operator()(int v) const { return minrep[cluster_anchor(v, pairlo, absorbed)] == v; }
 };
+typedef LoadIsRepT<2> LoadIsRep;
+
 struct EpiFacetWrite {  // kept facet f -> output row prefix (order preserving compaction)
     const int* mapped;
     int* Fout;
@@ -2308,8 +2311,9 @@ struct EpiFacetWrite {  // kept facet f -> output row prefix (order preserving c
         Fout[3 * pos + 2] = mapped[3 * f + 2];
     }
 };
-struct LoadKeep {  // facet survives: bypassed, or first occurrence of its non-degenerate triple
-    static constexpr int items = 2;  // slot -> table gather per item: short tiles
+template <int ITEMS>
+struct LoadKeepT {  // facet survives: bypassed, or first occurrence of its non-degenerate triple
+    static constexpr int items = ITEMS;  // slot -> table gather per item: short tiles
     const int* dM;
     const int* slot;
     const int* table;
@@ -2319,6 +2323,8 @@ struct LoadKeep {  // facet survives: bypassed, or first occurrence of its non-d
         return s == -2 ? 1 : (s >= 0 && table[s] == f);
     }
 };
+typedef LoadKeepT<2> LoadKeep;
+
 
 MF_DEV bool is_selected(int mode, uint64_t h, uint64_t l, uint64_t th, uint64_t tl) {
     return mode == 1 || (mode == 3 && !key_lt(th, tl, h, l));
