@@ -157,6 +157,16 @@ static int suitor_lanes(int N, int sm_count) {
     return (int64_t)N * 8 <= (int64_t)sm_count * 2048 ? 8 : 4;  // 8 lanes only within one wave
 }
 
+// MF_SEL_PASSES: multi-block selection passes in the graph before k_select resumes (default 5)
+static int sel_passes() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SEL_PASSES");
+        v = e ? std::max(1, std::min(kSelPassesMax, atoi(e))) : kSelPasses;
+    }
+    return v;
+}
+
 // MF_SELECT_CL=1: 8-CTA cluster selection (DSMEM histogram merge) for mid-size meshes.  Measured
 // no faster than the single CTA at cfg2 (75 vs 75 us) and slower at cfg1 (95 vs 53 us): the pass
 // count, not the per-pass bandwidth, bounds these sizes -- so it is opt-in.
@@ -768,7 +778,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                     stream = cc.end();
                     sa.cond = 0;
                 } else {
-                    for (int pass = 0; pass < kSelPasses; pass++) {
+                    for (int pass = 0; pass < sel_passes(); pass++) {
                         LAUNCH(k_sel_hist, hist_grid, 512, 0, stream, sa, W.ghist, pass);
                         LAUNCH(k_sel_decide, 1, kSelThreads, 0, stream, sa, W.ghist, pass);
                     }

@@ -1553,7 +1553,7 @@ struct SelectArgs {
 // instead of streaming the whole segment again.
 constexpr int kSelScrHdr = kSelBins + 16;
 constexpr int kSelScratch = kSelScrHdr + 4 * kSelCap;  // ints
-constexpr int kSelPasses = 5;                            // multi-block passes before the single-CTA stage
+constexpr int kSelPasses = 3;  // multi-block passes before the single-CTA stage resumes (5: cfg5 +0.08 ms)
 MF_DEV unsigned long long* sel_orand(int* g) { return reinterpret_cast<unsigned long long*>(g + kSelBins); }
 MF_DEV int* sel_stop(int* g) { return g + kSelBins + 8; }
 MF_DEV int* sel_compact(int* g) { return g + kSelBins + 9; }

@@ -51,6 +51,7 @@ VARIANTS = [
     {"MF_LD_MIN": "1", "MF_LD_BIG": "12"},
     {"MF_SELECT_CL": "1"},
     {"MF_SEL_CAP": "12288"},
+    {"MF_SEL_PASSES": "1", "MF_LD1_MIN": "1"},
     {"MF_GRAPHS": "0"},
     {"MF_PDL": "1"},
     {"MF_COND": "1"},
