@@ -105,7 +105,9 @@ int mf_context_create(int device, mf_context** out) {
     }
     c->c.sm_count = prop.multiProcessorCount;
     cudaFuncSetAttribute(k_adj_rank_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankSmem);
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_select<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSelBins * 4 + 8 * std::max(2 * kSelCapMax, kSelChiCap));
+    cudaFuncSetAttribute(k_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSelBins * 4 + 8 * std::max(2 * kSelCapMax, kSelChiCap));
     cudaFuncSetAttribute(k_select_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem);
     // keep freed stream-ordered allocations cached in the device pool

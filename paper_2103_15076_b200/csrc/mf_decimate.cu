@@ -795,8 +795,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                 sa.resume = 1;
             }
             if (B == 1 && !big && select_cluster()) LAUNCH(k_select_cl, kClCTAs, kClThreads, kClSmem, stream, sa);
+            else if (B == 1)
+                LAUNCH(k_select<1024>, 1, 1024, kSelBins * 4 + 8 * std::max(2 * sa.cap, sa.chicap), stream, sa);
             else
-                LAUNCH(k_select, std::min(B, ctx->sm_count * 2), kSelThreads,
+                LAUNCH(k_select<512>, std::min(B, ctx->sm_count * 2), 512,
                        kSelBins * 4 + 8 * std::max(2 * sa.cap, sa.chicap), stream, sa);
         };
         // budget truncation: keep the `budget` lowest-ranked matched pairs per mesh

@@ -1470,6 +1470,8 @@ constexpr int kSelBits = 11;
 constexpr int kSelBins = 1 << kSelBits;
 constexpr int kSelCap = 4096;  // keys held in shared memory (64 KiB; a larger carve-out measured slower)
 constexpr int kSelThreads = 1024;
+// k_select threads: 1024 for one mesh, 512 per mesh of a batch (cheaper barriers; measured
+// cfg4 selects 27 -> 19 us, while the single cfg2 mesh prefers 1024: 53 vs 57 us)
 constexpr int kSelSmem = kSelBins * 4 + 2 * kSelCap * 8;
 constexpr int kSelCapMax = 12288;  // largest stage k_select may be launched with (MF_SEL_CAP)
 constexpr int kSelChiCap = 27136;  // single-mesh two-phase path: primary keys + tie secondaries (212 KiB)
@@ -1709,7 +1711,8 @@ MF_DEV bool radix_kth_u64(const uint64_t* vals, int n, int& kr, uint64_t& p, int
     return false;
 }
 
-__global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_select(SelectArgs a) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
     extern __shared__ unsigned char s_raw[];
@@ -1904,7 +1907,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectArgs a) {
             }
             __syncthreads();
             // block scan over the bins: find digit d with cum(d) < kr <= cum(d) + hist[d]
-            const int per = kSelBins / kSelThreads;  // 2 bins per thread
+            const int per = kSelBins / NT;  // bins per thread
             int loc = 0;
             for (int j = 0; j < per; j++) loc += hist[threadIdx.x * per + j];
             int tot;
