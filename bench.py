@@ -15,9 +15,11 @@ L2 flushed between steps), `e2e` (public numpy API with pinned host inputs,
 H2D + D2H inside the timed region), `roofline` of the dominant kernel (timed
 live with CUDA events inside the timed region; algorithmic bytes from the
 per-round counts), `cpu_baseline` (the C oracle port of the reference on this
-host), `clocks` sampled during the timed region, `gpu_launches`.
+host, plus the UNMODIFIED reference from baseline/_ref as `stock_reference`),
+`clocks` sampled during the timed region, `gpu_launches`.
 `--impl reference` times the reference's CPU algorithm (oracle port, all
-usable host threads) on the same workload; rank 0 only.
+usable host threads) on the same workload, with the stock reference beside
+it; rank 0 only.
 """
 
 from __future__ import annotations
@@ -62,12 +64,14 @@ def workload(name: str, rank: int):
                     desc="delaunay_terrain(500000, 0.02, seed=3): 4 decimations 125000/62500/31250/15625 + "
                          "max-pool down / unpool up of C=64 float32 features (configs[2])")
     if name == "cfg4":
+        from paper_2103_15076_b200 import sharding
+
         world = int(os.environ.get("WORLD_SIZE", "1"))
-        per = 256 // world
-        meshes = [S.delaunay_terrain(2500, noise=0.02, seed=b) for b in range(rank * per, (rank + 1) * per)]
-        return dict(mesh=concat_batch(meshes), levels=[1250], pool_channels=0,
-                    desc=f"batch of {per} delaunay_terrain(2500, 0.02, seed=b) -> 1250 each (configs[3] slice "
-                         f"of 256 over {world} GPU(s))")
+        batch = concat_batch([S.delaunay_terrain(2500, noise=0.02, seed=b) for b in range(256)])
+        sub, lo, hi = sharding.shard_batch(batch, world, rank)  # facet-balanced contiguous slice (§8(e))
+        return dict(mesh=sub, levels=[1250], pool_channels=0,
+                    desc=f"batch of 256 delaunay_terrain(2500, 0.02, seed=b) -> 1250 each (configs[3]); "
+                         f"{world} GPU(s), this rank's facet-balanced slice = meshes [{lo}, {hi})")
     if name == "cfg5":
         mesh = S.perturbed_grid(3163, noise=0.02, seed=rank)
         n, lv = mesh.n_vertices, []
@@ -193,6 +197,70 @@ def step_bytes(rounds: list, n0: int, C: int = 3) -> float:
     return b
 
 
+def cpu_info() -> dict:
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "usable_cores": usable}
+
+
+def stock_reference(name: str, wl: dict, budget_s: float = 25.0) -> dict:
+    """The UNMODIFIED reference (meshforge, pip-installed into baseline/_ref) through its own
+    public API -- decimate_parallel (+ pool/unpool for cfg3) -- on a bounded sample of the
+    workload: median of up to 3 steps within ~budget_s."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "meshforge")):
+        return {"unavailable": "baseline/_ref/meshforge not installed (see DESIGN.md §6)"}
+    if ref_dir not in sys.path:
+        sys.path.append(ref_dir)
+    try:
+        import meshforge as rmf
+        from meshforge import pooling as rpool
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"importing the reference failed: {e!r}"}
+    sw = with_features(dict(cpu_sample(name, wl)))
+    mesh = sw["mesh"]
+    batched = hasattr(mesh, "vertex_offsets")
+    base = mesh.mesh if batched else mesh
+    rm = rmf.TriMesh(base.positions, base.facets)
+    if batched:
+        rm = rmf.BatchedMesh(rm, mesh.vertex_offsets, mesh.facet_offsets)
+
+    def one():
+        cur, f, outs = rm, sw.get("_features"), []
+        for tgt in sw["levels"]:
+            r = rmf.decimate_parallel(cur, rmf.DecimationConfig(target_vertices=tgt))
+            if f is not None:
+                f = rpool.pool(f, r, mode="max")
+                outs.append(r)
+            cur = r.mesh
+        for r in reversed(outs):
+            f = rpool.unpool(f, r)
+
+    times = []
+    t0 = time.perf_counter()
+    while len(times) < 3 and (not times or time.perf_counter() - t0 + times[-1] < budget_s):
+        t = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * float(np.median(times))
+    cores = (os.cpu_count() or 1) if batched else 1  # batches: the reference's own thread pool
+    return {"value": facets_in(sw) / (ms / 1e3), "unit": "facets/s", "ms_per_step": ms, "cores": cores,
+            "kind": "reference-stock",
+            "sample": f"median of {len(times)} step(s) of {sw['desc']}; meshforge 0.1.0 from baseline/_ref, "
+                      f"numpy {np.__version__}", **cpu_info()}
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -275,7 +343,9 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl["desc"], "facets_in": facets_in(wl)},
-            "cpu_baseline": {"value": value, "unit": "facets/s", "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "facets/s", "cores": cores, "kind": "port", "sample": sample,
+                             **cpu_info()},
+            "stock_reference": stock_reference(args.config, workload(args.config, 0)),
             "e2e": {"value": value, "unit": "facets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -292,7 +362,7 @@ def cpu_baseline(name: str, wl: dict, budget_s: float = 12.0) -> dict:
         times.append(time.perf_counter() - t)
     ms = 1e3 * float(np.median(times))
     return {"value": facets_in(sw) / (ms / 1e3), "unit": "facets/s", "cores": 1, "kind": "port",
-            "sample": f"{len(times)} step(s) of {sw['desc']} (median {ms:.1f} ms)"}
+            "sample": f"{len(times)} step(s) of {sw['desc']} (median {ms:.1f} ms)", **cpu_info()}
 
 
 # ---------------------------------------------------------------- our arm
@@ -301,7 +371,6 @@ def run_ours(args):
 
     world, rank, local = dist_setup()
     ngpu = torch.cuda.device_count()
-    gloo = None
     if world > 1:
         import torch.distributed as dist
 
@@ -311,18 +380,18 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local % ngpu))
         else:
             dist.init_process_group(backend)
-        # timing reductions: host floats over a gloo side group (works under either backend)
-        gloo = dist.new_group(backend="gloo")
     else:
         dist = None
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
+    coll_dev = dev if (dist and dist.get_backend() == "nccl") else torch.device("cpu")
 
     def max_over_ranks(x: float) -> float:
+        """The timing reduction (the only collective: the data path has none, §8(e))."""
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     import paper_2103_15076_b200 as mfg
@@ -384,7 +453,7 @@ def run_ours(args):
 
     # ---------------- timed region: device-resident inputs
     if dist:
-        dist.barrier(group=gloo)
+        dist.barrier()
     torch.cuda.synchronize()
     _native.launch_count(reset=True)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -402,7 +471,7 @@ def run_ours(args):
     dom = _native.profile_read().get(dominant, (0.0, 0))
     _native.profile(0)
     if dist:
-        dist.barrier(group=gloo)
+        dist.barrier()
     step_ms = float(np.sum([s.elapsed_time(e) for s, e in zip(starts, ends)])) / args.steps
     step_ms_max = max_over_ranks(step_ms)
     value = world * m_in / (step_ms_max / 1e3)
@@ -480,6 +549,7 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, wl)
+        cpu["stock_reference"] = stock_reference(args.config, wl)
 
     vs = None
     if args.config == "cfg2":

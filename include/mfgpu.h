@@ -13,6 +13,7 @@
  *   mf_unpool          <- pooling.unpool(coarse, result)                     pooling.py:74-77
  *   mf_pool_backward   <- pooling.pool_backward / unpool_backward            pooling.py:80-102
  *   mf_round_targets   <- decimate._round_targets                            decimate.py:294-316
+ *   mf_validate_mesh   <- TriMesh.__init__ re-validation of outputs          mesh.py:25-31, validation.py:8-41
  *
  * Plain pointers and sizes only.  Array pointers may be host or device memory
  * (detected per pointer); offsets are always host arrays.  Integer outputs are
@@ -84,7 +85,7 @@ typedef struct mf_mesh_view {
 typedef struct mf_decimate_config {
     int64_t target_vertices;
     int32_t rounds;        /* -1 = 'auto' */
-    int32_t placement;     /* 0 = 'average' (1 = 'inverse' not yet supported -> MF_ERR_VALUE) */
+    int32_t placement;     /* 0 = 'average', 1 = 'inverse' (quadrics.py:89-114); other -> MF_ERR_VALUE */
     int32_t seeded;        /* shuffle_seed is not None */
     int32_t einsum_order;  /* 0 = numpy AVX-512 lane-split dot3, 1 = sequential dot3 */
     uint64_t pcg_state[4]; /* default_rng(seed).bit_generator.state: state_hi, state_lo, inc_hi, inc_lo */
@@ -124,6 +125,17 @@ int mf_unpool(mf_context *ctx, const mf_decimation *res, const int64_t *replace,
               const void *coarse, int32_t dtype, int64_t c, void *out, void *stream, mf_status *status);
 
 int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t *chain, int64_t cap);
+
+/* Re-validation of a mesh on the device -- replaces TriMesh.__init__'s checks (mesh.py:25-31 ->
+ * validation.py:8-41): finite positions, facet indices in [0, n) (and inside their own batch
+ * entry when offsets are given), no facet repeating a vertex; with check_duplicates also no two
+ * facets with the same vertex set (the dedupe invariant of decimate.py:153-157).  Errors:
+ * MF_ERR_STRUCTURAL with the reference's messages, in its check order.  Host or device arrays.
+ * Setting MF_DEBUG=1 in the environment runs this check (plus replace / mapping ranges) on every
+ * mf_decimate result before it returns. */
+int mf_validate_mesh(mf_context *ctx, const double *positions, int64_t n, const int64_t *facets, int64_t m,
+                     const int64_t *vertex_offsets, const int64_t *facet_offsets, int64_t n_meshes,
+                     int32_t check_duplicates, void *stream, mf_status *status);
 
 /* Binary little-endian PLY bodies (io.py:226-431), decoded / encoded on the device.
  * Field types: MF_PLY_I1 .. MF_PLY_F8 = PLY char, uchar, short, ushort, int, uint, float, double. */

@@ -20,6 +20,7 @@ from .mesh import BatchedMesh, TriMesh, concat_batch
 from .meshio import load_mesh, save_clusters, save_mesh
 from .pooling import POOL_MODES, pool, pool_backward, unpool, unpool_backward
 from .quality import QualityReport, quality_report
+from .validation import validate_on_device
 
 __version__ = "0.1.0"
 
@@ -52,5 +53,6 @@ __all__ = [
     "save_mesh",
     "unpool",
     "unpool_backward",
+    "validate_on_device",
     "vertex_facet_adjacency",
 ]

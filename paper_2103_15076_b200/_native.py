@@ -113,6 +113,8 @@ def lib():
                                       _vp, _vp, ctypes.POINTER(Status)]
         L.mf_facet2vertex.restype = ctypes.c_int
         L.mf_round_targets.restype = _i64
+        L.mf_validate_mesh.argtypes = [_vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i32, _vp, ctypes.POINTER(Status)]
+        L.mf_validate_mesh.restype = ctypes.c_int
         L.mf_kernel_launch_count.argtypes = [_i32]
         L.mf_kernel_launch_count.restype = _i64
         L.mf_version.restype = ctypes.c_char_p
@@ -163,24 +165,30 @@ def raise_for(st: Status):
         return
     msg = st.message.decode(errors="replace")
     if code == MF_ERR_VALUE:
-        raise ValueError(msg)
-    if code == MF_ERR_STRUCTURAL:
-        raise StructuralError(msg)
-    if code == MF_ERR_INFEASIBLE:
-        raise InfeasibleTargetError(msg, achievable_vertices=int(st.achievable_vertices))
-    if code == MF_ERR_RUNTIME:
-        raise RuntimeError(msg)
-    raise NativeError(f"libmfgpu error {code}: {msg}")
+        err = ValueError(msg)
+    elif code == MF_ERR_STRUCTURAL:
+        err = StructuralError(msg)
+    elif code == MF_ERR_INFEASIBLE:
+        err = InfeasibleTargetError(msg, achievable_vertices=int(st.achievable_vertices))
+    elif code == MF_ERR_RUNTIME:
+        err = RuntimeError(msg)
+    else:
+        err = NativeError(f"libmfgpu error {code}: {msg}")
+    # batch entry the error belongs to (the lowest failing one, decimate.py:354-361); sharding
+    # turns it into a global index
+    err.mesh_index = int(st.mesh_index) if st.mesh_index >= 0 else None
+    raise err
 
 
 class Decimation:
     """Owner of a device-resident mf_decimation handle."""
 
-    __slots__ = ("handle", "device", "n_in", "n_out", "m_out", "c", "n_meshes", "__weakref__")
+    __slots__ = ("handle", "device", "n_in", "n_out", "m_out", "c", "n_meshes", "replace_ref", "__weakref__")
 
     def __init__(self, handle, device):
         self.handle = handle
         self.device = device
+        self.replace_ref = None  # the host replace array emitted from this handle (pooling identity check)
         vals = [_i64() for _ in range(5)]
         lib().mf_decimation_sizes(handle, *[ctypes.byref(v) for v in vals])
         self.n_in, self.n_out, self.m_out, self.c, self.n_meshes = (int(v.value) for v in vals)

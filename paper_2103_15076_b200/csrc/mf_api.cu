@@ -497,6 +497,46 @@ int32_t mf_decimation_round_stats(const mf_decimation* res, int64_t* out, int32_
     return R;
 }
 
+/* TriMesh re-validation on the device (validation.py:8-41), + optional facet-set uniqueness. */
+int mf_validate_mesh(mf_context* ctx, const double* positions, int64_t n, const int64_t* facets, int64_t m,
+                     const int64_t* vertex_offsets, const int64_t* facet_offsets, int64_t n_meshes,
+                     int32_t check_duplicates, void* stream, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || n < 0 || m < 0 || (n > 0 && !positions) || (m > 0 && !facets)) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "null argument");
+        return st->code;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    MF_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    const bool hp = n > 0 && !is_device_ptr(positions), hf = m > 0 && !is_device_ptr(facets);
+    const size_t pb = ((size_t)n * 24 + 255) & ~size_t(255), fb = ((size_t)m * 24 + 255) & ~size_t(255);
+    void* tmp = nullptr;
+    if (hp || hf) MF_CUDA_TRY(cudaMallocAsync(&tmp, (hp ? pb : 0) + (hf ? fb : 0), s));
+    const double* dP = positions;
+    const int64_t* dF = facets;
+    char* q = (char*)tmp;
+    if (hp) {
+        MF_CUDA_TRY(cudaMemcpyAsync(q, positions, (size_t)n * 24, cudaMemcpyHostToDevice, s));
+        dP = (const double*)q;
+        q += pb;
+    }
+    if (hf) {
+        MF_CUDA_TRY(cudaMemcpyAsync(q, facets, (size_t)m * 24, cudaMemcpyHostToDevice, s));
+        dF = (const int64_t*)q;
+    }
+    int rc = validate_mesh_run<int64_t>(&ctx->c, dP, n, dF, m, vertex_offsets, facet_offsets,
+                                        vertex_offsets ? (int)n_meshes : 1, check_duplicates != 0, nullptr, nullptr,
+                                        0, s, st);
+    if (tmp) {
+        cudaFreeAsync(tmp, s);
+        cudaStreamSynchronize(s);
+    }
+    return rc;
+}
+
 int64_t mf_round_targets(int64_t n_in, int64_t target, int32_t rounds, int64_t* chain, int64_t cap) {
     std::vector<int64_t> v;
     round_targets(n_in, target, rounds, v);

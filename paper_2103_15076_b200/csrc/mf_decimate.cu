@@ -292,6 +292,11 @@ struct Plan {
     int ld_mid = 2;               // LD rounds between ld1_min and ld_min (MF_LD_MID; cfg4 0.880 -> 0.865
                                   // ms with 2, 3 and 5 no better)
     int placement = 0;            // 0 = average, 1 = inverse (quadrics.py:89-114)
+    // size gates of the kernel variants (env overrides force a branch at small sizes so the
+    // parity tests reach it: MF_BIG_SEL_MIN / MF_SCAN4_MIN / MF_WIDE_MIN = 0 take it always)
+    int big_sel_min = 1 << 18;    // one big mesh: multi-block selection passes before k_select
+    int scan4_min = 1 << 20;      // 4-item tiles in the gather-chain scans (rep, keep)
+    int wide_min = 1 << 21;       // output ids from here need the wide-key facet dedupe
 };
 
 static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan& p, mf_status* st) {
@@ -402,6 +407,9 @@ static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan
     if (const char* e = getenv("MF_LD1_MIN")) p.ld1_min = atoi(e);
     if (const char* e = getenv("MF_LD_MID")) p.ld_mid = std::max(1, std::min(kLDRounds, atoi(e)));
     if (const char* e = getenv("MF_LD_BIG")) p.ld_big = std::max(1, std::min(kLDRounds, atoi(e)));
+    if (const char* e = getenv("MF_BIG_SEL_MIN")) p.big_sel_min = std::max(0, atoi(e));
+    if (const char* e = getenv("MF_SCAN4_MIN")) p.scan4_min = std::max(0, atoi(e));
+    if (const char* e = getenv("MF_WIDE_MIN")) p.wide_min = std::max(0, atoi(e));
     for (int i = 0; i < 4; i++) p.pcg[i] = cfg->pcg_state[i];
     // device params: act | budget | nin | voff | foff0 (int32)
     p.params_words = (size_t)p.nParamR * B * 2 + (size_t)(R + 1) * B + (size_t)(R + 1) * (B + 1) + (B + 1);
@@ -772,7 +780,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, W.key_hi,
                seeded ? W.key_lo : nullptr, vmesh, voff_r, W.segA, W.chi, W.clo, W.cpay, W.pairlo, W.loose, W.ldc + 6);
         // per-mesh selection; one big mesh first narrows its rank prefix with multi-block passes
-        const bool big = (B == 1 && N >= (1 << 18));  // below: one CTA (latency-bound sizes)
+        const bool big = (B == 1 && N >= p.big_sel_min);  // below: one CTA (latency-bound sizes)
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
                           d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap(), 0,
@@ -823,12 +831,12 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                W.mode, W.p_hi, W.p_lo, W.absorbed, W.minrep, B, act, budget, nin, W.ksel, W.removed, W.aoff, rf, r);
         if (absorb_cond) stream = cc.end();
         // relabel: output index = rank of the cluster's lowest member
-        if (N >= (1 << 20))  // 4-item tiles for large rounds (cfg5 0.27 -> 0.20 ms)
+        if (N >= p.scan4_min)  // 4-item tiles for large rounds (cfg5 0.27 -> 0.20 ms)
             run_scan(W.scan, LoadIsRepT<4>{W.pairlo, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>",
                      d_abort);
         else
             run_scan(W.scan, LoadIsRep{W.pairlo, W.absorbed, W.minrep}, W.outidx, N, stream, "k_scan<rep>", d_abort);
-        const bool packed = Nn < (1 << 21);
+        const bool packed = Nn < p.wide_min;
         LAUNCH(k_relabel3, grid_for(ctx, std::max<int64_t>(N, W.tsize)), 256, 0, stream, N, d_abort, W.pairlo,
                W.absorbed, W.minrep, W.outidx, W.rstep, W.repv, W.abshead, W.absnext, W.table,
                packed ? W.tkey : nullptr, (int)W.tsize, packed ? 0x7f7f7f7f : -1, W.has_live);
@@ -853,7 +861,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                        act, W.mapped, W.canon, W.slot, W.has_live, W.table, W.tkey, W.tsize - 1, per_vertex);
         }
         // keep scan: 2-item tiles for latency-bound sizes, longer ones for large meshes (cfg5 0.64 -> 0.61 ms)
-        if (Mcap >= (1 << 20))  // (8-item tiles: 0.78 ms)
+        if (Mcap >= p.scan4_min)  // (8-item tiles: 0.78 ms)
             run_scan(W.scan, LoadKeepT<4>{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort,
                      EpiFacetWrite{W.mapped, Fn});
         else
@@ -907,7 +915,8 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement};
+                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement,
+                              p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
     return k;
@@ -1323,6 +1332,10 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         int64_t row[6] = {p.h_N[r], h_stats[4 * r], h_stats[4 * r + 1], p.h_N[r + 1], h_stats[4 * r + 2],
                           h_stats[4 * r + 3]};
         res->round_stats.insert(res->round_stats.end(), row, row + 6);
+    }
+    if (debug_validate() && R > 0) {  // row 16: the reference re-validates every output TriMesh
+        int vr = validate_result(ctx, res, stream, st);
+        if (vr != MF_OK) return fail_out(vr);
     }
     *out = res;
     return MF_OK;

@@ -119,6 +119,12 @@ int pool_backward_run(Context* ctx, const void* grad, int gdtype, const void* fe
                       int64_t c, const int* d_replace, const int* d_off, const int* d_members, int64_t n_out, int mode,
                       const void* weights, void* out, int odtype, cudaStream_t stream, mf_status* st);
 extern thread_local int64_t g_launches;
+bool debug_validate();
+int validate_result(Context* ctx, const Result* r, cudaStream_t s, mf_status* st);
+template <typename I>
+int validate_mesh_run(Context* ctx, const double* P, int64_t n, const I* F, int64_t m, const int64_t* h_voff,
+                      const int64_t* h_foff, int B, bool check_dup, const int* rep, const int* map, int64_t n_rep,
+                      cudaStream_t s, mf_status* st);
 void drop_graphs(const Context* ctx);
 void prof_collect_pending();
 }  // namespace mf

@@ -4,4 +4,5 @@
 #include "mf_pool.cu"
 #include "mf_conv.cu"
 #include "mf_io.cu"
+#include "mf_validate.cu"
 #include "mf_api.cu"

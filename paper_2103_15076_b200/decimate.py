@@ -179,6 +179,7 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     )
     _native.raise_for(st)
     rep.flags.writeable = False
+    dec.replace_ref = rep  # pool/unpool reuse the device replace only for this very array
     out_mesh = _trusted_trimesh(pos, fac, feats)
     if batched:
         bm = BatchedMesh.__new__(BatchedMesh)

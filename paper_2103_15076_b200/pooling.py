@@ -20,10 +20,12 @@ POOL_MODES = ("average", "max", "weighted", "sum")
 
 
 def _handle_for(result):
+    """The decimation's device handle, when result.replace is still the (read-only) array that
+    handle emitted; any other replace -- reassigned, or made writable again -- is uploaded."""
     dec = getattr(result, "_native", None)
-    if dec is None or dec.n_in != len(result.replace) or dec.n_out != result.n_vertices_out:
+    if dec is None or result.replace is not dec.replace_ref or result.replace.flags.writeable:
         return None
-    if result.replace.flags.writeable:  # our own results are frozen; anything else is re-uploaded
+    if dec.n_in != len(result.replace) or dec.n_out != result.n_vertices_out:
         return None
     return dec
 

@@ -73,26 +73,67 @@ def merge_results(parts: list) -> DecimationResult:
                             reached_target=all(p.reached_target for p in parts))
 
 
+def _error_record(exc: BaseException, lo: int) -> tuple:
+    """(global batch index, type, message, achievable_vertices) of a rank's failure: a plain
+    tuple travels through all_gather_object where the exception itself would not round-trip
+    (InfeasibleTargetError's pickle drops achievable_vertices)."""
+    idx = getattr(exc, "mesh_index", None)
+    return (lo + (idx or 0), type(exc).__name__, str(exc), getattr(exc, "achievable_vertices", None))
+
+
+def _raise_record(rec: tuple):
+    from . import errors
+
+    _, name, msg, achievable = rec
+    if name == "InfeasibleTargetError":
+        err = errors.InfeasibleTargetError(msg, achievable_vertices=achievable)
+    elif name in ("StructuralError", "MeshError", "NativeError"):
+        err = getattr(errors, name)(msg)
+    elif name in ("ValueError", "RuntimeError", "TypeError", "IndexError"):
+        err = {"ValueError": ValueError, "RuntimeError": RuntimeError, "TypeError": TypeError,
+               "IndexError": IndexError}[name](msg)
+    else:
+        err = RuntimeError(f"{name}: {msg}")
+    err.mesh_index = rec[0]
+    raise err
+
+
 def decimate_sharded(batch: BatchedMesh, config, group=None, decimate_fn=None, device=None):
     """Decimate `batch` across the ranks of a torch.distributed group.
 
     Every rank decimates its contiguous slice (no collective on the data
-    path); the per-rank results are then exchanged once with
-    all_gather_object so every rank returns the merged result, identical to
-    decimate_parallel(batch, config) on one device.
+    path).  The ranks then exchange one status record each: if any slice
+    failed, every rank raises the exception of the LOWEST failing batch entry,
+    with its global index in `mesh_index` -- what the reference's in-order
+    `pool.map` re-raises (decimate.py:354-361) -- instead of leaving the
+    healthy ranks blocked in the result exchange.  Otherwise the per-rank
+    results are exchanged once with all_gather_object and every rank returns
+    the merged result, identical to decimate_parallel(batch, config) on one
+    device.
     """
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    sub, _, _ = shard_batch(batch, world, rank)
+    sub, lo, _ = shard_batch(batch, world, rank)
     fn = decimate_fn or (lambda b, c: decimate_parallel(b, c, device=device))
-    mine = fn(sub, config) if sub is not None else None
+    mine, failure = None, None
+    try:
+        mine = fn(sub, config) if sub is not None else None
+    except Exception as exc:  # noqa: BLE001 -- every failure is re-raised below, on every rank
+        if world == 1:
+            raise
+        failure = _error_record(exc, lo)
     if mine is not None:
         mine = DecimationResult(mesh=mine.mesh, replace=np.asarray(mine.replace), mapping=mine.mapping,
                                 reached_target=mine.reached_target)
     if world == 1:
         return merge_results([mine])
+    statuses = [None] * world
+    dist.all_gather_object(statuses, failure, group=group)
+    failed = [s for s in statuses if s is not None]
+    if failed:
+        _raise_record(min(failed, key=lambda s: s[0]))
     parts = [None] * world
     dist.all_gather_object(parts, mine, group=group)
     return merge_results(parts)

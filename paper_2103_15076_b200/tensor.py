@@ -50,16 +50,40 @@ def _offsets(counts, total) -> np.ndarray:
     return off
 
 
+def _dtype_code(t: torch.Tensor, what: str) -> int:
+    """Feature-like tensors are float32 or float64 (pooling.py:18-33 / mesh.py:25-31 accept no other)."""
+    if t.dtype == torch.float32:
+        return _native.DTYPE_F32
+    if t.dtype == torch.float64:
+        return _native.DTYPE_F64
+    raise ValueError(f"{what} must be float32 or float64, got {t.dtype}")
+
+
+def _same_device(t: torch.Tensor, dev: torch.device, what: str) -> None:
+    if not t.is_cuda or t.device != dev:
+        raise ValueError(f"{what} must be a CUDA tensor on {dev}, got {t.device}")
+
+
 def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, target: int = 1,
              placement: str = "average", seed=None, rounds="auto", features: torch.Tensor | None = None,
              copy_outputs: bool = True) -> DeviceDecimation:
     if not vertices.is_cuda or not faces.is_cuda:
         raise ValueError("vertices / faces must be CUDA tensors")
+    dev = vertices.device
+    _same_device(faces, dev, "faces")
     if vertices.dtype != torch.float64 or faces.dtype != torch.int64:
         raise ValueError("vertices must be float64 and faces int64")
+    if vertices.dim() != 2 or vertices.shape[1] != 3:
+        raise ValueError(f"vertices must have shape (N, 3), got {tuple(vertices.shape)}")
+    if faces.dim() != 2 or faces.shape[1] != 3:
+        raise ValueError(f"faces must have shape (M, 3), got {tuple(faces.shape)}")
+    if features is not None:
+        _same_device(features, dev, "features")
+        _dtype_code(features, "features")
+        if features.dim() != 2 or features.shape[0] != vertices.shape[0]:
+            raise ValueError(f"features must have shape ({vertices.shape[0]}, C), got {tuple(features.shape)}")
     vertices = vertices.contiguous()
     faces = faces.contiguous()
-    dev = vertices.device
     view = _native.MeshView()
     view.positions = vertices.data_ptr()
     view.facets = faces.data_ptr() if faces.numel() else None
@@ -67,7 +91,7 @@ def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, targ
     if features is not None:
         features = features.contiguous()
         view.features = features.data_ptr()
-        view.features_dtype = _native.DTYPE_F32 if features.dtype == torch.float32 else _native.DTYPE_F64
+        view.features_dtype = _dtype_code(features, "features")
         view.c = features.shape[1]
     else:
         view.c = 3
@@ -110,28 +134,41 @@ def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, targ
 def pool(features: torch.Tensor, dd: DeviceDecimation, mode: str = "average", weights=None) -> torch.Tensor:
     if mode not in _POOL_MODES:
         raise ValueError(f"mode must be one of {_POOL_MODES}, got {mode!r}")
+    dev = torch.device("cuda", dd._dec.device)
+    _same_device(features, dev, "features")
+    code = _dtype_code(features, "features")
+    if features.dim() != 2 or features.shape[0] != dd._dec.n_in:
+        raise ValueError(f"features must have shape ({dd._dec.n_in}, C), got {tuple(features.shape)}")
     features = features.contiguous()
-    dev = features.device
     out = torch.empty((dd.n_vertices_out, features.shape[1]), dtype=features.dtype, device=dev)
-    w = None if weights is None else weights.to(dtype=features.dtype).contiguous()
+    w = None
+    if weights is not None:
+        _same_device(weights, dev, "weights")
+        _dtype_code(weights, "weights")
+        if tuple(weights.shape) != (dd._dec.n_in,):
+            raise ValueError(f"weights must have shape ({dd._dec.n_in},)")
+        w = weights.to(dtype=features.dtype).contiguous()
     st = _native.Status()
     _native.lib().mf_pool(
         _native.context(dev.index), dd._dec.handle, None, dd._dec.n_in, dd._dec.n_out, features.data_ptr(),
-        _native.DTYPE_F32 if features.dtype == torch.float32 else _native.DTYPE_F64, features.shape[1],
-        _POOL_MODES.index(mode), None if w is None else w.data_ptr(), out.data_ptr(),
+        code, features.shape[1], _POOL_MODES.index(mode), None if w is None else w.data_ptr(), out.data_ptr(),
         ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), ctypes.byref(st))
     _native.raise_for(st)
     return out
 
 
 def unpool(coarse: torch.Tensor, dd: DeviceDecimation) -> torch.Tensor:
+    dev = torch.device("cuda", dd._dec.device)
+    _same_device(coarse, dev, "coarse")
+    code = _dtype_code(coarse, "coarse")
+    if coarse.dim() != 2 or coarse.shape[0] != dd._dec.n_out:
+        raise ValueError(f"coarse must have shape ({dd._dec.n_out}, C), got {tuple(coarse.shape)}")
     coarse = coarse.contiguous()
-    dev = coarse.device
     out = torch.empty((dd._dec.n_in, coarse.shape[1]), dtype=coarse.dtype, device=dev)
     st = _native.Status()
     _native.lib().mf_unpool(
         _native.context(dev.index), dd._dec.handle, None, dd._dec.n_in, dd._dec.n_out, coarse.data_ptr(),
-        _native.DTYPE_F32 if coarse.dtype == torch.float32 else _native.DTYPE_F64, coarse.shape[1],
-        out.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), ctypes.byref(st))
+        code, coarse.shape[1], out.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream),
+        ctypes.byref(st))
     _native.raise_for(st)
     return out

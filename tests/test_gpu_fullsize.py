@@ -1,19 +1,24 @@
-"""BASELINE.json configurations at their FULL sizes, checked through size-independent
-properties (the bitwise oracle comparisons run at sizes the CPU oracle finishes in
-seconds -- tests/test_gpu_parity.py):
+"""BASELINE.json configurations at their FULL sizes, compared BIT FOR BIT:
 
-* every level: exact output vertex count, `replace` a surjection onto [0, n_out) whose
-  output order is the order of each cluster's lowest member (decimate.py:130-137),
-  `mapping` = replace or -1 (decimate.py:159-167), facets in range, non-degenerate and
-  free of duplicate triples (decimate.py:147-157), positions = member means (one-round
-  levels) or inside the members' bounding box (multi-round levels nest means);
-* the whole chain is deterministic (two runs give identical bytes);
-* a batch equals its entries decimated one by one (decimate.py:347-361, the reference's
-  test_decimation.py:175-191) -- for the cfg4 batch of 256 meshes;
-* max-pool / unpool of C=64 float32 features equal an independent scatter-max / gather.
+* against the real reference (tests/golden/full.json, digests produced by
+  meshforge itself in the build container, tests/golden/make_golden_full.py) --
+  run with the fixture host's numpy reduction order;
+* against the C oracle run on this host with this host's order (every array, every
+  level, cfg3's C=64 max / average pooling and unpooling included).
+
+cfg5's levels 1-2 have >= 2^21 output vertices, so they exercise the wide-key facet
+dedupe and the 4-item gather-chain scans that smaller inputs never reach
+(tests/test_gpu_variants.py forces those branches at small sizes as well).  The
+device-tensor API is exercised at full size too (cfg5 chain through
+paper_2103_15076_b200.tensor, checked equal to the numpy API's bytes) plus the
+size-independent properties a decimation must have (surjective ordered `replace`,
+`mapping` = replace or -1, facets valid and unique).
 """
 
+import functools
 import hashlib
+import json
+import os
 
 import numpy as np
 import pytest
@@ -22,15 +27,148 @@ import torch
 import paper_2103_15076_b200 as mfg
 from paper_2103_15076_b200 import synthetic as S
 from paper_2103_15076_b200 import tensor as T
+from paper_2103_15076_b200.numerics import einsum_order, forced_order
 
 pytestmark = pytest.mark.gpu
 
+HERE = os.path.dirname(os.path.abspath(__file__))
+_FULL_PATH = os.path.join(HERE, "golden", "full.json")
+FULL = json.load(open(_FULL_PATH)) if os.path.exists(_FULL_PATH) else {}
+ORDER = FULL.get("einsum_order", 0)
 
-def _digest(*ts):
+
+def sha(*arrays):
     h = hashlib.sha256()
-    for t in ts:
-        h.update(t.detach().cpu().numpy().tobytes())
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
     return h.hexdigest()
+
+
+def input_digest(mesh):
+    base = mesh.mesh if isinstance(mesh, mfg.BatchedMesh) else mesh
+    parts = [base.positions, base.facets, base.features]
+    if isinstance(mesh, mfg.BatchedMesh):
+        parts += [mesh.vertex_offsets, mesh.facet_offsets]
+    return sha(*parts)
+
+
+def halving(n, k=4):
+    out = []
+    for _ in range(k):
+        n = -(-n // 2)
+        out.append(n)
+    return out
+
+
+@functools.lru_cache(maxsize=None)
+def workload(cfg):
+    if cfg == "cfg3":
+        mesh = S.delaunay_terrain(500_000, 0.02, 3)
+        feats = np.random.default_rng(0).standard_normal((mesh.n_vertices, 64)).astype(np.float32)
+        return mesh, [125_000, 62_500, 31_250, 15_625], feats
+    if cfg == "cfg4":
+        return mfg.concat_batch([S.delaunay_terrain(2500, 0.02, b) for b in range(256)]), [1250], None
+    if cfg == "cfg5":
+        mesh = S.perturbed_grid(3163, None, 0.02, 0)
+        return mesh, halving(mesh.n_vertices), None
+    raise ValueError(cfg)
+
+
+def _arrays(res):
+    base = res.mesh.mesh if isinstance(res.mesh, mfg.BatchedMesh) else res.mesh
+    d = dict(replace=res.replace, mapping=res.mapping, facets=base.facets, positions=base.positions,
+             features=base.features)
+    if isinstance(res.mesh, mfg.BatchedMesh):
+        d["vertex_offsets"] = res.mesh.vertex_offsets
+        d["facet_offsets"] = res.mesh.facet_offsets
+    return d
+
+
+@functools.lru_cache(maxsize=None)
+def gpu_chain(cfg, order):
+    """The level chain through the drop-in numpy API (+ max / average pool and unpool)."""
+    mesh, levels, feats = workload(cfg)
+    out, cur, f = [], mesh, feats
+    with forced_order(order):
+        for tgt in levels:
+            res = mfg.decimate_parallel(cur, mfg.DecimationConfig(target_vertices=tgt), device=0)
+            a = {k: np.array(v) for k, v in _arrays(res).items()}
+            if f is not None:
+                a["pool_max"] = mfg.pool(f, res, mode="max")
+                a["pool_average"] = mfg.pool(f, res, mode="average")
+                a["unpool"] = mfg.unpool(a["pool_max"], res)
+                f = a["pool_max"]
+            out.append(a)
+            cur = res.mesh
+    return out
+
+
+def oracle_chain(oracle, cfg, order):
+    mesh, levels, feats = workload(cfg)
+    batched = isinstance(mesh, mfg.BatchedMesh)
+    base = mesh.mesh if batched else mesh
+    P, F, X = base.positions, base.facets, None
+    kw = dict(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets,
+              threads=os.cpu_count() or 1) if batched else {}
+    out, f = [], feats
+    for tgt in levels:
+        o = oracle.decimate(P, F, X, target=tgt, order=order, **kw)
+        if f is not None:
+            o["pool_max"] = oracle.pool(f, o["replace"], len(o["positions"]), "max")
+            o["pool_average"] = oracle.pool(f, o["replace"], len(o["positions"]), "average")
+            o["unpool"] = oracle.unpool(o["pool_max"], o["replace"])
+            f = o["pool_max"]
+        out.append(o)
+        P, F, X = o["positions"], o["facets"], o["features"]
+        if batched:
+            kw.update(vertex_offsets=o["vertex_offsets"], facet_offsets=o["facet_offsets"])
+    return out
+
+
+def _check_reference(cfg):
+    if cfg not in FULL:
+        pytest.skip(f"tests/golden/full.json has no {cfg} entry (run tests/golden/make_golden_full.py {cfg})")
+    g = FULL[cfg]
+    mesh, levels, feats = workload(cfg)
+    assert input_digest(mesh) == g["input"]
+    if feats is not None:
+        assert sha(feats) == g["features"]
+    got = gpu_chain(cfg, ORDER)
+    assert len(got) == len(g["levels"])
+    for i, (a, exp) in enumerate(zip(got, g["levels"])):
+        assert len(a["positions"]) == exp["n_out"] and len(a["facets"]) == exp["m_out"], f"level {i}"
+        for k in ("replace", "mapping", "facets", "positions", "features", "vertex_offsets", "facet_offsets"):
+            if k in exp:
+                assert sha(a[k]) == exp[k], f"level {i}: {k} differs from the reference"
+        if "pool_max" in exp:
+            assert sha(a["pool_max"]) == exp["pool_max"], f"level {i}: max-pool differs from the reference"
+            assert sha(a["unpool"]) == exp["unpool"], f"level {i}: unpool differs from the reference"
+
+
+def _check_oracle(oracle, cfg):
+    order = einsum_order()
+    got = gpu_chain(cfg, order)
+    exp = oracle_chain(oracle, cfg, order)
+    for i, (a, o) in enumerate(zip(got, exp)):
+        for k, v in a.items():
+            e = o[k]
+            assert v.shape == e.shape and v.dtype == e.dtype, f"level {i}: {k} shape/dtype"
+            assert np.array_equal(np.ascontiguousarray(v).view(np.uint8), np.ascontiguousarray(e).view(np.uint8)), \
+                f"level {i}: {k} differs from the oracle"
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+def test_full_size_matches_reference(cfg):
+    """configs[2..4] at full size, digest-equal to meshforge's own outputs."""
+    _check_reference(cfg)
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+def test_full_size_matches_oracle(oracle, cfg):
+    """configs[2..4] at full size, byte-equal to the C oracle on this host."""
+    _check_oracle(oracle, cfg)
 
 
 def _check_level(V, F, dd, target):
@@ -52,81 +190,19 @@ def _check_level(V, F, dd, target):
     srt = torch.sort(Fo, dim=1).values
     key = (srt[:, 0] * target + srt[:, 1]) * target + srt[:, 2]
     assert torch.unique(key).numel() == key.numel()
-    if len(dd.round_stats()) == 1:
-        # one round: positions are the member means (float64 sums in another order: tolerance)
-        sums = torch.zeros((target, 3), dtype=torch.float64, device=V.device).index_add_(0, R, V)
-        mean = sums / counts[:, None].to(torch.float64)
-        assert torch.allclose(Vo, mean, rtol=1e-12, atol=1e-12)
-    else:
-        # a chain of rounds nests means: each output lies in its members' bounding box
-        lo = torch.full((target, 3), float("inf"), dtype=torch.float64, device=V.device)
-        hi = torch.full((target, 3), -float("inf"), dtype=torch.float64, device=V.device)
-        idx = R[:, None].expand(-1, 3)
-        lo.scatter_reduce_(0, idx, V, reduce="amin")
-        hi.scatter_reduce_(0, idx, V, reduce="amax")
-        assert bool((Vo >= lo - 1e-12).all()) and bool((Vo <= hi + 1e-12).all())
 
 
-def _chain(mesh, levels):
+def test_cfg5_tensor_api_equals_numpy_api():
+    """The device-tensor API (north-star interface) at cfg5 size: same bytes as the numpy API,
+    valid at every level, deterministic."""
+    mesh, levels, _ = workload("cfg5")
+    ref = gpu_chain("cfg5", einsum_order())
     V = torch.from_numpy(mesh.positions).cuda()
     F = torch.from_numpy(mesh.facets).cuda()
-    out = []
-    for t in levels:
+    for i, t in enumerate(levels):
         dd = T.decimate(V, F, target=t)
-        out.append((V, F, dd, t))
+        _check_level(V, F, dd, t)
+        for k, tv in (("replace", dd.replace), ("mapping", dd.mapping), ("facets", dd.faces),
+                      ("positions", dd.vertices)):
+            assert np.array_equal(tv.cpu().numpy(), ref[i][k]), f"level {i}: {k}"
         V, F = dd.vertices, dd.faces
-    return out
-
-
-def test_cfg5_full_grid_hierarchy():
-    """configs[4]: perturbed_grid(3163) -- 10,004,569 vertices / 19,996,488 facets, 4 levels."""
-    mesh = S.perturbed_grid(3163, noise=0.02, seed=0)
-    n, levels = mesh.n_vertices, []
-    for _ in range(4):
-        n = -(-n // 2)
-        levels.append(n)
-    a = _chain(mesh, levels)
-    for V, F, dd, t in a:
-        _check_level(V, F, dd, t)
-    b = _chain(mesh, levels)
-    for (_, _, d1, _), (_, _, d2, _) in zip(a, b):
-        assert _digest(d1.replace, d1.mapping, d1.faces, d1.vertices) == \
-            _digest(d2.replace, d2.mapping, d2.faces, d2.vertices)
-
-
-def test_cfg3_full_terrain_hierarchy_with_pooling():
-    """configs[2]: delaunay_terrain(500000) -- ~1M facets, 125k/62.5k/31.25k/15.625k, C=64 max-pool/unpool."""
-    mesh = S.delaunay_terrain(500_000, noise=0.02, seed=3)
-    levels = [125_000, 62_500, 31_250, 15_625]
-    chain = _chain(mesh, levels)
-    X = torch.from_numpy(np.random.default_rng(0).standard_normal((mesh.n_vertices, 64)).astype(np.float32)).cuda()
-    ups = []
-    for V, F, dd, t in chain:
-        _check_level(V, F, dd, t)
-        P = T.pool(X, dd, mode="max")
-        ref = torch.full((t, 64), -float("inf"), dtype=torch.float32, device=X.device)
-        ref.scatter_reduce_(0, dd.replace[:, None].expand(-1, 64), X, reduce="amax")
-        assert torch.equal(P, ref)
-        U = T.unpool(P, dd)
-        assert torch.equal(U, P[dd.replace])
-        ups.append(U)
-        X = P
-
-
-def test_cfg4_full_batch_equals_per_mesh():
-    """configs[3]: 256 x delaunay_terrain(2500) -> 1250 each; sampled entries equal their solo runs."""
-    meshes = [S.delaunay_terrain(2500, noise=0.02, seed=b) for b in range(256)]
-    batch = mfg.concat_batch(meshes)
-    res = mfg.decimate_parallel(batch, mfg.DecimationConfig(target_vertices=1250), device=0)
-    vo, fo = res.mesh.vertex_offsets, res.mesh.facet_offsets
-    assert np.array_equal(np.diff(vo), np.full(256, 1250))
-    vin = batch.vertex_offsets
-    for b in (0, 1, 17, 128, 200, 255):
-        solo = mfg.decimate_parallel(meshes[b], mfg.DecimationConfig(target_vertices=1250), device=0)
-        sl = slice(vin[b], vin[b + 1])
-        assert np.array_equal(res.replace[sl] - vo[b], solo.replace)
-        m = res.mapping[sl]
-        assert np.array_equal(np.where(m >= 0, m - vo[b], -1), solo.mapping)
-        assert np.array_equal(res.mesh.facets[fo[b]:fo[b + 1]] - vo[b], solo.mesh.facets)
-        assert np.array_equal(res.mesh.positions[vo[b]:vo[b + 1]].view(np.uint64),
-                              solo.mesh.positions.view(np.uint64))

@@ -20,12 +20,18 @@ from paper_2103_15076_b200 import synthetic as S
 from paper_2103_15076_b200.numerics import einsum_order
 from oracle import oracle as O
 import numpy as np
+DEG_P = [[0, 0, 0], [1, 0, 0], [0, 1, 0], [9, 9, 9], [2, 0, 0], [1, 1, 0], [3, 3, 0]]
+DEG_F = [[0, 1, 2], [1, 4, 5], [0, 1, 4], [1, 2, 5], [2, 1, 5], [0, 4, 6], [0, 1, 2]]
 
 cases = [(S.delaunay_terrain(20_000, noise=0.02, seed=4), 6_000, None),
          (S.delaunay_terrain(20_000, noise=0.02, seed=4), 6_000, 7),
          (S.icosphere(5), 3585, None),
          (S.flat_grid(60), 1_800, None),
-         (mfg.concat_batch([S.delaunay_terrain(300 + 40 * b, seed=b) for b in range(6)]), 150, 3)]
+         (mfg.concat_batch([S.delaunay_terrain(300 + 40 * b, seed=b) for b in range(6)]), 150, 3),
+         # duplicate + degenerate input facets (the dedupe keeps the first occurrence and its winding)
+         (mfg.TriMesh(np.array(DEG_P, float), np.array(DEG_F)), 4, None),
+         (mfg.TriMesh(np.array(DEG_P, float), np.array(DEG_F)), 5, 3),
+         (S.perturbed_grid(120, None, 0.02, 2), 2_000, None)]
 for mesh, target, seed in cases:
     res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=target, shuffle_seed=seed))
     kw = dict(target=target, seed=seed, order=einsum_order())
@@ -56,6 +62,12 @@ VARIANTS = [
     {"MF_PDL": "1"},
     {"MF_COND": "1"},
     {"MF_LD_MIN": "1", "MF_COND": "1"},
+    # size-gated branches that the defaults take only at cfg5 scale, forced at small sizes
+    {"MF_WIDE_MIN": "0"},
+    {"MF_SCAN4_MIN": "0"},
+    {"MF_BIG_SEL_MIN": "0"},
+    {"MF_BIG_SEL_MIN": "0", "MF_SEL_PASSES": "1"},
+    {"MF_WIDE_MIN": "0", "MF_SCAN4_MIN": "0", "MF_BIG_SEL_MIN": "0", "MF_LD_MIN": "1", "MF_SUITOR": "1"},
 ]
 
 

@@ -159,3 +159,29 @@ def test_pool_backward_golden(oracle, entry):
             out = oracle.pool_backward(G, Xb, rep, entry["n_out"], mode, w)
             exp = SMALL[f"{key}|bwd_{mode}_{gdt}"]
             assert out.dtype == exp.dtype and np.array_equal(out.view(np.uint8), exp.view(np.uint8)), (mode, gdt)
+
+
+FULL_PATH = os.path.join(HERE, "golden", "full.json")
+FULL = json.load(open(FULL_PATH)) if os.path.exists(FULL_PATH) else {}
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+def test_oracle_matches_reference_at_full_size(oracle, cfg):
+    """The C oracle at BASELINE.json's full sizes (cfg5: 10M vertices, 4 levels) against the
+    real reference's digests (tests/golden/make_golden_full.py) -- pins the checker the GPU
+    full-size tests compare with, on every level, pooled features included."""
+    import test_gpu_fullsize as G  # workload builders + digest helpers (no GPU needed for these)
+
+    if cfg not in FULL:
+        pytest.skip(f"no {cfg} in tests/golden/full.json")
+    g = FULL[cfg]
+    mesh, levels, feats = G.workload(cfg)
+    assert G.input_digest(mesh) == g["input"]
+    got = G.oracle_chain(oracle, cfg, FULL["einsum_order"])
+    for i, (o, exp) in enumerate(zip(got, g["levels"])):
+        assert len(o["positions"]) == exp["n_out"] and len(o["facets"]) == exp["m_out"]
+        for k in ("replace", "mapping", "facets", "positions", "features", "vertex_offsets", "facet_offsets"):
+            if k in exp:
+                assert sha(o[k]) == exp[k], f"level {i}: {k}"
+        if "pool_max" in exp:
+            assert sha(o["pool_max"]) == exp["pool_max"] and sha(o["unpool"]) == exp["unpool"], f"level {i}"
