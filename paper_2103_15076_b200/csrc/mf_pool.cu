@@ -196,6 +196,116 @@ __global__ void k_pool_bwd_max(int64_t n_out, int C, const int* __restrict__ off
     }
 }
 
+// ---- vectorised forms (C * sizeof(T) a multiple of 16 B): L lanes per row, 16-byte loads ----
+// A group of L lanes owns one output row; lane j handles 16-byte vectors j, j+L, ... of it.
+// Member loop unrolled by U: the U member ids (broadcast loads) and then their U row vectors are
+// in flight together before the in-order fold -- the fold order (ascending member, pooling.py
+// np.add.at / maximum.at) is unchanged, only the loads are hoisted.
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+    static constexpr int E = 4;
+    MF_DEV static void split(const uint4& u, float* x) {
+        x[0] = __uint_as_float(u.x), x[1] = __uint_as_float(u.y), x[2] = __uint_as_float(u.z),
+        x[3] = __uint_as_float(u.w);
+    }
+    MF_DEV static uint4 join(const float* x) {
+        return make_uint4(__float_as_uint(x[0]), __float_as_uint(x[1]), __float_as_uint(x[2]), __float_as_uint(x[3]));
+    }
+};
+template <>
+struct Vec16<double> {
+    static constexpr int E = 2;
+    MF_DEV static void split(const uint4& u, double* x) {
+        x[0] = __longlong_as_double(((long long)u.y << 32) | u.x);
+        x[1] = __longlong_as_double(((long long)u.w << 32) | u.z);
+    }
+    MF_DEV static uint4 join(const double* x) {
+        const unsigned long long a = (unsigned long long)__double_as_longlong(x[0]);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(x[1]);
+        return make_uint4((unsigned)a, (unsigned)(a >> 32), (unsigned)b, (unsigned)(b >> 32));
+    }
+};
+
+template <typename T, int L, int MODE>
+__global__ void __launch_bounds__(256) k_pool_vec(int n_out, int row16, const int* __restrict__ off,
+                                                  const int* __restrict__ members, const uint4* __restrict__ X,
+                                                  const T* __restrict__ w, uint4* __restrict__ out,
+                                                  int* __restrict__ zero_weight) {
+    MF_PDL_ENTRY;
+    constexpr int E = Vec16<T>::E;
+    constexpr int U = 4;
+    const int lane = threadIdx.x & (L - 1);
+    const int G = (int)(((int64_t)gridDim.x * blockDim.x) / L);
+    for (int r = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / L); r < n_out; r += G) {
+        const int s = off[r], e = off[r + 1];
+        for (int j = lane; j < row16; j += L) {
+            T acc[E], den = (T)0;
+#pragma unroll
+            for (int k = 0; k < E; k++) acc[k] = MODE == MF_POOL_MAX ? (T)-INFINITY : (T)0;
+            for (int i = s; i < e; i += U) {
+                int m[U];
+                uint4 raw[U];
+                T wv[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) m[u] = i + u < e ? __ldg(members + i + u) : -1;
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (m[u] >= 0) raw[u] = __ldg(X + (int64_t)m[u] * row16 + j);
+                    if (MODE == MF_POOL_WEIGHTED && m[u] >= 0) wv[u] = __ldg(w + m[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (m[u] < 0) break;
+                    T x[E];
+                    Vec16<T>::split(raw[u], x);
+#pragma unroll
+                    for (int k = 0; k < E; k++) {
+                        if (MODE == MF_POOL_MAX) acc[k] = (acc[k] != acc[k] || acc[k] > x[k]) ? acc[k] : x[k];
+                        else if (MODE == MF_POOL_WEIGHTED) acc[k] = x86_add(acc[k], x86_mul(x[k], wv[u]));
+                        else acc[k] = x86_add(acc[k], x[k]);
+                    }
+                    if (MODE == MF_POOL_WEIGHTED) den = x86_add(den, wv[u]);
+                }
+            }
+            if (MODE == MF_POOL_WEIGHTED) {
+                if (den == (T)0) atomicExch(zero_weight, 1);
+#pragma unroll
+                for (int k = 0; k < E; k++) acc[k] = x86_div(acc[k], den);
+            } else if (MODE == MF_POOL_AVERAGE) {
+#pragma unroll
+                for (int k = 0; k < E; k++) acc[k] = avg_div(acc[k], e - s);
+            }
+            out[(int64_t)r * row16 + j] = Vec16<T>::join(acc);
+        }
+    }
+}
+
+// unpool row gather: out[v] = coarse[rep[v]]; a group of L lanes per row, U rows in flight per
+// group (rows g, g+G, ... so every store instruction of the grid covers consecutive rows)
+template <int L, int U>
+__global__ void __launch_bounds__(256) k_unpool_rows(int n, int row16, const int* __restrict__ rep,
+                                                     const uint4* __restrict__ coarse, uint4* __restrict__ out) {
+    MF_PDL_ENTRY;
+    const int lane = threadIdx.x & (L - 1);
+    const int G = (int)(((int64_t)gridDim.x * blockDim.x) / L);
+    for (int v0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / L); v0 < n; v0 += G * U) {
+        int r[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) r[u] = v0 + u * G < n ? __ldg(rep + v0 + u * G) : -1;
+        for (int j = lane; j < row16; j += L) {
+            uint4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (r[u] >= 0) x[u] = __ldg(coarse + (int64_t)r[u] * row16 + j);
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (r[u] >= 0) __stcs(out + (int64_t)(v0 + u * G) * row16 + j, x[u]);
+        }
+    }
+}
+
 __global__ void k_unpool_vec(int64_t n, int64_t row16, const int* __restrict__ rep, const int4* __restrict__ coarse,
                              int4* __restrict__ out) {
     MF_PDL_ENTRY;
@@ -230,52 +340,260 @@ __global__ void k_unpool(int64_t n, int C, const int* __restrict__ rep, const T*
     }
 }
 
-static void scan_into(const Context* ctx, unsigned long long* status, const int* in, int* out, int n,
-                      cudaStream_t s) {
-    int tiles = std::max(1, (n + kScanTile - 1) / kScanTile);
-    cudaMemsetAsync(status, 0, (size_t)(tiles + 1) * sizeof(unsigned long long), s);
-    LAUNCH(k_scan_excl<LoadArr>, tiles, kScanBlock, 0, s, LoadArr{in}, n, out, status,
-           reinterpret_cast<int*>(status + tiles), (const int*)nullptr, EpiNone(), (unsigned long long*)nullptr, 0);
-    (void)ctx;
+
+// Scatter by key into CSR slots, counting each cluster's counter back down to 0 (no cursor
+// array to clear); the slot order within a cluster is fixed afterwards by the segment sort.
+__global__ void k_csr_scatter_dec(int n, const int* __restrict__ key, const int* __restrict__ off,
+                                  int* __restrict__ count, int* __restrict__ members) {
+    MF_PDL_ENTRY;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int r = key[v];
+        members[off[r] + atomicSub(count + r, 1) - 1] = v;
+    }
 }
 
-// CSR of the clusters of a device int32 replace (counts must already be
-// known to cover every output vertex).  Members ascending within a cluster.
+// Thread per cluster: <= 4 members sorted in registers (a sorting network: most clusters of a
+// decimation are pairs plus a few absorbed vertices), up to kSmallDeg by insertion sort, longer
+// ones to the heavy (block-sort) tier.
+__global__ void k_seg_sort_small4(int nseg, const int* __restrict__ off, int* __restrict__ members,
+                                  int* __restrict__ heavy, int* __restrict__ heavy_count) {
+    MF_PDL_ENTRY;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nseg; r += gridDim.x * blockDim.x) {
+        const int s = off[r], d = off[r + 1] - s;
+        if (d <= 1) continue;
+        if (d <= 4) {
+            int a = members[s], b = members[s + 1];
+            int c = d > 2 ? members[s + 2] : INT_MAX, e = d > 3 ? members[s + 3] : INT_MAX;
+            int t;
+#define MF_CSWAP(x, y) if (x > y) t = x, x = y, y = t
+            MF_CSWAP(a, b);
+            MF_CSWAP(c, e);
+            MF_CSWAP(a, c);
+            MF_CSWAP(b, e);
+            MF_CSWAP(b, c);
+#undef MF_CSWAP
+            members[s] = a;
+            members[s + 1] = b;
+            if (d > 2) members[s + 2] = c;
+            if (d > 3) members[s + 3] = e;
+            continue;
+        }
+        if (d > kSmallDeg) {
+            heavy[append_slot(heavy_count)] = r;
+            continue;
+        }
+        int k[kSmallDeg];
+        for (int i = 0; i < d; i++) k[i] = members[s + i];
+        isort<kSmallDeg>(k, d);
+        for (int i = 0; i < d; i++) members[s + i] = k[i];
+    }
+}
+
+// One cooperative launch builds the whole cluster CSR: count -> scan -> scatter -> segment
+// sort -> heavy segments, phases separated by a grid barrier (one block per SM, co-resident by
+// construction of the cooperative launch).  Replaces five launches + a look-back scan whose
+// fixed latencies dominated at pooling sizes (cfg3: ~107 us of CSR build per step).
+MF_DEV unsigned ld_volatile_u32(const unsigned* p) { return *(const volatile unsigned*)p; }
+MF_DEV void coop_bar(unsigned* bar, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_volatile_u32(bar) < target) __nanosleep(32);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) k_csr_coop(int n, int n_out, const int* __restrict__ key, int* __restrict__ cnt,
+                                                   int* __restrict__ off, int* __restrict__ members,
+                                                   int* __restrict__ heavy, int* __restrict__ ctr,
+                                                   int* __restrict__ bsum, int* __restrict__ tmp) {
+    MF_PDL_ENTRY;
+    __shared__ int s_scan[33];
+    __shared__ int s_sort[kChunk];
+    unsigned* bar = reinterpret_cast<unsigned*>(ctr + 1);
+    const unsigned G = gridDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    // 1. cluster sizes
+    for (int v = tid; v < n; v += nth) atomicAdd(cnt + key[v], 1);
+    coop_bar(bar, 1 * G);
+    // 2. exclusive scan: block b owns a contiguous chunk of the clusters
+    const int chunk = (n_out + (int)G - 1) / (int)G;
+    const int lo = min(n_out, (int)blockIdx.x * chunk), hi = min(n_out, lo + chunk);
+    int part = 0;
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) part += __ldcg(cnt + i);
+    int tot;
+    block_excl_scan(part, s_scan, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+    coop_bar(bar, 2 * G);
+    int pre = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += blockDim.x) pre += __ldcg(bsum + b);
+    block_excl_scan(pre, s_scan, &tot);
+    int run = tot;
+    for (int i0 = lo; i0 < hi; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const int x = i < hi ? __ldcg(cnt + i) : 0;
+        const int ex = block_excl_scan(x, s_scan, &tot);
+        if (i < hi) off[i] = run + ex;
+        run += tot;
+    }
+    if (tid == 0) off[n_out] = n;
+    coop_bar(bar, 3 * G);
+    // 3. scatter (each cluster's counter counts back down to 0)
+    for (int v = tid; v < n; v += nth) {
+        const int r = key[v];
+        members[__ldcg(off + r) + atomicSub(cnt + r, 1) - 1] = v;
+    }
+    coop_bar(bar, 4 * G);
+    // 4. ascending member order: <= 4 in registers, <= kSmallDeg by insertion, longer listed
+    for (int r = tid; r < n_out; r += nth) {
+        const int s0 = __ldcg(off + r), d = __ldcg(off + r + 1) - s0;
+        if (d <= 1) continue;
+        if (d <= 4) {
+            int a = __ldcg(members + s0), b = __ldcg(members + s0 + 1);
+            int c = d > 2 ? __ldcg(members + s0 + 2) : INT_MAX, e = d > 3 ? __ldcg(members + s0 + 3) : INT_MAX;
+            int t;
+#define MF_CSWAP(x, y) if (x > y) t = x, x = y, y = t
+            MF_CSWAP(a, b);
+            MF_CSWAP(c, e);
+            MF_CSWAP(a, c);
+            MF_CSWAP(b, e);
+            MF_CSWAP(b, c);
+#undef MF_CSWAP
+            members[s0] = a;
+            members[s0 + 1] = b;
+            if (d > 2) members[s0 + 2] = c;
+            if (d > 3) members[s0 + 3] = e;
+        } else if (d > kSmallDeg) {
+            heavy[atomicAdd(ctr, 1)] = r;
+        } else {
+            int k[kSmallDeg];
+            for (int i = 0; i < d; i++) k[i] = __ldcg(members + s0 + i);
+            isort<kSmallDeg>(k, d);
+            for (int i = 0; i < d; i++) members[s0 + i] = k[i];
+        }
+    }
+    coop_bar(bar, 5 * G);
+    // 5. long segments: one block each
+    const int H = __ldcg(ctr);
+    for (int h = blockIdx.x; h < H; h += gridDim.x) {
+        const int r = __ldcg(heavy + h);
+        const int s0 = __ldcg(off + r), d = __ldcg(off + r + 1) - s0;
+        block_sort_ints(members + s0, tmp + s0, d, s_sort);
+    }
+}
+
+// cooperative CSR build available (MF_CSR_COOP=0 forces the five-launch path for A/B runs)
+static int g_csr_blocks_per_sm = 1;
+static bool csr_coop_ok(const Context* ctx) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_CSR_COOP");
+        int occ = 0;
+        v = (e && e[0] == '0') ? 0 : 1;
+        if (v && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_coop, 1024, 0) != cudaSuccess || occ < 1))
+            v = 0;
+        cudaGetLastError();
+        g_csr_blocks_per_sm = std::max(1, std::min(occ, 2));
+    }
+    (void)ctx;
+    return v == 1;
+}
+
+// CSR of the clusters of a device int32 replace (every key in [0, n_out)).  Members ascending
+// within a cluster.  One clearing memset, then count -> scan -> scatter -> segment sort.
 int build_cluster_csr(Context* ctx, const int* d_replace, int64_t n, int64_t n_out, int** d_off, int** d_members,
                       void** block, cudaStream_t stream, mf_status* st) {
+    const int scan_tiles = std::max(1, (int)((n_out + kScanTile - 1) / kScanTile));
+    const int tiles = std::max(ctx->sm_count * 2, scan_tiles);  // the state words also hold the coop block sums
     Arena me;
     me.measuring = true;
-    auto lay = [&](Arena& A, int*& off, int*& mem, int*& cnt, int*& cur, int*& heavy, int*& tmp, int*& ctr,
+    auto lay = [&](Arena& A, int*& off, int*& mem, int*& cnt, int*& heavy, int*& tmp, int*& ctr,
                    unsigned long long*& sst) {
         off = A.take<int>((size_t)n_out + 1);
         mem = A.take<int>((size_t)n);
-        cnt = A.take<int>((size_t)n_out + 1);
-        cur = A.take<int>((size_t)n_out + 1);
         heavy = A.take<int>((size_t)n_out + 1);
         tmp = A.take<int>((size_t)n);
+        cnt = A.take<int>((size_t)n_out + 1);  // cnt | ctr | scan state: cleared by one memset
         ctr = A.take<int>(8);
-        sst = A.take<unsigned long long>((size_t)(n_out + 1) / kScanTile + 4);
+        sst = A.take<unsigned long long>((size_t)tiles + 4);
     };
-    int *off, *mem, *cnt, *cur, *heavy, *tmp, *ctr;
+    int *off, *mem, *cnt, *heavy, *tmp, *ctr;
     unsigned long long* sst;
-    lay(me, off, mem, cnt, cur, heavy, tmp, ctr, sst);
+    lay(me, off, mem, cnt, heavy, tmp, ctr, sst);
     MF_CUDA_TRY(cudaMallocAsync(block, me.off, stream));
     Arena A;
     A.base = (char*)*block;
     A.cap = me.off;
-    lay(A, off, mem, cnt, cur, heavy, tmp, ctr, sst);
-    MF_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)(n_out + 1) * sizeof(int), stream));
-    MF_CUDA_TRY(cudaMemsetAsync(cur, 0, (size_t)(n_out + 1) * sizeof(int), stream));
-    MF_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8 * sizeof(int), stream));
+    lay(A, off, mem, cnt, heavy, tmp, ctr, sst);
+    MF_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)((char*)(sst + tiles + 4) - (char*)cnt), stream));
+    if (csr_coop_ok(ctx)) {
+        // bsum reuses the scan-state words (tiles + 4 >= grid blocks is ensured by csr_coop_ok)
+        int* bsum = reinterpret_cast<int*>(sst);
+        int nn = (int)n, no = (int)n_out;
+        void* args[] = {&nn, &no, (void*)&d_replace, &cnt, &off, &mem, &heavy, &ctr, &bsum, &tmp};
+        prof_pre("k_csr_coop", stream);
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_csr_coop, dim3(ctx->sm_count * g_csr_blocks_per_sm),
+                                                    dim3(1024), args, 0, stream);
+        prof_post("k_csr_coop", stream);
+        g_launches++;
+        MF_CUDA_TRY(e);
+        *d_off = off;
+        *d_members = mem;
+        return MF_OK;
+    }
     LAUNCH(k_count_keys, grid_of(ctx, n), 256, 0, stream, n, d_replace, cnt);
-    scan_into(ctx, sst, cnt, off, (int)n_out, stream);
-    LAUNCH(k_csr_scatter, grid_of(ctx, n), 256, 0, stream, (int)n, nullptr, d_replace, off, cur, mem);
-    LAUNCH(k_seg_sort_small, grid_of(ctx, n_out), 256, 0, stream, (int)n_out, nullptr, off, mem, heavy, ctr);
+    LAUNCH(k_scan_excl<LoadArr>, scan_tiles, kScanBlock, 0, stream, LoadArr{cnt}, (int)n_out, off, sst,
+           reinterpret_cast<int*>(sst + tiles), (const int*)nullptr, EpiNone(), (unsigned long long*)nullptr, 0);
+    LAUNCH(k_csr_scatter_dec, grid_of(ctx, n), 256, 0, stream, (int)n, d_replace, off, cnt, mem);
+    LAUNCH(k_seg_sort_small4, grid_of(ctx, n_out), 256, 0, stream, (int)n_out, off, mem, heavy, ctr);
     LAUNCH(k_seg_sort_heavy, ctx->sm_count, 256, 0, stream, nullptr, off, mem, tmp, heavy, ctr);
     MF_CUDA_TRY(cudaGetLastError());
     *d_off = off;
     *d_members = mem;
     return MF_OK;
+}
+
+// MF_POOL_SCALAR=1: the thread-per-(cluster, channel) kernels even for 16-byte rows (A/B runs)
+static bool pool_scalar_forced() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_POOL_SCALAR");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+static int lanes_for(int row16) {  // lanes per row: the row's vectors, 4..32
+    int L = 4;
+    while (L < row16 && L < 32) L <<= 1;
+    return L;
+}
+
+template <typename T, int L>
+static void launch_pool_vec_l(Context* ctx, int64_t n_out, int row16, const int* off, const int* mem, const void* X,
+                              const void* W, int mode, void* O, int* flag, cudaStream_t s) {
+    const int grid = grid_of(ctx, n_out * L);
+    const uint4* x = (const uint4*)X;
+    uint4* o = (uint4*)O;
+    const T* w = (const T*)W;
+    if (mode == MF_POOL_MAX) LAUNCH((k_pool_vec<T, L, MF_POOL_MAX>), grid, 256, 0, s, (int)n_out, row16, off, mem, x, w, o, flag);
+    else if (mode == MF_POOL_WEIGHTED)
+        LAUNCH((k_pool_vec<T, L, MF_POOL_WEIGHTED>), grid, 256, 0, s, (int)n_out, row16, off, mem, x, w, o, flag);
+    else if (mode == MF_POOL_AVERAGE)
+        LAUNCH((k_pool_vec<T, L, MF_POOL_AVERAGE>), grid, 256, 0, s, (int)n_out, row16, off, mem, x, w, o, flag);
+    else LAUNCH((k_pool_vec<T, L, MF_POOL_SUM>), grid, 256, 0, s, (int)n_out, row16, off, mem, x, w, o, flag);
+}
+template <typename T>
+static void launch_pool_vec(Context* ctx, int64_t n_out, int row16, const int* off, const int* mem, const void* X,
+                            const void* W, int mode, void* O, int* flag, cudaStream_t s) {
+    switch (lanes_for(row16)) {
+        case 4: launch_pool_vec_l<T, 4>(ctx, n_out, row16, off, mem, X, W, mode, O, flag, s); break;
+        case 8: launch_pool_vec_l<T, 8>(ctx, n_out, row16, off, mem, X, W, mode, O, flag, s); break;
+        case 16: launch_pool_vec_l<T, 16>(ctx, n_out, row16, off, mem, X, W, mode, O, flag, s); break;
+        default: launch_pool_vec_l<T, 32>(ctx, n_out, row16, off, mem, X, W, mode, O, flag, s); break;
+    }
 }
 
 int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c, const int* d_replace,
@@ -289,12 +607,18 @@ int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c
     size_t xb = (size_t)(n * c) * es, wb = (mode == MF_POOL_WEIGHTED) ? (size_t)n * es : 0,
            ob = (size_t)(n_out * c) * es;
     bool hx = !is_device_ptr(features), hw = wb && !is_device_ptr(weights), ho = !is_device_ptr(out);
-    size_t need = (hx ? xb : 0) + (hw ? wb : 0) + (ho ? ob : 0) + 256 * 4;
-    MF_CUDA_TRY(cudaMallocAsync(&tmp, need, stream));
-    char* p = (char*)tmp;
-    int* d_flag = (int*)p;
-    p += 256;
-    MF_CUDA_TRY(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
+    // device buffers and no data-dependent error to report: stream-ordered, no allocation, no wait
+    const bool wait = hx || hw || ho || mode == MF_POOL_WEIGHTED;
+    int* d_flag = nullptr;
+    char* p = nullptr;
+    if (wait) {
+        size_t need = (hx ? xb : 0) + (hw ? wb : 0) + (ho ? ob : 0) + 256 * 4;
+        MF_CUDA_TRY(cudaMallocAsync(&tmp, need, stream));
+        p = (char*)tmp;
+        d_flag = (int*)p;
+        p += 256;
+        MF_CUDA_TRY(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
+    }
     if (hx) {
         MF_CUDA_TRY(cudaMemcpyAsync(p, features, xb, cudaMemcpyHostToDevice, stream));
         dX = p;
@@ -307,12 +631,22 @@ int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c
     }
     if (ho) dO = p;
     if (n_out * c > 0) {
-        if (dtype == MF_DTYPE_F32)
+        const size_t row = (size_t)c * es;
+        if (row % 16 == 0 && ((uintptr_t)dX % 16) == 0 && ((uintptr_t)dO % 16) == 0 && !pool_scalar_forced()) {
+            if (dtype == MF_DTYPE_F32) launch_pool_vec<float>(ctx, n_out, (int)(row / 16), d_off, d_members, dX, dW,
+                                                              mode, dO, d_flag, stream);
+            else launch_pool_vec<double>(ctx, n_out, (int)(row / 16), d_off, d_members, dX, dW, mode, dO, d_flag,
+                                         stream);
+        } else if (dtype == MF_DTYPE_F32)
             LAUNCH(k_pool<float>, grid_of(ctx, n_out * c), 256, 0, stream, n_out, (int)c, d_off, d_members,
                    (const float*)dX, (const float*)dW, mode, (float*)dO, d_flag);
         else
             LAUNCH(k_pool<double>, grid_of(ctx, n_out * c), 256, 0, stream, n_out, (int)c, d_off, d_members,
                    (const double*)dX, (const double*)dW, mode, (double*)dO, d_flag);
+    }
+    if (!wait) {
+        MF_CUDA_TRY(cudaGetLastError());
+        return MF_OK;
     }
     if (ho) MF_CUDA_TRY(cudaMemcpyAsync(out, dO, ob, cudaMemcpyDeviceToHost, stream));
     int h_flag = 0;
@@ -398,8 +732,9 @@ int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64
     size_t cb = (size_t)(n_out * c) * es, ob = (size_t)(n * c) * es;
     bool hc = !is_device_ptr(coarse), ho = !is_device_ptr(out);
     void* tmp = nullptr;
+    const bool wait = hc || ho;  // device buffers only: stream-ordered, no allocation, no wait
     size_t need = (hc ? cb + 256 : 0) + (ho ? ob + 256 : 0) + 256;
-    MF_CUDA_TRY(cudaMallocAsync(&tmp, need, stream));
+    if (wait) MF_CUDA_TRY(cudaMallocAsync(&tmp, need, stream));
     char* p = (char*)tmp;
     const void* dC = coarse;
     void* dO = out;
@@ -411,7 +746,26 @@ int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64
     if (ho) dO = p;
     const size_t row = (size_t)c * es;
     if (n * c > 0) {
-        if (row % 16 == 0 && ((uintptr_t)dC % 16) == 0 && ((uintptr_t)dO % 16) == 0) {
+        if (row % 16 == 0 && ((uintptr_t)dC % 16) == 0 && ((uintptr_t)dO % 16) == 0 && !pool_scalar_forced()) {
+            const int row16 = (int)(row / 16);
+            const int L = lanes_for(row16);
+            // up to two waves of groups: one row per group (latency-bound sizes); beyond, 4 rows in
+            // flight per group
+            const bool deep = (int64_t)n * L > (int64_t)ctx->sm_count * 2048 * 2;
+            const int grid = grid_of(ctx, deep ? (n * L + 3) / 4 : n * L);
+            const uint4* x = (const uint4*)dC;
+            uint4* o = (uint4*)dO;
+#define MF_UNPOOL(LL)                                                                                   \
+    do {                                                                                               \
+        if (deep) LAUNCH((k_unpool_rows<LL, 4>), grid, 256, 0, stream, (int)n, row16, d_replace, x, o); \
+        else LAUNCH((k_unpool_rows<LL, 1>), grid, 256, 0, stream, (int)n, row16, d_replace, x, o);      \
+    } while (0)
+            if (L == 4) MF_UNPOOL(4);
+            else if (L == 8) MF_UNPOOL(8);
+            else if (L == 16) MF_UNPOOL(16);
+            else MF_UNPOOL(32);
+#undef MF_UNPOOL
+        } else if (row % 16 == 0 && ((uintptr_t)dC % 16) == 0 && ((uintptr_t)dO % 16) == 0) {
             int64_t row16 = (int64_t)(row / 16);
             LAUNCH(k_unpool_vec, grid_of(ctx, n * row16), 256, 0, stream, n, row16, d_replace, (const int4*)dC,
                    (int4*)dO);
@@ -422,6 +776,10 @@ int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64
             LAUNCH(k_unpool<double>, grid_of(ctx, n * c), 256, 0, stream, n, (int)c, d_replace, (const double*)dC,
                    (double*)dO);
         }
+    }
+    if (!wait) {
+        MF_CUDA_TRY(cudaGetLastError());
+        return MF_OK;
     }
     if (ho) MF_CUDA_TRY(cudaMemcpyAsync(out, dO, ob, cudaMemcpyDeviceToHost, stream));
     MF_CUDA_TRY(cudaFreeAsync(tmp, stream));
