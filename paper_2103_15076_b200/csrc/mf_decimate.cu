@@ -200,6 +200,16 @@ static bool use_cond() {
     return v == 1;
 }
 
+// MF_FUSE_PLANE=0: separate k_compose / k_facet_plane launches between rounds (A/B runs)
+static bool fuse_plane() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_FUSE_PLANE");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // grid-stride kernels launch at most MF_GRID_CAP blocks per SM
 static int grid_cap_mult() {
     static int v = -1;
@@ -458,7 +468,7 @@ struct WS {
     unsigned long long* tkey;
     ScanBuf scan;
     int* status;  // [8] flags | foff_final[B+1] | fail[3B] | stats[4R]
-    size_t status_words;
+    size_t status_words, params_pad, status_pad, upload_bytes;
 };
 
 // memcmp(a, b, bytes) != 0, split over host threads above 8 MB
@@ -487,8 +497,14 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     const int B = p.B, R = p.R, N0 = p.N0, N1 = p.N1, Mcap = p.Mcap, Ecap = p.Ecap, Nfin = p.Nfin;
     const int64_t C = p.C;
     const bool alias = p.alias;
-    W.params = A.take<int>(p.params_words);
-    W.vo64 = A.take<int64_t>((size_t)2 * (B + 1));
+    // one upload block: params | initial status words | vertex / facet offsets (int64)
+    W.status_words = 8 + (size_t)(B + 1) + 3 * (size_t)B + 4 * (size_t)std::max(R, 1);
+    W.params_pad = (p.params_words + 63) & ~size_t(63);
+    W.status_pad = (W.status_words + 63) & ~size_t(63);
+    W.upload_bytes = (W.params_pad + W.status_pad) * 4 + (size_t)2 * (B + 1) * 8;
+    W.params = A.take<int>(W.upload_bytes / 4);
+    W.status = W.params ? W.params + W.params_pad : nullptr;
+    W.vo64 = W.params ? reinterpret_cast<int64_t*>(W.status + W.status_pad) : nullptr;
     W.fo64 = W.vo64 ? W.vo64 + (B + 1) : nullptr;
     W.F64 = A.take<int64_t>((size_t)Mcap * 3);
     W.Xf32 = (!alias && p.fdtype == MF_DTYPE_F32) ? A.take<float>((size_t)N0 * C) : nullptr;
@@ -588,8 +604,6 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.scan.buf[0] = A.take<unsigned long long>((size_t)W.scan.words);
     W.scan.buf[1] = A.take<unsigned long long>((size_t)W.scan.words);
     W.scan.cur = 0;
-    W.status_words = 8 + (size_t)(B + 1) + 3 * (size_t)B + 4 * (size_t)std::max(R, 1);
-    W.status = A.take<int>(W.status_words);
 }
 
 // ------------------------------------------------------------------------
@@ -645,6 +659,15 @@ struct CondCapture {
     }
 };
 
+// k_init_inputs of the recording: its arguments and (when captured) its graph node, so a replay
+// can point it at the call's own input buffers; g_in_* = this call's inputs when they are device
+// buffers the kernel may read in place (else the staging buffers W.F64 / W.P0)
+thread_local InitArgs g_init_args;
+thread_local int g_init_grid = 1;
+thread_local cudaGraphNode_t g_init_node = nullptr;
+thread_local const int64_t* g_in_F64 = nullptr;
+thread_local const double* g_in_P = nullptr;
+
 static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream, cudaStream_t body0 = nullptr,
                    cudaStream_t body1 = nullptr) {
     CondCapture cc;
@@ -666,13 +689,25 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     int* d_foff0 = d_voff + (size_t)(R + 1) * (B + 1);
 
     g_pdl = true;
-    LAUNCH(k_graph_init, grid_for(ctx, std::max<int64_t>({(int64_t)N0 + 1, (int64_t)W.scan.words, (int64_t)W.status_words})),
-           256, 0, stream, W.status, (int)W.status_words, (int)(d_fail - W.status), (int)(d_fail - W.status) + 3 * B,
-           W.foff_a, d_foff0, B, W.deg, W.cursor, W.lowfill, N0 + 1, W.counters, W.scan.buf[0], W.scan.buf[1], W.scan.words,
-           W.ghist, kSelScratch);
-    if (m > 0 || n > 0)
-        LAUNCH(k_inputs_in, grid_for(ctx, std::max<int64_t>(m, 3 * n)), 256, 0, stream, m, W.F64, W.F0, B, W.vo64,
-               W.fo64, d_badf, 3 * n, W.P0, d_badp);
+    {
+        // status words arrive initialised with the params upload; the input pointers (caller
+        // device buffers or the host staging) are patched into this node on every replay
+        InitArgs ia{W.foff_a, d_foff0, B, W.deg, W.cursor, W.lowfill, N0 + 1, W.counters, W.scan.buf[0],
+                    W.scan.buf[1], W.scan.words, W.ghist, kSelScratch, m, g_in_F64 ? g_in_F64 : W.F64, W.F0, W.vo64,
+                    W.fo64, d_badf, 3 * n, g_in_P ? g_in_P : W.P0, W.P0, d_badp};
+        const int grid = grid_for(ctx, std::max<int64_t>({(int64_t)N0 + 1, (int64_t)W.scan.words, m, 3 * n}));
+        LAUNCH(k_init_inputs, grid, 256, 0, stream, ia);
+        g_init_args = ia;
+        g_init_grid = grid;
+        g_init_node = nullptr;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        if (cudaStreamGetCaptureInfo(stream, &cs, nullptr, nullptr, &deps, &nd) == cudaSuccess &&
+            cs == cudaStreamCaptureStatusActive && nd == 1)
+            g_init_node = deps[0];
+        cudaGetLastError();
+    }
     if (W.Xf32 && n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, W.X0);
 
     const double* Pc = W.P0;
@@ -685,6 +720,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     int* d_heavy_c = W.counters + 12;
     int* d_mid_n = W.counters + 20;
     int* d_scratch_used = W.counters + 24;
+    bool plane_done = false;  // this round's facet planes were computed by the previous round's epilogue
     for (int r = 0; r < R; r++) {
         const int N = p.h_N[r];
         const int Nn = p.h_N[r + 1];
@@ -703,7 +739,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_vmesh, grid_for(ctx, N), 256, 0, stream, d_abort, N, voff_r, B, vmesh);
         }
         // facet planes + incidence CSR (corner-major order)
-        LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, Pc, dM, vmesh, act, W.plane, W.deg, order);
+        if (!plane_done)
+            LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, Pc, dM, vmesh, act, W.plane, W.deg,
+                   order);
+        plane_done = false;
         run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", d_abort);
         LAUNCH(k_inc_scatter, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, dM, Mcap, vmesh, act, W.inc_off, W.cursor,
                W.inc);
@@ -839,17 +878,18 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const bool packed = Nn < p.wide_min;
         LAUNCH(k_relabel3, grid_for(ctx, std::max<int64_t>(N, W.tsize)), 256, 0, stream, N, d_abort, W.pairlo,
                W.absorbed, W.minrep, W.outidx, W.rstep, W.repv, W.abshead, W.absnext, W.table,
-               packed ? W.tkey : nullptr, (int)W.tsize, packed ? 0x7f7f7f7f : -1, W.has_live);
+               packed ? W.tkey : nullptr, (int)W.tsize, packed ? 0x7f7f7f7f : -1, W.has_live, W.deg, W.cursor,
+               W.lowfill, last ? 0 : Nn + 1);
         // contraction over member lists (no cluster CSR needed)
+        // the heavy-cluster tier runs in k_contract's last block (counters[30] = finished blocks)
         if (p.placement)
             LAUNCH(k_contract<1>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.pairlo, W.e1,
-                   W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c);
+                   W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c,
+                   W.cmem, W.best, d_scratch_used, W.counters + 30);
         else
             LAUNCH(k_contract<0>, grid_for(ctx, Nn), 256, 0, stream, Nn, d_abort, W.repv, W.mate, W.pairlo, W.e1,
-                   W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c);
-        LAUNCH(k_contract_heavy, ctx->sm_count, 256, 0, stream, d_abort, W.heavy, d_heavy_c, W.repv, W.mate, W.pairlo,
-               W.e1, W.absorbed, W.abshead, W.absnext, Pc, Xc, (int)C, Pn, Xn, W.vq, p.placement, W.cmem, W.best,
-               d_scratch_used);
+                   W.absorbed, W.abshead, W.absnext, vmesh, act, Pc, Xc, (int)C, Pn, Xn, W.vq, W.heavy, d_heavy_c,
+                   W.cmem, W.best, d_scratch_used, W.counters + 30);
         // output facets: remap, drop degenerate, drop later duplicates (hash, min facet id wins)
         {
             const unsigned per_vertex = std::max(1u, W.tsize / (unsigned)std::max(Nn, 1));
@@ -867,9 +907,16 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         else
             run_scan(W.scan, LoadKeep{dM, W.slot, W.table}, W.kout, Mcap, stream, "k_scan<keep>", d_abort,
                      EpiFacetWrite{W.mapped, Fn});
-        LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh, act,
-               W.rt, W.mt, r == 0, B, W.kout, foff_c, foff_n, last ? d_foff_fin : nullptr, d_stats + 4 * r,
-               W.aoff + N, W.ldc + 2, W.deg, W.cursor, W.lowfill, last ? 0 : Nn + 1, W.counters);
+        if (B == 1 && !last && fuse_plane()) {  // + the next round's facet planes, one launch
+            LAUNCH(k_compose_plane, grid_for(ctx, std::max<int64_t>(N0, Mcap)), 256, 0, stream, N0, d_abort, W.rstep,
+                   W.inc_off, W.has_live, act, W.rt, W.mt, r == 0, W.kout, foff_c, foff_n, d_stats + 4 * r,
+                   W.aoff + N, W.ldc + 2, W.counters, Fn, Pn, d_act + (size_t)(r + 1) * B, W.plane, W.deg, order);
+            plane_done = true;
+        } else {
+            LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh,
+                   act, W.rt, W.mt, r == 0, B, W.kout, foff_c, foff_n, last ? d_foff_fin : nullptr, d_stats + 4 * r,
+                   W.aoff + N, W.ldc + 2, W.counters);
+        }
         Pc = Pn;
         Xc = Xn;
         Fc = Fn;
@@ -884,6 +931,9 @@ struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     std::vector<ProfRec> prof;
     int64_t kernels = 0;  // kernel nodes (launch accounting on replay)
+    cudaGraphNode_t init_node = nullptr;  // k_init_inputs (its input pointers change per call)
+    InitArgs init_args;
+    int init_grid = 1;
 };
 struct GraphCache {
     std::map<std::vector<int64_t>, GraphEntry> entries;
@@ -915,7 +965,7 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement,
+                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
@@ -1113,8 +1163,8 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         A.cap = ctx->arena_bytes;
         layout(A, W, p);
     }
-    // ---- pinned staging: params + readback
-    size_t pin_need = p.params_words * 4 + 2 * (size_t)(B + 1) * 8 + W.status_words * 4 + 1024;
+    // ---- pinned staging: [params | initial status words | offsets] (one upload) + readback
+    size_t pin_need = W.upload_bytes + W.status_words * 4 + 1024;
     if (ctx->pinned_bytes < pin_need) {
         MF_CUDA_TRY(cudaStreamSynchronize(stream));
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -1130,18 +1180,28 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         q = std::copy(p.h_nin.begin(), p.h_nin.end(), q);
         q = std::copy(p.h_voff.begin(), p.h_voff.end(), q);
         for (int b = 0; b <= B; b++) *q++ = (int)p.foff[b];
+        // status words: [1] = no bad facet yet (atomicMin), fail words = -1, the rest 0
+        int* hs = hp + W.params_pad;
+        const size_t fail_lo = 8 + (size_t)(B + 1), fail_hi = fail_lo + 3 * (size_t)B;
+        for (size_t i = 0; i < W.status_words; i++) hs[i] = (i == 1) ? 0x7f7f7f7f : ((i >= fail_lo && i < fail_hi) ? -1 : 0);
     }
-    int64_t* h_o64 = (int64_t*)((char*)ctx->pinned + ((p.params_words * 4 + 255) & ~size_t(255)));
+    int64_t* h_o64 = (int64_t*)(hp + W.params_pad + W.status_pad);
     for (int b = 0; b <= B; b++) {
         h_o64[b] = p.voff[b];
         h_o64[B + 1 + b] = p.foff[b];
     }
-    int* h_status = (int*)(h_o64 + 2 * (B + 1));
-    // ---- stage params + inputs (outside the graph: host pointers / caller buffers change per call)
-    MF_CUDA_TRY(cudaMemcpyAsync(W.params, hp, p.params_words * 4, cudaMemcpyHostToDevice, stream));
-    MF_CUDA_TRY(cudaMemcpyAsync(W.vo64, h_o64, 2 * (size_t)(B + 1) * 8, cudaMemcpyHostToDevice, stream));
-    if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, P_src, (size_t)n * 24, cudaMemcpyDefault, stream));
-    if (m) MF_CUDA_TRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 24, cudaMemcpyDefault, stream));
+    int* h_status = (int*)((char*)ctx->pinned + ((W.upload_bytes + 255) & ~size_t(255)));
+    // ---- stage params + inputs (outside the graph: host pointers / caller buffers change per call).
+    // Device-resident inputs of a real chain are read in place by k_init_inputs (its graph node is
+    // re-pointed per call); host inputs are uploaded into the staging buffers it reads instead.
+    MF_CUDA_TRY(cudaMemcpyAsync(W.params, hp, W.upload_bytes, cudaMemcpyHostToDevice, stream));
+    const bool in_place = R > 0 && (n == 0 || is_device_ptr(P_src)) && (m == 0 || is_device_ptr(mv->facets));
+    g_in_P = in_place && n ? (const double*)P_src : nullptr;
+    g_in_F64 = in_place && m ? mv->facets : nullptr;
+    if (!in_place) {
+        if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, P_src, (size_t)n * 24, cudaMemcpyDefault, stream));
+        if (m) MF_CUDA_TRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 24, cudaMemcpyDefault, stream));
+    }
     if (!p.alias && n * C > 0) {
         if (!mv->features)
             MF_CUDA_TRY(cudaMemcpyAsync(W.X0, P_src, (size_t)n * 24, cudaMemcpyDefault, stream));
@@ -1195,8 +1255,29 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             MF_CUDA_TRY(ie);
             e.prof.assign(g_prof_recs.begin() + rec0, g_prof_recs.end());
             e.kernels = nk;
+            e.init_node = g_init_node;
+            e.init_args = g_init_args;
+            e.init_grid = g_init_grid;
             g_prof_recs.resize(rec0);
             it = gc.entries.emplace(key, std::move(e)).first;
+        }
+        {  // point k_init_inputs at this call's inputs (device buffers in place, else the staging)
+            GraphEntry& ge = it->second;
+            const int64_t* f_src = g_in_F64 ? g_in_F64 : W.F64;
+            const double* p_src = g_in_P ? g_in_P : W.P0;
+            if (ge.init_args.F64 != f_src || ge.init_args.Psrc != p_src) {
+                if (!ge.init_node) return rec_fail();
+                ge.init_args.F64 = f_src;
+                ge.init_args.Psrc = p_src;
+                cudaKernelNodeParams kp = {};
+                void* kargs[] = {&ge.init_args};
+                kp.func = (void*)k_init_inputs;
+                kp.gridDim = dim3(ge.init_grid);
+                kp.blockDim = dim3(256);
+                kp.sharedMemBytes = 0;
+                kp.kernelParams = kargs;
+                MF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(ge.exec, ge.init_node, &kp));
+            }
         }
         MF_CUDA_TRY(cudaGraphLaunch(it->second.exec, stream));
         g_launches += it->second.kernels;
@@ -1235,15 +1316,16 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         res->replace = rb.take<int>((size_t)p.N0);
         res->mapping = rb.take<int>((size_t)p.N0);
     }
-    if (R > 0) {
-        if (p.Nfin) cudaMemcpyAsync(res->positions, W.Pfin, (size_t)p.Nfin * 24, cudaMemcpyDeviceToDevice, stream);
-        if (!p.alias && p.Nfin * C > 0)
-            cudaMemcpyAsync(res->features, W.Xfin, (size_t)(p.Nfin * C) * 8, cudaMemcpyDeviceToDevice, stream);
-        cudaMemcpyAsync(res->facets, W.Ffin, (size_t)p.Mcap * 12, cudaMemcpyDeviceToDevice, stream);
+    if (R > 0) {  // the result arrays out of the workspace: one launch instead of five copies
+        EmitJobs jobs;
+        if (p.Nfin) jobs.add(kEmitF64, W.Pfin, res->positions, (int64_t)p.Nfin * 3);
+        if (!p.alias && p.Nfin * C > 0) jobs.add(kEmitF64, W.Xfin, res->features, (int64_t)p.Nfin * C);
+        jobs.add(kEmitW32, W.Ffin, res->facets, (int64_t)p.Mcap * 3);
         if (n) {
-            cudaMemcpyAsync(res->replace, W.rt, (size_t)n * 4, cudaMemcpyDeviceToDevice, stream);
-            cudaMemcpyAsync(res->mapping, W.mt, (size_t)n * 4, cudaMemcpyDeviceToDevice, stream);
+            jobs.add(kEmitW32, W.rt, res->replace, n);
+            jobs.add(kEmitW32, W.mt, res->mapping, n);
         }
+        LAUNCH(k_emit, grid_for(ctx, std::max<int64_t>(1, jobs.total() / 4)), 256, 0, stream, jobs);
     } else {
         // identity (decimate.py:172-174, 367-370): inputs verbatim, replace = mapping = arange
         if (m > 0) LAUNCH(k_facets_in, grid_for(ctx, m), 256, 0, stream, m, W.F64, res->facets, B, W.vo64, W.fo64,

@@ -134,13 +134,10 @@ __global__ void k_vmesh(const int* __restrict__ abort_flag, int N, const int* __
 }
 
 // K1: facet plane (mesh.py:77-87) + incidence degrees.
-__global__ void k_facet_plane(const int* __restrict__ abort_flag, const int* __restrict__ F, const double* __restrict__ P, const int* __restrict__ dM,
-                              const int* __restrict__ vmesh, const int* __restrict__ act, Plane* __restrict__ plane,
-                              int* __restrict__ deg, int order) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
-    const int M = *dM;
-    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
+MF_DEV void facet_plane_body(int M, const int* __restrict__ F, const double* __restrict__ P,
+                             const int* __restrict__ vmesh, const int* __restrict__ act, Plane* __restrict__ plane,
+                             int* __restrict__ deg, int order, int tid, int nth) {
+    for (int f = tid; f < M; f += nth) {
         int ia = F[3 * f], ib = F[3 * f + 1], ic = F[3 * f + 2];
         if (!act[mesh_of(vmesh, ia)]) continue;
         double x0 = P[3 * ia], y0 = P[3 * ia + 1], z0 = P[3 * ia + 2];
@@ -162,6 +159,14 @@ __global__ void k_facet_plane(const int* __restrict__ abort_flag, const int* __r
         atomicAdd(deg + ib, 1);
         atomicAdd(deg + ic, 1);
     }
+}
+__global__ void k_facet_plane(const int* __restrict__ abort_flag, const int* __restrict__ F, const double* __restrict__ P, const int* __restrict__ dM,
+                              const int* __restrict__ vmesh, const int* __restrict__ act, Plane* __restrict__ plane,
+                              int* __restrict__ deg, int order) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    facet_plane_body(*dM, F, P, vmesh, act, plane, deg, order, blockIdx.x * blockDim.x + threadIdx.x,
+                     gridDim.x * blockDim.x);
 }
 
 // K2: corner-major incidence scatter; key k = corner*Mcap + f keeps the
@@ -2523,9 +2528,17 @@ __global__ void k_relabel3(int N, const int* __restrict__ abort_flag, const int*
                            const int* __restrict__ minrep, const int* __restrict__ outidx, int* __restrict__ rstep,
                            int* __restrict__ repv, int* __restrict__ abshead, int* __restrict__ absnext,
                            int* __restrict__ table, unsigned long long* __restrict__ tkey, int tsize, int table_init,
-                           unsigned char* __restrict__ has_live) {
+                           unsigned char* __restrict__ has_live, int* __restrict__ deg, int* __restrict__ cursor,
+                           int* __restrict__ lowfill, int n1_next) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
+    // the next round's degree / incidence cursor / lower-slot fill words (this round is past
+    // the last kernels that use them: k_facet_plane, k_inc_scatter, k_edges)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n1_next; i += gridDim.x * blockDim.x) {
+        deg[i] = 0;
+        cursor[i] = 0;
+        lowfill[i] = 0;
+    }
     // reset the facet dedupe table and the live-facet flags for k_facet_remap
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tsize; i += gridDim.x * blockDim.x) {
         table[i] = table_init;
@@ -2588,9 +2601,7 @@ __global__ void __launch_bounds__(256) k_seg_sort_heavy(const int* __restrict__ 
     }
 }
 
-// K8: contraction by member mean (decimate.py:280-283) and feature mean
-// (decimate.py:142-145): fold from +0.0 in ascending member order, then
-// divide by the count.  Inactive (bypassed) meshes copy rows verbatim.
+// Member fold of one output cluster: from +0.0 in ascending member order, then / count.
 template <int PLACEMENT>
 MF_DEV void fold_members(const int* m, int d, const double* __restrict__ P, const double* __restrict__ X, int C,
                          const double* __restrict__ vq, int r, double* __restrict__ Pout, double* __restrict__ Xout) {
@@ -2626,11 +2637,56 @@ MF_DEV void fold_members(const int* m, int d, const double* __restrict__ P, cons
     }
 }
 
+
 // K8: contraction by member mean (decimate.py:280-283) and feature mean
 // (decimate.py:142-145): members = anchor, its matched partner and the
 // vertices absorbed into it, folded from +0.0 in ascending order, then / count.
-// Inactive (bypassed) meshes copy rows verbatim; clusters of more than
-// kSmallDeg members go to the block tier.
+// Inactive (bypassed) meshes copy rows verbatim.  Clusters of <= 4 members (nearly all: a
+// pair plus a few absorbed vertices) are sorted and folded in registers; up to kSmallDeg in a
+// local array; larger ones are listed and folded by the LAST block of the grid (block sort over
+// scratch), so the rare heavy tier costs no extra launch.
+template <int PLACEMENT>
+MF_DEV void fold_members4(int m0, int m1, int m2, int m3, int d, const double* __restrict__ P,
+                          const double* __restrict__ X, int C, const double* __restrict__ vq, int r,
+                          double* __restrict__ Pout, double* __restrict__ Xout) {
+    const int m[4] = {m0, m1, m2, m3};
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+        if (i < d) {
+            sx = sx + P[3 * m[i]];
+            sy = sy + P[3 * m[i] + 1];
+            sz = sz + P[3 * m[i] + 2];
+        }
+    const double cnt = (double)d;
+    double avg[3] = {sx / cnt, sy / cnt, sz / cnt};
+    if (PLACEMENT) {
+        double acc[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            if (i < d) {
+                const double* q = vq + 10 * (size_t)m[i];
+#pragma unroll
+                for (int k = 0; k < 10; k++) acc[k] = acc[k] + q[k];
+            }
+        double t[3];
+        mf_optimal_position(acc, acc + 6, avg, t);
+        avg[0] = t[0]; avg[1] = t[1]; avg[2] = t[2];
+    }
+    Pout[3 * r] = avg[0];
+    Pout[3 * r + 1] = avg[1];
+    Pout[3 * r + 2] = avg[2];
+    if (X) {
+        for (int k = 0; k < C; k++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                if (i < d) acc = acc + X[(size_t)m[i] * C + k];
+            Xout[(size_t)r * C + k] = acc / cnt;
+        }
+    }
+}
+
 template <int PLACEMENT>
 __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const int* __restrict__ repv,
                            const int* __restrict__ mate, const int* __restrict__ pairlo, const int* __restrict__ e1,
@@ -2638,8 +2694,11 @@ __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const i
                            const int* __restrict__ absnext, const int* __restrict__ vmesh,
                            const int* __restrict__ act, const double* __restrict__ P, const double* __restrict__ X,
                            int C, double* __restrict__ Pout, double* __restrict__ Xout,
-                           const double* __restrict__ vq, int* __restrict__ heavy, int* __restrict__ heavy_count) {
+                           const double* __restrict__ vq, int* __restrict__ heavy, int* __restrict__ heavy_count,
+                           int* __restrict__ scratch, int* __restrict__ tmp, int* __restrict__ scratch_used,
+                           int* __restrict__ done_blocks) {
     MF_PDL_ENTRY;
+    __shared__ int s_last;
     if (*abort_flag) return;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < Nout; r += gridDim.x * blockDim.x) {
         const int v0 = repv[r];
@@ -2652,17 +2711,44 @@ __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const i
             continue;
         }
         const int anc = cluster_anchor(v0, pairlo, absorbed);
+        const int me = mate[anc];
+        int a = anc, b = INT_MAX, c = INT_MAX, e = INT_MAX;
+        int d = 1;
+        if (me >= 0) b = e1[me], d = 2;
+        int x = abshead[anc];
+        if (x >= 0) {
+            if (d == 1) b = x; else c = x;
+            d++;
+            x = absnext[x];
+            while (x >= 0 && d < 4) {
+                if (d == 2) c = x; else e = x;
+                d++;
+                x = absnext[x];
+            }
+        }
+        if (x < 0) {  // at most 4 members: sorting network + register fold
+            int t;
+#define MF_CSWAP(p, q) if (p > q) t = p, p = q, q = t
+            MF_CSWAP(a, b);
+            MF_CSWAP(c, e);
+            MF_CSWAP(a, c);
+            MF_CSWAP(b, e);
+            MF_CSWAP(b, c);
+#undef MF_CSWAP
+            fold_members4<PLACEMENT>(a, b, c, e, d, P, X, C, vq, r, Pout, Xout);
+            continue;
+        }
         int m[kSmallDeg];
-        int d = 0;
+        d = 0;
         m[d++] = anc;
-        if (mate[anc] >= 0) m[d++] = e1[mate[anc]];
+        if (me >= 0) m[d++] = e1[me];
         bool big = false;
-        for (int a = abshead[anc]; a >= 0; a = absnext[a]) {
+        for (int y = abshead[anc]; y >= 0; y = absnext[y]) {
             if (d == kSmallDeg) {
                 big = true;
                 break;
             }
-            m[d++] = a;
+            m[d++] = y;
         }
         if (big) {
             heavy[atomicAdd(heavy_count, 1)] = r;
@@ -2671,49 +2757,37 @@ __global__ void k_contract(int Nout, const int* __restrict__ abort_flag, const i
         isort<kSmallDeg>(m, d);
         fold_members<PLACEMENT>(m, d, P, X, C, vq, r, Pout, Xout);
     }
-}
-
-// block tier: collect the member list into scratch, sort it, fold on thread 0
-__global__ void __launch_bounds__(256) k_contract_heavy(const int* __restrict__ abort_flag,
-                                                        const int* __restrict__ heavy,
-                                                        const int* __restrict__ heavy_count,
-                                                        const int* __restrict__ repv, const int* __restrict__ mate,
-                                                        const int* __restrict__ pairlo, const int* __restrict__ e1,
-                                                        const int* __restrict__ absorbed,
-                                                        const int* __restrict__ abshead,
-                                                        const int* __restrict__ absnext, const double* __restrict__ P,
-                                                        const double* __restrict__ X, int C,
-                                                        double* __restrict__ Pout, double* __restrict__ Xout,
-                                                        const double* __restrict__ vq, int placement,
-                                                        int* __restrict__ scratch, int* __restrict__ tmp,
-                                                        int* __restrict__ scratch_used) {
-    MF_PDL_ENTRY;
+    // the last block to finish folds the listed heavy clusters (block tier)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(done_blocks, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     __shared__ int smem[kChunk];
     __shared__ int s_d, s_base;
-    if (*abort_flag) return;
-    const int H = *heavy_count;
-    for (int h = blockIdx.x; h < H; h += gridDim.x) {
+    const int H = ld_volatile(heavy_count);
+    for (int h = 0; h < H; h++) {
         const int r = heavy[h];
         const int anc = cluster_anchor(repv[r], pairlo, absorbed);
         if (threadIdx.x == 0) {  // clusters are disjoint: their member lists fit in N slots in total
             int d = 1 + (mate[anc] >= 0);
-            for (int a = abshead[anc]; a >= 0; a = absnext[a]) d++;
+            for (int y = abshead[anc]; y >= 0; y = absnext[y]) d++;
             s_d = d;
             s_base = atomicAdd(scratch_used, d);
             int* m = scratch + s_base;
             int i = 0;
             m[i++] = anc;
             if (mate[anc] >= 0) m[i++] = e1[mate[anc]];
-            for (int a = abshead[anc]; a >= 0; a = absnext[a]) m[i++] = a;
+            for (int y = abshead[anc]; y >= 0; y = absnext[y]) m[i++] = y;
         }
         __syncthreads();
         const int d = s_d;
         int* m = scratch + s_base;
         block_sort_ints(m, tmp + s_base, d, smem);
-        if (threadIdx.x == 0) {
-            if (placement) fold_members<1>(m, d, P, X, C, vq, r, Pout, Xout);
-            else fold_members<0>(m, d, P, X, C, vq, r, Pout, Xout);
-        }
+        if (threadIdx.x == 0) fold_members<PLACEMENT>(m, d, P, X, C, vq, r, Pout, Xout);
         __syncthreads();
     }
 }
@@ -2847,17 +2921,15 @@ __global__ void k_identity_index(int n, int* __restrict__ a, int* __restrict__ b
 
 // K10: chain replace / mapping across rounds (decimate.py:380-381); the
 // round's mapping (decimate.py:159-167) is formed on the fly.
-__global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int* __restrict__ rstep,
-                          const int* __restrict__ inc_off, const unsigned char* __restrict__ has_live,
-                          const int* __restrict__ vmesh, const int* __restrict__ act, int* __restrict__ rt,
-                          int* __restrict__ mt, int first_round, int B, const int* __restrict__ kout,
-                          const int* __restrict__ foff_in, int* __restrict__ foff_out, int* __restrict__ foff_fin,
-                          int* __restrict__ stats, const int* __restrict__ n_edges, const int* __restrict__ ld_rounds,
-                          int* __restrict__ deg, int* __restrict__ cursor, int* __restrict__ lowfill, int n1_next,
-                          int* __restrict__ counters) {
-    MF_PDL_ENTRY;
-    if (*abort_flag) return;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+// Round epilogue: per-mesh output facet offsets, per-round counts, the next round's counter
+// words cleared, and replace / mapping composed over the original vertices
+// (decimate.py:380-381; mapping -1 where a vertex had facets but none survived, :159-167).
+MF_DEV void compose_body(int N0, const int* __restrict__ rstep, const int* __restrict__ inc_off,
+                         const unsigned char* __restrict__ has_live, const int* __restrict__ vmesh,
+                         const int* __restrict__ act, int* __restrict__ rt, int* __restrict__ mt, int first_round, int B,
+                         const int* __restrict__ kout, const int* __restrict__ foff_in, int* __restrict__ foff_out,
+                         int* __restrict__ foff_fin, int* __restrict__ stats, const int* __restrict__ n_edges,
+                         const int* __restrict__ ld_rounds, int* __restrict__ counters, int tid, int nth) {
     // per-mesh output facet offsets = keep-scan prefix at each mesh's first input facet
     for (int b = tid; b <= B; b += nth) {
         foff_out[b] = kout[foff_in[b]];
@@ -2869,14 +2941,8 @@ __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int*
         stats[2] = kout[foff_in[B]];
         stats[3] = *ld_rounds;
     }
-    // clear the next round's degree / cursor / lower-slot fill arrays and counters
-    for (int i = tid; i < n1_next; i += nth) {
-        deg[i] = 0;
-        cursor[i] = 0;
-        lowfill[i] = 0;
-    }
     for (int i = tid; i < 64; i += nth) counters[i] = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N0; i += gridDim.x * blockDim.x) {
+    for (int i = tid; i < N0; i += nth) {
         int r = first_round ? i : rt[i];
         rt[i] = rstep[r];
         int m = first_round ? i : mt[i];
@@ -2888,6 +2954,37 @@ __global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int*
         if (act[mesh_of(vmesh, m)] && inc_off[m + 1] > inc_off[m] && !has_live[m]) ms = -1;
         mt[i] = ms;
     }
+}
+__global__ void k_compose(int N0, const int* __restrict__ abort_flag, const int* __restrict__ rstep,
+                          const int* __restrict__ inc_off, const unsigned char* __restrict__ has_live,
+                          const int* __restrict__ vmesh, const int* __restrict__ act, int* __restrict__ rt,
+                          int* __restrict__ mt, int first_round, int B, const int* __restrict__ kout,
+                          const int* __restrict__ foff_in, int* __restrict__ foff_out, int* __restrict__ foff_fin,
+                          int* __restrict__ stats, const int* __restrict__ n_edges, const int* __restrict__ ld_rounds,
+                          int* __restrict__ counters) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    compose_body(N0, rstep, inc_off, has_live, vmesh, act, rt, mt, first_round, B, kout, foff_in, foff_out, foff_fin,
+                 stats, n_edges, ld_rounds, counters, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+// One mesh, not its last round: the round epilogue fused with the NEXT round's facet planes
+// (independent work -- the planes read this round's output facets / positions; the facet
+// count is this round's keep-scan total).  Saves a kernel boundary per round.
+__global__ void k_compose_plane(int N0, const int* __restrict__ abort_flag, const int* __restrict__ rstep,
+                                const int* __restrict__ inc_off, const unsigned char* __restrict__ has_live,
+                                const int* __restrict__ act, int* __restrict__ rt, int* __restrict__ mt,
+                                int first_round, const int* __restrict__ kout, const int* __restrict__ foff_in,
+                                int* __restrict__ foff_out, int* __restrict__ stats, const int* __restrict__ n_edges,
+                                const int* __restrict__ ld_rounds, int* __restrict__ counters,
+                                const int* __restrict__ Fn, const double* __restrict__ Pn,
+                                const int* __restrict__ act_next, Plane* __restrict__ plane, int* __restrict__ deg,
+                                int order) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    facet_plane_body(kout[foff_in[1]], Fn, Pn, nullptr, act_next, plane, deg, order, tid, nth);
+    compose_body(N0, rstep, inc_off, has_live, nullptr, act, rt, mt, first_round, 1, kout, foff_in, foff_out, nullptr,
+                 stats, n_edges, ld_rounds, counters, tid, nth);
 }
 
 // ------------------------------------------------------------------------
@@ -2916,6 +3013,76 @@ __global__ void k_graph_init(int* __restrict__ status, int status_words, int fai
     }
     // selection scratch: histogram + OR words zero, AND words all-ones (see kSelScratch)
     for (int i = tid; i < nghist; i += nth) ghist[i] = (i >= kSelBins + 4 && i < kSelBins + 8) ? -1 : 0;
+}
+
+// Start of every round chain, one launch: the workspace clears k_graph_init did (the status
+// words now arrive pre-initialised with the params upload) fused with the input conversion of
+// k_inputs_in -- facets int64 -> int32 with range / repeat validation, positions checked for
+// NaN / inf and copied into the workspace.  The input pointers are per call: the captured graph
+// node's arguments are updated on replay (device inputs are read in place, no staging copy).
+struct InitArgs {
+    int* foff_a;
+    const int* foff0;
+    int B;
+    int* deg;
+    int* cursor;
+    int* lowfill;
+    int n1;
+    int* counters;
+    unsigned long long* scan_a;
+    unsigned long long* scan_b;
+    int scan_words;
+    int* ghist;
+    int nghist;
+    int64_t M;
+    const int64_t* F64;
+    int* F32;
+    const int64_t* voff;
+    const int64_t* foff;
+    int* badf;
+    int64_t n3;
+    const double* Psrc;
+    double* P0;
+    int* badp;
+};
+__global__ void k_init_inputs(InitArgs a) {
+    MF_PDL_ENTRY;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int b = tid; b <= a.B; b += nth) a.foff_a[b] = a.foff0[b];
+    for (int i = tid; i < a.n1; i += nth) {
+        a.deg[i] = 0;
+        a.cursor[i] = 0;
+        a.lowfill[i] = 0;
+    }
+    for (int i = tid; i < 64; i += nth) a.counters[i] = 0;
+    for (int i = tid; i < a.scan_words; i += nth) {
+        a.scan_a[i] = 0ull;
+        a.scan_b[i] = 0ull;
+    }
+    // selection scratch: histogram + OR words zero, AND words all-ones (see kSelScratch)
+    for (int i = tid; i < a.nghist; i += nth) a.ghist[i] = (i >= kSelBins + 4 && i < kSelBins + 8) ? -1 : 0;
+    const bool copy_p = a.Psrc != a.P0;
+    const int64_t T = a.M > a.n3 ? a.M : a.n3;
+    for (int64_t f = tid; f < T; f += nth) {
+        if (f < a.n3) {
+            const double x = a.Psrc[f];
+            if (!isfinite(x)) atomicExch(a.badp, 1);
+            if (copy_p) a.P0[f] = x;
+        }
+        if (f >= a.M) continue;
+        int lo = 0, hi = a.B;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (a.foff[mid] <= f) lo = mid; else hi = mid;
+        }
+        const int64_t vlo = a.voff[lo], vhi = a.voff[lo + 1];
+        const int64_t x = a.F64[3 * f], y = a.F64[3 * f + 1], z = a.F64[3 * f + 2];
+        const bool ok = x >= vlo && x < vhi && y >= vlo && y < vhi && z >= vlo && z < vhi && x != y && y != z && x != z;
+        if (!ok) atomicMin(a.badf, (int)min(f, (int64_t)0x7ffffffe));
+        a.F32[3 * f] = (int)x;
+        a.F32[3 * f + 1] = (int)y;
+        a.F32[3 * f + 2] = (int)z;
+    }
 }
 
 // ------------------------------------------------------------------------
@@ -2984,7 +3151,7 @@ __global__ void k_words_differ(int64_t n, const unsigned long long* __restrict__
 }
 // Fused result emission (mf_decimation_copy): up to 8 jobs, each widening int32 -> int64,
 // copying float64, or narrowing float64 -> float32 into a device-writable destination.
-constexpr int kEmitI32 = 0, kEmitF64 = 1, kEmitF32 = 2;
+constexpr int kEmitI32 = 0, kEmitF64 = 1, kEmitF32 = 2, kEmitW32 = 3;  // W32: int32 copied as is
 struct EmitJobs {
     const void* src[8];
     void* dst[8];
@@ -3010,6 +3177,18 @@ __global__ void k_emit(EmitJobs j) {
     for (int q = 0; q < j.count; q++) {
         const int64_t n = j.n[q];
         const int k = j.kind[q];
+        if (k == kEmitW32) {
+            const int* sp = (const int*)j.src[q];
+            int* dp = (int*)j.dst[q];
+            int64_t done = 0;
+            if ((((uintptr_t)dp | (uintptr_t)sp) & 15) == 0) {  // four words per thread, 16-byte moves
+                const int64_t h = n >> 2;
+                for (int64_t i = tid; i < h; i += nth) ((int4*)dp)[i] = ((const int4*)sp)[i];
+                done = h << 2;
+            }
+            for (int64_t i = done + tid; i < n; i += nth) dp[i] = sp[i];
+            continue;
+        }
         // two elements per thread as one 16-byte store when both ends are 16-byte aligned
         if (k != kEmitF32 && (((uintptr_t)j.dst[q] | (uintptr_t)j.src[q]) & 15) == 0) {
             const int64_t h = n >> 1;

@@ -393,17 +393,8 @@ __global__ void k_seg_sort_small4(int nseg, const int* __restrict__ off, int* __
 // sort -> heavy segments, phases separated by a grid barrier (one block per SM, co-resident by
 // construction of the cooperative launch).  Replaces five launches + a look-back scan whose
 // fixed latencies dominated at pooling sizes (cfg3: ~107 us of CSR build per step).
-MF_DEV unsigned ld_volatile_u32(const unsigned* p) { return *(const volatile unsigned*)p; }
-MF_DEV void coop_bar(unsigned* bar, unsigned target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
-        while (ld_volatile_u32(bar) < target) __nanosleep(32);
-        __threadfence();
-    }
-    __syncthreads();
-}
+// grid barrier of the cooperative launch (cooperative_groups grid sync)
+MF_DEV void coop_bar(unsigned*, unsigned) { cooperative_groups::this_grid().sync(); }
 
 __global__ void __launch_bounds__(1024) k_csr_coop(int n, int n_out, const int* __restrict__ key, int* __restrict__ cnt,
                                                    int* __restrict__ off, int* __restrict__ members,
@@ -495,7 +486,7 @@ static bool csr_coop_ok(const Context* ctx) {
         if (v && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_coop, 1024, 0) != cudaSuccess || occ < 1))
             v = 0;
         cudaGetLastError();
-        g_csr_blocks_per_sm = std::max(1, std::min(occ, 2));
+        g_csr_blocks_per_sm = 1;  // one block per SM: fewest barrier arrivals
     }
     (void)ctx;
     return v == 1;
