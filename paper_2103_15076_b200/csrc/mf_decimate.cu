@@ -929,6 +929,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
 // graph cache (per context): key = every host value baked into the sequence
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;  // kept alive: node updates address its nodes
     std::vector<ProfRec> prof;
     int64_t kernels = 0;  // kernel nodes (launch accounting on replay)
     cudaGraphNode_t init_node = nullptr;  // k_init_inputs (its input pointers change per call)
@@ -942,8 +943,10 @@ struct GraphCache {
     cudaStream_t body[2] = {nullptr, nullptr};  // conditional-node body captures
     ~GraphCache() { clear(); }
     void clear() {
-        for (auto& kv : entries)
+        for (auto& kv : entries) {
             if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+            if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+        }
         entries.clear();
     }
 };
@@ -1251,8 +1254,9 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             MF_CUDA_TRY(ce);
             GraphEntry e;
             cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
-            cudaGraphDestroy(g);
+            if (ie != cudaSuccess) cudaGraphDestroy(g);
             MF_CUDA_TRY(ie);
+            e.graph = g;
             e.prof.assign(g_prof_recs.begin() + rec0, g_prof_recs.end());
             e.kernels = nk;
             e.init_node = g_init_node;
