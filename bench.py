@@ -581,6 +581,10 @@ def run_ours(args):
 
 
 def main():
+    import faulthandler
+
+    # a stuck call prints every thread's Python stack and ends the run instead of hanging it
+    faulthandler.dump_traceback_later(int(os.environ.get("MF_BENCH_WATCHDOG_S", "900")), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)

@@ -200,6 +200,20 @@ static bool use_cond() {
     return v == 1;
 }
 
+// MF_VERTEX_SCAN=0: k_vertex_t + k_vertex_tiers + the offset scans instead of k_vertex_scan (A/B)
+static int vertex_scan() {
+    static int v = -1;
+    if (v < 0) {
+        // 0 off (default), 1 = 128 threads per 128-vertex tile, 2 = 256.  Measured (B200, r2i): cfg2
+        // 0.501 / 0.518 / 0.504 ms, cfg5 11.98 / 13.07 / 13.35 ms -- the tile's mid-degree vertices
+        // serialise on the block's few warps, which costs more than the two launches it saves
+        const char* e = getenv("MF_VERTEX_SCAN");
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v > 2) v = 0;
+    }
+    return v;
+}
+
 // MF_FUSE_PLANE=0: separate k_compose / k_facet_plane launches between rounds (A/B runs)
 static bool fuse_plane() {
     static int v = -1;
@@ -467,6 +481,8 @@ struct WS {
     int* table;
     unsigned long long* tkey;
     ScanBuf scan;
+    unsigned long long* vs;  // k_vertex_scan look-back buffers (two, alternating by round)
+    int vs_words;
     int* status;  // [8] flags | foff_final[B+1] | fail[3B] | stats[4R]
     size_t status_words, params_pad, status_pad, upload_bytes;
 };
@@ -604,6 +620,8 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.scan.buf[0] = A.take<unsigned long long>((size_t)W.scan.words);
     W.scan.buf[1] = A.take<unsigned long long>((size_t)W.scan.words);
     W.scan.cur = 0;
+    W.vs_words = (N0 + kVsTile - 1) / kVsTile + 8;  // per buffer: tile words + ticket
+    W.vs = A.take<unsigned long long>((size_t)2 * W.vs_words);
 }
 
 // ------------------------------------------------------------------------
@@ -694,9 +712,13 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // device buffers or the host staging) are patched into this node on every replay
         InitArgs ia{W.foff_a, d_foff0, B, W.deg, W.cursor, W.lowfill, N0 + 1, W.counters, W.scan.buf[0],
                     W.scan.buf[1], W.scan.words, W.ghist, kSelScratch, m, g_in_F64 ? g_in_F64 : W.F64, W.F0, W.vo64,
-                    W.fo64, d_badf, 3 * n, g_in_P ? g_in_P : W.P0, W.P0, d_badp};
+                    W.fo64, d_badf, 3 * n, g_in_P ? g_in_P : W.P0, W.P0, d_badp, W.vs, 2 * W.vs_words};
         const int grid = grid_for(ctx, std::max<int64_t>({(int64_t)N0 + 1, (int64_t)W.scan.words, m, 3 * n}));
-        LAUNCH(k_init_inputs, grid, 256, 0, stream, ia);
+        // launched by hand (not LAUNCH): its graph node is read back right after the launch,
+        // before a profiling event node can follow it
+        prof_pre("k_init_inputs", stream);
+        rec_check(launch_ex(k_init_inputs, dim3(grid), dim3(256), 0, stream, ia), __LINE__);
+        g_launches++;
         g_init_args = ia;
         g_init_grid = grid;
         g_init_node = nullptr;
@@ -704,9 +726,12 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const cudaGraphNode_t* deps = nullptr;
         size_t nd = 0;
         if (cudaStreamGetCaptureInfo(stream, &cs, nullptr, nullptr, &deps, &nd) == cudaSuccess &&
-            cs == cudaStreamCaptureStatusActive && nd == 1)
-            g_init_node = deps[0];
+            cs == cudaStreamCaptureStatusActive && nd == 1) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(deps[0], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) g_init_node = deps[0];
+        }
         cudaGetLastError();
+        prof_post("k_init_inputs", stream);
     }
     if (W.Xf32 && n * C > 0) LAUNCH(k_f32_to_f64, grid_for(ctx, n * C), 256, 0, stream, n * C, W.Xf32, W.X0);
 
@@ -746,16 +771,28 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", d_abort);
         LAUNCH(k_inc_scatter, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, dM, Mcap, vmesh, act, W.inc_off, W.cursor,
                W.inc);
-        // vertex quadrics + unique neighbour lists
-        LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap,
-               W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
-        LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, d_abort, W.mid, d_mid_n, W.heavy, d_heavy_n,
-               W.inc_off, W.inc, W.inc_tmp, Fc, W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
-        // lexicographic edges + pair costs + rank keys
-        // compact adjacency offsets (2 slots per edge); seeded rounds also need the dense
-        // lexicographic edge index (the PCG64 key-stream position, decimate.py:190)
-        run_scan(W.scan, LoadArr{W.ucnt}, W.aoff, N, stream, "k_scan<adj>", d_abort);
-        if (seeded) run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
+        // vertex quadrics + unique neighbour lists (+ the adjacency / edge offset scans)
+        if (vertex_scan()) {
+            unsigned long long* vs_cur = W.vs + (size_t)(r & 1) * W.vs_words;
+            unsigned long long* vs_nxt = W.vs + (size_t)((r + 1) & 1) * W.vs_words;
+            const int tiles = (N + kVsTile - 1) / kVsTile;
+            VertexScanArgs va{d_abort, N, W.inc_off, W.inc, W.inc_tmp, Fc, W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp,
+                              W.ucnt, W.upcnt, W.aoff, seeded ? W.eoff : nullptr, vs_cur,
+                              reinterpret_cast<int*>(vs_cur + W.vs_words - 4), last ? nullptr : vs_nxt,
+                              last ? 0 : W.vs_words};
+            const int vg = std::max(1, std::min(tiles, ctx->sm_count * 16));
+            if (vertex_scan() == 2) LAUNCH(k_vertex_scan<256>, vg, 256, 0, stream, va);
+            else LAUNCH(k_vertex_scan<128>, vg, 128, 0, stream, va);
+        } else {
+            LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap,
+                   W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
+            LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, d_abort, W.mid, d_mid_n, W.heavy, d_heavy_n,
+                   W.inc_off, W.inc, W.inc_tmp, Fc, W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
+            // compact adjacency offsets (2 slots per edge); seeded rounds also need the dense
+            // lexicographic edge index (the PCG64 key-stream position, decimate.py:190)
+            run_scan(W.scan, LoadArr{W.ucnt}, W.aoff, N, stream, "k_scan<adj>", d_abort);
+            if (seeded) run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
+        }
         {
             // unseeded: the unsorted slots are written straight into e1 / key_hi (+ seid_u), and
             // k_adj_rank_tiled sorts them out of place into snbr / adj_eid / adj_k32
@@ -968,7 +1005,7 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(),
+                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);

@@ -880,6 +880,328 @@ __global__ void __launch_bounds__(256) k_vertex_tiers(const int* __restrict__ ab
 }
 
 // ------------------------------------------------------------------------
+// K3 fused: every tier of the vertex fold + the adjacency-offset scans in ONE launch.
+// A block owns a tile of 128 consecutive vertices (tickets in launch order): thread tier
+// (deg <= 8) as k_vertex_t; the tile's degree 9..32 vertices one warp each (mid body), any
+// larger one by the whole block (heavy body); then the tile's ucnt / upcnt totals are chained
+// through a decoupled look-back (one 64-bit word carries both sums) and the block writes the
+// compact adjacency offsets aoff (and the dense lexicographic edge offsets eoff) itself --
+// replacing k_vertex_tiers and the k_scan<adj> (+ k_scan<edges>) launches.
+constexpr unsigned long long kVsAgg = 1ull << 62, kVsPre = 2ull << 62;
+constexpr int kVsTile = 128;
+MF_DEV unsigned long long vs_pack(int u, int up) { return ((unsigned long long)(unsigned)u << 31) | (unsigned)up; }
+MF_DEV int vs_u(unsigned long long w) { return (int)((w >> 31) & 0x7fffffffull); }
+MF_DEV int vs_up(unsigned long long w) { return (int)(w & 0x7fffffffull); }
+
+// one degree-9..32 vertex by warp g of the block (vertex_mid_body's per-vertex step); the
+// unique neighbour list goes to `out`, the counts to ucnt / upcnt
+MF_DEV void vertex_mid_one(int v, int s, int d, const int* __restrict__ inc, const int* __restrict__ F,
+                           const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq, int* out,
+                           int* __restrict__ ucnt, int* __restrict__ upcnt, double (*s_q)[10], int* s_c) {
+    const int l = threadIdx.x & 31;
+    const unsigned mask = 0xffffffffu;
+    int k = (l < d) ? inc[s + l] : 0x7fffffff;
+#pragma unroll
+    for (int kk = 2; kk <= kMid; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            int y = __shfl_xor_sync(mask, k, j);
+            bool up = ((l & kk) == 0), lower = ((l & j) == 0);
+            k = (lower == up) ? min(k, y) : max(k, y);
+        }
+    }
+    int a = 0x7fffffff, b = 0x7fffffff;
+    if (l < d) {
+        int corner, f;
+        decode_inc(k, Mcap, corner, f);
+        Plane p = plane[f];
+        other_two(F, f, corner, a, b);
+        double* q = s_q[l];
+        q[0] = p.n0 * p.n0; q[1] = p.n0 * p.n1; q[2] = p.n0 * p.n2;
+        q[3] = p.n1 * p.n1; q[4] = p.n1 * p.n2; q[5] = p.n2 * p.n2;
+        q[6] = p.d * p.n0; q[7] = p.d * p.n1; q[8] = p.d * p.n2;
+        q[9] = p.d * p.d;
+    }
+    s_c[2 * l] = a;
+    s_c[2 * l + 1] = b;
+    __syncwarp(mask);
+    if (l < 10) {  // quadrics.py:72-76: fold each component in incidence order from +0.0
+        double acc = 0.0;
+        for (int i = 0; i < d; i++) acc = acc + s_q[i][l];
+        vq[10 * (size_t)v + l] = acc;
+    }
+    for (int kk = 2; kk <= 2 * kMid; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            int i = ((l & ~(j - 1)) << 1) | (l & (j - 1));
+            int x = s_c[i], y = s_c[i + j];
+            bool up = ((i & kk) == 0);
+            if ((x > y) == up) { s_c[i] = y; s_c[i + j] = x; }
+            __syncwarp(mask);
+        }
+    }
+    int x0 = s_c[2 * l], x1 = s_c[2 * l + 1];
+    int prev = (l == 0) ? -1 : s_c[2 * l - 1];
+    bool k0 = (2 * l < 2 * d) && x0 != prev;
+    bool k1 = (2 * l + 1 < 2 * d) && x1 != x0;
+    unsigned b0 = __ballot_sync(mask, k0), b1 = __ballot_sync(mask, k1);
+    unsigned u0 = __ballot_sync(mask, k0 && x0 > v), u1 = __ballot_sync(mask, k1 && x1 > v);
+    unsigned below = (1u << l) - 1u;
+    int pos = __popc(b0 & below) + __popc(b1 & below);
+    if (k0) out[pos++] = x0;
+    if (k1) out[pos] = x1;
+    if (l == 0) {
+        ucnt[v] = __popc(b0) + __popc(b1);
+        upcnt[v] = __popc(u0) + __popc(u1);
+    }
+    __syncwarp(mask);
+}
+
+// one vertex of any degree by the whole block (vertex_heavy_body's per-vertex step): the
+// incidences sorted in place, the fold staged kVsTile planes at a time, the neighbour
+// candidates sorted / de-duplicated in nbr (scratch nbr_tmp)
+MF_DEV void vertex_heavy_one(int v, int s, int d, int* __restrict__ inc, int* __restrict__ inc_tmp,
+                             const int* __restrict__ F, const Plane* __restrict__ plane, int Mcap,
+                             double* __restrict__ vq, int* __restrict__ nbr, int* __restrict__ nbr_tmp,
+                             int* __restrict__ ucnt, int* __restrict__ upcnt, int* smem, Plane* s_pl, int* s_scan) {
+    block_sort_ints(inc + s, inc_tmp + s, d, smem);
+    Q10 q;
+    q_zero(q);
+    for (int c0 = 0; c0 < d; c0 += kVsTile) {
+        const int len = min(kVsTile, d - c0);
+        for (int i = threadIdx.x; i < len; i += blockDim.x) {
+            int corner, f;
+            decode_inc(inc[s + c0 + i], Mcap, corner, f);
+            s_pl[i] = plane[f];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < len; i++) q_add_plane(q, s_pl[i]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) q_store(vq, v, q);
+    int* cand = nbr + 2 * (size_t)s;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        int corner, f, a, b;
+        decode_inc(inc[s + i], Mcap, corner, f);
+        other_two(F, f, corner, a, b);
+        cand[2 * i] = a;
+        cand[2 * i + 1] = b;
+    }
+    __syncthreads();
+    block_sort_ints(cand, nbr_tmp + 2 * (size_t)s, 2 * d, smem);
+    int* tmpo = nbr_tmp + 2 * (size_t)s;
+    int base = 0, nup = 0;
+    for (int c0 = 0; c0 < 2 * d; c0 += blockDim.x) {
+        int i = c0 + threadIdx.x;
+        int keep = 0, x = 0;
+        if (i < 2 * d) {
+            x = cand[i];
+            keep = (i == 0) || (x != cand[i - 1]);
+        }
+        int tot;
+        int pos = block_excl_scan(keep, s_scan, &tot);
+        if (keep) tmpo[base + pos] = x;
+        int upk = keep && x > v;
+        int totu;
+        block_excl_scan(upk, s_scan, &totu);
+        base += tot;
+        nup += totu;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < base; i += blockDim.x) cand[i] = tmpo[i];
+    if (threadIdx.x == 0) {
+        ucnt[v] = base;
+        upcnt[v] = nup;
+    }
+    __syncthreads();
+}
+
+struct VertexScanArgs {
+    const int* abort_flag;
+    int N;
+    const int* inc_off;
+    int* inc;
+    int* inc_tmp;
+    const int* F;
+    const Plane* plane;
+    int Mcap;
+    double* vq;
+    int* nbr;
+    int* nbr_tmp;
+    int* ucnt;
+    int* upcnt;
+    int* aoff;  // compact adjacency offsets (exclusive scan of ucnt), [N+1]
+    int* eoff;  // dense edge offsets (exclusive scan of upcnt), [N+1]
+    unsigned long long* state;  // look-back words, zero on entry; the ticket follows them
+    int* ticket;
+    unsigned long long* clear;  // the other round's look-back buffer, cleared here for the next round
+    int clear_words;
+};
+
+// THREADS = 128 or 256 per block for a tile of 128 vertices: the extra warps only share the
+// tile's mid-degree vertices (one warp each) and the heavy / scan / write-out phases.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_vertex_scan(VertexScanArgs a) {
+    MF_PDL_ENTRY;
+    __shared__ int s_nb[kVtStage];
+    __shared__ union {
+        struct {
+            double q[THREADS / 32][kMid][10];
+            int c[THREADS / 32][2 * kMid];
+        } mid;
+        struct {
+            int sort[kChunk];
+            Plane pl[kVsTile];
+        } heavy;
+    } sc;
+    __shared__ int s_list[kVsTile];
+    __shared__ int s_nmid, s_nheavy, s_tile;
+    __shared__ int s_scan[33];
+    __shared__ int s_pre[2];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.clear_words; i += gridDim.x * blockDim.x)
+        a.clear[i] = 0ull;
+    if (*a.abort_flag) return;
+    const int N = a.N;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    while (true) {
+        if (tid == 0) {
+            s_tile = atomicAdd(a.ticket, 1);
+            s_nmid = 0;
+            s_nheavy = 0;
+        }
+        __syncthreads();
+        const int tile = s_tile;
+        const int base = tile * kVsTile;
+        if (base >= N) break;
+        const int v = base + tid;
+        const bool mine = tid < kVsTile && v < N;  // the thread-tier owner of vertex v
+        const int r0 = a.inc_off[base], r1 = a.inc_off[min(N, base + kVsTile)];
+        const bool staged = 2 * (r1 - r0) <= kVtStage;  // block-uniform
+        int s = 0, d = 0, nu = 0, nup = 0;
+        if (mine) {
+            s = a.inc_off[v];
+            d = a.inc_off[v + 1] - s;
+            if (d > kThreadDeg) {
+                if (d <= kMid) s_list[atomicAdd(&s_nmid, 1)] = v;
+                else s_list[kVsTile - 1 - atomicAdd(&s_nheavy, 1)] = v;
+            } else {
+                int k[kThreadDeg];
+#pragma unroll
+                for (int i = 0; i < kThreadDeg; i++) k[i] = (i < d) ? a.inc[s + i] : 0x7fffffff;
+                reg_sort(k);
+                Q10 q;
+                q_zero(q);
+                int c[2 * kThreadDeg];
+#pragma unroll
+                for (int i = 0; i < kThreadDeg; i++) {
+                    c[2 * i] = 0x7fffffff;
+                    c[2 * i + 1] = 0x7fffffff;
+                    if (i < d) {
+                        int corner, f;
+                        decode_inc(k[i], a.Mcap, corner, f);
+                        Plane p = a.plane[f];
+                        q_add_plane(q, p);
+                        other_two(a.F, f, corner, c[2 * i], c[2 * i + 1]);
+                    }
+                }
+                q_store(a.vq, v, q);
+                reg_sort(c);
+                int* out = staged ? s_nb + 2 * (s - r0) : a.nbr + 2 * (size_t)s;
+#pragma unroll
+                for (int i = 0; i < 2 * kThreadDeg; i++) {
+                    const int x = c[i];
+                    const bool keep = (x != 0x7fffffff) && (i == 0 || x != c[i > 0 ? i - 1 : 0]);
+                    if (keep) {
+                        out[nu++] = x;
+                        nup += x > v;
+                    }
+                }
+                a.ucnt[v] = nu;
+                a.upcnt[v] = nup;
+            }
+        }
+        __syncthreads();
+        const int nmid = s_nmid, nheavy = s_nheavy;
+        for (int i = warp; i < nmid; i += THREADS / 32) {
+            const int w = s_list[i];
+            const int ws = a.inc_off[w], wd = a.inc_off[w + 1] - ws;
+            int* out = staged ? s_nb + 2 * (ws - r0) : a.nbr + 2 * (size_t)ws;
+            vertex_mid_one(w, ws, wd, a.inc, a.F, a.plane, a.Mcap, a.vq, out, a.ucnt, a.upcnt, sc.mid.q[warp],
+                           sc.mid.c[warp]);
+        }
+        __syncthreads();
+        for (int i = 0; i < nheavy; i++) {
+            const int w = s_list[kVsTile - 1 - i];
+            const int ws = a.inc_off[w], wd = a.inc_off[w + 1] - ws;
+            vertex_heavy_one(w, ws, wd, a.inc, a.inc_tmp, a.F, a.plane, a.Mcap, a.vq, a.nbr, a.nbr_tmp, a.ucnt,
+                             a.upcnt, sc.heavy.sort, sc.heavy.pl, s_scan);
+            if (staged) {  // the heavy list lives in global memory: copy it into the stage
+                const int cnt = a.ucnt[w];
+                for (int j = tid; j < cnt; j += THREADS) s_nb[2 * (ws - r0) + j] = a.nbr[2 * (size_t)ws + j];
+            }
+            __syncthreads();
+        }
+        // this tile's counts (mid / heavy ones were written by other threads of the block)
+        if (mine && d > kThreadDeg) {
+            nu = a.ucnt[v];
+            nup = a.upcnt[v];
+        }
+        int tot_u, tot_up;
+        const int ex_u = block_excl_scan(nu, s_scan, &tot_u);
+        const int ex_up = block_excl_scan(nup, s_scan, &tot_up);
+        if (warp == 0) {  // decoupled look-back over the tiles before this one
+            if (lane == 0) {
+                const unsigned long long word = (tile == 0 ? kVsPre : kVsAgg) | vs_pack(tot_u, tot_up);
+                __threadfence();
+                atomicExch(a.state + tile, word);
+            }
+            int pu = 0, pup = 0;
+            if (tile > 0) {
+                int pred = tile - 1;
+                while (true) {
+                    const int idx = pred - lane;
+                    unsigned long long w = idx >= 0 ? ld_volatile(a.state + idx) : kVsPre;
+                    while (__any_sync(0xffffffffu, (w >> 62) == 0ull))
+                        if ((w >> 62) == 0ull) w = ld_volatile(a.state + idx);
+                    const unsigned pmask = __ballot_sync(0xffffffffu, (w >> 62) == 2ull);
+                    const int first = pmask ? (__ffs(pmask) - 1) : 32;
+                    pu += warp_sum(lane <= first ? vs_u(w) : 0);
+                    pup += warp_sum(lane <= first ? vs_up(w) : 0);
+                    if (pmask) break;
+                    pred -= 32;
+                }
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(a.state + tile, kVsPre | vs_pack(pu + tot_u, pup + tot_up));
+                }
+            }
+            if (lane == 0) {
+                s_pre[0] = pu;
+                s_pre[1] = pup;
+            }
+        }
+        __syncthreads();
+        if (mine) {
+            a.aoff[v] = s_pre[0] + ex_u;
+            if (a.eoff) a.eoff[v] = s_pre[1] + ex_up;
+            if (v == N - 1) {
+                a.aoff[N] = s_pre[0] + tot_u;
+                if (a.eoff) a.eoff[N] = s_pre[1] + tot_up;
+            }
+        }
+        if (staged) {
+            int* dst = a.nbr + 2 * (size_t)r0;
+            for (int i = tid; i < 2 * (r1 - r0); i += THREADS) dst[i] = s_nb[i];
+        }
+        __syncthreads();
+    }
+    if (N == 0 && blockIdx.x == 0 && tid == 0) {
+        a.aoff[0] = 0;
+        if (a.eoff) a.eoff[0] = 0;
+    }
+}
+
+// ------------------------------------------------------------------------
 // Seeded shuffle keys (decimate.py:184-191).
 __global__ void k_cost_minmax(const int* __restrict__ abort_flag, const int* __restrict__ dE, const double* __restrict__ cost, const int* __restrict__ e0,
                               const int* __restrict__ vmesh, unsigned long long* __restrict__ mlo,
@@ -3044,6 +3366,8 @@ struct InitArgs {
     const double* Psrc;
     double* P0;
     int* badp;
+    unsigned long long* vs;  // both look-back buffers of k_vertex_scan
+    int vs_words;
 };
 __global__ void k_init_inputs(InitArgs a) {
     MF_PDL_ENTRY;
@@ -3061,6 +3385,7 @@ __global__ void k_init_inputs(InitArgs a) {
     }
     // selection scratch: histogram + OR words zero, AND words all-ones (see kSelScratch)
     for (int i = tid; i < a.nghist; i += nth) a.ghist[i] = (i >= kSelBins + 4 && i < kSelBins + 8) ? -1 : 0;
+    for (int i = tid; i < a.vs_words; i += nth) a.vs[i] = 0ull;
     const bool copy_p = a.Psrc != a.P0;
     const int64_t T = a.M > a.n3 ? a.M : a.n3;
     for (int64_t f = tid; f < T; f += nth) {
