@@ -74,7 +74,8 @@ typedef struct mf_mesh_view {
     const int64_t *facets;          /* [m,3] int64 */
     const void *features;           /* [n,c] float64/float32, or NULL = copy of positions (mesh.py:28-29) */
     int32_t features_dtype;         /* MF_DTYPE_* */
-    int32_t reserved;
+    int32_t facets_i32;             /* 1: facets is a DEVICE int32 [m,3] array (e.g. a previous result's,
+                                       mf_decimation_device_arrays) -- a decimation with >= 1 round only */
     int64_t n, m, c;
     const int64_t *vertex_offsets;  /* host [n_meshes+1], or NULL for one mesh */
     const int64_t *facet_offsets;   /* host [n_meshes+1], or NULL */
@@ -105,6 +106,12 @@ int mf_decimation_copy(const mf_decimation *res, double *positions, int64_t *fac
                        int32_t features_dtype, int64_t *replace, int64_t *mapping, int64_t *vertex_offsets,
                        int64_t *facet_offsets, void *stream, mf_status *status);
 void mf_decimation_free(mf_decimation *res);
+/* Device views of a result's mesh (valid while `res` lives): positions float64 [n_out,3],
+ * facets int32 [m_out,3]; *features_alias = 1 when the features are the positions bitwise.
+ * Feeding them back as the next call's mesh_view (facets_i32 = 1) chains a decimation
+ * hierarchy without a host round trip. */
+int mf_decimation_device_arrays(const mf_decimation *res, const double **positions, const int32_t **facets,
+                                int32_t *features_alias);
 /* Per-round counts of the call (rows of 6: N, M, E, N_out, M_out, matching iterations);
  * returns the number of rounds. */
 int32_t mf_decimation_round_stats(const mf_decimation *res, int64_t *out, int32_t cap_rounds);

@@ -26,7 +26,7 @@ class MeshView(ctypes.Structure):
         ("facets", ctypes.c_void_p),
         ("features", ctypes.c_void_p),
         ("features_dtype", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("facets_i32", ctypes.c_int32),
         ("n", ctypes.c_int64),
         ("m", ctypes.c_int64),
         ("c", ctypes.c_int64),
@@ -91,6 +91,9 @@ def lib():
         L.mf_decimation_copy.argtypes = [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(Status)]
         L.mf_decimation_copy.restype = ctypes.c_int
         L.mf_decimation_free.argtypes = [_vp]
+        L.mf_decimation_device_arrays.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                                  ctypes.POINTER(_i32)]
+        L.mf_decimation_device_arrays.restype = ctypes.c_int
         L.mf_pool.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _i32, _i64, _i32, _vp, _vp, _vp, ctypes.POINTER(Status)]
         L.mf_pool.restype = ctypes.c_int
         L.mf_pool_backward.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _i32, _vp, _i32, _i64, _i32, _vp, _vp, _i32,

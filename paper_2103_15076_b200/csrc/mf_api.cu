@@ -218,6 +218,15 @@ int mf_decimation_copy(const mf_decimation* res, double* positions, int64_t* fac
     return MF_OK;
 }
 
+int mf_decimation_device_arrays(const mf_decimation* res, const double** positions, const int32_t** facets,
+                                int32_t* features_alias) {
+    if (!res) return MF_ERR_VALUE;
+    if (positions) *positions = res->r.positions;
+    if (facets) *facets = res->r.facets;
+    if (features_alias) *features_alias = res->r.features_alias;
+    return MF_OK;
+}
+
 void mf_decimation_free(mf_decimation* res) {
     if (!res) return;
     cudaSetDevice(res->r.device);
@@ -444,9 +453,9 @@ int mf_quality_errors(mf_context* ctx, const mf_mesh_view* original, const mf_de
     mf_status local;
     mf_status* st = status ? status : &local;
     clear_status(st);
-    if (!ctx || !original) {
+    if (!ctx || !original || original->facets_i32) {
         st->code = MF_ERR_VALUE;
-        snprintf(st->message, sizeof(st->message), "context and original mesh are required");
+        snprintf(st->message, sizeof(st->message), "context and an int64-facet original mesh are required");
         return st->code;
     }
     cudaStream_t s = (cudaStream_t)stream;

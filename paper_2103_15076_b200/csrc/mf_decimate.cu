@@ -683,7 +683,8 @@ struct CondCapture {
 thread_local InitArgs g_init_args;
 thread_local int g_init_grid = 1;
 thread_local cudaGraphNode_t g_init_node = nullptr;
-thread_local const int64_t* g_in_F64 = nullptr;
+thread_local const void* g_in_F64 = nullptr;
+thread_local int g_in_f32 = 0;
 thread_local const double* g_in_P = nullptr;
 
 static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream, cudaStream_t body0 = nullptr,
@@ -711,7 +712,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // status words arrive initialised with the params upload; the input pointers (caller
         // device buffers or the host staging) are patched into this node on every replay
         InitArgs ia{W.foff_a, d_foff0, B, W.deg, W.cursor, W.lowfill, N0 + 1, W.counters, W.scan.buf[0],
-                    W.scan.buf[1], W.scan.words, W.ghist, kSelScratch, m, g_in_F64 ? g_in_F64 : W.F64, W.F0, W.vo64,
+                    W.scan.buf[1], W.scan.words, W.ghist, kSelScratch, m,
+                    g_in_F64 ? g_in_F64 : (const void*)W.F64, g_in_F64 ? g_in_f32 : 0, W.F0, W.vo64,
                     W.fo64, d_badf, 3 * n, g_in_P ? g_in_P : W.P0, W.P0, d_badp, W.vs, 2 * W.vs_words};
         const int grid = grid_for(ctx, std::max<int64_t>({(int64_t)N0 + 1, (int64_t)W.scan.words, m, 3 * n}));
         // launched by hand (not LAUNCH): its graph node is read back right after the launch,
@@ -1236,8 +1238,15 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     // re-pointed per call); host inputs are uploaded into the staging buffers it reads instead.
     MF_CUDA_TRY(cudaMemcpyAsync(W.params, hp, W.upload_bytes, cudaMemcpyHostToDevice, stream));
     const bool in_place = R > 0 && (n == 0 || is_device_ptr(P_src)) && (m == 0 || is_device_ptr(mv->facets));
+    if (mv->facets_i32 && (!in_place || R == 0)) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message),
+                 "int32 facets (facets_i32) must be device arrays of a call with at least one round");
+        return st->code;
+    }
     g_in_P = in_place && n ? (const double*)P_src : nullptr;
-    g_in_F64 = in_place && m ? mv->facets : nullptr;
+    g_in_F64 = in_place && m ? (const void*)mv->facets : nullptr;
+    g_in_f32 = mv->facets_i32 ? 1 : 0;
     if (!in_place) {
         if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, P_src, (size_t)n * 24, cudaMemcpyDefault, stream));
         if (m) MF_CUDA_TRY(cudaMemcpyAsync(W.F64, mv->facets, (size_t)m * 24, cudaMemcpyDefault, stream));
@@ -1304,11 +1313,13 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         }
         {  // point k_init_inputs at this call's inputs (device buffers in place, else the staging)
             GraphEntry& ge = it->second;
-            const int64_t* f_src = g_in_F64 ? g_in_F64 : W.F64;
+            const void* f_src = g_in_F64 ? g_in_F64 : (const void*)W.F64;
+            const int f32 = g_in_F64 ? g_in_f32 : 0;
             const double* p_src = g_in_P ? g_in_P : W.P0;
-            if (ge.init_args.F64 != f_src || ge.init_args.Psrc != p_src) {
+            if (ge.init_args.F64 != f_src || ge.init_args.Psrc != p_src || ge.init_args.f_is32 != f32) {
                 if (!ge.init_node) return rec_fail();
                 ge.init_args.F64 = f_src;
+                ge.init_args.f_is32 = f32;
                 ge.init_args.Psrc = p_src;
                 cudaKernelNodeParams kp = {};
                 void* kargs[] = {&ge.init_args};

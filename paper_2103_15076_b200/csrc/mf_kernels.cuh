@@ -3357,7 +3357,8 @@ struct InitArgs {
     int* ghist;
     int nghist;
     int64_t M;
-    const int64_t* F64;
+    const void* F64;  // int64 [M,3], or int32 when f_is32 (a previous result's device facets)
+    int f_is32;
     int* F32;
     const int64_t* voff;
     const int64_t* foff;
@@ -3401,7 +3402,14 @@ __global__ void k_init_inputs(InitArgs a) {
             if (a.foff[mid] <= f) lo = mid; else hi = mid;
         }
         const int64_t vlo = a.voff[lo], vhi = a.voff[lo + 1];
-        const int64_t x = a.F64[3 * f], y = a.F64[3 * f + 1], z = a.F64[3 * f + 2];
+        int64_t x, y, z;
+        if (a.f_is32) {
+            const int* F = (const int*)a.F64;
+            x = F[3 * f], y = F[3 * f + 1], z = F[3 * f + 2];
+        } else {
+            const int64_t* F = (const int64_t*)a.F64;
+            x = F[3 * f], y = F[3 * f + 1], z = F[3 * f + 2];
+        }
         const bool ok = x >= vlo && x < vhi && y >= vlo && y < vhi && z >= vlo && z < vhi && x != y && y != z && x != z;
         if (!ok) atomicMin(a.badf, (int)min(f, (int64_t)0x7ffffffe));
         a.F32[3 * f] = (int)x;

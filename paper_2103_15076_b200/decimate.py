@@ -11,6 +11,7 @@ every round of its chain on one device.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -122,6 +123,38 @@ def _make_config(config: DecimationConfig) -> _native.Config:
     return cfg
 
 
+# Output meshes of this package whose device copy is still alive: id(positions) -> weak refs of
+# (positions, facets, features, handle).  A later call given exactly those (read-only) arrays --
+# the next level of a hierarchy -- reads the handle's device arrays instead of uploading them.
+_CHAIN: dict = {}
+
+
+def _register_chain(pos, fac, feats, dec) -> None:
+    key = id(pos)
+
+    def _drop(_ref, key=key):
+        _CHAIN.pop(key, None)
+
+    _CHAIN[key] = (weakref.ref(pos, _drop), weakref.ref(fac), weakref.ref(feats), weakref.ref(dec))
+
+
+def _device_source(base, device):
+    """The live handle whose output arrays `base` still is (unmodified: they are read-only)."""
+    ent = _CHAIN.get(id(base.positions))
+    if ent is None:
+        return None
+    pos, fac, feats, dec = (r() for r in ent)
+    if pos is not base.positions or fac is not base.facets or feats is not base.features or dec is None:
+        return None
+    if pos.flags.writeable or fac.flags.writeable or feats.flags.writeable or dec.device != device:
+        return None
+    p, f, alias = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int32()
+    _native.lib().mf_decimation_device_arrays(dec.handle, ctypes.byref(p), ctypes.byref(f), ctypes.byref(alias))
+    if not alias.value:  # only the default features (a copy of the positions) travel implicitly
+        return None
+    return dec, p.value, f.value
+
+
 def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None) -> DecimationResult:
     """Cluster decimation to an exact vertex count (decimate.py:344-382), on the GPU.
 
@@ -144,13 +177,18 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     view.features_dtype = _native.DTYPE_F32 if (Xc is not None and Xc.dtype == np.float32) else _native.DTYPE_F64
     view.n, view.m = P.shape[0], F.shape[0]
     view.c = X.shape[1]
+    if device is None:
+        device = _native.default_device()
+    src = None
+    if config.rounds != 0 and not _all_identity(mesh, config):
+        src = _device_source(base, device)
+    if src is not None:  # the previous level's device arrays, no upload (features = positions)
+        view.positions, view.facets, view.features, view.facets_i32 = src[1], src[2] if F.size else None, None, 1
     if batched:
         vo = np.ascontiguousarray(mesh.vertex_offsets, dtype=np.int64)
         fo = np.ascontiguousarray(mesh.facet_offsets, dtype=np.int64)
         view.vertex_offsets, view.facet_offsets, view.n_meshes = vo.ctypes.data, fo.ctypes.data, len(vo) - 1
     cfg = _make_config(config)
-    if device is None:
-        device = _native.default_device()
     ctx = _native.context(device)
     handle = ctypes.c_void_p()
     st = _native.Status()
@@ -180,6 +218,11 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     _native.raise_for(st)
     rep.flags.writeable = False
     dec.replace_ref = rep  # pool/unpool reuse the device replace only for this very array
+    # the output mesh arrays are read-only views of library-owned pinned memory (np.array(x) gives a
+    # writable copy): a hierarchy's next level then reads their device copy instead of uploading
+    for a in (pos, fac, feats):
+        a.flags.writeable = False
+    _register_chain(pos, fac, feats, dec)
     out_mesh = _trusted_trimesh(pos, fac, feats)
     if batched:
         bm = BatchedMesh.__new__(BatchedMesh)

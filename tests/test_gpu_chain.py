@@ -1,0 +1,62 @@
+"""Device-resident hierarchies through the drop-in numpy API: feeding a result's mesh back in
+(the next level) reads the library's device copy instead of re-uploading it.  The chained
+levels must be bit-identical to levels computed from fresh host copies, for single meshes and
+batches, seeded or not; the output arrays are read-only (so the device copy cannot go stale),
+and a modified copy is uploaded as usual."""
+
+import numpy as np
+import pytest
+
+import paper_2103_15076_b200 as mfg
+from paper_2103_15076_b200 import decimate as D
+from paper_2103_15076_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _arrays(res):
+    base = res.mesh.mesh if isinstance(res.mesh, mfg.BatchedMesh) else res.mesh
+    return [res.replace, res.mapping, base.positions, base.facets, base.features]
+
+
+def _fresh(mesh):
+    if isinstance(mesh, mfg.BatchedMesh):
+        b = mesh.mesh
+        return mfg.BatchedMesh(mfg.TriMesh(np.array(b.positions), np.array(b.facets)), np.array(mesh.vertex_offsets),
+                               np.array(mesh.facet_offsets))
+    return mfg.TriMesh(np.array(mesh.positions), np.array(mesh.facets))
+
+
+@pytest.mark.parametrize("case", ["terrain", "grid_seeded", "batch"])
+def test_chained_levels_equal_fresh_uploads(case):
+    if case == "terrain":
+        mesh, levels, seed = S.delaunay_terrain(60_000, noise=0.02, seed=3), [20_000, 9_000, 4_000, 1_500], None
+    elif case == "grid_seeded":
+        mesh, levels, seed = S.perturbed_grid(200, None, 0.02, 1), [20_000, 10_000, 5_000], 7
+    else:
+        mesh = mfg.concat_batch([S.delaunay_terrain(3000 + 500 * b, seed=b) for b in range(5)])
+        levels, seed = [1500, 700, 300], 2
+    cur_a, cur_b = mesh, mesh
+    for t in levels:
+        cfg = mfg.DecimationConfig(target_vertices=t, shuffle_seed=seed)
+        src = D._device_source(cur_a.mesh if hasattr(cur_a, "vertex_offsets") else cur_a, 0)
+        assert (src is not None) == (cur_a is not mesh)  # every level after the first is chained
+        ra = mfg.decimate_parallel(cur_a, cfg, device=0)
+        rb = mfg.decimate_parallel(_fresh(cur_b), cfg, device=0)
+        for x, y in zip(_arrays(ra), _arrays(rb)):
+            assert x.shape == y.shape and np.array_equal(x.view(np.uint8), y.view(np.uint8))
+        cur_a, cur_b = ra.mesh, rb.mesh
+
+
+def test_outputs_are_read_only_and_copies_upload():
+    mesh = S.delaunay_terrain(20_000, noise=0.02, seed=5)
+    r1 = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=8_000), device=0)
+    for a in (r1.mesh.positions, r1.mesh.facets, r1.mesh.features, r1.replace):
+        assert not a.flags.writeable
+        with pytest.raises(ValueError):
+            a[0] = a[0]
+    moved = mfg.TriMesh(np.array(r1.mesh.positions) + 1.0, np.array(r1.mesh.facets))
+    assert D._device_source(moved, 0) is None
+    r2 = mfg.decimate_parallel(moved, mfg.DecimationConfig(target_vertices=3_000), device=0)
+    r3 = mfg.decimate_parallel(_fresh(moved), mfg.DecimationConfig(target_vertices=3_000), device=0)
+    assert np.array_equal(r2.mesh.positions, r3.mesh.positions) and np.array_equal(r2.replace, r3.replace)
