@@ -214,6 +214,16 @@ static int vertex_scan() {
     return v;
 }
 
+// MF_EDGES_RANK=0: unseeded rounds through k_edges + k_adj_rank_tiled instead of k_edges_rank
+static bool edges_rank() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_EDGES_RANK");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // MF_FUSE_PLANE=0: separate k_compose / k_facet_plane launches between rounds (A/B runs)
 static bool fuse_plane() {
     static int v = -1;
@@ -795,7 +805,21 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             run_scan(W.scan, LoadArr{W.ucnt}, W.aoff, N, stream, "k_scan<adj>", d_abort);
             if (seeded) run_scan(W.scan, LoadArr{W.upcnt}, W.eoff, N, stream, "k_scan<edges>", d_abort);
         }
-        {
+        const int ld_rounds = N >= p.ld_min ? p.ld_big : (N >= p.ld1_min ? p.ld_mid : 0);
+        const bool use_ld = ld_rounds > 0;
+        const bool fused_rank = !seeded && edges_rank();
+        if (fused_rank) {  // edges + costs + rank-ordered adjacency in one pass (k_edges_rank)
+            EdgeRankOut ro{W.e0,   W.e1,       W.key_hi, W.snbr,    W.adj_eid, W.adj_k32, W.acur,
+                           use_ld ? W.best : nullptr, W.bestu, W.mate, W.minrep, W.absorbed, W.abshead,
+                           W.suitor, W.mlo, W.mhi, W.segA, W.ldc, W.segB};
+            const int eg = grid_for(ctx, (int64_t)N * 8);
+            if (p.placement)
+                LAUNCH(k_edges_rank<1>, eg, 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.aoff, W.vq, Pc, ro,
+                       order, B);
+            else
+                LAUNCH(k_edges_rank<0>, eg, 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.aoff, W.vq, Pc, ro,
+                       order, B);
+        } else {
             // unseeded: the unsorted slots are written straight into e1 / key_hi (+ seid_u), and
             // k_adj_rank_tiled sorts them out of place into snbr / adj_eid / adj_k32
             EdgeOut eo{W.e0,      W.e1,   seeded ? W.cost : nullptr, nullptr, seeded ? W.snbr : W.e1,
@@ -816,13 +840,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_seed_keys, grid_for(ctx, (Ecap + kSeedRun - 1) / kSeedRun), 256, 0, stream, d_abort, dE, W.cost, W.e0,
                    vmesh, W.eoff, voff_r, W.mlo, W.mhi, p.pcg[0], p.pcg[1], p.pcg[2], p.pcg[3], W.key_hi, W.key_lo);
         }
-        // large meshes: locally-dominant rounds first (round 0's picks written by k_adj_rank),
-        // then Suitor proposals on the residual frontier; smaller meshes: Suitor only
-        // locally-dominant rounds: all 12 from ld_min vertices; below, from ld1_min, only round
-        // 0 (the mutual best edges, matched before the proposals start)
-        const int ld_rounds = N >= p.ld_min ? p.ld_big : (N >= p.ld1_min ? p.ld_mid : 0);
-        const bool use_ld = ld_rounds > 0;
-        if (seeded)
+        // large meshes: locally-dominant rounds first (round 0's picks written by k_adj_rank /
+        // k_edges_rank), then Suitor proposals on the residual frontier; smaller meshes: Suitor only
+        if (fused_rank) {
+        } else if (seeded)
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
                    nullptr, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         else
@@ -1007,7 +1028,7 @@ void drop_graphs(const Context* ctx) {
 static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
-                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(),
+                              g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);

@@ -590,6 +590,140 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
     }
 }
 
+// K4 fused (unseeded rounds): edges, pair costs and the RANK-ORDERED adjacency in one pass,
+// no atomics.  Every vertex evaluates all of its incident edges itself -- 8 lanes per vertex,
+// lane j owns slot j -- with the pair cost taken in (lower, upper) argument order, so both ends
+// produce the same bits; the edge id is the lower end's slot (aoff[lower] + position of the
+// upper end in the lower end's sorted neighbour list; a lower neighbour is found by a binary
+// search of its list).  A vertex of degree <= 8 then sorts its slots across the lanes by the
+// rank key (cost key, edge id) and writes them in rank order; larger degrees keep neighbour
+// order (acur = -1, scanned in full) with the argmin as the LD round-0 pick.  The lower end
+// also writes the edge arrays (e0 = owner of every slot, e1 / key_hi at the edge id).  This
+// replaces k_edges' lower-slot atomics + scattered slot writes AND the k_adj_rank_tiled pass
+// that re-read and re-sorted them; the price is evaluating each pair cost twice (FP64 is
+// idle here) and a second gather of each neighbour's quadric (L2-resident).
+struct EdgeRankOut {
+    int* e0;
+    int* e1;
+    uint64_t* key_hi;
+    int* snbr;          // rank-ordered slots: neighbour, edge id, 32-bit key prefix
+    int* adj_eid;
+    unsigned* adj_k32;
+    int* acur;
+    int* best;          // LD round-0 picks (nullptr when no LD rounds)
+    int* bestu;
+    int* mate;
+    int* minrep;
+    int* absorbed;
+    int* abshead;
+    unsigned long long* suitor;
+    unsigned long long* mlo;
+    unsigned long long* mhi;
+    int* seg_cnt;
+    int* ldc;
+    int* seg_cnt2;
+};
+
+template <int PLACEMENT>
+__global__ void __launch_bounds__(256) k_edges_rank(const int* __restrict__ abort_flag, int N,
+                                                    const int* __restrict__ inc_off, const int* __restrict__ nbr,
+                                                    const int* __restrict__ ucnt, const int* __restrict__ aoff,
+                                                    const double* __restrict__ vq, const double* __restrict__ P,
+                                                    EdgeRankOut o, int order, int B) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+        o.mlo[b] = ~0ull;
+        o.mhi[b] = 0ull;
+        o.seg_cnt[b] = 0;
+        o.seg_cnt2[b] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 8) o.ldc[threadIdx.x] = 0;
+    const int l = threadIdx.x & 7;
+    const unsigned mask = 0xFFu << (threadIdx.x & 24);
+    const int groups = gridDim.x * (blockDim.x >> 3);
+    for (int v = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); v < N; v += groups) {
+        if (l == 0) {
+            o.mate[v] = -1;
+            o.minrep[v] = v;
+            o.absorbed[v] = -1;
+            o.abshead[v] = -1;
+            o.suitor[v] = ~0ull;
+        }
+        const int nu = ucnt[v];
+        const size_t s2 = (size_t)aoff[v];
+        const size_t sn = 2 * (size_t)inc_off[v];
+        Q10 qv;
+        q_load(vq, v, qv);
+        const double px = P[3 * v], py = P[3 * v + 1], pz = P[3 * v + 2];
+        uint64_t bh = ~0ull, bl = ~0ull;  // this lane's best slot (degree > 8: argmin over its slots)
+        int bu = -1, be = -1;
+        for (int j0 = 0; j0 < nu; j0 += 8) {  // group-uniform trip count
+            const int j = j0 + l;
+            uint64_t h = ~0ull, lo = ~0ull;
+            int u = -1, e = -1;
+            if (j < nu) {
+                u = nbr[sn + j];
+                Q10 qu;
+                q_load(vq, u, qu);
+                const double ux = P[3 * u], uy = P[3 * u + 1], uz = P[3 * u + 2];
+                o.e0[s2 + j] = v;  // slot owner (read as e0 only at the lower end's slots)
+                double c;
+                if (u > v) {
+                    c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, ux, uy, uz, order);
+                    e = (int)(s2 + j);
+                } else {
+                    c = pair_cost<PLACEMENT>(qu, qv, ux, uy, uz, px, py, pz, order);
+                    const int* lu = nbr + 2 * (size_t)inc_off[u];
+                    int a = 0, z = ucnt[u];  // lower_bound of v in u's sorted neighbour list
+                    while (a < z) {
+                        const int m = (a + z) >> 1;
+                        if (lu[m] < v) a = m + 1; else z = m;
+                    }
+                    e = aoff[u] + a;
+                }
+                h = f64_key(c);
+                lo = (uint64_t)(unsigned)e;
+                if (u > v) {
+                    o.e1[e] = u;
+                    o.key_hi[e] = h;
+                }
+            }
+            if (nu <= 8) {
+                sort8_by_key(h, lo, u, e, mask);
+                if (l < nu) {
+                    o.snbr[s2 + l] = u;
+                    o.adj_eid[s2 + l] = e;
+                    o.adj_k32[s2 + l] = (unsigned)(h >> 32);
+                }
+                bh = h, bl = lo, bu = u, be = e;  // lane 0 holds the lowest-ranked slot
+            } else {
+                if (j < nu) {
+                    o.snbr[s2 + j] = u;
+                    o.adj_eid[s2 + j] = e;
+                    o.adj_k32[s2 + j] = (unsigned)(h >> 32);
+                    if (key_lt(h, lo, bh, bl)) bh = h, bl = lo, bu = u, be = e;
+                }
+            }
+        }
+        if (nu > 8) {
+#pragma unroll
+            for (int off = 4; off > 0; off >>= 1) {
+                const uint64_t ph = __shfl_xor_sync(mask, bh, off, 8), pl = __shfl_xor_sync(mask, bl, off, 8);
+                const int pu = __shfl_xor_sync(mask, bu, off, 8), pe = __shfl_xor_sync(mask, be, off, 8);
+                if (key_lt(ph, pl, bh, bl)) bh = ph, bl = pl, bu = pu, be = pe;
+            }
+        }
+        if (l == 0) {
+            o.acur[v] = nu > 8 ? -1 : 0;
+            if (o.best) {
+                o.best[v] = nu ? be : -1;
+                o.bestu[v] = nu ? bu : -1;
+            }
+        }
+    }
+}
+
 // K4b: rank-ordered adjacency.  Every vertex of degree <= 8 has its slots
 // sorted in place by the full rank key of their edge -- one thread per vertex,
 // register bitonic network on (key_hi, key_lo | edge id) -- so the matching
