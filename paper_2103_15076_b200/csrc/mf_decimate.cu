@@ -214,12 +214,15 @@ static int vertex_scan() {
     return v;
 }
 
-// MF_EDGES_RANK=0: unseeded rounds through k_edges + k_adj_rank_tiled instead of k_edges_rank
+// MF_EDGES_RANK=1: unseeded rounds through the fused k_edges_rank instead of k_edges +
+// k_adj_rank_tiled.  Opt-in: measured slower on B200 (r2n, 92 registers / 8 lanes per vertex:
+// cfg2 0.557 vs 0.501 ms, cfg5 18.4 vs 12.0 ms) -- every pair cost evaluated twice plus a
+// binary search of the lower end's list cost more latency than the atomics and the re-sort save.
 static bool edges_rank() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MF_EDGES_RANK");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = (e && e[0] == '1') ? 1 : 0;
     }
     return v == 1;
 }

@@ -625,7 +625,7 @@ struct EdgeRankOut {
 };
 
 template <int PLACEMENT>
-__global__ void __launch_bounds__(256) k_edges_rank(const int* __restrict__ abort_flag, int N,
+__global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges_rank(const int* __restrict__ abort_flag, int N,
                                                     const int* __restrict__ inc_off, const int* __restrict__ nbr,
                                                     const int* __restrict__ ucnt, const int* __restrict__ aoff,
                                                     const double* __restrict__ vq, const double* __restrict__ P,
