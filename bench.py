@@ -180,12 +180,33 @@ def kernel_bytes(name: str, r: dict, C: int = 3) -> float | None:
         "k_facet_remap": 12 * M + 4 * N + 12 * M + 16 * M + 4 * M + N,
         "k_inc_scatter": 12 * M + 4 * N + 12 * M,
         "k_compose": 8 * r.get("N0", N) + 4 * N,
+        # round 1 only: facets int64 in -> int32 out, positions in (+ copied into the workspace)
+        "k_init_inputs": (24 * M + 12 * M + 24 * N + 24 * N) if r.get("first") else 0,
+        # round epilogue + the NEXT round's facet planes (its facets are this round's outputs)
+        "k_compose_plane": 8 * r.get("N0", N) + 4 * N + 12 * Mn + 24 * Nn + 32 * Mn + 4 * Nn,
         # one per call (after its last round): replace / mapping int32 -> int64, positions and
         # facets out (features alias the positions in the bench workloads)
-        "k_emit": (12 * r.get("N0", N) * 2 + 24 * Nn + 8 * 3 * Mn + 4 * 3 * Mn + 24 * Nn) if r.get("last") else 0,
+        # after the call's last round: the result copy-out (int32 / float64 words as they are) and
+        # the caller's emission (int32 -> int64, float64) -- two launches per call
+        "k_emit": ((4 + 4 + 8 + 8) * r.get("N0", N) + 2 * (24 * Nn + 12 * Mn) + 24 * Nn + 24 * Mn + 24 * Nn)
+        if r.get("last") else 0,
     }
     v = table.get(name)
     return None if v is None else float(v)
+
+
+def call_bytes(name: str, call: dict) -> float | None:
+    """Algorithmic bytes of the pooling-side kernels per decimate call (n_in -> n_out, C channels,
+    float32): SURVEY.md §8(d) pool 4CN + 8N + 4CN', unpool 8N + 4CN' + 4CN; the cluster CSR build
+    reads replace and writes offsets + members once (counts and the in-place sort included)."""
+    name = name.split("<")[0].strip("(")
+    n, no, C = call["n_in"], call["n_out"], call.get("C", 0)
+    if not C:
+        return None
+    table = {"k_pool_vec": 4 * C * n + 8 * n + 4 * C * no, "k_pool": 4 * C * n + 8 * n + 4 * C * no,
+             "k_unpool_rows": 8 * n + 4 * C * no + 4 * C * n, "k_unpool_vec": 8 * n + 4 * C * no + 4 * C * n,
+             "k_csr_coop": 4 * n + 4 * no + 4 * n + 4 * no + 4 * n + 4 * n}
+    return table.get(name)
 
 
 def step_bytes(rounds: list, n0: int, C: int = 3) -> float:
@@ -436,13 +457,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     breakdown = _native.profile_read()
     _native.profile(0)
-    rounds = []
+    rounds, calls = [], []
     for dd in dds:
         rs = dd.round_stats()
         for i, r in enumerate(rs):
             r["N0"] = dd._dec.n_in
+            r["first"] = i == 0
             r["last"] = i == len(rs) - 1  # the call's outputs are emitted after its last round
             rounds.append(r)
+        calls.append({"n_in": dd._dec.n_in, "n_out": dd._dec.n_out, "C": wl.get("pool_channels", 0)})
     total_ms = sum(v[0] for v in breakdown.values())
     dominant = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
     # the timed region times the dominant kernel live: warm that graph variant first
@@ -526,6 +549,8 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel
     peak, peak_kind = load_peaks()
     per_round = [kernel_bytes(dominant, r) for r in rounds]
+    if any(b is None for b in per_round):  # a pooling-side kernel: its bytes follow the calls
+        per_round = [call_bytes(dominant, c) for c in calls]
     dom_ms_per_step = dom[0] / args.steps if dom[1] else None
     roof = {"kernel": dominant, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_kind}
     if dom_ms_per_step and all(b is not None for b in per_round):
@@ -544,6 +569,15 @@ def run_ours(args):
     roof["traffic"] = traffic
     whole = sum(step_bytes([r], r["N0"]) - 16.0 * r["N0"] for r in rounds) + 16.0 * n_in
     roof["step_alg_bytes"] = whole
+    if wl.get("pool_channels"):  # pool / unpool against the same peak (profiled warm-up step)
+        pr = {}
+        for fam in ("k_pool_vec", "k_unpool_rows", "k_csr_coop"):
+            ms = sum(v[0] for k, v in breakdown.items() if fam in k)
+            b = sum(call_bytes(fam, c) or 0 for c in calls)
+            if ms > 0 and b > 0:
+                pr[fam] = {"ms_per_step": ms, "alg_bytes_per_step": b, "achieved": b / (ms / 1e3) / 1e9,
+                           "frac": b / (ms / 1e3) / 1e9 / peak, "source": "CUDA events, profiled warm-up step"}
+        roof["pooling"] = pr
     roof["step_frac"] = whole / (step_ms / 1e3) / 1e9 / peak
 
     cpu = None

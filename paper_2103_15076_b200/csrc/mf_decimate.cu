@@ -227,6 +227,17 @@ static bool edges_rank() {
     return v == 1;
 }
 
+// thread tier up to degree 16 in rounds below 2^20 vertices (latency-bound: the warp tier is then
+// usually empty); MF_VT16=0 / 1 forces the degree-8 / degree-16 form
+static bool vt16(int N) {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("MF_VT16");
+        v = e ? (e[0] == '1') : -1;
+    }
+    return v == -1 ? N < (1 << 20) : v == 1;
+}
+
 // MF_FUSE_PLANE=0: separate k_compose / k_facet_plane launches between rounds (A/B runs)
 static bool fuse_plane() {
     static int v = -1;
@@ -799,8 +810,12 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             if (vertex_scan() == 2) LAUNCH(k_vertex_scan<256>, vg, 256, 0, stream, va);
             else LAUNCH(k_vertex_scan<128>, vg, 128, 0, stream, va);
         } else {
-            LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc, W.plane, Mcap,
-                   W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
+            if (vt16(N))
+                LAUNCH(k_vertex_t<16>, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc,
+                       W.plane, Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
+            else
+                LAUNCH(k_vertex_t<8>, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc,
+                       W.plane, Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
             LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, d_abort, W.mid, d_mid_n, W.heavy, d_heavy_n,
                    W.inc_off, W.inc, W.inc_tmp, Fc, W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
             // compact adjacency offsets (2 slots per edge); seeded rounds also need the dense
@@ -1032,6 +1047,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
+                              vt16(1), vt16(1 << 21),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
@@ -1134,8 +1150,8 @@ int quality_run(Context* ctx, const mf_mesh_view* mv, const int* d_off, const in
         run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", misc);
         if (m) LAUNCH(k_inc_scatter, grid_for(ctx, m), 256, 0, stream, misc, W.F0, misc + 2, Mc, (const int*)nullptr,
                       misc + 3, W.inc_off, W.cursor, W.inc);
-        LAUNCH(k_vertex_t, grid_for(ctx, N, 128), 128, 0, stream, misc, N, W.inc_off, W.inc, W.F0, W.plane, Mc, W.vq,
-               W.nbr, W.ucnt, W.upcnt, W.mid, misc + 12, W.heavy, misc + 8);
+        LAUNCH(k_vertex_t<8>, grid_for(ctx, N, 128), 128, 0, stream, misc, N, W.inc_off, W.inc, W.F0, W.plane, Mc,
+               W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, misc + 12, W.heavy, misc + 8);
         LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, misc, W.mid, misc + 12, W.heavy, misc + 8,
                W.inc_off, W.inc, W.inc_tmp, W.F0, W.plane, Mc, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
     }

@@ -180,12 +180,15 @@ __global__ void k_inc_scatter(const int* __restrict__ abort_flag, const int* __r
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M; f += gridDim.x * blockDim.x) {
         int t[3] = {F[3 * f], F[3 * f + 1], F[3 * f + 2]};
         if (!act[mesh_of(vmesh, t[0])]) continue;
+        // the three cursor atomics and offset loads are independent: all in flight before any store
+        int slot[3], base[3];
 #pragma unroll
         for (int c = 0; c < 3; c++) {
-            int v = t[c];
-            int pos = inc_off[v] + atomicAdd(cursor + v, 1);
-            inc[pos] = c * Mcap + f;
+            slot[c] = atomicAdd(cursor + t[c], 1);
+            base[c] = inc_off[t[c]];
         }
+#pragma unroll
+        for (int c = 0; c < 3; c++) inc[base[c] + slot[c]] = c * Mcap + f;
     }
 }
 
@@ -313,6 +316,51 @@ MF_DEV void reg_sort(int (&a)[L]) {
 constexpr int kThreadDeg = 8;
 constexpr int kMid = 32;
 constexpr int kVtStage = 4096;  // k_vertex_t neighbour-list stage (ints): 128 vertices of mean degree <= 16
+// One vertex of the thread tier: its DEG-padded incidence list sorted in registers (corner-major
+// key = np.add.at order), the planes folded from +0.0 in that order, the 2*DEG neighbour candidates
+// sorted and de-duplicated into `out`.  DEG = 8 for nearly all vertices; degrees 9..16 take the
+// DEG = 16 instance (a divergent branch of the same warp) instead of the warp-per-vertex tier.
+template <int DEG>
+MF_DEV void vertex_thread_tier(int v, int s, int d, const int* __restrict__ inc, const int* __restrict__ F,
+                               const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq, int* out,
+                               int* __restrict__ ucnt, int* __restrict__ upcnt) {
+    int k[DEG];
+#pragma unroll
+    for (int i = 0; i < DEG; i++) k[i] = (i < d) ? inc[s + i] : 0x7fffffff;
+    reg_sort(k);
+    Q10 q;
+    q_zero(q);
+    int c[2 * DEG];
+#pragma unroll
+    for (int i = 0; i < DEG; i++) {
+        c[2 * i] = 0x7fffffff;
+        c[2 * i + 1] = 0x7fffffff;
+        if (i < d) {
+            int corner, f;
+            decode_inc(k[i], Mcap, corner, f);
+            Plane p = plane[f];
+            q_add_plane(q, p);
+            other_two(F, f, corner, c[2 * i], c[2 * i + 1]);
+        }
+    }
+    q_store(vq, v, q);
+    reg_sort(c);
+    int nu = 0, nup = 0;
+#pragma unroll
+    for (int i = 0; i < 2 * DEG; i++) {
+        const int x = c[i];
+        const bool keep = (x != 0x7fffffff) && (i == 0 || x != c[i > 0 ? i - 1 : 0]);
+        if (keep) {
+            out[nu++] = x;
+            nup += x > v;
+        }
+    }
+    ucnt[v] = nu;
+    upcnt[v] = nup;
+}
+// TMAX: largest degree of the thread tier (8: 62 registers, for the bandwidth-bound large rounds;
+// 16: 90 registers, degrees 9..16 in-thread instead of the warp tier -- latency-bound rounds)
+template <int TMAX>
 __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ inc,
                                                   const int* __restrict__ F, const Plane* __restrict__ plane,
@@ -337,7 +385,7 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
         if (v < N) {
             s = inc_off[v];
             d = inc_off[v + 1] - s;
-            if (d > kThreadDeg) {
+            if (d > TMAX) {
                 if (d <= kMid) mid[append_slot(mid_count)] = v;
                 else heavy[append_slot(heavy_count)] = v;
             } else {
@@ -345,40 +393,10 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
             }
         }
         if (work) {
-            int k[kThreadDeg];
-#pragma unroll
-            for (int i = 0; i < kThreadDeg; i++) k[i] = (i < d) ? inc[s + i] : 0x7fffffff;
-            reg_sort(k);
-            Q10 q;
-            q_zero(q);
-            int c[2 * kThreadDeg];
-#pragma unroll
-            for (int i = 0; i < kThreadDeg; i++) {
-                c[2 * i] = 0x7fffffff;
-                c[2 * i + 1] = 0x7fffffff;
-                if (i < d) {
-                    int corner, f;
-                    decode_inc(k[i], Mcap, corner, f);
-                    Plane p = plane[f];
-                    q_add_plane(q, p);
-                    other_two(F, f, corner, c[2 * i], c[2 * i + 1]);
-                }
-            }
-            q_store(vq, v, q);
-            reg_sort(c);
-            int nu = 0, nup = 0;
             int* out = staged ? s_nb + 2 * (s - r0) : nbr + 2 * (size_t)s;
-#pragma unroll
-            for (int i = 0; i < 2 * kThreadDeg; i++) {
-                const int x = c[i];
-                const bool keep = (x != 0x7fffffff) && (i == 0 || x != c[i > 0 ? i - 1 : 0]);
-                if (keep) {
-                    out[nu++] = x;
-                    nup += x > v;
-                }
-            }
-            ucnt[v] = nu;
-            upcnt[v] = nup;
+            if (TMAX == kThreadDeg || d <= kThreadDeg)
+                vertex_thread_tier<kThreadDeg>(v, s, d, inc, F, plane, Mcap, vq, out, ucnt, upcnt);
+            else vertex_thread_tier<TMAX>(v, s, d, inc, F, plane, Mcap, vq, out, ucnt, upcnt);
         }
         if (staged) {
             __syncthreads();
@@ -3334,13 +3352,11 @@ __global__ void k_facet_remap(const int* __restrict__ dM, const int* __restrict_
         unsigned h = ((unsigned)lo * per_vertex + (tri_hash(lo, mid, hi) & 7u)) & tmask;
         if (PACKED) {
             const unsigned long long key = ((unsigned long long)lo << 42) | ((unsigned long long)mid << 21) | hi;
+            // CAS first: it returns the occupant, so a probe costs one round trip (a load before
+            // the CAS made the common empty-slot case two)
             while (true) {
-                unsigned long long cur = __ldcg(tkey + h);
-                if (cur == kEmptyKey) {
-                    cur = atomicCAS(tkey + h, kEmptyKey, key);
-                    if (cur == kEmptyKey) cur = key;
-                }
-                if (cur == key) {
+                unsigned long long cur = atomicCAS(tkey + h, kEmptyKey, key);
+                if (cur == kEmptyKey || cur == key) {
                     atomicMin(table + h, f);
                     break;
                 }
