@@ -227,15 +227,17 @@ static bool edges_rank() {
     return v == 1;
 }
 
-// thread tier up to degree 16 in rounds below 2^20 vertices (latency-bound: the warp tier is then
-// usually empty); MF_VT16=0 / 1 forces the degree-8 / degree-16 form
+// MF_VT16=1: thread tier up to degree 16 (90 registers) instead of 8 + the warp tier.  Opt-in:
+// measured (r2o) cfg2 0.506 / 0.501 vs 0.496 / 0.494 ms -- the occupancy it costs outweighs the
+// warp-tier launch it empties
 static bool vt16(int N) {
-    static int v = -2;
-    if (v == -2) {
+    static int v = -1;
+    if (v < 0) {
         const char* e = getenv("MF_VT16");
-        v = e ? (e[0] == '1') : -1;
+        v = (e && e[0] == '1') ? 1 : 0;
     }
-    return v == -1 ? N < (1 << 20) : v == 1;
+    (void)N;
+    return v == 1;
 }
 
 // MF_FUSE_PLANE=0: separate k_compose / k_facet_plane launches between rounds (A/B runs)
