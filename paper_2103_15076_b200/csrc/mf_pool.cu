@@ -306,6 +306,85 @@ __global__ void __launch_bounds__(256) k_unpool_rows(int n, int row16, const int
     }
 }
 
+// ---- TMA (bulk-copy engine) form of the row gather: every lane of a warp issues one
+// cp.async.bulk global->shared copy of a coarse row (the gather), an mbarrier with a transaction
+// count tracks the tile's bytes, and one lane writes the tile's 32 consecutive output rows with a
+// single cp.async.bulk shared->global store.  Two tiles per warp double-buffer so the next gather
+// overlaps the current store.  The SM issues 33 bulk instructions per 32 rows instead of
+// 32 x row16 vector loads + stores.
+MF_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+MF_DEV void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+MF_DEV void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+MF_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n LAB_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LAB_WAIT;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+MF_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+MF_DEV void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+MF_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+MF_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+MF_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
+constexpr int kTmaWarps = 4;
+// dynamic smem: per warp 2 buffers x 32 rows x row bytes, then 2 mbarriers per warp
+__global__ void __launch_bounds__(kTmaWarps * 32) k_unpool_tma(int n, int row_bytes, const int* __restrict__ rep,
+                                                                  const char* __restrict__ coarse, char* __restrict__ out) {
+    MF_PDL_ENTRY;
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t tile_bytes = (size_t)32 * row_bytes;
+    unsigned char* buf0 = tma_smem + (size_t)warp * 2 * tile_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tma_smem + (size_t)kTmaWarps * 2 * tile_bytes) + warp * 2;
+    if (lane == 0) {
+        mbar_init(bars, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int tiles = (n + 31) / 32;
+    const int gw = blockIdx.x * kTmaWarps + warp, nw = gridDim.x * kTmaWarps;
+    unsigned phase[2] = {0u, 0u};
+    int k = 0;
+    for (int t = gw; t < tiles; t += nw, k ^= 1) {
+        unsigned char* buf = buf0 + (size_t)k * tile_bytes;
+        const int v0 = t * 32;
+        const int rows = min(32, n - v0);
+        // the store that last used this buffer (two tiles ago) must have read it
+        if (lane == 0) bulk_wait_read1();
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(bars + k, (unsigned)(rows * row_bytes));
+        __syncwarp();
+        if (lane < rows) bulk_g2s(buf + (size_t)lane * row_bytes, coarse + (size_t)__ldg(rep + v0 + lane) * row_bytes,
+                                  (unsigned)row_bytes, bars + k);
+        mbar_wait(bars + k, phase[k]);
+        phase[k] ^= 1u;
+        if (lane == 0) {
+            bulk_s2g(out + (size_t)v0 * row_bytes, buf, (unsigned)(rows * row_bytes));
+            bulk_commit();
+        }
+    }
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
+}
+
 __global__ void k_unpool_vec(int64_t n, int64_t row16, const int* __restrict__ rep, const int4* __restrict__ coarse,
                              int4* __restrict__ out) {
     MF_PDL_ENTRY;
@@ -556,6 +635,16 @@ static bool pool_scalar_forced() {
     return v == 1;
 }
 
+// MF_UNPOOL_TMA=1: the bulk-copy (TMA) row gather instead of the LSU one (A/B runs)
+static bool unpool_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_UNPOOL_TMA");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static int lanes_for(int row16) {  // lanes per row: the row's vectors, 4..32
     int L = 4;
     while (L < row16 && L < 32) L <<= 1;
@@ -737,7 +826,18 @@ int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64
     if (ho) dO = p;
     const size_t row = (size_t)c * es;
     if (n * c > 0) {
-        if (row % 16 == 0 && ((uintptr_t)dC % 16) == 0 && ((uintptr_t)dO % 16) == 0 && !pool_scalar_forced()) {
+        if (unpool_tma() && row % 16 == 0 && row <= 1024 && ((uintptr_t)dC % 16) == 0 && ((uintptr_t)dO % 16) == 0) {
+            const size_t smem = (size_t)kTmaWarps * 2 * 32 * row + kTmaWarps * 2 * 8;
+            static size_t configured = 0;
+            if (smem > configured) {
+                cudaFuncSetAttribute(k_unpool_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                configured = smem;
+            }
+            const int tiles = (int)((n + 31) / 32);
+            const int grid = std::max(1, std::min((tiles + kTmaWarps - 1) / kTmaWarps, ctx->sm_count * 8));
+            LAUNCH(k_unpool_tma, grid, kTmaWarps * 32, smem, stream, (int)n, (int)row, d_replace, (const char*)dC,
+                   (char*)dO);
+        } else if (row % 16 == 0 && ((uintptr_t)dC % 16) == 0 && ((uintptr_t)dO % 16) == 0 && !pool_scalar_forced()) {
             const int row16 = (int)(row / 16);
             const int L = lanes_for(row16);
             // up to two waves of groups: one row per group (latency-bound sizes); beyond, 4 rows in

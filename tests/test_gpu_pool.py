@@ -133,3 +133,50 @@ def test_adjoint_identities_gpu():
     assert (mfg.pool(x, res, "sum") * y).sum() == pytest.approx((x * mfg.unpool(y, res)).sum(), rel=1e-12)
     g = mfg.pool_backward(y, x, res, mode="average")
     assert (mfg.pool(x, res, "average") * y).sum() == pytest.approx((x * g).sum(), rel=1e-12)
+
+
+POOL_VARIANT_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import torch
+import paper_2103_15076_b200 as mfg
+from paper_2103_15076_b200 import synthetic as S
+from paper_2103_15076_b200 import tensor as T
+from oracle import oracle as O
+mesh = S.delaunay_terrain(30_000, noise=0.02, seed=8)
+res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=9_001))
+dd = T.decimate(torch.from_numpy(mesh.positions).cuda(), torch.from_numpy(mesh.facets).cuda(), target=9_001)
+rng = np.random.default_rng(3)
+for c, dt in ((64, np.float32), (16, np.float64), (4, np.float32), (3, np.float64), (100, np.float32)):
+    X = rng.standard_normal((mesh.n_vertices, c)).astype(dt)
+    for mode in mfg.POOL_MODES:
+        w = rng.random(mesh.n_vertices).astype(dt) + 0.5
+        got = mfg.pool(X, res, mode=mode, weights=w if mode == "weighted" else None)
+        exp = O.pool(X, res.replace, res.n_vertices_out, mode, w)
+        assert np.array_equal(got.view(np.uint8), exp.view(np.uint8)), (c, mode)
+        gt = T.pool(torch.from_numpy(X).cuda(), dd, mode=mode,
+                    weights=torch.from_numpy(w).cuda() if mode == "weighted" else None)
+        assert np.array_equal(gt.cpu().numpy().view(np.uint8), exp.view(np.uint8)), (c, mode, "tensor")
+    up = mfg.unpool(got, res)
+    assert np.array_equal(up.view(np.uint8), O.unpool(got, res.replace).view(np.uint8)), c
+    ut = T.unpool(torch.from_numpy(got).cuda(), dd).cpu().numpy()
+    assert np.array_equal(ut.view(np.uint8), O.unpool(got, res.replace).view(np.uint8)), (c, "tensor")
+print("POOL-VARIANT-OK")
+"""
+
+POOL_VARIANTS = [{}, {"MF_UNPOOL_TMA": "1"}, {"MF_POOL_SCALAR": "1"}, {"MF_CSR_COOP": "0"}]
+
+
+@pytest.mark.parametrize("env", POOL_VARIANTS, ids=[",".join(f"{k}={v}" for k, v in e.items()) or "default"
+                                                     for e in POOL_VARIANTS])
+def test_pool_unpool_variants_match_oracle(env):
+    """Every pooling kernel variant (vectorised / scalar pool, LSU / TMA bulk-copy unpool,
+    cooperative / multi-launch cluster CSR) bit-exact against the oracle, host and device API."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", POOL_VARIANT_SCRIPT.format(root=root)], cwd=root,
+                         env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert "POOL-VARIANT-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
