@@ -21,4 +21,9 @@ run racecheck variants_small MF_SAN_N=20000 MF_WIDE_MIN=0 MF_SCAN4_MIN=0 MF_BIG_
 run memcheck suitor8_cluster MF_SAN_N=20000 MF_SUITOR=8 MF_SELECT_CL=1 MF_LD1_MIN=1
 run racecheck suitor8_cluster MF_SAN_N=20000 MF_SUITOR=8 MF_SELECT_CL=1 MF_LD1_MIN=1
 run memcheck nographs MF_SAN_N=20000 MF_GRAPHS=0
+run memcheck pool_variants MF_SAN_N=20000 MF_UNPOOL_TMA=1 MF_CSR_COOP=0 MF_DEBUG=1
+run racecheck pool_variants MF_SAN_N=20000 MF_UNPOOL_TMA=1 MF_CSR_COOP=0 MF_DEBUG=1
+run synccheck pool_variants MF_SAN_N=20000 MF_UNPOOL_TMA=1
+run memcheck fused_opt_in MF_SAN_N=20000 MF_VERTEX_SCAN=2 MF_EDGES_RANK=1 MF_VT16=1 MF_FUSE_PLANE=0
+run racecheck fused_opt_in MF_SAN_N=20000 MF_VERTEX_SCAN=2 MF_EDGES_RANK=1 MF_VT16=1
 run initcheck default MF_SAN_N=20000 MF_GRAPHS=0
