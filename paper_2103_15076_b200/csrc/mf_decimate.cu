@@ -485,7 +485,7 @@ struct WS {
     int* snbr;    // adjacency slots in rank order (k_adj_rank output; nbr keeps neighbour order)
     int* seid_u;  // unseeded: edge ids of the unsorted slots (their neighbours / keys are e1 / key_hi)
     int* lowfill;
-    unsigned long long* suitor;
+    ulonglong2* suitor;  // 16-byte suitor words (proposal key | edge, proposer)
     int *bestu, *front0, *front1, *ldc, *loose;
     unsigned* bar;
     int* selstate;
@@ -582,7 +582,7 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.snbr = A.take<int>((size_t)2 * Ecap);
     W.seid_u = p.seeded ? nullptr : A.take<int>((size_t)2 * Ecap);
     W.lowfill = A.take<int>((size_t)N0 + 1);
-    W.suitor = A.take<unsigned long long>((size_t)N0);
+    W.suitor = A.take<ulonglong2>((size_t)N0);
     W.bestu = A.take<int>((size_t)N0);
     W.front0 = A.take<int>((size_t)N0);
     W.front1 = A.take<int>((size_t)N0);
@@ -1414,7 +1414,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         EmitJobs jobs;
         if (p.Nfin) jobs.add(kEmitF64, W.Pfin, res->positions, (int64_t)p.Nfin * 3);
         if (!p.alias && p.Nfin * C > 0) jobs.add(kEmitF64, W.Xfin, res->features, (int64_t)p.Nfin * C);
-        jobs.add(kEmitW32, W.Ffin, res->facets, (int64_t)p.Mcap * 3);
+        jobs.add(kEmitW32, W.Ffin, res->facets, (int64_t)p.Mcap * 3, W.status + 8 + B);  // m_out rows
         if (n) {
             jobs.add(kEmitW32, W.rt, res->replace, n);
             jobs.add(kEmitW32, W.mt, res->mapping, n);
