@@ -485,7 +485,7 @@ struct WS {
     int* snbr;    // adjacency slots in rank order (k_adj_rank output; nbr keeps neighbour order)
     int* seid_u;  // unseeded: edge ids of the unsorted slots (their neighbours / keys are e1 / key_hi)
     int* lowfill;
-    ulonglong2* suitor;  // 16-byte suitor words (proposal key | edge, proposer)
+    unsigned long long* suitor;
     int *bestu, *front0, *front1, *ldc, *loose;
     unsigned* bar;
     int* selstate;
@@ -582,7 +582,7 @@ static void layout(Arena& A, WS& W, const Plan& p) {
     W.snbr = A.take<int>((size_t)2 * Ecap);
     W.seid_u = p.seeded ? nullptr : A.take<int>((size_t)2 * Ecap);
     W.lowfill = A.take<int>((size_t)N0 + 1);
-    W.suitor = A.take<ulonglong2>((size_t)N0);
+    W.suitor = A.take<unsigned long long>((size_t)N0);
     W.bestu = A.take<int>((size_t)N0);
     W.front0 = A.take<int>((size_t)N0);
     W.front1 = A.take<int>((size_t)N0);

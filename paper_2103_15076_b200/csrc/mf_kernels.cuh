@@ -523,7 +523,7 @@ struct EdgeOut {
     int* minrep;
     int* absorbed;
     int* abshead;
-    ulonglong2* suitor;
+    unsigned long long* suitor;
     unsigned long long* mlo;
     unsigned long long* mhi;
     int* seg_cnt;
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
             o.minrep[v] = v;
             o.absorbed[v] = -1;
             o.abshead[v] = -1;
-            o.suitor[v] = make_ulonglong2(~0ull, ~0ull);
+            o.suitor[v] = ~0ull;
         }
         // every per-vertex word is loaded up front (one latency), the neighbour list's offset
         // included -- loaded after the nup branch it cost a dependent round trip (ncu stalls)
@@ -634,7 +634,7 @@ struct EdgeRankOut {
     int* minrep;
     int* absorbed;
     int* abshead;
-    ulonglong2* suitor;
+    unsigned long long* suitor;
     unsigned long long* mlo;
     unsigned long long* mhi;
     int* seg_cnt;
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges_rank(const int
             o.minrep[v] = v;
             o.absorbed[v] = -1;
             o.abshead[v] = -1;
-            o.suitor[v] = make_ulonglong2(~0ull, ~0ull);
+            o.suitor[v] = ~0ull;
         }
         const int nu = ucnt[v];
         const size_t s2 = (size_t)aoff[v];
@@ -1458,28 +1458,6 @@ __global__ void k_seed_keys(const int* __restrict__ abort_flag, const int* __res
 // then proposes again.  Keys are unique, so the fixed point is the unique
 // greedy matching of the rank order -- exactly the sequential scan of
 // decimate.py:256-263 run to exhaustion -- with no grid-wide barrier.
-// Suitor word: x = (rank-key prefix << 32) | edge id of the best proposal received, y = its
-// proposer (~0 = none).  Carrying the proposer saves the displaced proposer's edge-endpoint
-// gather on every displacement (one dependent round trip per link of a proposal chain); the two
-// halves change together through a 128-bit CAS (sm_90+ atom.cas.b128).
-MF_DEV ulonglong2 ld_suitor(const ulonglong2* p) {
-    ulonglong2 r;
-    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
-    return r;
-}
-MF_DEV ulonglong2 cas_suitor(ulonglong2* p, ulonglong2 cmp, ulonglong2 val) {
-    ulonglong2 old;
-    asm volatile(
-        "{\n .reg .b128 c, v, o;\n"
-        " mov.b128 c, {%2, %3};\n mov.b128 v, {%4, %5};\n"
-        " atom.relaxed.gpu.global.cas.b128 o, [%6], c, v;\n"
-        " mov.b128 {%0, %1}, o;\n}"
-        : "=l"(old.x), "=l"(old.y)
-        : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
-        : "memory");
-    return old;
-}
-
 struct MatchArgs {
     int N;
     const int* aoff;      // compact adjacency offsets
@@ -1491,7 +1469,7 @@ struct MatchArgs {
     const int* e1;
     const uint64_t* key_hi;
     const uint64_t* key_lo;  // nullptr -> secondary key is the edge id
-    ulonglong2* suitor;  // per vertex: best proposal received (see ld_suitor), ~0 = none
+    unsigned long long* suitor;  // per vertex: (k32 << 32) | edge of the best proposal received, ~0 = none
     const int* abort_flag;
     const int* mate;       // nullable: vertices matched by the LD rounds are not eligible
     const int* front0;     // nullable: proposers = residual LD frontier, else all vertices
@@ -1543,7 +1521,7 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
             const int nu = a.ucnt[cur];
             int be = -1, bv = -1;
             unsigned bk = 0xffffffffu;
-            unsigned long long bsw = ~0ull, bswp = ~0ull;  // the suitor word seen when the slot was judged winnable
+            unsigned long long bsw = ~0ull;  // the suitor word seen when the slot was judged winnable
             const int c0 = a.acur[cur];
             if (c0 >= 0) {
                 // rank-ordered adjacency: the best winnable edge is the first winnable slot.
@@ -1555,16 +1533,14 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                     bool ok = false;
                     unsigned ke = 0;
                     int e = -1, v = -1;
-                    unsigned long long sw = ~0ull, swp = ~0ull;
+                    unsigned long long sw = ~0ull;
                     if (j < nu) {
                         e = a.adj_eid[s + j];
                         ke = a.adj_k32[s + j];
                         v = a.nbr[s + j];
                         ok = !(a.mate && __ldcg(a.mate + v) >= 0);
                         if (ok) {
-                            const ulonglong2 w2 = ld_suitor(a.suitor + v);
-                            sw = w2.x;
-                            swp = w2.y;
+                            sw = ld_volatile(a.suitor + v);
                             ok = sw == ~0ull || edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw);
                         }
                     }
@@ -1575,7 +1551,6 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                         be = __shfl_sync(mask, e, f, L);
                         bv = __shfl_sync(mask, v, f, L);
                         bsw = __shfl_sync(mask, sw, f, L);
-                        bswp = __shfl_sync(mask, swp, f, L);
                         c += f;
                         break;
                     }
@@ -1588,33 +1563,32 @@ __global__ void __launch_bounds__(256) k_suitor(MatchArgs a) {
                     if (be >= 0 && !edge_lt(a, ke, e, bk, be)) continue;
                     const int v = a.nbr[s + j];
                     if (a.mate && __ldcg(a.mate + v) >= 0) continue;
-                    const ulonglong2 w2 = ld_suitor(a.suitor + v);
-                    const unsigned long long sw = w2.x;
+                    const unsigned long long sw = ld_volatile(a.suitor + v);
                     if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
-                    bk = ke; be = e; bv = v; bsw = sw; bswp = w2.y;
+                    bk = ke; be = e; bv = v; bsw = sw;
                 }
 #pragma unroll
                 for (int o = L / 2; o > 0; o >>= 1) {
                     unsigned ok = __shfl_xor_sync(mask, bk, o, L);
                     int oe = __shfl_xor_sync(mask, be, o, L), ov = __shfl_xor_sync(mask, bv, o, L);
                     unsigned long long osw = __shfl_xor_sync(mask, bsw, o, L);
-                    unsigned long long oswp = __shfl_xor_sync(mask, bswp, o, L);
-                    if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) {
-                        bk = ok; be = oe; bv = ov; bsw = osw; bswp = oswp;
-                    }
+                    if (oe >= 0 && (be < 0 || edge_lt(a, ok, oe, bk, be))) { bk = ok; be = oe; bv = ov; bsw = osw; }
                 }
             }
             if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
             int next = -2;      // -2: lost a race, re-scan cur
             if (l == 0) {
-                const ulonglong2 mine = make_ulonglong2(((unsigned long long)bk << 32) | (unsigned)be,
-                                                        (unsigned long long)(unsigned)cur);
-                ulonglong2 sw = make_ulonglong2(bsw, bswp);  // a stale expected value only costs one failed CAS
+                const unsigned long long mine = ((unsigned long long)bk << 32) | (unsigned)be;
+                unsigned long long sw = bsw;  // a stale expected value only costs one failed CAS
                 while (true) {
-                    if (sw.x != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw.x >> 32), (int)(unsigned)sw.x)) break;
-                    const ulonglong2 old = cas_suitor(a.suitor + bv, sw, mine);
-                    if (old.x == sw.x && old.y == sw.y) {
-                        next = sw.x == ~0ull ? -1 : (int)(unsigned)sw.y;  // the displaced proposer
+                    if (sw != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw >> 32), (int)(unsigned)sw)) break;
+                    unsigned long long old = atomicCAS(a.suitor + bv, sw, mine);
+                    if (old == sw) {
+                        if (sw == ~0ull) next = -1;
+                        else {
+                            int se = (int)(unsigned)sw;
+                            next = (a.e0[se] == bv) ? a.e1[se] : a.e0[se];
+                        }
                         break;
                     }
                     sw = old;
@@ -1649,7 +1623,7 @@ __global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
             const int nu = a.ucnt[cur];
             int be = -1, bv = -1;
             unsigned bk = 0xffffffffu;
-            unsigned long long bsw = ~0ull, bswp = ~0ull;
+            unsigned long long bsw = ~0ull;
             int c = a.acur[cur];
             if (c >= 0) {
                 for (; c < nu; c++) {
@@ -1657,10 +1631,9 @@ __global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
                     if (a.mate && __ldcg(a.mate + v) >= 0) continue;
                     const int e = a.adj_eid[s + c];
                     const unsigned ke = a.adj_k32[s + c];
-                    const ulonglong2 w2 = ld_suitor(a.suitor + v);
-                    const unsigned long long sw = w2.x;
+                    const unsigned long long sw = ld_volatile(a.suitor + v);
                     if (sw == ~0ull || edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) {
-                        bk = ke; be = e; bv = v; bsw = sw; bswp = w2.y;
+                        bk = ke; be = e; bv = v; bsw = sw;
                         break;
                     }
                 }
@@ -1672,22 +1645,24 @@ __global__ void __maxnreg__(48) k_suitor1(MatchArgs a) {
                     if (be >= 0 && !edge_lt(a, ke, e, bk, be)) continue;
                     const int v = a.nbr[s + j];
                     if (a.mate && __ldcg(a.mate + v) >= 0) continue;
-                    const ulonglong2 w2 = ld_suitor(a.suitor + v);
-                    const unsigned long long sw = w2.x;
+                    const unsigned long long sw = ld_volatile(a.suitor + v);
                     if (sw != ~0ull && !edge_lt(a, ke, e, (unsigned)(sw >> 32), (int)(unsigned)sw)) continue;
-                    bk = ke; be = e; bv = v; bsw = sw; bswp = w2.y;
+                    bk = ke; be = e; bv = v; bsw = sw;
                 }
             }
             if (be < 0) break;  // nothing winnable: cur stays unmatched unless proposed to
-            const ulonglong2 mine = make_ulonglong2(((unsigned long long)bk << 32) | (unsigned)be,
-                                                    (unsigned long long)(unsigned)cur);
-            ulonglong2 sw = make_ulonglong2(bsw, bswp);  // a stale expected value only costs one failed CAS
+            const unsigned long long mine = ((unsigned long long)bk << 32) | (unsigned)be;
+            unsigned long long sw = bsw;  // a stale expected value only costs one failed CAS
             int next = -2;  // -2: lost a race, re-scan cur (the lost slot is dead now)
             while (true) {
-                if (sw.x != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw.x >> 32), (int)(unsigned)sw.x)) break;
-                const ulonglong2 old = cas_suitor(a.suitor + bv, sw, mine);
-                if (old.x == sw.x && old.y == sw.y) {
-                    next = sw.x == ~0ull ? -1 : (int)(unsigned)sw.y;  // the displaced proposer
+                if (sw != ~0ull && !edge_lt(a, bk, be, (unsigned)(sw >> 32), (int)(unsigned)sw)) break;
+                const unsigned long long old = atomicCAS(a.suitor + bv, sw, mine);
+                if (old == sw) {
+                    if (sw == ~0ull) next = -1;
+                    else {
+                        const int se = (int)(unsigned)sw;
+                        next = (a.e0[se] == bv) ? a.e1[se] : a.e0[se];
+                    }
                     break;
                 }
                 sw = old;
@@ -1917,7 +1892,7 @@ MF_DEV int seg_slot_uniform(bool keep, const int* __restrict__ vmesh, const int*
 // mate = the suitor edge when the proposal is mutual (or the LD match); every
 // matched pair is also appended once (from its e0 end) as a budget-truncation
 // candidate keyed by its rank (decimate.py:256-258).
-__global__ void k_mates(const int* __restrict__ abort_flag, int N, const ulonglong2* __restrict__ suitor,
+__global__ void k_mates(const int* __restrict__ abort_flag, int N, const unsigned long long* __restrict__ suitor,
                         const int* __restrict__ e0, const int* __restrict__ e1, int* __restrict__ mate,
                         const uint64_t* __restrict__ key_hi, const uint64_t* __restrict__ key_lo,
                         const int* __restrict__ vmesh, const int* __restrict__ voff, int* __restrict__ seg_cnt,
@@ -1934,20 +1909,14 @@ __global__ void k_mates(const int* __restrict__ abort_flag, int N, const ulonglo
         bool cand = false;
         if (v < N) {
             m = mate[v];
-            const ulonglong2 w = m >= 0 ? make_ulonglong2(~0ull, ~0ull) : suitor[v];  // m >= 0: LD-matched
-            int lo = -1;
-            if (w.x != ~0ull) {  // mutual proposal: the proposer's own suitor word holds the same edge
-                const int e = (int)(unsigned)w.x;
-                const int u = (int)(unsigned)w.y;
-                const unsigned long long wu = suitor[u].x;
-                if (wu != ~0ull && (int)(unsigned)wu == e) {
-                    m = e;
-                    lo = min(u, v);  // the edge's lower end (e0)
-                }
-            } else if (m >= 0) {
-                lo = e0[m];
+            unsigned long long w = m >= 0 ? ~0ull : suitor[v];  // m >= 0: matched by the LD rounds
+            if (w != ~0ull) {
+                int e = (int)(unsigned)w;
+                int u = e0[e] == v ? e1[e] : e0[e];
+                if ((int)(unsigned)suitor[u] == e && suitor[u] != ~0ull) m = e;
             }
             mate[v] = m;
+            const int lo = m >= 0 ? e0[m] : -1;
             pairlo[v] = lo;
             cand = lo == v;
         }
