@@ -9,6 +9,7 @@
  *                         (TriMesh and BatchedMesh; round chain decimate.py:294-316;
  *                          batch merge decimate.py:319-341)
  *   mf_decimation_*    <- DecimationResult fields mesh / replace / mapping   decimate.py:74-92
+ *   mf_decimate_into   <- decimate_parallel with the result arrays emitted into caller buffers
  *   mf_pool            <- pooling.pool(features, result, mode, weights)      pooling.py:49-71
  *   mf_unpool          <- pooling.unpool(coarse, result)                     pooling.py:74-77
  *   mf_pool_backward   <- pooling.pool_backward / unpool_backward            pooling.py:80-102
@@ -97,6 +98,28 @@ void mf_context_destroy(mf_context *ctx);
 
 int mf_decimate(mf_context *ctx, const mf_mesh_view *mesh, const mf_decimate_config *cfg, void *stream,
                 mf_decimation **out, mf_status *status);
+
+/* Caller-owned result buffers for mf_decimate_into: device memory or pinned host memory (written
+ * through its mapped device address); NULL skips an array.  facets needs room for the input facet
+ * count (the output count is known only at the end); n_out = target_vertices * n_meshes. */
+typedef struct mf_outputs {
+    double *positions;         /* [n_out, 3] float64 */
+    int64_t *facets;           /* [facets_capacity, 3] int64; rows [0, m_out) are written */
+    int64_t facets_capacity;   /* rows available in facets (>= the input facet count) */
+    void *features;            /* [n_out, c] of features_dtype */
+    int32_t features_dtype;    /* MF_DTYPE_* */
+    int32_t reserved;
+    int64_t *replace;          /* [n_in] int64 */
+    int64_t *mapping;          /* [n_in] int64 */
+    int64_t *vertex_offsets;   /* host [n_meshes + 1] */
+    int64_t *facet_offsets;    /* host [n_meshes + 1] */
+} mf_outputs;
+
+/* mf_decimate + mf_decimation_copy in one call: the outputs are emitted by the same launch that
+ * fills the handle's arrays, before the call's single synchronisation.  The handle is still
+ * returned (pooling reuses it). */
+int mf_decimate_into(mf_context *ctx, const mf_mesh_view *mesh, const mf_decimate_config *cfg, void *stream,
+                     const mf_outputs *outputs, mf_decimation **out, mf_status *status);
 
 int mf_decimation_sizes(const mf_decimation *res, int64_t *n_in, int64_t *n_out, int64_t *m_out, int64_t *c,
                         int64_t *n_meshes);

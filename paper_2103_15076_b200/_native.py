@@ -47,6 +47,23 @@ class Config(ctypes.Structure):
     ]
 
 
+class Outputs(ctypes.Structure):
+    """mf_outputs (include/mfgpu.h): caller buffers of mf_decimate_into."""
+
+    _fields_ = [
+        ("positions", ctypes.c_void_p),
+        ("facets", ctypes.c_void_p),
+        ("facets_capacity", ctypes.c_int64),
+        ("features", ctypes.c_void_p),
+        ("features_dtype", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("replace", ctypes.c_void_p),
+        ("mapping", ctypes.c_void_p),
+        ("vertex_offsets", ctypes.c_void_p),
+        ("facet_offsets", ctypes.c_void_p),
+    ]
+
+
 class Status(ctypes.Structure):
     _fields_ = [
         ("code", ctypes.c_int32),
@@ -87,6 +104,9 @@ def lib():
         L.mf_decimate.argtypes = [_vp, ctypes.POINTER(MeshView), ctypes.POINTER(Config), _vp, ctypes.POINTER(_vp),
                                   ctypes.POINTER(Status)]
         L.mf_decimate.restype = ctypes.c_int
+        L.mf_decimate_into.argtypes = [_vp, ctypes.POINTER(MeshView), ctypes.POINTER(Config), _vp,
+                                       ctypes.POINTER(Outputs), ctypes.POINTER(_vp), ctypes.POINTER(Status)]
+        L.mf_decimate_into.restype = ctypes.c_int
         L.mf_decimation_sizes.argtypes = [_vp] + [ctypes.POINTER(_i64)] * 5
         L.mf_decimation_copy.argtypes = [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(Status)]
         L.mf_decimation_copy.restype = ctypes.c_int

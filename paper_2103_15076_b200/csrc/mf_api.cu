@@ -50,7 +50,7 @@ static int copy_i32_as_i64(const int* src, int64_t n, int64_t* dst, cudaStream_t
 
 // Destination the device can write: device memory as is, pinned host memory through its
 // mapped device address; nullptr for pageable host memory.
-static void* device_writable(void* p) {
+void* device_writable(void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
@@ -146,6 +146,27 @@ int mf_decimate(mf_context* ctx, const mf_mesh_view* mesh, const mf_decimate_con
     *out = nullptr;
     Result* r = nullptr;
     int rc = decimate_run(&ctx->c, mesh, cfg, (cudaStream_t)stream, &r, st);
+    if (rc != MF_OK) return rc;
+    mf_decimation* d = new mf_decimation();
+    d->r = *r;
+    delete r;
+    *out = d;
+    return MF_OK;
+}
+
+int mf_decimate_into(mf_context* ctx, const mf_mesh_view* mesh, const mf_decimate_config* cfg, void* stream,
+                     const mf_outputs* outputs, mf_decimation** out, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || !mesh || !cfg || !out || !outputs) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "null argument");
+        return st->code;
+    }
+    *out = nullptr;
+    Result* r = nullptr;
+    int rc = decimate_run(&ctx->c, mesh, cfg, (cudaStream_t)stream, &r, st, false, outputs);
     if (rc != MF_OK) return rc;
     mf_decimation* d = new mf_decimation();
     d->r = *r;

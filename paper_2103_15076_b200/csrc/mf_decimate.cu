@@ -1174,8 +1174,43 @@ done:
     return rc;
 }
 
+// The caller's result buffers (mf_decimate_into) as k_emit jobs next to the copy-out; false when
+// one of them cannot be written by the device (pageable host memory) or is too small.
+static bool add_caller_jobs(EmitJobs& jobs, const mf_outputs* o, const double* P, const double* X, int64_t xc,
+                            const int* F, int64_t fcap_rows, const int* frows, const int* rt, const int* mt,
+                            int64_t n_out, int64_t n_in) {
+    if (!o) return true;
+    auto dev = [](void* p) { return p ? device_writable(p) : nullptr; };
+    if (o->positions && n_out) {
+        void* d = dev(o->positions);
+        if (!d) return false;
+        jobs.add(kEmitF64, P, d, n_out * 3);
+    }
+    if (o->features && n_out * xc > 0) {
+        void* d = dev(o->features);
+        if (!d) return false;
+        jobs.add(o->features_dtype == MF_DTYPE_F32 ? kEmitF32 : kEmitF64, X, d, n_out * xc);
+    }
+    if (o->facets && fcap_rows) {
+        void* d = dev(o->facets);
+        if (!d || o->facets_capacity < fcap_rows) return false;
+        jobs.add(kEmitI32, F, d, fcap_rows * 3, frows);
+    }
+    if (o->replace && n_in) {
+        void* d = dev(o->replace);
+        if (!d) return false;
+        jobs.add(kEmitI32, rt, d, n_in);
+    }
+    if (o->mapping && n_in) {
+        void* d = dev(o->mapping);
+        if (!d) return false;
+        jobs.add(kEmitI32, mt, d, n_in);
+    }
+    return true;
+}
+
 int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,
-                 Result** out, mf_status* st, bool force_carry) {
+                 Result** out, mf_status* st, bool force_carry, const mf_outputs* outs) {
     st->code = MF_OK;
     st->mesh_index = -1;
     st->achievable_vertices = 0;
@@ -1419,6 +1454,16 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             jobs.add(kEmitW32, W.rt, res->replace, n);
             jobs.add(kEmitW32, W.mt, res->mapping, n);
         }
+        // mf_decimate_into: the caller's buffers in the same launch (int32 -> int64 widened there)
+        if (!add_caller_jobs(jobs, outs, W.Pfin, p.alias ? W.Pfin : W.Xfin, C, W.Ffin, p.Mcap, W.status + 8 + B, W.rt,
+                             W.mt, p.Nfin, n)) {
+            cudaFreeAsync(res->block, stream);
+            delete res;
+            st->code = MF_ERR_VALUE;
+            snprintf(st->message, sizeof(st->message),
+                     "mf_decimate_into: outputs must be device or pinned host memory, facets >= the input facet count");
+            return st->code;
+        }
         LAUNCH(k_emit, grid_for(ctx, std::max<int64_t>(1, jobs.total() / 4)), 256, 0, stream, jobs);
     } else {
         // identity (decimate.py:172-174, 367-370): inputs verbatim, replace = mapping = arange
@@ -1430,6 +1475,19 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
             else cudaMemcpyAsync(res->features, W.X0, (size_t)(n * C) * 8, cudaMemcpyDeviceToDevice, stream);
         }
         if (n) LAUNCH(k_identity_index, grid_for(ctx, n), 256, 0, stream, (int)n, res->replace, res->mapping);
+        if (outs) {  // the caller's buffers from the handle's arrays (the identity has no graph)
+            EmitJobs jobs;
+            if (!add_caller_jobs(jobs, outs, res->positions, p.alias ? res->positions : res->features, C, res->facets,
+                                 m, nullptr, res->replace, res->mapping, n, n)) {
+                cudaFreeAsync(res->block, stream);
+                delete res;
+                st->code = MF_ERR_VALUE;
+                snprintf(st->message, sizeof(st->message),
+                         "mf_decimate_into: outputs must be device or pinned host memory, facets >= the input facet count");
+                return st->code;
+            }
+            if (jobs.count) LAUNCH(k_emit, grid_for(ctx, std::max<int64_t>(1, jobs.total() / 4)), 256, 0, stream, jobs);
+        }
     }
     // ---- verify the optimistic features alias (overlapped with the chain)
     int h_diff = 0;
@@ -1447,7 +1505,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     if (h_diff) {  // features of the positions' shape that differ from them: carry them
         cudaFreeAsync(res->block, stream);
         delete res;
-        return decimate_run(ctx, mv, cfg, stream, out, st, true);
+        return decimate_run(ctx, mv, cfg, stream, out, st, true, outs);
     }
     if (graph_prof) prof_collect(*graph_prof);
     prof_collect_pending();
@@ -1508,6 +1566,10 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         int64_t row[6] = {p.h_N[r], h_stats[4 * r], h_stats[4 * r + 1], p.h_N[r + 1], h_stats[4 * r + 2],
                           h_stats[4 * r + 3]};
         res->round_stats.insert(res->round_stats.end(), row, row + 6);
+    }
+    if (outs) {  // host offsets of the caller's result
+        if (outs->vertex_offsets) std::copy(res->vertex_offsets.begin(), res->vertex_offsets.end(), outs->vertex_offsets);
+        if (outs->facet_offsets) std::copy(res->facet_offsets.begin(), res->facet_offsets.end(), outs->facet_offsets);
     }
     if (debug_validate() && R > 0) {  // row 16: the reference re-validates every output TriMesh
         int vr = validate_result(ctx, res, stream, st);

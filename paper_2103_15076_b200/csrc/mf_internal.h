@@ -71,7 +71,10 @@ struct Result {
 };
 
 int decimate_run(Context* ctx, const mf_mesh_view* mesh, const mf_decimate_config* cfg, cudaStream_t stream,
-                 Result** out, mf_status* st, bool force_carry = false);
+                 Result** out, mf_status* st, bool force_carry = false, const mf_outputs* outs = nullptr);
+// device address the GPU can write for p (device memory, or pinned host memory's mapped
+// address); nullptr for pageable host memory
+void* device_writable(void* p);
 int pool_run(Context* ctx, const void* features, int dtype, int64_t n, int64_t c, const int* d_replace,
              const int* d_off, const int* d_members, int64_t n_out, int mode, const void* weights, void* out,
              cudaStream_t stream, mf_status* st);

@@ -3635,12 +3635,13 @@ __global__ void k_words_differ(int64_t n, const unsigned long long* __restrict__
 // Fused result emission (mf_decimation_copy): up to 8 jobs, each widening int32 -> int64,
 // copying float64, or narrowing float64 -> float32 into a device-writable destination.
 constexpr int kEmitI32 = 0, kEmitF64 = 1, kEmitF32 = 2, kEmitW32 = 3;  // W32: int32 copied as is
+constexpr int kEmitMax = 12;
 struct EmitJobs {
-    const void* src[8];
-    void* dst[8];
-    int64_t n[8];
-    int kind[8];
-    const int* ndev[8];  // when set, the job moves min(n, *ndev * 3) elements (a device-side count)
+    const void* src[kEmitMax];
+    void* dst[kEmitMax];
+    int64_t n[kEmitMax];
+    int kind[kEmitMax];
+    const int* ndev[kEmitMax];  // when set, the job moves min(n, *ndev * 3) elements (a device-side count)
     int count = 0;
     void add(int k, const void* s, void* d, int64_t cnt, const int* rows3 = nullptr) {
         src[count] = s;

@@ -192,30 +192,60 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
     ctx = _native.context(device)
     handle = ctypes.c_void_p()
     st = _native.Status()
-    _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(handle), ctypes.byref(st))
-    _native.raise_for(st)
-    dec = _native.Decimation(handle, device)
-    n_out, m_out, c = dec.n_out, dec.m_out, view.c
-    pos = hostmem.empty((n_out, 3), np.float64)
-    fac = hostmem.empty((m_out, 3), np.int64)
+    B = len(mesh.vertex_offsets) - 1 if batched else 1
+    nv = np.diff(np.asarray(mesh.vertex_offsets)) if batched else np.array([view.n])
+    c = view.c
     feats_dtype = np.float64
     # the identity result keeps the input feature dtype (decimate.py:172-174); any real round folds into float64
     if Xc is not None and Xc.dtype == np.float32 and _all_identity(mesh, config):
         feats_dtype = np.float32
-    feats = hostmem.empty((n_out, c), feats_dtype)
-    rep = hostmem.empty((dec.n_in,), np.int64)
-    mp = hostmem.empty((dec.n_in,), np.int64)
-    B = dec.n_meshes
-    vo_out = np.empty(B + 1, dtype=np.int64)
-    fo_out = np.empty(B + 1, dtype=np.int64)
-    st = _native.Status()
-    _native.lib().mf_decimation_copy(
-        dec.handle, pos.ctypes.data, fac.ctypes.data if fac.size else None, feats.ctypes.data if feats.size else None,
-        _native.DTYPE_F32 if feats_dtype == np.float32 else _native.DTYPE_F64,
-        rep.ctypes.data if rep.size else None, mp.ctypes.data if mp.size else None,
-        vo_out.ctypes.data, fo_out.ctypes.data, None, ctypes.byref(st),
-    )
-    _native.raise_for(st)
+    if B > 0 and int(config.target_vertices) <= int(nv.min()):
+        # every entry ends at exactly target_vertices (or the call raises): pinned outputs allocated up
+        # front, emitted by the launch that fills the handle (mf_decimate_into, one synchronisation);
+        # the facet buffer holds the input facet count and is narrowed to the output count
+        n_out = int(config.target_vertices) * B
+        pos = hostmem.empty((n_out, 3), np.float64)
+        fac_cap = hostmem.empty((max(view.m, 1), 3), np.int64)
+        feats = hostmem.empty((n_out, c), feats_dtype)
+        rep = hostmem.empty((view.n,), np.int64)
+        mp = hostmem.empty((view.n,), np.int64)
+        vo_out = np.empty(B + 1, dtype=np.int64)
+        fo_out = np.empty(B + 1, dtype=np.int64)
+        outs = _native.Outputs()
+        outs.positions = pos.ctypes.data if pos.size else None
+        outs.facets, outs.facets_capacity = fac_cap.ctypes.data, fac_cap.shape[0]
+        outs.features = feats.ctypes.data if feats.size else None
+        outs.features_dtype = _native.DTYPE_F32 if feats_dtype == np.float32 else _native.DTYPE_F64
+        outs.replace = rep.ctypes.data if rep.size else None
+        outs.mapping = mp.ctypes.data if mp.size else None
+        outs.vertex_offsets, outs.facet_offsets = vo_out.ctypes.data, fo_out.ctypes.data
+        _native.lib().mf_decimate_into(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(outs),
+                                       ctypes.byref(handle), ctypes.byref(st))
+        _native.raise_for(st)
+        dec = _native.Decimation(handle, device)
+        fac = fac_cap[:dec.m_out]
+    else:  # the library raises the reference's error for an oversized target
+        _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(handle),
+                                  ctypes.byref(st))
+        _native.raise_for(st)
+        dec = _native.Decimation(handle, device)
+        n_out, m_out = dec.n_out, dec.m_out
+        pos = hostmem.empty((n_out, 3), np.float64)
+        fac = hostmem.empty((m_out, 3), np.int64)
+        feats = hostmem.empty((n_out, c), feats_dtype)
+        rep = hostmem.empty((dec.n_in,), np.int64)
+        mp = hostmem.empty((dec.n_in,), np.int64)
+        vo_out = np.empty(B + 1, dtype=np.int64)
+        fo_out = np.empty(B + 1, dtype=np.int64)
+        st = _native.Status()
+        _native.lib().mf_decimation_copy(
+            dec.handle, pos.ctypes.data, fac.ctypes.data if fac.size else None,
+            feats.ctypes.data if feats.size else None,
+            _native.DTYPE_F32 if feats_dtype == np.float32 else _native.DTYPE_F64,
+            rep.ctypes.data if rep.size else None, mp.ctypes.data if mp.size else None,
+            vo_out.ctypes.data, fo_out.ctypes.data, None, ctypes.byref(st),
+        )
+        _native.raise_for(st)
     rep.flags.writeable = False
     dec.replace_ref = rep  # pool/unpool reuse the device replace only for this very array
     # the output mesh arrays are read-only views of library-owned pinned memory (np.array(x) gives a

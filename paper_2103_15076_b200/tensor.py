@@ -105,27 +105,36 @@ def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, targ
     ctx = _native.context(dev.index)
     handle = ctypes.c_void_p()
     st = _native.Status()
-    _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), ctypes.c_void_p(stream),
-                              ctypes.byref(handle), ctypes.byref(st))
-    _native.raise_for(st)
-    dec = _native.Decimation(handle, dev.index)
     if not copy_outputs:
-        return DeviceDecimation(dec, None, None, None, None, None, None, None)
-    B = dec.n_meshes
-    V = torch.empty((dec.n_out, 3), dtype=torch.float64, device=dev)
-    Fo = torch.empty((dec.m_out, 3), dtype=torch.int64, device=dev)
-    X = torch.empty((dec.n_out, dec.c), dtype=torch.float64, device=dev)
-    R = torch.empty(dec.n_in, dtype=torch.int64, device=dev)
-    Mp = torch.empty(dec.n_in, dtype=torch.int64, device=dev)
+        _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), ctypes.c_void_p(stream),
+                                  ctypes.byref(handle), ctypes.byref(st))
+        _native.raise_for(st)
+        return DeviceDecimation(_native.Decimation(handle, dev.index), None, None, None, None, None, None, None)
+    # every entry ends at exactly `target` vertices (or the call raises): the outputs are allocated
+    # up front and emitted by the same launch that fills the handle (mf_decimate_into); the facet
+    # buffer holds the input facet count and is narrowed to the output count afterwards
+    B = 1 if vo is None else len(vo) - 1
+    n_out = int(target) * B
+    c = view.c
+    V = torch.empty((n_out, 3), dtype=torch.float64, device=dev)
+    Fo = torch.empty((max(view.m, 1), 3), dtype=torch.int64, device=dev)
+    X = torch.empty((n_out, c), dtype=torch.float64, device=dev)
+    R = torch.empty(view.n, dtype=torch.int64, device=dev)
+    Mp = torch.empty(view.n, dtype=torch.int64, device=dev)
     vo_out = np.empty(B + 1, dtype=np.int64)
     fo_out = np.empty(B + 1, dtype=np.int64)
-    st = _native.Status()
-    _native.lib().mf_decimation_copy(
-        dec.handle, V.data_ptr() if V.numel() else None, Fo.data_ptr() if Fo.numel() else None,
-        X.data_ptr() if X.numel() else None, _native.DTYPE_F64, R.data_ptr() if R.numel() else None,
-        Mp.data_ptr() if Mp.numel() else None, vo_out.ctypes.data, fo_out.ctypes.data, ctypes.c_void_p(stream),
-        ctypes.byref(st))
+    outs = _native.Outputs()
+    outs.positions = V.data_ptr() if V.numel() else None
+    outs.facets, outs.facets_capacity = Fo.data_ptr(), Fo.shape[0]
+    outs.features, outs.features_dtype = (X.data_ptr() if X.numel() else None), _native.DTYPE_F64
+    outs.replace = R.data_ptr() if R.numel() else None
+    outs.mapping = Mp.data_ptr() if Mp.numel() else None
+    outs.vertex_offsets, outs.facet_offsets = vo_out.ctypes.data, fo_out.ctypes.data
+    _native.lib().mf_decimate_into(ctx, ctypes.byref(view), ctypes.byref(cfg), ctypes.c_void_p(stream),
+                                   ctypes.byref(outs), ctypes.byref(handle), ctypes.byref(st))
     _native.raise_for(st)
+    dec = _native.Decimation(handle, dev.index)
+    Fo = Fo[:dec.m_out]
     nv_out = torch.from_numpy(np.diff(vo_out))
     mf_out = torch.from_numpy(np.diff(fo_out))
     return DeviceDecimation(dec, V, Fo, X, nv_out, mf_out, R, Mp)
