@@ -121,6 +121,13 @@ typedef struct mf_outputs {
 int mf_decimate_into(mf_context *ctx, const mf_mesh_view *mesh, const mf_decimate_config *cfg, void *stream,
                      const mf_outputs *outputs, mf_decimation **out, mf_status *status);
 
+/* mf_decimate_into split in two: _begin validates, stages and launches the round chain and returns
+ * without waiting; _end emits the results (into `outputs`, which may be NULL) and synchronises.
+ * One begun call per context at a time; the mesh buffers must stay alive until _end. */
+int mf_decimate_begin(mf_context *ctx, const mf_mesh_view *mesh, const mf_decimate_config *cfg, void *stream,
+                      mf_status *status);
+int mf_decimate_end(mf_context *ctx, const mf_outputs *outputs, mf_decimation **out, mf_status *status);
+
 int mf_decimation_sizes(const mf_decimation *res, int64_t *n_in, int64_t *n_out, int64_t *m_out, int64_t *c,
                         int64_t *n_meshes);
 /* Copy results into caller buffers (host or device; NULL skips an array).

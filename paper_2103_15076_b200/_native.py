@@ -107,6 +107,11 @@ def lib():
         L.mf_decimate_into.argtypes = [_vp, ctypes.POINTER(MeshView), ctypes.POINTER(Config), _vp,
                                        ctypes.POINTER(Outputs), ctypes.POINTER(_vp), ctypes.POINTER(Status)]
         L.mf_decimate_into.restype = ctypes.c_int
+        L.mf_decimate_begin.argtypes = [_vp, ctypes.POINTER(MeshView), ctypes.POINTER(Config), _vp,
+                                        ctypes.POINTER(Status)]
+        L.mf_decimate_begin.restype = ctypes.c_int
+        L.mf_decimate_end.argtypes = [_vp, ctypes.POINTER(Outputs), ctypes.POINTER(_vp), ctypes.POINTER(Status)]
+        L.mf_decimate_end.restype = ctypes.c_int
         L.mf_decimation_sizes.argtypes = [_vp] + [ctypes.POINTER(_i64)] * 5
         L.mf_decimation_copy.argtypes = [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(Status)]
         L.mf_decimation_copy.restype = ctypes.c_int
@@ -208,13 +213,15 @@ class Decimation:
 
     __slots__ = ("handle", "device", "n_in", "n_out", "m_out", "c", "n_meshes", "replace_ref", "__weakref__")
 
-    def __init__(self, handle, device):
+    def __init__(self, handle, device, sizes=None):
         self.handle = handle
         self.device = device
         self.replace_ref = None  # the host replace array emitted from this handle (pooling identity check)
-        vals = [_i64() for _ in range(5)]
-        lib().mf_decimation_sizes(handle, *[ctypes.byref(v) for v in vals])
-        self.n_in, self.n_out, self.m_out, self.c, self.n_meshes = (int(v.value) for v in vals)
+        if sizes is None:  # (n_in, n_out, m_out, c, n_meshes) when the caller already knows them
+            vals = [_i64() for _ in range(5)]
+            lib().mf_decimation_sizes(handle, *[ctypes.byref(v) for v in vals])
+            sizes = (int(v.value) for v in vals)
+        self.n_in, self.n_out, self.m_out, self.c, self.n_meshes = sizes
 
     def __del__(self):
         h = getattr(self, "handle", None)

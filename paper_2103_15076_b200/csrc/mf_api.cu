@@ -125,6 +125,7 @@ void mf_context_destroy(mf_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     drop_graphs(&ctx->c);
+    delete ctx->c.pending;
     if (ctx->c.arena) cudaFree(ctx->c.arena);
     if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
     if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
@@ -167,6 +168,50 @@ int mf_decimate_into(mf_context* ctx, const mf_mesh_view* mesh, const mf_decimat
     *out = nullptr;
     Result* r = nullptr;
     int rc = decimate_run(&ctx->c, mesh, cfg, (cudaStream_t)stream, &r, st, false, outputs);
+    if (rc != MF_OK) return rc;
+    mf_decimation* d = new mf_decimation();
+    d->r = *r;
+    delete r;
+    *out = d;
+    return MF_OK;
+}
+
+int mf_decimate_begin(mf_context* ctx, const mf_mesh_view* mesh, const mf_decimate_config* cfg, void* stream,
+                      mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || !mesh || !cfg) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "null argument");
+        return st->code;
+    }
+    if (!ctx->c.pending) ctx->c.pending = new DecCall();
+    if (ctx->c.pending->active) {  // a begun call its caller abandoned: finish and discard it
+        mf_status drop;
+        clear_status(&drop);
+        Result* r = nullptr;
+        if (decimate_end(&ctx->c, *ctx->c.pending, nullptr, &r, &drop) == MF_OK && r) {
+            if (r->block) cudaFree(r->block);
+            delete r;
+        }
+        clear_status(st);
+    }
+    return decimate_begin(&ctx->c, mesh, cfg, (cudaStream_t)stream, st, false, *ctx->c.pending);
+}
+
+int mf_decimate_end(mf_context* ctx, const mf_outputs* outputs, mf_decimation** out, mf_status* status) {
+    mf_status local;
+    mf_status* st = status ? status : &local;
+    clear_status(st);
+    if (!ctx || !out || !ctx->c.pending || !ctx->c.pending->active) {
+        st->code = MF_ERR_VALUE;
+        snprintf(st->message, sizeof(st->message), "mf_decimate_end: no begun call on this context");
+        return st->code;
+    }
+    *out = nullptr;
+    Result* r = nullptr;
+    int rc = decimate_end(&ctx->c, *ctx->c.pending, outputs, &r, st);
     if (rc != MF_OK) return rc;
     mf_decimation* d = new mf_decimation();
     d->r = *r;

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <map>
 #include <string>
 #include <thread>
@@ -266,6 +267,38 @@ static int grid_for(const Context* ctx, int64_t n, int block = 256) {
     if (g < 1) g = 1;
     return (int)g;
 }
+
+// MF_HOST_TIMING=1: host-side phase timestamps of every mf_decimate call on stderr (profiling aid)
+struct HostClock {
+    bool on;
+    double t0, last;
+    std::string line;
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+    }
+    HostClock() {
+        static int v = -1;
+        if (v < 0) {
+            const char* e = getenv("MF_HOST_TIMING");
+            v = (e && e[0] == '1') ? 1 : 0;
+        }
+        on = v == 1;
+        t0 = last = on ? now() : 0.0;
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        const double t = now();
+        char b[64];
+        snprintf(b, sizeof(b), " %s=%.1f", what, t - last);
+        line += b;
+        last = t;
+    }
+    ~HostClock() {
+        if (on) fprintf(stderr, "mf_decimate host us:%s total=%.1f\n", line.c_str(), now() - t0);
+    }
+};
 
 // _round_targets (decimate.py:294-316)
 int64_t round_targets(int64_t n_in, int64_t target, int rounds, std::vector<int64_t>& chain) {
@@ -1174,6 +1207,25 @@ done:
     return rc;
 }
 
+// One decimation between its two halves (decimate_begin launches the round chain, decimate_end
+// emits the results and synchronises): the host may prepare the result buffers in between.
+struct DecCall {
+    Plan p;
+    WS W;
+    mf_mesh_view mv;
+    mf_decimate_config cfg;
+    cudaStream_t stream = nullptr;
+    bool force_carry = false;
+    bool active = false;
+    const void* X_src = nullptr;
+    void* alias_tmp = nullptr;
+    int* d_diff = nullptr;
+    bool host_check = false;
+    size_t pbytes = 0;
+    int* h_status = nullptr;
+    std::vector<ProfRec>* graph_prof = nullptr;
+};
+
 // The caller's result buffers (mf_decimate_into) as k_emit jobs next to the copy-out; false when
 // one of them cannot be written by the device (pageable host memory) or is too small.
 static bool add_caller_jobs(EmitJobs& jobs, const mf_outputs* o, const double* P, const double* X, int64_t xc,
@@ -1209,14 +1261,21 @@ static bool add_caller_jobs(EmitJobs& jobs, const mf_outputs* o, const double* P
     return true;
 }
 
-int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,
-                 Result** out, mf_status* st, bool force_carry, const mf_outputs* outs) {
+// First half of a call: plan, stage, launch the round chain (nothing waits for the device).
+int decimate_begin(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,
+                   mf_status* st, bool force_carry, DecCall& call) {
+    call.mv = *mv;
+    call.cfg = *cfg;
+    call.stream = stream;
+    call.force_carry = force_carry;
     st->code = MF_OK;
     st->mesh_index = -1;
     st->achievable_vertices = 0;
     st->message[0] = 0;
-    Plan p;
+    HostClock hc;
+    Plan& p = call.p;
     if (make_plan(mv, cfg, p, st) != MF_OK) return st->code;
+    hc.mark("plan");
     const int B = p.B, R = p.R;
     const int64_t n = p.n, m = p.m, C = p.C;
     MF_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -1231,11 +1290,12 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     const void* P_src = mv->positions;
     const void* X_src = mv->features;
     void* alias_tmp = nullptr;
-    struct TmpFree {
+    struct TmpFree {  // freed here only if the call fails before the device work is launched
         void*& p;
         cudaStream_t s;
+        bool keep = false;
         ~TmpFree() {
-            if (p) cudaFreeAsync(p, s);
+            if (p && !keep) cudaFreeAsync(p, s);
         }
     } tmp_free{alias_tmp, stream};
     const size_t pbytes = (size_t)n * 24;
@@ -1262,7 +1322,7 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     }
 
     // ---- workspace (grown on demand; cached graphs are tied to the arena address)
-    WS W;
+    WS& W = call.W;
     {
         Arena meas;
         meas.measuring = true;
@@ -1408,13 +1468,52 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
                 MF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(ge.exec, ge.init_node, &kp));
             }
         }
+        hc.mark("pre-launch");
         MF_CUDA_TRY(cudaGraphLaunch(it->second.exec, stream));
+        hc.mark("graph-launch");
         g_launches += it->second.kernels;
         graph_prof = &it->second.prof;
     } else {
         record(ctx, p, W, stream);
         if (g_rec_err != cudaSuccess) return rec_fail();
     }
+    tmp_free.keep = true;
+    call.X_src = X_src;
+    call.alias_tmp = alias_tmp;
+    call.d_diff = d_diff;
+    call.host_check = host_check;
+    call.pbytes = pbytes;
+    call.h_status = h_status;
+    call.graph_prof = graph_prof;
+    call.active = true;
+    return MF_OK;
+}
+
+// Second half: result arrays (+ the caller's buffers), the readback and the one synchronisation.
+int decimate_end(Context* ctx, DecCall& call, const mf_outputs* outs, Result** out, mf_status* st) {
+    HostClock hc;
+    call.active = false;
+    const Plan& p = call.p;
+    WS& W = call.W;
+    const mf_mesh_view* mv = &call.mv;
+    const mf_decimate_config* cfg = &call.cfg;
+    cudaStream_t stream = call.stream;
+    const int B = p.B, R = p.R;
+    const int64_t n = p.n, m = p.m, C = p.C;
+    const void* X_src = call.X_src;
+    int* d_diff = call.d_diff;
+    const bool host_check = call.host_check;
+    const size_t pbytes = call.pbytes;
+    int* h_status = call.h_status;
+    std::vector<ProfRec>* graph_prof = call.graph_prof;
+    struct TmpFree {
+        void* p;
+        cudaStream_t s;
+        ~TmpFree() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } tmp_free{call.alias_tmp, stream};
+    MF_CUDA_TRY(cudaSetDevice(ctx->device));
     // ---- result: copy outputs out of the workspace
     Result* res = new Result();
     res->device = ctx->device;
@@ -1498,14 +1597,18 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
         MF_CUDA_TRY(cudaMemcpyAsync(&h_diff, d_diff, 4, cudaMemcpyDeviceToHost, stream));
     }
     if (host_check) h_diff = host_differ(mv->positions, mv->features, pbytes);  // while the GPU works
+    hc.mark("result-enqueued");
     // ---- single readback
     MF_CUDA_TRY(cudaMemcpyAsync(h_status, W.status, W.status_words * 4, cudaMemcpyDeviceToHost, stream));
     MF_CUDA_TRY(cudaStreamSynchronize(stream));
     MF_CUDA_TRY(cudaGetLastError());
+    hc.mark("synced");
     if (h_diff) {  // features of the positions' shape that differ from them: carry them
         cudaFreeAsync(res->block, stream);
         delete res;
-        return decimate_run(ctx, mv, cfg, stream, out, st, true, outs);
+        const mf_mesh_view mv2 = *mv;
+        const mf_decimate_config cfg2 = *cfg;
+        return decimate_run(ctx, &mv2, &cfg2, stream, out, st, true, outs);
     }
     if (graph_prof) prof_collect(*graph_prof);
     prof_collect_pending();
@@ -1577,6 +1680,18 @@ int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config*
     }
     *out = res;
     return MF_OK;
+}
+
+int decimate_run(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,
+                 Result** out, mf_status* st, bool force_carry, const mf_outputs* outs) {
+    st->code = MF_OK;
+    st->mesh_index = -1;
+    st->achievable_vertices = 0;
+    st->message[0] = 0;
+    DecCall call;
+    const int rc = decimate_begin(ctx, mv, cfg, stream, st, force_carry, call);
+    if (rc != MF_OK) return rc;
+    return decimate_end(ctx, call, outs, out, st);
 }
 
 }  // namespace mf

@@ -19,8 +19,11 @@ struct DevStatus {
     int pad;
 };
 
+struct DecCall;  // mf_decimate.cu: a call between mf_decimate_begin and mf_decimate_end
+
 struct Context {
     int device = 0;
+    DecCall* pending = nullptr;  // the begun, not yet ended call of this context
     int sm_count = 148;
     // workspace arena (grown on demand, kept across calls)
     void* arena = nullptr;
@@ -72,6 +75,9 @@ struct Result {
 
 int decimate_run(Context* ctx, const mf_mesh_view* mesh, const mf_decimate_config* cfg, cudaStream_t stream,
                  Result** out, mf_status* st, bool force_carry = false, const mf_outputs* outs = nullptr);
+int decimate_begin(Context* ctx, const mf_mesh_view* mv, const mf_decimate_config* cfg, cudaStream_t stream,
+                   mf_status* st, bool force_carry, DecCall& call);
+int decimate_end(Context* ctx, DecCall& call, const mf_outputs* outs, Result** out, mf_status* st);
 // device address the GPU can write for p (device memory, or pinned host memory's mapped
 // address); nullptr for pageable host memory
 void* device_writable(void* p);

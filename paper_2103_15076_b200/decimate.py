@@ -204,6 +204,9 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
         # front, emitted by the launch that fills the handle (mf_decimate_into, one synchronisation);
         # the facet buffer holds the input facet count and is narrowed to the output count
         n_out = int(config.target_vertices) * B
+        # the round chain is launched first; the pinned outputs are allocated while it runs
+        if _native.lib().mf_decimate_begin(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(st)):
+            _native.raise_for(st)
         pos = hostmem.empty((n_out, 3), np.float64)
         fac_cap = hostmem.empty((max(view.m, 1), 3), np.int64)
         feats = hostmem.empty((n_out, c), feats_dtype)
@@ -219,11 +222,11 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
         outs.replace = rep.ctypes.data if rep.size else None
         outs.mapping = mp.ctypes.data if mp.size else None
         outs.vertex_offsets, outs.facet_offsets = vo_out.ctypes.data, fo_out.ctypes.data
-        _native.lib().mf_decimate_into(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(outs),
-                                       ctypes.byref(handle), ctypes.byref(st))
-        _native.raise_for(st)
-        dec = _native.Decimation(handle, device)
-        fac = fac_cap[:dec.m_out]
+        if _native.lib().mf_decimate_end(ctx, ctypes.byref(outs), ctypes.byref(handle), ctypes.byref(st)):
+            _native.raise_for(st)
+        m_out = int(fo_out[-1])
+        dec = _native.Decimation(handle, device, (view.n, n_out, m_out, c, B))
+        fac = fac_cap[:m_out]
     else:  # the library raises the reference's error for an oversized target
         _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(handle),
                                   ctypes.byref(st))

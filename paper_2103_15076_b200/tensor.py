@@ -23,13 +23,22 @@ _POOL_MODES = ("average", "max", "weighted", "sum")
 
 
 class DeviceDecimation:
-    """Outputs of one device decimation plus the library handle (reused by pool/unpool)."""
+    """Outputs of one device decimation plus the library handle (reused by pool/unpool).
+    `nv` / `mf` (per-mesh output vertex / facet counts) are built from the offsets on first use."""
 
-    def __init__(self, dec, vertices, faces, features, nv, mf, replace, mapping):
+    def __init__(self, dec, vertices, faces, features, vo, fo, replace, mapping):
         self._dec = dec
         self.vertices, self.faces, self.features = vertices, faces, features
-        self.nv, self.mf = nv, mf
+        self._vo, self._fo = vo, fo
         self.replace, self.mapping = replace, mapping
+
+    @property
+    def nv(self):
+        return None if self._vo is None else torch.from_numpy(np.diff(self._vo))
+
+    @property
+    def mf(self):
+        return None if self._fo is None else torch.from_numpy(np.diff(self._fo))
 
     @property
     def n_vertices_out(self) -> int:
@@ -110,12 +119,15 @@ def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, targ
                                   ctypes.byref(handle), ctypes.byref(st))
         _native.raise_for(st)
         return DeviceDecimation(_native.Decimation(handle, dev.index), None, None, None, None, None, None, None)
-    # every entry ends at exactly `target` vertices (or the call raises): the outputs are allocated
-    # up front and emitted by the same launch that fills the handle (mf_decimate_into); the facet
-    # buffer holds the input facet count and is narrowed to the output count afterwards
+    # the round chain is launched first (mf_decimate_begin); the result tensors are allocated while
+    # it runs -- every entry ends at exactly `target` vertices or the call raises, and the facet
+    # buffer holds the input facet count -- and mf_decimate_end emits into them, synchronising once
     B = 1 if vo is None else len(vo) - 1
     n_out = int(target) * B
     c = view.c
+    if _native.lib().mf_decimate_begin(ctx, ctypes.byref(view), ctypes.byref(cfg), ctypes.c_void_p(stream),
+                                       ctypes.byref(st)):
+        _native.raise_for(st)
     V = torch.empty((n_out, 3), dtype=torch.float64, device=dev)
     Fo = torch.empty((max(view.m, 1), 3), dtype=torch.int64, device=dev)
     X = torch.empty((n_out, c), dtype=torch.float64, device=dev)
@@ -123,21 +135,15 @@ def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, targ
     Mp = torch.empty(view.n, dtype=torch.int64, device=dev)
     vo_out = np.empty(B + 1, dtype=np.int64)
     fo_out = np.empty(B + 1, dtype=np.int64)
-    outs = _native.Outputs()
-    outs.positions = V.data_ptr() if V.numel() else None
-    outs.facets, outs.facets_capacity = Fo.data_ptr(), Fo.shape[0]
-    outs.features, outs.features_dtype = (X.data_ptr() if X.numel() else None), _native.DTYPE_F64
-    outs.replace = R.data_ptr() if R.numel() else None
-    outs.mapping = Mp.data_ptr() if Mp.numel() else None
-    outs.vertex_offsets, outs.facet_offsets = vo_out.ctypes.data, fo_out.ctypes.data
-    _native.lib().mf_decimate_into(ctx, ctypes.byref(view), ctypes.byref(cfg), ctypes.c_void_p(stream),
-                                   ctypes.byref(outs), ctypes.byref(handle), ctypes.byref(st))
-    _native.raise_for(st)
-    dec = _native.Decimation(handle, dev.index)
-    Fo = Fo[:dec.m_out]
-    nv_out = torch.from_numpy(np.diff(vo_out))
-    mf_out = torch.from_numpy(np.diff(fo_out))
-    return DeviceDecimation(dec, V, Fo, X, nv_out, mf_out, R, Mp)
+    outs = _native.Outputs(V.data_ptr() if n_out else None, Fo.data_ptr(), Fo.shape[0],
+                           X.data_ptr() if n_out * c else None, _native.DTYPE_F64, 0,
+                           R.data_ptr() if view.n else None, Mp.data_ptr() if view.n else None,
+                           vo_out.ctypes.data, fo_out.ctypes.data)
+    if _native.lib().mf_decimate_end(ctx, ctypes.byref(outs), ctypes.byref(handle), ctypes.byref(st)):
+        _native.raise_for(st)
+    m_out = int(fo_out[-1])
+    dec = _native.Decimation(handle, dev.index, (view.n, n_out, m_out, c, B))
+    return DeviceDecimation(dec, V, Fo[:m_out], X, vo_out, fo_out, R, Mp)
 
 
 def pool(features: torch.Tensor, dd: DeviceDecimation, mode: str = "average", weights=None) -> torch.Tensor:

@@ -60,3 +60,33 @@ def test_outputs_are_read_only_and_copies_upload():
     r2 = mfg.decimate_parallel(moved, mfg.DecimationConfig(target_vertices=3_000), device=0)
     r3 = mfg.decimate_parallel(_fresh(moved), mfg.DecimationConfig(target_vertices=3_000), device=0)
     assert np.array_equal(r2.mesh.positions, r3.mesh.positions) and np.array_equal(r2.replace, r3.replace)
+
+
+def test_begin_end_split_and_abandoned_call():
+    """mf_decimate_begin / _end (the APIs launch before allocating their outputs): equal to the
+    one-shot call; a begun call that is never ended is finished by the next begin."""
+    import ctypes
+
+    import torch
+
+    from paper_2103_15076_b200 import _native
+    from paper_2103_15076_b200 import tensor as T
+
+    mesh = S.delaunay_terrain(30_000, noise=0.02, seed=9)
+    V = torch.from_numpy(mesh.positions).cuda()
+    F = torch.from_numpy(mesh.facets).cuda()
+    ref = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=9_000), device=0)
+    dd = T.decimate(V, F, target=9_000)
+    assert np.array_equal(dd.replace.cpu().numpy(), ref.replace)
+    assert np.array_equal(dd.faces.cpu().numpy(), ref.mesh.facets)
+    # abandon a begun call, then decimate again on the same context
+    view = _native.MeshView()
+    view.positions, view.facets, view.n, view.m, view.c = V.data_ptr(), F.data_ptr(), V.shape[0], F.shape[0], 3
+    cfg = D._make_config(mfg.DecimationConfig(target_vertices=9_000))
+    st = _native.Status()
+    assert _native.lib().mf_decimate_begin(_native.context(0), ctypes.byref(view), ctypes.byref(cfg),
+                                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                           ctypes.byref(st)) == 0
+    dd2 = T.decimate(V, F, target=9_000)
+    assert np.array_equal(dd2.replace.cpu().numpy(), ref.replace)
+    assert torch.equal(dd2.nv, torch.tensor([9_000])) and int(dd2.mf[0]) == ref.mesh.n_facets
