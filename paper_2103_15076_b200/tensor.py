@@ -12,12 +12,14 @@ torch is only the allocator / stream here; all compute runs in libmfgpu.so.
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 import torch
 
 from . import _native
 from .decimate import DecimationConfig, _make_config
+from .numerics import einsum_order
 
 _POOL_MODES = ("average", "max", "weighted", "sum")
 
@@ -57,6 +59,19 @@ def _offsets(counts, total) -> np.ndarray:
     if off[-1] != total:
         raise ValueError(f"counts sum to {off[-1]}, expected {total}")
     return off
+
+
+@functools.lru_cache(maxsize=64)
+def _config(target, placement, seed, rounds, order):
+    """The validated mf_decimate_config of these settings (the C side copies it; order = the
+    host's numpy reduction order, part of the key because tests may force it)."""
+    return _make_config(DecimationConfig(target_vertices=target, placement=placement, shuffle_seed=seed,
+                                         rounds=rounds))
+
+
+def _current_stream(index: int) -> int:
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    return raw(index) if raw is not None else torch.cuda.current_stream(index).cuda_stream
 
 
 def _dtype_code(t: torch.Tensor, what: str) -> int:
@@ -108,9 +123,8 @@ def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, targ
     fo = _offsets(mf, view.m)
     if vo is not None:
         view.vertex_offsets, view.facet_offsets, view.n_meshes = vo.ctypes.data, fo.ctypes.data, len(vo) - 1
-    cfg = _make_config(DecimationConfig(target_vertices=target, placement=placement, shuffle_seed=seed,
-                                        rounds=rounds))
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    cfg = _config(int(target), placement, seed, rounds, einsum_order())
+    stream = _current_stream(dev.index)
     ctx = _native.context(dev.index)
     handle = ctypes.c_void_p()
     st = _native.Status()
@@ -167,7 +181,7 @@ def pool(features: torch.Tensor, dd: DeviceDecimation, mode: str = "average", we
     _native.lib().mf_pool(
         _native.context(dev.index), dd._dec.handle, None, dd._dec.n_in, dd._dec.n_out, features.data_ptr(),
         code, features.shape[1], _POOL_MODES.index(mode), None if w is None else w.data_ptr(), out.data_ptr(),
-        ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), ctypes.byref(st))
+        ctypes.c_void_p(_current_stream(dev.index)), ctypes.byref(st))
     _native.raise_for(st)
     return out
 
@@ -183,7 +197,7 @@ def unpool(coarse: torch.Tensor, dd: DeviceDecimation) -> torch.Tensor:
     st = _native.Status()
     _native.lib().mf_unpool(
         _native.context(dev.index), dd._dec.handle, None, dd._dec.n_in, dd._dec.n_out, coarse.data_ptr(),
-        code, coarse.shape[1], out.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream),
+        code, coarse.shape[1], out.data_ptr(), ctypes.c_void_p(_current_stream(dev.index)),
         ctypes.byref(st))
     _native.raise_for(st)
     return out
