@@ -215,6 +215,16 @@ static int vertex_scan() {
     return v;
 }
 
+// MF_ZERO_COPY_IN=0: pinned host inputs are staged by a copy instead of read in place
+static bool zero_copy_inputs() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_ZERO_COPY_IN");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // MF_EDGES_RANK=1: unseeded rounds through the fused k_edges_rank instead of k_edges +
 // k_adj_rank_tiled.  Opt-in: measured slower on B200 (r2n, 92 registers / 8 lanes per vertex:
 // cfg2 0.557 vs 0.501 ms, cfg5 18.4 vs 12.0 ms) -- every pair cost evaluated twice plus a
@@ -1374,15 +1384,23 @@ int decimate_begin(Context* ctx, const mf_mesh_view* mv, const mf_decimate_confi
     // Device-resident inputs of a real chain are read in place by k_init_inputs (its graph node is
     // re-pointed per call); host inputs are uploaded into the staging buffers it reads instead.
     MF_CUDA_TRY(cudaMemcpyAsync(W.params, hp, W.upload_bytes, cudaMemcpyHostToDevice, stream));
-    const bool in_place = R > 0 && (n == 0 || is_device_ptr(P_src)) && (m == 0 || is_device_ptr(mv->facets));
+    // pinned host inputs may be read in place too, through their mapped addresses (the conversion
+    // kernel then streams them over the link itself: no staging copy; MF_ZERO_COPY_IN=0 stages)
+    auto readable = [&](const void* q) -> const void* {
+        if (is_device_ptr(q)) return q;
+        return zero_copy_inputs() ? device_writable(const_cast<void*>(q)) : nullptr;
+    };
+    const void* P_dev = (R > 0 && n) ? readable(P_src) : nullptr;
+    const void* F_dev = (R > 0 && m) ? readable(mv->facets) : nullptr;
+    const bool in_place = R > 0 && (n == 0 || P_dev) && (m == 0 || F_dev);
     if (mv->facets_i32 && (!in_place || R == 0)) {
         st->code = MF_ERR_VALUE;
         snprintf(st->message, sizeof(st->message),
                  "int32 facets (facets_i32) must be device arrays of a call with at least one round");
         return st->code;
     }
-    g_in_P = in_place && n ? (const double*)P_src : nullptr;
-    g_in_F64 = in_place && m ? (const void*)mv->facets : nullptr;
+    g_in_P = in_place && n ? (const double*)P_dev : nullptr;
+    g_in_F64 = in_place && m ? F_dev : nullptr;
     g_in_f32 = mv->facets_i32 ? 1 : 0;
     if (!in_place) {
         if (n) MF_CUDA_TRY(cudaMemcpyAsync(W.P0, P_src, (size_t)n * 24, cudaMemcpyDefault, stream));

@@ -90,3 +90,34 @@ def test_begin_end_split_and_abandoned_call():
     dd2 = T.decimate(V, F, target=9_000)
     assert np.array_equal(dd2.replace.cpu().numpy(), ref.replace)
     assert torch.equal(dd2.nv, torch.tensor([9_000])) and int(dd2.mf[0]) == ref.mesh.n_facets
+
+
+@pytest.mark.parametrize("zero_copy", ["1", "0"])
+def test_pinned_host_inputs_read_in_place(zero_copy):
+    """Pinned host inputs are read by the conversion kernel through their mapped addresses (no
+    staging copy, MF_ZERO_COPY_IN=1) -- same bytes as staged and as pageable inputs."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import sys
+sys.path.insert(0, %r)
+import numpy as np, torch
+import paper_2103_15076_b200 as mfg
+from paper_2103_15076_b200 import synthetic as S
+mesh = S.delaunay_terrain(40_000, noise=0.02, seed=2)
+P = torch.empty((mesh.n_vertices, 3), dtype=torch.float64, pin_memory=True).numpy(); P[:] = mesh.positions
+F = torch.empty((mesh.n_facets, 3), dtype=torch.int64, pin_memory=True).numpy(); F[:] = mesh.facets
+cfg = mfg.DecimationConfig(target_vertices=12_000, shuffle_seed=4)
+a = mfg.decimate_parallel(mfg.TriMesh(P, F), cfg)
+b = mfg.decimate_parallel(mesh, cfg)
+for x, y in ((a.replace, b.replace), (a.mapping, b.mapping), (a.mesh.facets, b.mesh.facets),
+             (a.mesh.positions, b.mesh.positions)):
+    assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+print("PINNED-OK")
+''' % root
+    out = subprocess.run([sys.executable, "-c", script], cwd=root, env={**os.environ, "MF_ZERO_COPY_IN": zero_copy},
+                         capture_output=True, text=True, timeout=300)
+    assert "PINNED-OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
