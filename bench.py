@@ -517,7 +517,9 @@ def run_ours(args):
             res = mfg.decimate_parallel(cur, mfg.DecimationConfig(target_vertices=tgt))
             outs.append(res)
             o = res.mesh.mesh if batched else res.mesh
-            d2h += o.positions.nbytes + o.facets.nbytes + o.features.nbytes + res.replace.nbytes + res.mapping.nbytes
+            d2h += o.positions.nbytes + o.facets.nbytes + res.replace.nbytes + res.mapping.nbytes
+            if not np.shares_memory(o.features, o.positions):  # features that ARE the positions share it
+                d2h += o.features.nbytes
             if X is not None:
                 X = mfg.pool(X, res, mode="max")
                 d2h += X.nbytes

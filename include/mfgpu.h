@@ -108,7 +108,10 @@ typedef struct mf_outputs {
     int64_t facets_capacity;   /* rows available in facets (>= the input facet count) */
     void *features;            /* [n_out, c] of features_dtype */
     int32_t features_dtype;    /* MF_DTYPE_* */
-    int32_t reserved;
+    int32_t features_if_distinct; /* 1: leave `features` unwritten when the result's features are
+                                     known to be the positions bitwise (omitted input features, or
+                                     host features equal to the positions); the caller then shares
+                                     the positions' array -- mf_decimation_device_arrays reports it */
     int64_t *replace;          /* [n_in] int64 */
     int64_t *mapping;          /* [n_in] int64 */
     int64_t *vertex_offsets;   /* host [n_meshes + 1] */

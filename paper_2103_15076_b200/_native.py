@@ -56,7 +56,7 @@ class Outputs(ctypes.Structure):
         ("facets_capacity", ctypes.c_int64),
         ("features", ctypes.c_void_p),
         ("features_dtype", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("features_if_distinct", ctypes.c_int32),
         ("replace", ctypes.c_void_p),
         ("mapping", ctypes.c_void_p),
         ("vertex_offsets", ctypes.c_void_p),
@@ -231,6 +231,13 @@ class Decimation:
             except Exception:
                 pass
             self.handle = None
+
+
+def features_alias(dec) -> bool:
+    """Whether a result's features are its positions bitwise (then not emitted separately)."""
+    alias = _i32()
+    lib().mf_decimation_device_arrays(dec.handle, None, None, ctypes.byref(alias))
+    return bool(alias.value)
 
 
 def round_stats(dec) -> list:

@@ -1532,6 +1532,16 @@ int decimate_end(Context* ctx, DecCall& call, const mf_outputs* outs, Result** o
         }
     } tmp_free{call.alias_tmp, stream};
     MF_CUDA_TRY(cudaSetDevice(ctx->device));
+    // host features checked against the positions while the round chain still runs; features
+    // known to BE the positions need not be emitted when the caller shares the positions' array
+    const int host_diff = host_check ? (int)host_differ(mv->positions, mv->features, pbytes) : 0;
+    const bool alias_known = p.alias && (!mv->features || (host_check && !host_diff));
+    mf_outputs outs_local;
+    if (outs && outs->features_if_distinct == 1 && alias_known) {
+        outs_local = *outs;
+        outs_local.features = nullptr;
+        outs = &outs_local;
+    }
     // ---- result: copy outputs out of the workspace
     Result* res = new Result();
     res->device = ctx->device;
@@ -1614,7 +1624,7 @@ int decimate_end(Context* ctx, DecCall& call, const mf_outputs* outs, Result** o
                (const unsigned long long*)X_src, d_diff);
         MF_CUDA_TRY(cudaMemcpyAsync(&h_diff, d_diff, 4, cudaMemcpyDeviceToHost, stream));
     }
-    if (host_check) h_diff = host_differ(mv->positions, mv->features, pbytes);  // while the GPU works
+    if (host_check) h_diff = host_diff;
     hc.mark("result-enqueued");
     // ---- single readback
     MF_CUDA_TRY(cudaMemcpyAsync(h_status, W.status, W.status_words * 4, cudaMemcpyDeviceToHost, stream));

@@ -219,6 +219,10 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
         outs.facets, outs.facets_capacity = fac_cap.ctypes.data, fac_cap.shape[0]
         outs.features = feats.ctypes.data if feats.size else None
         outs.features_dtype = _native.DTYPE_F32 if feats_dtype == np.float32 else _native.DTYPE_F64
+        # features that turn out to be the positions (the default) are not copied out: the result
+        # shares the (read-only) positions array
+        share = c == 3 and feats_dtype == np.float64
+        outs.features_if_distinct = int(share)
         outs.replace = rep.ctypes.data if rep.size else None
         outs.mapping = mp.ctypes.data if mp.size else None
         outs.vertex_offsets, outs.facet_offsets = vo_out.ctypes.data, fo_out.ctypes.data
@@ -227,6 +231,8 @@ def decimate_parallel(mesh, config: DecimationConfig, device: int | None = None)
         m_out = int(fo_out[-1])
         dec = _native.Decimation(handle, device, (view.n, n_out, m_out, c, B))
         fac = fac_cap[:m_out]
+        if share and _native.features_alias(dec):
+            feats = pos
     else:  # the library raises the reference's error for an oversized target
         _native.lib().mf_decimate(ctx, ctypes.byref(view), ctypes.byref(cfg), None, ctypes.byref(handle),
                                   ctypes.byref(st))

@@ -149,14 +149,18 @@ def decimate(vertices: torch.Tensor, faces: torch.Tensor, nv=None, mf=None, targ
     Mp = torch.empty(view.n, dtype=torch.int64, device=dev)
     vo_out = np.empty(B + 1, dtype=np.int64)
     fo_out = np.empty(B + 1, dtype=np.int64)
+    # features that turn out to be the positions (the default) share the positions' tensor
+    share = c == 3
     outs = _native.Outputs(V.data_ptr() if n_out else None, Fo.data_ptr(), Fo.shape[0],
-                           X.data_ptr() if n_out * c else None, _native.DTYPE_F64, 0,
+                           X.data_ptr() if n_out * c else None, _native.DTYPE_F64, int(share),
                            R.data_ptr() if view.n else None, Mp.data_ptr() if view.n else None,
                            vo_out.ctypes.data, fo_out.ctypes.data)
     if _native.lib().mf_decimate_end(ctx, ctypes.byref(outs), ctypes.byref(handle), ctypes.byref(st)):
         _native.raise_for(st)
     m_out = int(fo_out[-1])
     dec = _native.Decimation(handle, dev.index, (view.n, n_out, m_out, c, B))
+    if share and _native.features_alias(dec):
+        X = V
     return DeviceDecimation(dec, V, Fo[:m_out], X, vo_out, fo_out, R, Mp)
 
 
