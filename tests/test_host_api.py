@@ -1,12 +1,11 @@
 """Host-side boundary logic that needs no device: config validation, mesh
 containers and their error types (reference decimate.py:45-71,
-mesh.py:13-205, validation.py:8-65, io.py:434-457, runtime.py)."""
+mesh.py:13-205, validation.py:8-65, io.py:434-457)."""
 
 import numpy as np
 import pytest
 
 import paper_2103_15076_b200 as mfg
-from paper_2103_15076_b200 import runtime
 from paper_2103_15076_b200.numerics import einsum_order
 
 
@@ -51,14 +50,6 @@ def test_concat_and_split_roundtrip():
         mfg.BatchedMesh(batch.mesh, [0, 2, 6], [0, 1, 2])
     with pytest.raises(ValueError):
         mfg.concat_batch([])
-
-
-def test_worker_count(monkeypatch):
-    monkeypatch.setenv(runtime.THREADS_ENV, "3")
-    assert runtime.worker_count() == 3
-    monkeypatch.setenv(runtime.THREADS_ENV, "x")
-    with pytest.raises(ValueError):
-        runtime.worker_count()
 
 
 def test_einsum_order_probe_matches_numpy():
