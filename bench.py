@@ -602,7 +602,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "facets/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": vs, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "facets_in": m_in, "vertices_in": n_in, "levels": levels,
+        "config": {"workload": wl["desc"], "facets_in": m_in, "facets_total": int(total_facets), "vertices_in": n_in, "levels": levels,
                    "rounds": len(rounds), "l2": "flushed between timed steps (512 MiB memset, outside events)",
                    "parallelism": f"{world} GPUs, independent work per GPU, no collective" if world > 1 else "1 GPU"},
         "clocks": clk.summary(),
