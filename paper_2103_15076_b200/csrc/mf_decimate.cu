@@ -104,11 +104,15 @@ static void rec_check(cudaError_t e, int line) {
 // every launch carries the programmatic-stream-serialization attribute, so the
 // captured graph's kernel->kernel edges are programmatic (PDL) edges.
 thread_local bool g_pdl = false;
-static bool pdl_enabled() {  // measured a few % slower at cfg2 on B200, so opt-in (MF_PDL=1)
+// Programmatic dependent launch on the graph's kernel->kernel edges: each node's launch overlaps
+// its predecessor's tail.  Default on since round 2 (r2z: cfg2 0.4433 / 0.4432 vs 0.4458 / 0.4472
+// ms, cfg5 11.48 vs 11.52 ms; measured a few % slower in round 1, before the graph lost its
+// memset / memcpy nodes); MF_PDL=0 turns it off.
+static bool pdl_enabled() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MF_PDL");
-        v = (e && e[0] == '1') ? 1 : 0;
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
 }

@@ -59,9 +59,9 @@ VARIANTS = [
     {"MF_SEL_CAP": "12288"},
     {"MF_SEL_PASSES": "1", "MF_LD1_MIN": "1"},
     {"MF_GRAPHS": "0"},
-    {"MF_PDL": "1"},
-    {"MF_COND": "1"},
-    {"MF_LD_MIN": "1", "MF_COND": "1"},
+    {"MF_PDL": "0"},
+    {"MF_COND": "1", "MF_PDL": "0"},
+    {"MF_LD_MIN": "1", "MF_COND": "1", "MF_PDL": "0"},
     # size-gated branches that the defaults take only at cfg5 scale, forced at small sizes
     {"MF_WIDE_MIN": "0"},
     {"MF_SCAN4_MIN": "0"},
