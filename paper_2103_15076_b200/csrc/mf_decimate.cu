@@ -219,6 +219,17 @@ static int vertex_scan() {
     return v;
 }
 
+// unseeded rounds from this many vertices take the two-pass adjacency (k_edges lite + k_adj_build);
+// MF_TWO_PASS_MIN overrides (0 = always, a huge value = never)
+static int two_pass_min() {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("MF_TWO_PASS_MIN");
+        v = e ? std::max(0, atoi(e)) : (1 << 20);
+    }
+    return v;
+}
+
 // MF_ZERO_COPY_IN=0: pinned host inputs are staged by a copy instead of read in place
 static bool zero_copy_inputs() {
     static int v = -1;
@@ -875,6 +886,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         const int ld_rounds = N >= p.ld_min ? p.ld_big : (N >= p.ld1_min ? p.ld_mid : 0);
         const bool use_ld = ld_rounds > 0;
         const bool fused_rank = !seeded && edges_rank();
+        // unseeded large rounds: edge arrays only, then k_adj_build (no lower-slot atomics / re-sort)
+        const bool two_pass = !seeded && !fused_rank && N >= two_pass_min();
         if (fused_rank) {  // edges + costs + rank-ordered adjacency in one pass (k_edges_rank)
             EdgeRankOut ro{W.e0,   W.e1,       W.key_hi, W.snbr,    W.adj_eid, W.adj_k32, W.acur,
                            use_ld ? W.best : nullptr, W.bestu, W.mate, W.minrep, W.absorbed, W.abshead,
@@ -892,7 +905,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             EdgeOut eo{W.e0,      W.e1,   seeded ? W.cost : nullptr, nullptr, seeded ? W.snbr : W.e1,
                        seeded ? W.adj_eid : W.seid_u, seeded ? nullptr : W.key_hi,
                        W.lowfill, W.mate, W.minrep, W.absorbed, W.abshead, W.suitor, W.mlo, W.mhi,
-                       W.segA,    W.ldc,  W.segB};
+                       W.segA,    W.ldc,  W.segB, two_pass ? 1 : 0};
             const int eg = grid_for(ctx, (int64_t)N * kEdgeLanes);
             if (p.placement)
                 LAUNCH(k_edges<1>, eg, 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.aoff, W.eoff, W.vq,
@@ -910,7 +923,10 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // large meshes: locally-dominant rounds first (round 0's picks written by k_adj_rank /
         // k_edges_rank), then Suitor proposals on the residual frontier; smaller meshes: Suitor only
         if (fused_rank) {
-        } else if (seeded)
+        } else if (two_pass)
+            LAUNCH(k_adj_build, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.inc_off, W.nbr, W.ucnt, W.upcnt, W.aoff,
+                   W.key_hi, W.snbr, W.adj_eid, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
+        else if (seeded)
             LAUNCH(k_adj_rank<true>, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.aoff, W.ucnt, W.snbr, W.adj_eid,
                    nullptr, W.key_hi, W.key_lo, W.adj_k32, W.acur, use_ld ? W.best : nullptr, W.bestu);
         else
@@ -1096,7 +1112,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
-                              vt16(1), vt16(1 << 21),
+                              vt16(1), vt16(1 << 21), two_pass_min(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);

@@ -529,6 +529,8 @@ struct EdgeOut {
     int* seg_cnt;
     int* ldc;
     int* seg_cnt2;  // absorb-candidate segments (appended while the truncation runs)
+    int lite;       // unseeded two-pass form: only the edge arrays (e0, e1 / key_hi at the edge id);
+                    // k_adj_build assembles the rank-ordered adjacency (no lower-slot atomics)
 };
 
 constexpr int kEdgeLanes = 4;
@@ -585,11 +587,14 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
             const double ux = P[3 * u], uy = P[3 * u + 1], uz = P[3 * u + 2];
             // the other end's slot: its atomic and the key-independent stores go out while the
             // quadric gathers are in flight
-            const size_t su = (size_t)aoff[u] + atomicAdd(o.lowfill + u, 1);
+            size_t su = 0;
+            if (!o.lite) {
+                su = (size_t)aoff[u] + atomicAdd(o.lowfill + u, 1);
+                o.seid[s2 + j] = eid;
+                o.snbr[su] = v;
+                o.seid[su] = eid;
+            }
             o.snbr[s2 + j] = u;
-            o.seid[s2 + j] = eid;
-            o.snbr[su] = v;
-            o.seid[su] = eid;
             const double c = pair_cost<PLACEMENT>(qv, qu, px, py, pz, ux, uy, uz, order);
             // unseeded: the rank key IS the order-preserving cost (f64_key is invertible, so no
             // cost array), and the slot arrays double as e1 / key_hi (o.snbr = e1, o.skey = key_hi:
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges(const int* __r
             }
             if (!seeded) {
                 o.skey[s2 + j] = key;
-                o.skey[su] = key;
+                if (!o.lite) o.skey[su] = key;
             }
         }
     }
@@ -738,6 +743,131 @@ __global__ void __launch_bounds__(256, PLACEMENT ? 1 : 4) k_edges_rank(const int
                 o.best[v] = nu ? be : -1;
                 o.bestu[v] = nu ? bu : -1;
             }
+        }
+    }
+}
+
+// K4b (unseeded two-pass form): the rank-ordered adjacency assembled from the edge arrays k_edges
+// wrote in its lite form.  Thread per vertex: an upper neighbour's edge id is the vertex's own
+// slot; a lower neighbour u's is u's slot of this vertex (aoff[u] + the position of v in u's
+// sorted neighbour list -- a binary search of a few L1/L2-resident ints); the rank key is
+// key_hi[edge].  Degree <= 8 is sorted in registers by (key, edge id); larger degrees keep
+// neighbour order (acur = -1) with the argmin as the LD round-0 pick.  A block's 256 vertices'
+// slots are staged in shared memory and written out coalesced.  Replaces the lower-slot atomics
+// and scattered slot writes of k_edges and the re-read of k_adj_rank_tiled.
+constexpr int kBuildCap = 2048;  // staged slots per block (256 vertices of mean degree <= 8)
+MF_DEV int slot_of_lower(const int* __restrict__ nbr, const int* __restrict__ inc_off, const int* __restrict__ ucnt,
+                         const int* __restrict__ aoff, int u, int v) {
+    const int* lu = nbr + 2 * (size_t)inc_off[u];
+    int a = 0, z = ucnt[u];
+    while (a < z) {
+        const int m = (a + z) >> 1;
+        if (lu[m] < v) a = m + 1; else z = m;
+    }
+    return aoff[u] + a;
+}
+
+__global__ void __launch_bounds__(256) k_adj_build(const int* __restrict__ abort_flag, int N,
+                                                   const int* __restrict__ inc_off, const int* __restrict__ nbr,
+                                                   const int* __restrict__ ucnt, const int* __restrict__ upcnt,
+                                                   const int* __restrict__ aoff, const uint64_t* __restrict__ key_hi,
+                                                   int* __restrict__ snbr, int* __restrict__ seid,
+                                                   unsigned* __restrict__ adj_k32, int* __restrict__ acur,
+                                                   int* __restrict__ best, int* __restrict__ bestu) {
+    MF_PDL_ENTRY;
+    if (*abort_flag) return;
+    __shared__ int s_n[kBuildCap];
+    __shared__ int s_e[kBuildCap];
+    __shared__ unsigned s_32[kBuildCap];
+    const int T = blockDim.x;
+    for (int v0 = blockIdx.x * T; v0 < N; v0 += gridDim.x * T) {
+        const int v1 = min(N, v0 + T);
+        const int base = aoff[v0], cnt = aoff[v1] - base;
+        const bool staged = cnt <= kBuildCap;  // block-uniform
+        const int v = v0 + threadIdx.x;
+        if (v < v1) {
+            const int nu = ucnt[v], nlow = nu - upcnt[v];
+            const int s2 = aoff[v];
+            const size_t sn = 2 * (size_t)inc_off[v];
+            int* on = staged ? s_n + (s2 - base) : snbr + s2;
+            int* oe = staged ? s_e + (s2 - base) : seid + s2;
+            unsigned* ok = staged ? s_32 + (s2 - base) : adj_k32 + s2;
+            if (nu <= 8) {
+                uint64_t h[8];
+                unsigned lo[8];
+                int u[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    h[i] = ~0ull;
+                    lo[i] = ~0u;
+                    u[i] = -1;
+                    if (i < nu) {
+                        u[i] = nbr[sn + i];
+                        const int e = i >= nlow ? s2 + i : slot_of_lower(nbr, inc_off, ucnt, aoff, u[i], v);
+                        lo[i] = (unsigned)e;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    if (i < nu) h[i] = key_hi[lo[i]];
+#pragma unroll
+                for (int k = 2; k <= 8; k <<= 1) {
+#pragma unroll
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            const int ixj = i ^ j;
+                            if (ixj > i) {
+                                const bool up = ((i & k) == 0);
+                                const bool gt = h[i] > h[ixj] || (h[i] == h[ixj] && lo[i] > lo[ixj]);
+                                if (gt == up) {
+                                    uint64_t th = h[i]; h[i] = h[ixj]; h[ixj] = th;
+                                    unsigned tl = lo[i]; lo[i] = lo[ixj]; lo[ixj] = tl;
+                                    int tu = u[i]; u[i] = u[ixj]; u[ixj] = tu;
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    if (i < nu) {
+                        on[i] = u[i];
+                        oe[i] = (int)lo[i];
+                        ok[i] = (unsigned)(h[i] >> 32);
+                    }
+                acur[v] = 0;
+                if (best) {
+                    best[v] = nu ? (int)lo[0] : -1;
+                    bestu[v] = nu ? u[0] : -1;
+                }
+            } else {
+                uint64_t bh = ~0ull, bl = ~0ull;
+                int be = -1, bu = -1;
+                for (int i = 0; i < nu; i++) {
+                    const int ui = nbr[sn + i];
+                    const int e = i >= nlow ? s2 + i : slot_of_lower(nbr, inc_off, ucnt, aoff, ui, v);
+                    const uint64_t hk = key_hi[e];
+                    on[i] = ui;
+                    oe[i] = e;
+                    ok[i] = (unsigned)(hk >> 32);
+                    if (key_lt(hk, (uint64_t)(unsigned)e, bh, bl)) bh = hk, bl = (uint64_t)(unsigned)e, be = e, bu = ui;
+                }
+                acur[v] = -1;
+                if (best) {
+                    best[v] = be;
+                    bestu[v] = bu;
+                }
+            }
+        }
+        if (staged) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < cnt; i += T) {
+                snbr[base + i] = s_n[i];
+                seid[base + i] = s_e[i];
+                adj_k32[base + i] = s_32[i];
+            }
+            __syncthreads();
         }
     }
 }

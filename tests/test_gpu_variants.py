@@ -69,6 +69,8 @@ VARIANTS = [
     {"MF_BIG_SEL_MIN": "0", "MF_SEL_PASSES": "1"},
     {"MF_WIDE_MIN": "0", "MF_SCAN4_MIN": "0", "MF_BIG_SEL_MIN": "0", "MF_LD_MIN": "1", "MF_SUITOR": "1"},
     {"MF_FUSE_PLANE": "0"},
+    {"MF_TWO_PASS_MIN": "0"},
+    {"MF_TWO_PASS_MIN": "0", "MF_LD_MIN": "1"},
     {"MF_VT16": "1"},
     {"MF_EDGES_RANK": "1"},
     {"MF_EDGES_RANK": "1", "MF_LD_MIN": "1"},
