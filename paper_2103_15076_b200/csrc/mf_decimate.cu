@@ -17,6 +17,7 @@
 // because a zero-budget round is not an identity (it drops duplicate facets
 // and normalises -0.0), see SURVEY.md App. C.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -219,13 +220,15 @@ static int vertex_scan() {
     return v;
 }
 
-// unseeded rounds from this many vertices take the two-pass adjacency (k_edges lite + k_adj_build);
-// MF_TWO_PASS_MIN overrides (0 = always, a huge value = never)
+// MF_TWO_PASS_MIN=k: unseeded rounds from k vertices take the two-pass adjacency (k_edges lite +
+// k_adj_build) instead of the lower-slot atomics + k_adj_rank_tiled.  Opt-in (default never):
+// measured (r3c) cfg5 11.90 vs 11.74 ms -- k_edges 2.22 -> 1.78 ms, but k_adj_build's per-slot
+// binary searches cost 1.67 vs 1.06 ms for k_adj_rank_tiled; cfg2 0.493 vs 0.449 ms (k = 0)
 static int two_pass_min() {
     static int v = -2;
     if (v == -2) {
         const char* e = getenv("MF_TWO_PASS_MIN");
-        v = e ? std::max(0, atoi(e)) : (1 << 20);
+        v = e ? std::max(0, atoi(e)) : INT_MAX;
     }
     return v;
 }
