@@ -134,14 +134,17 @@ static cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 }
 
 #ifndef LAUNCH
-#define LAUNCH(kernel, grid, block, smem, stream, ...)                                            \
+// LAUNCH_AS: a kernel picked at run time (a function pointer) under a fixed profiling name
+#define LAUNCH_AS(name, kernel, grid, block, smem, stream, ...)                                   \
     do {                                                                                          \
-        prof_pre(#kernel, stream);                                                                \
+        prof_pre(name, stream);                                                                   \
         rec_check(launch_ex(kernel, dim3(grid), dim3(block), (smem), (stream), __VA_ARGS__),      \
                   __LINE__);                                                                      \
-        prof_post(#kernel, stream);                                                               \
+        prof_post(name, stream);                                                                  \
         g_launches++;                                                                             \
     } while (0)
+#define LAUNCH(kernel, grid, block, smem, stream, ...) \
+    LAUNCH_AS(#kernel, kernel, grid, block, smem, stream, __VA_ARGS__)
 #endif
 
 // Suitor variant per round size: 8 lanes per proposer below 2^18 vertices (more warps to hide
@@ -228,6 +231,18 @@ static int two_pass_min() {
     static int v = -2;
     if (v == -2) {
         const char* e = getenv("MF_TWO_PASS_MIN");
+        v = e ? std::max(0, atoi(e)) : INT_MAX;
+    }
+    return v;
+}
+
+// rounds from this many vertices recompute facet planes in the vertex fold instead of reading the
+// materialised k_facet_plane output (MF_RECOMPUTE_MIN; 0 = always). Off by default: on cfg5 the
+// recomputing k_vertex_t<8> costs 2.33 ms against 1.31 + 0.63 ms for fold + plane pass
+static int recompute_min() {
+    static int v = -2;
+    if (v == -2) {
+        const char* e = getenv("MF_RECOMPUTE_MIN");
         v = e ? std::max(0, atoi(e)) : INT_MAX;
     }
     return v;
@@ -853,9 +868,13 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_vmesh, grid_for(ctx, N), 256, 0, stream, d_abort, N, voff_r, B, vmesh);
         }
         // facet planes + incidence CSR (corner-major order)
+        // large rounds recompute each facet's plane in the vertex fold instead of materialising
+        // 32 bytes per facet (write + gather); the plane kernel then only counts degrees
+        const bool recompute = N >= recompute_min();
+        const PlaneSrc ps{recompute ? nullptr : W.plane, Fc, Pc, order};
         if (!plane_done)
-            LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, Pc, dM, vmesh, act, W.plane, W.deg,
-                   order);
+            LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, Pc, dM, vmesh, act,
+                   recompute ? nullptr : W.plane, W.deg, order);
         plane_done = false;
         run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", d_abort);
         LAUNCH(k_inc_scatter, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, dM, Mcap, vmesh, act, W.inc_off, W.cursor,
@@ -865,7 +884,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             unsigned long long* vs_cur = W.vs + (size_t)(r & 1) * W.vs_words;
             unsigned long long* vs_nxt = W.vs + (size_t)((r + 1) & 1) * W.vs_words;
             const int tiles = (N + kVsTile - 1) / kVsTile;
-            VertexScanArgs va{d_abort, N, W.inc_off, W.inc, W.inc_tmp, Fc, W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp,
+            VertexScanArgs va{d_abort, N, W.inc_off, W.inc, W.inc_tmp, Fc, ps, Mcap, W.vq, W.nbr, W.nbr_tmp,
                               W.ucnt, W.upcnt, W.aoff, seeded ? W.eoff : nullptr, vs_cur,
                               reinterpret_cast<int*>(vs_cur + W.vs_words - 4), last ? nullptr : vs_nxt,
                               last ? 0 : W.vs_words};
@@ -873,14 +892,15 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             if (vertex_scan() == 2) LAUNCH(k_vertex_scan<256>, vg, 256, 0, stream, va);
             else LAUNCH(k_vertex_scan<128>, vg, 128, 0, stream, va);
         } else {
-            if (vt16(N))
-                LAUNCH(k_vertex_t<16>, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc,
-                       W.plane, Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
-            else
-                LAUNCH(k_vertex_t<8>, grid_for(ctx, N, 128), 128, 0, stream, d_abort, N, W.inc_off, W.inc, Fc,
-                       W.plane, Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy, d_heavy_n);
-            LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, d_abort, W.mid, d_mid_n, W.heavy, d_heavy_n,
-                   W.inc_off, W.inc, W.inc_tmp, Fc, W.plane, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
+            const bool t16 = vt16(N);
+            auto* vt = t16 ? (recompute ? k_vertex_t<16, true> : k_vertex_t<16, false>)
+                           : (recompute ? k_vertex_t<8, true> : k_vertex_t<8, false>);
+            LAUNCH_AS(t16 ? "k_vertex_t<16>" : "k_vertex_t<8>", vt, grid_for(ctx, N, 128), 128, 0, stream, d_abort,
+                      N, W.inc_off, W.inc, Fc, ps, Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy,
+                      d_heavy_n);
+            LAUNCH_AS("k_vertex_tiers", recompute ? k_vertex_tiers<true> : k_vertex_tiers<false>, ctx->sm_count * 8,
+                      256, 0, stream, d_abort, W.mid, d_mid_n, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
+                      ps, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
             // compact adjacency offsets (2 slots per edge); seeded rounds also need the dense
             // lexicographic edge index (the PCG64 key-stream position, decimate.py:190)
             run_scan(W.scan, LoadArr{W.ucnt}, W.aoff, N, stream, "k_scan<adj>", d_abort);
@@ -1056,7 +1076,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         if (B == 1 && !last && fuse_plane()) {  // + the next round's facet planes, one launch
             LAUNCH(k_compose_plane, grid_for(ctx, std::max<int64_t>(N0, Mcap)), 256, 0, stream, N0, d_abort, W.rstep,
                    W.inc_off, W.has_live, act, W.rt, W.mt, r == 0, W.kout, foff_c, foff_n, d_stats + 4 * r,
-                   W.aoff + N, W.ldc + 2, W.counters, Fn, Pn, d_act + (size_t)(r + 1) * B, W.plane, W.deg, order);
+                   W.aoff + N, W.ldc + 2, W.counters, Fn, Pn, d_act + (size_t)(r + 1) * B,
+                   Nn >= recompute_min() ? nullptr : W.plane, W.deg, order);
             plane_done = true;
         } else {
             LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh,
@@ -1115,7 +1136,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
-                              vt16(1), vt16(1 << 21), two_pass_min(),
+                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
@@ -1218,10 +1239,12 @@ int quality_run(Context* ctx, const mf_mesh_view* mv, const int* d_off, const in
         run_scan(W.scan, LoadArr{W.deg}, W.inc_off, N, stream, "k_scan<deg>", misc);
         if (m) LAUNCH(k_inc_scatter, grid_for(ctx, m), 256, 0, stream, misc, W.F0, misc + 2, Mc, (const int*)nullptr,
                       misc + 3, W.inc_off, W.cursor, W.inc);
-        LAUNCH(k_vertex_t<8>, grid_for(ctx, N, 128), 128, 0, stream, misc, N, W.inc_off, W.inc, W.F0, W.plane, Mc,
-               W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, misc + 12, W.heavy, misc + 8);
-        LAUNCH(k_vertex_tiers, ctx->sm_count * 8, 256, 0, stream, misc, W.mid, misc + 12, W.heavy, misc + 8,
-               W.inc_off, W.inc, W.inc_tmp, W.F0, W.plane, Mc, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
+        LAUNCH_AS("k_vertex_t<8>", (k_vertex_t<8, false>), grid_for(ctx, N, 128), 128, 0, stream, misc, N,
+                  W.inc_off, W.inc, W.F0, PlaneSrc{W.plane, W.F0, d_P, order}, Mc, W.vq, W.nbr, W.ucnt, W.upcnt,
+                  W.mid, misc + 12, W.heavy, misc + 8);
+        LAUNCH(k_vertex_tiers<false>, ctx->sm_count * 8, 256, 0, stream, misc, W.mid, misc + 12, W.heavy, misc + 8,
+               W.inc_off, W.inc, W.inc_tmp, W.F0, PlaneSrc{W.plane, W.F0, d_P, order}, Mc, W.vq, W.nbr, W.nbr_tmp,
+               W.ucnt, W.upcnt);
     }
     if (n_out) LAUNCH(k_quality, grid_for(ctx, n_out), 256, 0, stream, (int)n_out, d_off, d_mem, W.vq, d_Pout, order,
                       d_err);

@@ -134,27 +134,58 @@ __global__ void k_vmesh(const int* __restrict__ abort_flag, int N, const int* __
 }
 
 // K1: facet plane (mesh.py:77-87) + incidence degrees.
+MF_DEV Plane facet_plane_of(const int* __restrict__ F, const double* __restrict__ P, int f, int order) {
+    const int ia = F[3 * f], ib = F[3 * f + 1], ic = F[3 * f + 2];
+    const double x0 = P[3 * ia], y0 = P[3 * ia + 1], z0 = P[3 * ia + 2];
+    const double ax = P[3 * ib] - x0, ay = P[3 * ib + 1] - y0, az = P[3 * ib + 2] - z0;
+    const double bx = P[3 * ic] - x0, by = P[3 * ic + 1] - y0, bz = P[3 * ic + 2] - z0;
+    const double cx = ay * bz - az * by;
+    const double cy = az * bx - ax * bz;
+    const double cz = ax * by - ay * bx;
+    const double nrm = sqrt((cx * cx + cy * cy) + cz * cz);
+    Plane p;
+    if (nrm == 0.0) {
+        p.n0 = 0.0; p.n1 = 0.0; p.n2 = 0.0;
+    } else {
+        p.n0 = cx / nrm; p.n1 = cy / nrm; p.n2 = cz / nrm;
+    }
+    p.d = -dot3(p.n0, p.n1, p.n2, x0, y0, z0, order);
+    return p;
+}
+// Where the vertex fold gets a facet's plane: the materialised array (k_facet_plane wrote it), or
+// recomputed from the facet's corners (plane == nullptr: the planes are never written -- the
+// same arithmetic, so the same bits)
+struct PlaneSrc {
+    const Plane* plane;
+    const int* F;
+    const double* P;
+    int order;
+    MF_DEV Plane get(int f) const { return plane ? plane[f] : facet_plane_of(F, P, f, order); }
+};
+// compile-time form for the hot kernels (the recompute path would otherwise cost the gather form
+// ~24 registers)
+template <bool RC>
+struct PlaneSrcT {
+    const Plane* plane;
+    const int* F;
+    const double* P;
+    int order;
+    MF_DEV Plane get(int f) const {
+        if constexpr (RC) return facet_plane_of(F, P, f, order);
+        else return plane[f];
+    }
+};
+template <bool RC>
+MF_DEV PlaneSrcT<RC> plane_src(const PlaneSrc& p) {
+    return PlaneSrcT<RC>{p.plane, p.F, p.P, p.order};
+}
 MF_DEV void facet_plane_body(int M, const int* __restrict__ F, const double* __restrict__ P,
                              const int* __restrict__ vmesh, const int* __restrict__ act, Plane* __restrict__ plane,
                              int* __restrict__ deg, int order, int tid, int nth) {
     for (int f = tid; f < M; f += nth) {
         int ia = F[3 * f], ib = F[3 * f + 1], ic = F[3 * f + 2];
         if (!act[mesh_of(vmesh, ia)]) continue;
-        double x0 = P[3 * ia], y0 = P[3 * ia + 1], z0 = P[3 * ia + 2];
-        double ax = P[3 * ib] - x0, ay = P[3 * ib + 1] - y0, az = P[3 * ib + 2] - z0;
-        double bx = P[3 * ic] - x0, by = P[3 * ic + 1] - y0, bz = P[3 * ic + 2] - z0;
-        double cx = ay * bz - az * by;
-        double cy = az * bx - ax * bz;
-        double cz = ax * by - ay * bx;
-        double nrm = sqrt((cx * cx + cy * cy) + cz * cz);
-        Plane p;
-        if (nrm == 0.0) {
-            p.n0 = 0.0; p.n1 = 0.0; p.n2 = 0.0;
-        } else {
-            p.n0 = cx / nrm; p.n1 = cy / nrm; p.n2 = cz / nrm;
-        }
-        p.d = -dot3(p.n0, p.n1, p.n2, x0, y0, z0, order);
-        plane[f] = p;
+        if (plane) plane[f] = facet_plane_of(F, P, f, order);  // nullptr: degrees only (planes recomputed)
         atomicAdd(deg + ia, 1);
         atomicAdd(deg + ib, 1);
         atomicAdd(deg + ic, 1);
@@ -320,9 +351,9 @@ constexpr int kVtStage = 4096;  // k_vertex_t neighbour-list stage (ints): 128 v
 // key = np.add.at order), the planes folded from +0.0 in that order, the 2*DEG neighbour candidates
 // sorted and de-duplicated into `out`.  DEG = 8 for nearly all vertices; degrees 9..16 take the
 // DEG = 16 instance (a divergent branch of the same warp) instead of the warp-per-vertex tier.
-template <int DEG>
+template <int DEG, class PS>
 MF_DEV void vertex_thread_tier(int v, int s, int d, const int* __restrict__ inc, const int* __restrict__ F,
-                               const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq, int* out,
+                               PS plane, int Mcap, double* __restrict__ vq, int* out,
                                int* __restrict__ ucnt, int* __restrict__ upcnt) {
     int k[DEG];
 #pragma unroll
@@ -338,7 +369,7 @@ MF_DEV void vertex_thread_tier(int v, int s, int d, const int* __restrict__ inc,
         if (i < d) {
             int corner, f;
             decode_inc(k[i], Mcap, corner, f);
-            Plane p = plane[f];
+            Plane p = plane.get(f);
             q_add_plane(q, p);
             other_two(F, f, corner, c[2 * i], c[2 * i + 1]);
         }
@@ -360,10 +391,10 @@ MF_DEV void vertex_thread_tier(int v, int s, int d, const int* __restrict__ inc,
 }
 // TMAX: largest degree of the thread tier (8: 62 registers, for the bandwidth-bound large rounds;
 // 16: 90 registers, degrees 9..16 in-thread instead of the warp tier -- latency-bound rounds)
-template <int TMAX>
+template <int TMAX, bool RC>
 __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_flag, int N,
                                                   const int* __restrict__ inc_off, const int* __restrict__ inc,
-                                                  const int* __restrict__ F, const Plane* __restrict__ plane,
+                                                  const int* __restrict__ F, PlaneSrc plane,
                                                   int Mcap, double* __restrict__ vq, int* __restrict__ nbr,
                                                   int* __restrict__ ucnt, int* __restrict__ upcnt,
                                                   int* __restrict__ mid, int* __restrict__ mid_count,
@@ -395,8 +426,8 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
         if (work) {
             int* out = staged ? s_nb + 2 * (s - r0) : nbr + 2 * (size_t)s;
             if (TMAX == kThreadDeg || d <= kThreadDeg)
-                vertex_thread_tier<kThreadDeg>(v, s, d, inc, F, plane, Mcap, vq, out, ucnt, upcnt);
-            else vertex_thread_tier<TMAX>(v, s, d, inc, F, plane, Mcap, vq, out, ucnt, upcnt);
+                vertex_thread_tier<kThreadDeg>(v, s, d, inc, F, plane_src<RC>(plane), Mcap, vq, out, ucnt, upcnt);
+            else vertex_thread_tier<TMAX>(v, s, d, inc, F, plane_src<RC>(plane), Mcap, vq, out, ucnt, upcnt);
         }
         if (staged) {
             __syncthreads();
@@ -408,10 +439,11 @@ __global__ void __launch_bounds__(128) k_vertex_t(const int* __restrict__ abort_
 }
 
 // Mid tier (degree 9..32): one full warp per vertex, one incidence per lane.
+template <class PS>
 MF_DEV void vertex_mid_body(const int* __restrict__ list,
                                                 const int* __restrict__ list_count, const int* __restrict__ inc_off,
                                                 const int* __restrict__ inc, const int* __restrict__ F,
-                                                const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
+                                                PS plane, int Mcap, double* __restrict__ vq,
                                                 int* __restrict__ nbr, int* __restrict__ ucnt,
                                                 int* __restrict__ upcnt, int* __restrict__ heavy,
                                                 int* __restrict__ heavy_count) {
@@ -439,7 +471,7 @@ MF_DEV void vertex_mid_body(const int* __restrict__ list,
         if (l < d) {
             int corner, f;
             decode_inc(k, Mcap, corner, f);
-            Plane p = plane[f];
+            Plane p = plane.get(f);
             other_two(F, f, corner, a, b);
             double* q = s_q[g][l];
             q[0] = p.n0 * p.n0; q[1] = p.n0 * p.n1; q[2] = p.n0 * p.n2;
@@ -1073,10 +1105,11 @@ __global__ void __launch_bounds__(256) k_adj_rank_tiled(const int* __restrict__ 
 }
 
 // K3h: heavy tier -- one block per high-degree vertex (any degree).
+template <class PS>
 MF_DEV void vertex_heavy_body(const int* __restrict__ heavy, const int* __restrict__ heavy_count,
                                                       const int* __restrict__ inc_off, int* __restrict__ inc,
                                                       int* __restrict__ inc_tmp, const int* __restrict__ F,
-                                                      const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
+                                                      PS plane, int Mcap, double* __restrict__ vq,
                                                       int* __restrict__ nbr, int* __restrict__ nbr_tmp,
                                                       int* __restrict__ ucnt, int* __restrict__ upcnt) {
     __shared__ int smem[kChunk];
@@ -1095,7 +1128,7 @@ MF_DEV void vertex_heavy_body(const int* __restrict__ heavy, const int* __restri
             if ((int)threadIdx.x < len) {
                 int corner, f;
                 decode_inc(inc[s + c0 + threadIdx.x], Mcap, corner, f);
-                s_pl[threadIdx.x] = plane[f];
+                s_pl[threadIdx.x] = plane.get(f);
             }
             __syncthreads();
             if (threadIdx.x == 0)
@@ -1147,18 +1180,21 @@ MF_DEV void vertex_heavy_body(const int* __restrict__ heavy, const int* __restri
 
 // Mid (degree 9..32, a warp per vertex) and heavy (a block per vertex) tiers in one
 // launch: both lists are complete once k_vertex_t has run, and they are disjoint.
+template <bool RC>
 __global__ void __launch_bounds__(256) k_vertex_tiers(const int* __restrict__ abort_flag, const int* __restrict__ mid,
                                                       const int* __restrict__ mid_count, const int* __restrict__ heavy,
                                                       const int* __restrict__ heavy_count,
                                                       const int* __restrict__ inc_off, int* __restrict__ inc,
                                                       int* __restrict__ inc_tmp, const int* __restrict__ F,
-                                                      const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq,
+                                                      PlaneSrc plane, int Mcap, double* __restrict__ vq,
                                                       int* __restrict__ nbr, int* __restrict__ nbr_tmp,
                                                       int* __restrict__ ucnt, int* __restrict__ upcnt) {
     MF_PDL_ENTRY;
     if (*abort_flag) return;
-    vertex_heavy_body(heavy, heavy_count, inc_off, inc, inc_tmp, F, plane, Mcap, vq, nbr, nbr_tmp, ucnt, upcnt);
-    vertex_mid_body(mid, mid_count, inc_off, inc, F, plane, Mcap, vq, nbr, ucnt, upcnt, nullptr, nullptr);
+    vertex_heavy_body(heavy, heavy_count, inc_off, inc, inc_tmp, F, plane_src<RC>(plane), Mcap, vq, nbr, nbr_tmp,
+                      ucnt, upcnt);
+    vertex_mid_body(mid, mid_count, inc_off, inc, F, plane_src<RC>(plane), Mcap, vq, nbr, ucnt, upcnt, nullptr,
+                    nullptr);
 }
 
 // ------------------------------------------------------------------------
@@ -1177,8 +1213,9 @@ MF_DEV int vs_up(unsigned long long w) { return (int)(w & 0x7fffffffull); }
 
 // one degree-9..32 vertex by warp g of the block (vertex_mid_body's per-vertex step); the
 // unique neighbour list goes to `out`, the counts to ucnt / upcnt
+template <class PS>
 MF_DEV void vertex_mid_one(int v, int s, int d, const int* __restrict__ inc, const int* __restrict__ F,
-                           const Plane* __restrict__ plane, int Mcap, double* __restrict__ vq, int* out,
+                           PS plane, int Mcap, double* __restrict__ vq, int* out,
                            int* __restrict__ ucnt, int* __restrict__ upcnt, double (*s_q)[10], int* s_c) {
     const int l = threadIdx.x & 31;
     const unsigned mask = 0xffffffffu;
@@ -1196,7 +1233,7 @@ MF_DEV void vertex_mid_one(int v, int s, int d, const int* __restrict__ inc, con
     if (l < d) {
         int corner, f;
         decode_inc(k, Mcap, corner, f);
-        Plane p = plane[f];
+        Plane p = plane.get(f);
         other_two(F, f, corner, a, b);
         double* q = s_q[l];
         q[0] = p.n0 * p.n0; q[1] = p.n0 * p.n1; q[2] = p.n0 * p.n2;
@@ -1241,8 +1278,9 @@ MF_DEV void vertex_mid_one(int v, int s, int d, const int* __restrict__ inc, con
 // one vertex of any degree by the whole block (vertex_heavy_body's per-vertex step): the
 // incidences sorted in place, the fold staged kVsTile planes at a time, the neighbour
 // candidates sorted / de-duplicated in nbr (scratch nbr_tmp)
+template <class PS>
 MF_DEV void vertex_heavy_one(int v, int s, int d, int* __restrict__ inc, int* __restrict__ inc_tmp,
-                             const int* __restrict__ F, const Plane* __restrict__ plane, int Mcap,
+                             const int* __restrict__ F, PS plane, int Mcap,
                              double* __restrict__ vq, int* __restrict__ nbr, int* __restrict__ nbr_tmp,
                              int* __restrict__ ucnt, int* __restrict__ upcnt, int* smem, Plane* s_pl, int* s_scan) {
     block_sort_ints(inc + s, inc_tmp + s, d, smem);
@@ -1253,7 +1291,7 @@ MF_DEV void vertex_heavy_one(int v, int s, int d, int* __restrict__ inc, int* __
         for (int i = threadIdx.x; i < len; i += blockDim.x) {
             int corner, f;
             decode_inc(inc[s + c0 + i], Mcap, corner, f);
-            s_pl[i] = plane[f];
+            s_pl[i] = plane.get(f);
         }
         __syncthreads();
         if (threadIdx.x == 0)
@@ -1305,7 +1343,7 @@ struct VertexScanArgs {
     int* inc;
     int* inc_tmp;
     const int* F;
-    const Plane* plane;
+    PlaneSrc plane;
     int Mcap;
     double* vq;
     int* nbr;
@@ -1381,7 +1419,7 @@ __global__ void __launch_bounds__(THREADS) k_vertex_scan(VertexScanArgs a) {
                     if (i < d) {
                         int corner, f;
                         decode_inc(k[i], a.Mcap, corner, f);
-                        Plane p = a.plane[f];
+                        Plane p = a.plane.get(f);
                         q_add_plane(q, p);
                         other_two(a.F, f, corner, c[2 * i], c[2 * i + 1]);
                     }
