@@ -1710,20 +1710,48 @@ int decimate_end(Context* ctx, DecCall& call, const mf_outputs* outs, Result** o
                 bf = b;
                 break;
             }
+        // read before a rerun below reuses the context's status buffer
+        const int ach = bf >= 0 ? h_fail[bf] : 0, rr = bf >= 0 ? h_fail[B + bf] : 0;
+        const int no_edges = bf >= 0 ? h_fail[2 * B + bf] : 0;
+        if (bf > 0 && mv->vertex_offsets && mv->facet_offsets) {
+            // the batch stopped at the round entry bf failed in; an earlier entry with a longer round
+            // chain may fail in a later round, and the reference raises the LOWEST failing entry's
+            // error (decimate.py:354-361, entries decimated independently) -- so decimate the
+            // entries before bf on their own (a prefix of the same arrays) and report theirs if any
+            bool later = false;
+            for (int b = 0; b < bf && !later; b++) later = (int)p.chains[b].size() > rr + 1;
+            if (later) {
+                mf_mesh_view pre = *mv;
+                pre.n_meshes = bf;
+                pre.n = mv->vertex_offsets[bf];
+                pre.m = mv->facet_offsets[bf];
+                const mf_decimate_config cfg2 = *cfg;
+                Result* r2 = nullptr;
+                mf_status st2;
+                const int rc2 = decimate_run(ctx, &pre, &cfg2, stream, &r2, &st2, call.force_carry, nullptr);
+                if (rc2 != MF_OK) {
+                    *st = st2;
+                    return fail_out(rc2);
+                }
+                if (r2) {
+                    cudaFree(r2->block);
+                    delete r2;
+                }
+            }
+        }
         st->mesh_index = bf;
         if (bf >= 0) {
-            st->achievable_vertices = h_fail[bf];
-            int rr = h_fail[B + bf];
+            st->achievable_vertices = ach;
             st->target_vertices = p.chains[bf][rr];
-            st->no_edges = h_fail[2 * B + bf];
+            st->no_edges = no_edges;
             if (st->no_edges)
                 snprintf(st->message, sizeof(st->message),
                          "mesh has no edges; cannot reach %lld vertices (achievable minimum is %d)",
-                         (long long)st->target_vertices, h_fail[bf]);
+                         (long long)st->target_vertices, ach);
             else
                 snprintf(st->message, sizeof(st->message),
                          "cannot reach %lld vertices in one pass; achievable minimum is %d",
-                         (long long)st->target_vertices, h_fail[bf]);
+                         (long long)st->target_vertices, ach);
         }
         return fail_out(MF_ERR_INFEASIBLE);
     }

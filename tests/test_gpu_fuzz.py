@@ -4,6 +4,8 @@ unseeded / seeded ranks, `rounds` fixed or auto, omitted / float32 / float64 fea
 1-7 channels, shuffled vertex ids, disconnected unions, duplicate input facets; the numpy
 API (pinned and pageable inputs), the device-tensor API, and a chained second level."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -83,7 +85,14 @@ def _same(a, b):
     return a.shape == b.shape and a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
-@pytest.mark.parametrize("seed", range(120))
+# MF_FUZZ_SEEDS=a:b widens the sweep (the default 120 cases run in the round-end suite)
+_LO, _HI = (int(x) for x in os.environ.get("MF_FUZZ_SEEDS", "0:120").split(":"))
+# found by wider sweeps: batches whose lowest failing entry fails in a LATER round than a
+# higher entry (decimate.py:354-361 raises the lowest entry's error)
+_REGRESSIONS = [966, 1120, 3338, 8790]
+
+
+@pytest.mark.parametrize("seed", sorted(set(range(_LO, _HI)) | set(_REGRESSIONS)))
 def test_random_configuration_matches_oracle(oracle, seed):
     mesh, target, shuffle, rounds = _case(seed)
     cfg = mfg.DecimationConfig(target_vertices=target, shuffle_seed=shuffle, rounds=rounds)
