@@ -159,9 +159,15 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, in
     __shared__ int s_tile;
     __shared__ int s_warp[kScanBlock / 32];
     __shared__ int s_prefix;
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
-    __syncthreads();
-    const int tile = s_tile;
+    // tiles in launch order by ticket -- needed for forward progress only when the grid can be
+    // larger than what is resident at once (ticket == nullptr: the host knows every tile is
+    // co-resident, blockIdx.x is the tile and one L2 atomic round trip is saved)
+    int tile = blockIdx.x;
+    if (ticket) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+        __syncthreads();
+        tile = s_tile;
+    }
     constexpr int kItems = ScanItems<LoadOp>::value;
     const long long base = (long long)tile * (kScanBlock * kItems) + (long long)threadIdx.x * kItems;
     int v[kItems];
@@ -196,9 +202,10 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, in
         if (lane < kScanBlock / 32) s_warp[lane] = wi - w;  // exclusive per warp
         int agg = __shfl_sync(0xffffffffu, wi, kScanBlock / 32 - 1);
         // publish + look back
+        // the flag and the value share one 64-bit word, so publishing needs no fence: nothing
+        // else the consumer reads is ordered by it (the clears above belong to the NEXT scan)
         if (lane == 0) {
             unsigned long long word = (tile == 0 ? kFlagPre : kFlagAgg) | (unsigned)agg;
-            __threadfence();
             atomicExch(status + tile, word);
         }
         int excl = 0;
@@ -217,10 +224,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(LoadOp load, int n, in
                 if (pmask) break;
                 pred -= 32;
             }
-            if (lane == 0) {
-                __threadfence();
-                atomicExch(status + tile, kFlagPre | (unsigned)(excl + agg));
-            }
+            if (lane == 0) atomicExch(status + tile, kFlagPre | (unsigned)(excl + agg));
         }
         if (lane == 0) s_prefix = excl;
     }

@@ -376,7 +376,18 @@ struct ScanBuf {
     unsigned long long* buf[2] = {nullptr, nullptr};
     int words = 0;
     int cur = 0;
+    int resident = 0;  // tiles a ticketless launch may have (sm_count * 4)
 };
+
+// MF_SCAN_TICKET=1: every scan takes its tiles by ticket (A/B)
+static bool scan_ticketless() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SCAN_TICKET");
+        v = (e && atoi(e) == 1) ? 0 : 1;
+    }
+    return v == 1;
+}
 
 template <typename LoadOp, typename Epi = EpiNone>
 static void run_scan(ScanBuf& sb, LoadOp op, int* out, int n, cudaStream_t s, const char* name,
@@ -385,9 +396,11 @@ static void run_scan(ScanBuf& sb, LoadOp op, int* out, int n, cudaStream_t s, co
     int tiles = std::max(1, (n + tile - 1) / tile);
     unsigned long long* st = sb.buf[sb.cur];
     unsigned long long* other = sb.buf[sb.cur ^ 1];
+    // grids of at most 4 scan blocks per SM (of 8 resident) run all tiles at once: no ticket
+    int* ticket = (scan_ticketless() && tiles <= sb.resident) ? nullptr : reinterpret_cast<int*>(st + tiles);
     prof_pre(name, s);
-    rec_check(launch_ex(k_scan_excl<LoadOp, Epi>, dim3(tiles), dim3(kScanBlock), 0, s, op, n, out, st,
-                        reinterpret_cast<int*>(st + tiles), abort_flag, epi, other, sb.words),
+    rec_check(launch_ex(k_scan_excl<LoadOp, Epi>, dim3(tiles), dim3(kScanBlock), 0, s, op, n, out, st, ticket,
+                        abort_flag, epi, other, sb.words),
               __LINE__);
     prof_post(name, s);
     g_launches++;
@@ -794,6 +807,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
     CondCapture cc;
     cc.body[0] = body0;
     cc.body[1] = body1;
+    W.scan.resident = ctx->sm_count * 4;
     const int B = p.B, R = p.R, N0 = p.N0, Mcap = p.Mcap, Ecap = p.Ecap;
     const int64_t n = p.n, m = p.m, C = p.C;
     const bool seeded = p.seeded;
@@ -1136,7 +1150,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
-                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(),
+                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
