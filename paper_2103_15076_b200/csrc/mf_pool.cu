@@ -554,6 +554,16 @@ __global__ void __launch_bounds__(1024) k_csr_coop(int n, int n_out, const int* 
     }
 }
 
+// vertices per k_csr_coop block (MF_CSR_PER_BLOCK; a huge value = one block, 1 = one per SM)
+static int64_t csr_per_block() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_CSR_PER_BLOCK");
+        v = e ? std::max(1, atoi(e)) : 1;
+    }
+    return v;
+}
+
 // cooperative CSR build available (MF_CSR_COOP=0 forces the five-launch path for A/B runs)
 static int g_csr_blocks_per_sm = 1;
 static bool csr_coop_ok(const Context* ctx) {
@@ -603,9 +613,13 @@ int build_cluster_csr(Context* ctx, const int* d_replace, int64_t n, int64_t n_o
         int* bsum = reinterpret_cast<int*>(sst);
         int nn = (int)n, no = (int)n_out;
         void* args[] = {&nn, &no, (void*)&d_replace, &cnt, &off, &mem, &heavy, &ctr, &bsum, &tmp};
+        // one block per SM (MF_CSR_PER_BLOCK=n: a block per n vertices -- fewer barrier arrivals
+        // for small levels -- measured slower: cfg3 k_csr_coop 0.162 ms at 8192, 0.106 ms at 1)
+        const int64_t want = (n + csr_per_block() - 1) / csr_per_block();
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, ctx->sm_count * g_csr_blocks_per_sm));
         prof_pre("k_csr_coop", stream);
-        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_csr_coop, dim3(ctx->sm_count * g_csr_blocks_per_sm),
-                                                    dim3(1024), args, 0, stream);
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_csr_coop, dim3(blocks), dim3(1024), args, 0,
+                                                    stream);
         prof_post("k_csr_coop", stream);
         g_launches++;
         MF_CUDA_TRY(e);

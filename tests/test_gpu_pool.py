@@ -165,7 +165,8 @@ for c, dt in ((64, np.float32), (16, np.float64), (4, np.float32), (3, np.float6
 print("POOL-VARIANT-OK")
 """
 
-POOL_VARIANTS = [{}, {"MF_UNPOOL_TMA": "1"}, {"MF_POOL_SCALAR": "1"}, {"MF_CSR_COOP": "0"}]
+POOL_VARIANTS = [{}, {"MF_UNPOOL_TMA": "1"}, {"MF_POOL_SCALAR": "1"}, {"MF_CSR_COOP": "0"}, {"MF_CSR_PER_BLOCK": "1"},
+                 {"MF_CSR_PER_BLOCK": "100000000"}]
 
 
 @pytest.mark.parametrize("env", POOL_VARIANTS, ids=[",".join(f"{k}={v}" for k, v in e.items()) or "default"
