@@ -50,7 +50,7 @@ def test_bench_line_single_gpu():
 def test_bench_line_world2():
     d = _run(["--config", "cfg4", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"], world=2)
     assert KEYS <= set(d), KEYS - set(d)
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"  # cfg4: one batch sharded
     assert d["value"] > 0 and d["e2e"]["value"] > 0
 
 
