@@ -26,4 +26,6 @@ run racecheck pool_variants MF_SAN_N=20000 MF_UNPOOL_TMA=1 MF_CSR_COOP=0 MF_DEBU
 run synccheck pool_variants MF_SAN_N=20000 MF_UNPOOL_TMA=1
 run memcheck fused_opt_in MF_SAN_N=20000 MF_VERTEX_SCAN=2 MF_EDGES_RANK=1 MF_VT16=1 MF_FUSE_PLANE=0
 run racecheck fused_opt_in MF_SAN_N=20000 MF_VERTEX_SCAN=2 MF_EDGES_RANK=1 MF_VT16=1
+run memcheck recompute_ticket MF_SAN_N=20000 MF_RECOMPUTE_MIN=0 MF_TWO_PASS_MIN=0 MF_SCAN_TICKET=1
+run racecheck recompute_ticket MF_SAN_N=20000 MF_RECOMPUTE_MIN=0 MF_TWO_PASS_MIN=0 MF_SCAN_TICKET=1
 run initcheck default MF_SAN_N=20000 MF_GRAPHS=0

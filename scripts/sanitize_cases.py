@@ -43,4 +43,14 @@ for mode in mfg.POOL_MODES:
 up = mfg.unpool(got, res)
 assert np.array_equal(up, O.unpool(got, res.replace))
 mfg.validate_on_device(res.mesh)
+# a batch whose lowest failing entry fails in a later round than a higher one (the prefix rerun)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import test_gpu_fuzz as FZ  # noqa: E402
+
+mesh, target, seed, rounds = FZ._case(1120)
+try:
+    mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=target, shuffle_seed=seed, rounds=rounds))
+    raise AssertionError("expected InfeasibleTargetError")
+except mfg.InfeasibleTargetError as e:
+    assert e.achievable_vertices == 63, e
 print("SANITIZE-CASES-OK")
