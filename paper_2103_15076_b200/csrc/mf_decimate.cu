@@ -884,7 +884,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         // facet planes + incidence CSR (corner-major order)
         // large rounds recompute each facet's plane in the vertex fold instead of materialising
         // 32 bytes per facet (write + gather); the plane kernel then only counts degrees
-        const bool recompute = N >= recompute_min();
+        const bool recompute = N >= recompute_min() && vertex_scan() == 0;  // k_vertex_scan reads planes
         const PlaneSrc ps{recompute ? nullptr : W.plane, Fc, Pc, order};
         if (!plane_done)
             LAUNCH(k_facet_plane, grid_for(ctx, Mcap), 256, 0, stream, d_abort, Fc, Pc, dM, vmesh, act,
@@ -1091,7 +1091,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH(k_compose_plane, grid_for(ctx, std::max<int64_t>(N0, Mcap)), 256, 0, stream, N0, d_abort, W.rstep,
                    W.inc_off, W.has_live, act, W.rt, W.mt, r == 0, W.kout, foff_c, foff_n, d_stats + 4 * r,
                    W.aoff + N, W.ldc + 2, W.counters, Fn, Pn, d_act + (size_t)(r + 1) * B,
-                   Nn >= recompute_min() ? nullptr : W.plane, W.deg, order);
+                   (Nn >= recompute_min() && vertex_scan() == 0) ? nullptr : W.plane, W.deg, order);
             plane_done = true;
         } else {
             LAUNCH(k_compose, grid_for(ctx, N0), 256, 0, stream, N0, d_abort, W.rstep, W.inc_off, W.has_live, vmesh,

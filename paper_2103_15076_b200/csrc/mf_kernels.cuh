@@ -1419,7 +1419,7 @@ __global__ void __launch_bounds__(THREADS) k_vertex_scan(VertexScanArgs a) {
                     if (i < d) {
                         int corner, f;
                         decode_inc(k[i], a.Mcap, corner, f);
-                        Plane p = a.plane.get(f);
+                        Plane p = a.plane.plane[f];  // materialised planes (no recompute here)
                         q_add_plane(q, p);
                         other_two(a.F, f, corner, c[2 * i], c[2 * i + 1]);
                     }
@@ -1446,14 +1446,14 @@ __global__ void __launch_bounds__(THREADS) k_vertex_scan(VertexScanArgs a) {
             const int w = s_list[i];
             const int ws = a.inc_off[w], wd = a.inc_off[w + 1] - ws;
             int* out = staged ? s_nb + 2 * (ws - r0) : a.nbr + 2 * (size_t)ws;
-            vertex_mid_one(w, ws, wd, a.inc, a.F, a.plane, a.Mcap, a.vq, out, a.ucnt, a.upcnt, sc.mid.q[warp],
+            vertex_mid_one(w, ws, wd, a.inc, a.F, plane_src<false>(a.plane), a.Mcap, a.vq, out, a.ucnt, a.upcnt, sc.mid.q[warp],
                            sc.mid.c[warp]);
         }
         __syncthreads();
         for (int i = 0; i < nheavy; i++) {
             const int w = s_list[kVsTile - 1 - i];
             const int ws = a.inc_off[w], wd = a.inc_off[w + 1] - ws;
-            vertex_heavy_one(w, ws, wd, a.inc, a.inc_tmp, a.F, a.plane, a.Mcap, a.vq, a.nbr, a.nbr_tmp, a.ucnt,
+            vertex_heavy_one(w, ws, wd, a.inc, a.inc_tmp, a.F, plane_src<false>(a.plane), a.Mcap, a.vq, a.nbr, a.nbr_tmp, a.ucnt,
                              a.upcnt, sc.heavy.sort, sc.heavy.pl, s_scan);
             if (staged) {  // the heavy list lives in global memory: copy it into the stage
                 const int cnt = a.ucnt[w];
