@@ -379,6 +379,16 @@ struct ScanBuf {
     int resident = 0;  // tiles a ticketless launch may have (sm_count * 4)
 };
 
+// k_vertex_tiers blocks per SM (MF_TIERS_PER_SM, A/B)
+static int tiers_per_sm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_TIERS_PER_SM");
+        v = e ? std::max(1, atoi(e)) : 8;
+    }
+    return v;
+}
+
 // MF_SCAN_TICKET=1: every scan takes its tiles by ticket (A/B)
 static bool scan_ticketless() {
     static int v = -1;
@@ -912,7 +922,8 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
             LAUNCH_AS(t16 ? "k_vertex_t<16>" : "k_vertex_t<8>", vt, grid_for(ctx, N, 128), 128, 0, stream, d_abort,
                       N, W.inc_off, W.inc, Fc, ps, Mcap, W.vq, W.nbr, W.ucnt, W.upcnt, W.mid, d_mid_n, W.heavy,
                       d_heavy_n);
-            LAUNCH_AS("k_vertex_tiers", recompute ? k_vertex_tiers<true> : k_vertex_tiers<false>, ctx->sm_count * 8,
+            LAUNCH_AS("k_vertex_tiers", recompute ? k_vertex_tiers<true> : k_vertex_tiers<false>,
+                      ctx->sm_count * tiers_per_sm(),
                       256, 0, stream, d_abort, W.mid, d_mid_n, W.heavy, d_heavy_n, W.inc_off, W.inc, W.inc_tmp, Fc,
                       ps, Mcap, W.vq, W.nbr, W.nbr_tmp, W.ucnt, W.upcnt);
             // compact adjacency offsets (2 slots per edge); seeded rounds also need the dense
@@ -1150,7 +1161,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
-                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(),
+                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(), tiers_per_sm(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
