@@ -842,11 +842,8 @@ int unpool_run(Context* ctx, const void* coarse, int dtype, int64_t n_out, int64
     if (n * c > 0) {
         if (unpool_tma() && row % 16 == 0 && row <= 1024 && ((uintptr_t)dC % 16) == 0 && ((uintptr_t)dO % 16) == 0) {
             const size_t smem = (size_t)kTmaWarps * 2 * 32 * row + kTmaWarps * 2 * 8;
-            static size_t configured = 0;
-            if (smem > configured) {
-                cudaFuncSetAttribute(k_unpool_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                configured = smem;
-            }
+            // per call: the attribute is per device, and calls may come from several threads
+            cudaFuncSetAttribute(k_unpool_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             const int tiles = (int)((n + 31) / 32);
             const int grid = std::max(1, std::min((tiles + kTmaWarps - 1) / kTmaWarps, ctx->sm_count * 8));
             LAUNCH(k_unpool_tma, grid, kTmaWarps * 32, smem, stream, (int)n, (int)row, d_replace, (const char*)dC,
