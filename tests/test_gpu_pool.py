@@ -46,6 +46,25 @@ def test_pool_modes(oracle, dtype, sizes):
     assert bits_equal(mfg.unpool(coarse, res), oracle.unpool(coarse, rep))
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("c", [1, 2, 3, 7, 63, 65, 129, 257, 1000])
+def test_pool_channel_widths(oracle, dtype, c):
+    """Row widths around the 16-byte vector / lane-count boundaries of k_pool_vec / k_unpool_rows
+    (odd widths take the scalar path), and rows wider than one warp's vectors."""
+    n, n_out = 3000, 900
+    rng = np.random.default_rng(c)
+    rep = rng.integers(0, n_out, n)
+    rep[:n_out] = np.arange(n_out)
+    X = rng.standard_normal((n, c)).astype(dtype)
+    X[rng.integers(0, n, 5), rng.integers(0, c, 5)] = np.nan
+    w = (0.5 + rng.random(n)).astype(dtype)
+    res = hand_result(rep, n_out)
+    for mode in mfg.POOL_MODES:
+        assert bits_equal(mfg.pool(X, res, mode=mode, weights=w), oracle.pool(X, rep, n_out, mode, w)), mode
+    coarse = rng.standard_normal((n_out, c)).astype(dtype)
+    assert bits_equal(mfg.unpool(coarse, res), oracle.unpool(coarse, rep))
+
+
 def test_pool_on_decimation_handle(oracle):
     mesh = S.delaunay_terrain(30_000, noise=0.02, seed=3)
     res = mfg.decimate_parallel(mesh, mfg.DecimationConfig(target_vertices=7_500))
