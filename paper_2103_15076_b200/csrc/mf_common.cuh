@@ -85,6 +85,32 @@ MF_DEV unsigned long long ld_volatile(const unsigned long long* p) {
 }
 
 // ------------------------------------------------------------------------
+// Bulk-copy engine (TMA, non-tensor form): an mbarrier with a transaction count tracks the bytes
+// of cp.async.bulk global->shared copies (k_unpool_tma, k_select's key stage).
+MF_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+MF_DEV void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+MF_DEV void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+MF_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n LAB_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LAB_WAIT;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+MF_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// ------------------------------------------------------------------------
 // Software grid barrier for persistent kernels.  The launch must guarantee
 // co-residency (cudaLaunchCooperativeKernel with an occupancy-bounded grid).
 // `bar` = {arrive counter, generation}; zeroed once per launch.

@@ -379,6 +379,16 @@ struct ScanBuf {
     int resident = 0;  // tiles a ticketless launch may have (sm_count * 4)
 };
 
+// k_select's two-phase key stage by the bulk-copy engine (MF_SEL_BULK=0: per-thread loads, A/B)
+static int sel_bulk() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SEL_BULK");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v;
+}
+
 // k_vertex_tiers blocks per SM (MF_TIERS_PER_SM, A/B)
 static int tiers_per_sm() {
     static int v = -1;
@@ -1014,7 +1024,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
                           d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap(), 0,
-                          B == 1 ? kSelChiCap : 0};
+                          B == 1 ? kSelChiCap : 0, sel_bulk()};
             if (big) {
                 const int hist_grid = std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2);
                 if (cc.on() && cc.depth < 2) {  // passes until decided / handed over (WHILE node)
@@ -1161,7 +1171,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
-                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(), tiers_per_sm(),
+                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(), tiers_per_sm(), sel_bulk(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);

@@ -2193,6 +2193,7 @@ struct SelectArgs {
     int cap;            // k_select: keys its shared-memory stage holds (>= kSelCap)
     cudaGraphConditionalHandle cond;  // device-driven multi-block passes (WHILE node), 0 = fixed passes
     int chicap;         // k_select: primary keys the stage holds for the two-phase path (0 = off)
+    int bulk;           // k_select: two-phase keys staged by the bulk-copy engine
 };
 
 // Multi-block pass scratch (ints): histogram | OR (2 u64), AND (2 u64) | stop |
@@ -2362,7 +2363,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_select(SelectArgs a) {
     MF_PDL_ENTRY;
     if (*a.abort_flag) return;
-    extern __shared__ unsigned char s_raw[];
+    extern __shared__ __align__(16) unsigned char s_raw[];
     int* hist = reinterpret_cast<int*>(s_raw);                          // kSelBins
     uint64_t* sh = reinterpret_cast<uint64_t*>(s_raw + kSelBins * 4);   // kSelCap
     uint64_t* sl = sh + a.cap;                                          // a.cap
@@ -2371,6 +2372,7 @@ __global__ void __launch_bounds__(NT) k_select(SelectArgs a) {
     __shared__ int s_ncomp;
     __shared__ unsigned long long s_oa[4];
     __shared__ uint64_t s_bucket[kSelBucket];  // the two-phase path's compacted digit bucket
+    __shared__ __align__(8) uint64_t s_mbar;    // its bulk key stage
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         const int c0 = a.voff[b], c1 = c0 + a.seg_cnt[b];
         const int cnt = c1 - c0;
@@ -2396,27 +2398,56 @@ __global__ void __launch_bounds__(NT) k_select(SelectArgs a) {
             }
             kr = k;
         }
-        if (!a.resume && cnt <= a.chicap) {
+        if (!a.resume && cnt + 1 <= a.chicap) {
             // mid-size segment: the 64-bit primary keys fit the stage -- select on them in
             // shared memory (one coalesced load), then, only among the keys equal to the
             // k-th primary key, on the secondary half gathered from global memory
-            uint64_t* sv = sh;  // a.chicap keys
+            const uint64_t* src = a.chi + c0;
+            // key i sits at sv[i]; the stage is shifted by one key when the segment starts
+            // 8 bytes off a 16-byte boundary, so global and shared addresses agree mod 16
+            const int lead = min(cnt, (int)(((uintptr_t)src >> 3) & 1));
+            uint64_t* sv = sh + lead;  // a.chicap - 1 keys
             uint64_t o = 0, an = ~0ull;
             if (threadIdx.x < 2) s_oa[threadIdx.x] = threadIdx.x ? ~0ull : 0ull;
-            for (int i0 = threadIdx.x; i0 < cnt; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
-                uint64_t v8[8];
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const int i = i0 + q * blockDim.x;
-                    v8[q] = i < cnt ? __ldcg(a.chi + c0 + i) : 0;
+            if (a.bulk) {
+                // the bulk-copy engine streams the aligned body (one thread issues, the mbarrier
+                // counts the bytes); the <= 2 unaligned end keys are plain loads
+                const int body = ((cnt - lead) >> 1) << 1;
+                if (threadIdx.x == 0) {
+                    mbar_init(&s_mbar, 1);
+                    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
                 }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    mbar_expect_tx(&s_mbar, (unsigned)body * 8u);
+                    constexpr int kChunk = 4096;  // keys per bulk copy (32 KiB)
+                    for (int off = 0; off < body; off += kChunk)
+                        bulk_g2s(sv + lead + off, src + lead + off, (unsigned)min(kChunk, body - off) * 8u, &s_mbar);
+                }
+                if (threadIdx.x == 32 && lead) sv[0] = __ldcg(src);
+                if (threadIdx.x == 64 && lead + body < cnt) sv[cnt - 1] = __ldcg(src + cnt - 1);
+                mbar_wait(&s_mbar, 0);
+                __syncthreads();
+                for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+                    o |= sv[i];
+                    an &= sv[i];
+                }
+            } else {
+                for (int i0 = threadIdx.x; i0 < cnt; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+                    uint64_t v8[8];
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const int i = i0 + q * blockDim.x;
-                    if (i < cnt) {
-                        sv[i] = v8[q];
-                        o |= v8[q];
-                        an &= v8[q];
+                    for (int q = 0; q < 8; q++) {
+                        const int i = i0 + q * blockDim.x;
+                        v8[q] = i < cnt ? __ldcg(src + i) : 0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const int i = i0 + q * blockDim.x;
+                        if (i < cnt) {
+                            sv[i] = v8[q];
+                            o |= v8[q];
+                            an &= v8[q];
+                        }
                     }
                 }
             }
@@ -2458,7 +2489,7 @@ __global__ void __launch_bounds__(NT) k_select(SelectArgs a) {
                 if (threadIdx.x == 0) s_ncomp = 0;
                 __syncthreads();
                 uint64_t* sq = sv + cnt;  // secondary halves of the primary-key ties
-                const int room = a.chicap - cnt;
+                const int room = a.chicap - cnt - lead;
                 for (int i = threadIdx.x; i < cnt; i += blockDim.x)
                     if (sv[i] == t) {
                         const int slot = atomicAdd(&s_ncomp, 1);
