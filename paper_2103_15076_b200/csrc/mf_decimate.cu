@@ -539,7 +539,10 @@ static int make_plan(const mf_mesh_view* mv, const mf_decimate_config* cfg, Plan
     for (int r = 0; r < R; r++)
         for (int b = 0; b < B; b++) {
             int nin = p.h_nin[(size_t)r * B + b];
-            bool a = b < p.first_err && r < (int)p.chains[b].size();
+            // a round whose target is its input size is _identity_result (decimate.py:231-233):
+            // bypassed like a finished chain (positions and facets verbatim) -- run as a
+            // zero-budget round it would move 'inverse' singletons to their optimal positions
+            bool a = b < p.first_err && r < (int)p.chains[b].size() && p.chains[b][r] != nin;
             p.h_act[(size_t)r * B + b] = a;
             int tgt = a ? (int)p.chains[b][r] : nin;
             p.h_budget[(size_t)r * B + b] = nin - tgt;

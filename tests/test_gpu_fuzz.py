@@ -72,9 +72,14 @@ def _case(seed):
     return mesh, target, seed_, rounds
 
 
-def _oracle(oracle, mesh, target, seed, rounds):
+def _placement(seed):
+    # drawn from its own stream so the cases of _case(seed) stay what they were
+    return "inverse" if np.random.default_rng([seed, 7]).random() < 0.25 else "average"
+
+
+def _oracle(oracle, mesh, target, seed, rounds, placement="average"):
     base = mesh.mesh if isinstance(mesh, mfg.BatchedMesh) else mesh
-    kw = dict(target=target, seed=seed, rounds=rounds, order=einsum_order())
+    kw = dict(target=target, seed=seed, rounds=rounds, order=einsum_order(), placement=placement)
     if isinstance(mesh, mfg.BatchedMesh):
         kw.update(vertex_offsets=mesh.vertex_offsets, facet_offsets=mesh.facet_offsets)
     return oracle.decimate(base.positions, base.facets, base.features, **kw)
@@ -92,12 +97,31 @@ _LO, _HI = (int(x) for x in os.environ.get("MF_FUZZ_SEEDS", "0:120").split(":"))
 _REGRESSIONS = [966, 1120, 3338, 8790]
 
 
+@pytest.mark.parametrize("placement", ["average", "inverse"])
+def test_identity_rounds_inside_a_chain(oracle, placement):
+    """A fixed round count that interpolates to targets equal to the input size (16 -> 16 -> 16
+    -> 15): those rounds are _identity_result (decimate.py:231-233), and 'inverse' singletons
+    must not move; alone and as entries of a batch beside meshes with real rounds."""
+    small = S.perturbed_grid(4, noise=0.01, seed=3)
+    big = S.delaunay_terrain(40, seed=5)  # 40 -> 29 -> 21 -> 15: real rounds
+    for mesh in (small, mfg.concat_batch([small, big, small])):
+        base = mesh.mesh if isinstance(mesh, mfg.BatchedMesh) else mesh
+        cfg = mfg.DecimationConfig(target_vertices=15, rounds=3, placement=placement)
+        res = mfg.decimate_parallel(mesh, cfg, device=0)
+        exp = _oracle(oracle, mesh, 15, None, 3, placement)
+        got = res.mesh.mesh if isinstance(res.mesh, mfg.BatchedMesh) else res.mesh
+        for key, g in (("replace", res.replace), ("mapping", res.mapping), ("facets", got.facets),
+                       ("positions", got.positions)):
+            assert _same(g, exp[key]), key
+
+
 @pytest.mark.parametrize("seed", sorted(set(range(_LO, _HI)) | set(_REGRESSIONS)))
 def test_random_configuration_matches_oracle(oracle, seed):
     mesh, target, shuffle, rounds = _case(seed)
-    cfg = mfg.DecimationConfig(target_vertices=target, shuffle_seed=shuffle, rounds=rounds)
+    placement = _placement(seed)
+    cfg = mfg.DecimationConfig(target_vertices=target, shuffle_seed=shuffle, rounds=rounds, placement=placement)
     try:
-        exp = _oracle(oracle, mesh, target, shuffle, rounds)
+        exp = _oracle(oracle, mesh, target, shuffle, rounds, placement)
     except oracle.OracleInfeasible as e:
         with pytest.raises(mfg.InfeasibleTargetError) as err:
             mfg.decimate_parallel(mesh, cfg, device=0)
@@ -118,19 +142,19 @@ def test_random_configuration_matches_oracle(oracle, seed):
     X = None if src.features is src.positions or src.features.shape[1] == 3 and np.array_equal(
         src.features, src.positions) else torch.from_numpy(np.ascontiguousarray(src.features)).cuda()
     dd = T.decimate(torch.from_numpy(src.positions).cuda(), torch.from_numpy(src.facets).cuda(), nv, nf,
-                    target=target, seed=shuffle, rounds=rounds, features=X)
+                    target=target, seed=shuffle, rounds=rounds, features=X, placement=placement)
     assert np.array_equal(dd.replace.cpu().numpy(), exp["replace"])
     assert np.array_equal(dd.mapping.cpu().numpy(), exp["mapping"])
     assert np.array_equal(dd.faces.cpu().numpy(), exp["facets"])
     assert _same(dd.vertices.cpu().numpy(), exp["positions"])
     # a chained second level (the result's mesh fed back in) equals the oracle's second level
     t2 = max(1, target // 2)
-    cfg2 = mfg.DecimationConfig(target_vertices=t2, shuffle_seed=shuffle)
+    cfg2 = mfg.DecimationConfig(target_vertices=t2, shuffle_seed=shuffle, placement=placement)
     try:
         exp2 = _oracle(oracle, mfg.BatchedMesh(mfg.TriMesh(exp["positions"], exp["facets"], exp["features"]),
                                                 exp["vertex_offsets"], exp["facet_offsets"])
                        if isinstance(mesh, mfg.BatchedMesh) else
-                       mfg.TriMesh(exp["positions"], exp["facets"], exp["features"]), t2, shuffle, "auto")
+                       mfg.TriMesh(exp["positions"], exp["facets"], exp["features"]), t2, shuffle, "auto", placement)
     except (oracle.OracleInfeasible, oracle.OracleStructural):
         return
     except ValueError:

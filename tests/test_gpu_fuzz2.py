@@ -16,6 +16,8 @@ from paper_2103_15076_b200.numerics import einsum_order
 pytestmark = pytest.mark.gpu
 
 _LO, _HI = (int(x) for x in os.environ.get("MF_FUZZ2_SEEDS", "0:60").split(":"))
+# found by wider sweeps: 'inverse' with a fixed round count whose first rounds are identities
+_REGRESSIONS = [2709]
 
 
 def _soup(rng):
@@ -74,7 +76,7 @@ def _same(a, b):
     return a.shape == b.shape and a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
-@pytest.mark.parametrize("seed", range(_LO, _HI))
+@pytest.mark.parametrize("seed", sorted(set(range(_LO, _HI)) | set(_REGRESSIONS)))
 def test_structure_fuzz_matches_oracle(oracle, seed):
     rng = np.random.default_rng(10_000 + seed)
     mesh = _KINDS[seed % len(_KINDS)](rng)
