@@ -2,7 +2,8 @@
 test_gpu_fuzz.py never produce -- random facet soups (non-manifold edges, isolated vertices),
 high-degree fans (the heavy / mid vertex tiers), flat grids (all-zero costs, ties broken by the
 edge order), coincident vertices -- under both placements, followed by pool (4 modes, float32
-and float64, weights), unpool and pool_backward of random features over the result."""
+and float64, weights), unpool and pool_backward of random features over the result, and
+quality_report's per-output-vertex quadric errors."""
 
 import os
 
@@ -98,6 +99,12 @@ def test_structure_fuzz_matches_oracle(oracle, seed):
     for key, got in (("replace", res.replace), ("mapping", res.mapping), ("facets", res.mesh.facets),
                      ("positions", res.mesh.positions), ("features", res.mesh.features)):
         assert _same(got, exp[key]), key
+    # quality_report's per-output-vertex errors (decimate.py:580-602)
+    from paper_2103_15076_b200.quality import quadric_errors
+
+    qe = quadric_errors(mesh, res)
+    assert _same(np.asarray(qe), oracle.quality_errors(mesh.positions, mesh.facets, exp["replace"], exp["positions"],
+                                                       einsum_order()))
     # pooling over the result
     n_out = len(exp["positions"])
     dt = np.float32 if rng.random() < 0.5 else np.float64
