@@ -1,4 +1,5 @@
-"""The C oracle against the REAL reference, live, on the seeded fuzz generators of the GPU suite
+"""The C oracle against the REAL reference, live (decimation and pooling), on the seeded fuzz
+generators of the GPU suite
 (test_gpu_fuzz.py: terrains / grids / icospheres / unions / shuffled ids with duplicate facets,
 batches, float32 / float64 features, seeded ranks, fixed or auto rounds, both placements;
 test_gpu_fuzz2.py: facet soups, hub fans, flat grids, isolated and coincident vertices).  The GPU
@@ -93,3 +94,31 @@ def test_structure_cases_oracle_equals_reference(ref, oracle, seed):
              lambda: oracle.decimate(mesh.positions, mesh.facets, None, target=target, seed=shuffle, rounds=rounds,
                                      order=einsum_order(), placement=placement),
              dict(target_vertices=target, placement=placement, shuffle_seed=shuffle, rounds=rounds))
+
+
+@pytest.mark.parametrize("seed", range(0, 200, 10))
+def test_pooling_oracle_equals_reference(ref, oracle, seed):
+    """pool (4 modes, f32 / f64, weights) and unpool over the reference's own decimation of a
+    structure-fuzz mesh: the oracle's restatement against meshforge.pooling, bit for bit."""
+    sys.path.insert(0, HERE)
+    import test_gpu_fuzz2 as T2
+
+    rng = np.random.default_rng(20_000 + seed)
+    mesh = T2._KINDS[seed % len(T2._KINDS)](rng)
+    n = mesh.n_vertices
+    try:
+        r = ref.decimate_parallel(ref.TriMesh(mesh.positions, mesh.facets),
+                                  ref.DecimationConfig(target_vertices=max(1, n // 2)))
+    except ref.InfeasibleTargetError:
+        return
+    n_out = r.n_vertices_out
+    for dt in (np.float32, np.float64):
+        X = rng.standard_normal((n, int(rng.integers(1, 9)))).astype(dt)
+        X[rng.integers(0, n, 3), 0] = np.nan
+        w = rng.uniform(0.1, 2.0, n).astype(dt)
+        for mode in ("average", "max", "weighted", "sum"):
+            got = ref.pool(X, r, mode=mode, weights=w if mode == "weighted" else None)
+            exp = oracle.pool(X, r.replace, n_out, mode, weights=w if mode == "weighted" else None)
+            assert _same(np.asarray(got), exp), (mode, dt)
+        coarse = rng.standard_normal((n_out, X.shape[1])).astype(dt)
+        assert _same(np.asarray(ref.unpool(coarse, r)), oracle.unpool(coarse, r.replace))
