@@ -389,6 +389,16 @@ static int sel_bulk() {
     return v;
 }
 
+// k_suitor<L> blocks per SM cap (MF_SUITOR_BPSM, 0 = one thread group per proposer; A/B)
+static int suitor_bpsm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SUITOR_BPSM");
+        v = e ? std::max(0, atoi(e)) : 0;
+    }
+    return v;
+}
+
 // k_vertex_tiers blocks per SM (MF_TIERS_PER_SM, A/B)
 static int tiers_per_sm() {
     static int v = -1;
@@ -1015,9 +1025,13 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
                          seeded ? W.key_lo : nullptr, W.suitor, d_abort, use_ld ? W.mate : nullptr,
                          use_ld ? W.front0 : nullptr, W.front1, W.ldc, W.acur};
             const int sl = suitor_lanes(N, ctx->sm_count);
-            if (sl == 8) LAUNCH(k_suitor<8>, grid_for(ctx, (int64_t)N * 8), 256, 0, stream, ma);
-            else if (sl == 4) LAUNCH(k_suitor<4>, grid_for(ctx, (int64_t)N * 4), 256, 0, stream, ma);
-            else if (sl == 2) LAUNCH(k_suitor<2>, grid_for(ctx, (int64_t)N * 2), 256, 0, stream, ma);
+            auto sg = [&](int lanes) {  // MF_SUITOR_BPSM=k: at most k blocks per SM (grid-stride), A/B
+                const int g = grid_for(ctx, (int64_t)N * lanes);
+                return suitor_bpsm() > 0 ? std::min(g, ctx->sm_count * suitor_bpsm()) : g;
+            };
+            if (sl == 8) LAUNCH(k_suitor<8>, sg(8), 256, 0, stream, ma);
+            else if (sl == 4) LAUNCH(k_suitor<4>, sg(4), 256, 0, stream, ma);
+            else if (sl == 2) LAUNCH(k_suitor<2>, sg(2), 256, 0, stream, ma);
             else LAUNCH(k_suitor1, grid_for(ctx, N), 256, 0, stream, ma);
         }
         LAUNCH(k_mates, grid_for(ctx, N), 256, 0, stream, d_abort, N, W.suitor, W.e0, W.e1, W.mate, W.key_hi,
@@ -1174,7 +1188,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
-                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(), tiers_per_sm(), sel_bulk(),
+                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(), tiers_per_sm(), sel_bulk(), suitor_bpsm(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);
