@@ -1,7 +1,7 @@
 """Golden digests of the REAL reference at BASELINE.json's FULL sizes (run in the
 build container, where /root/reference exists; the GPU box only reads the json).
 
-    python tests/golden/make_golden_full.py [cfg3] [cfg4] [cfg5]
+    python tests/golden/make_golden_full.py [cfg3] [cfg4] [cfg5] [cfg3_inverse] [cfg4_inverse]
 
 Writes tests/golden/full.json: per config the input digest and, per level, the
 sha256 of replace / mapping / facets / positions / features (and, for cfg3, of
@@ -41,11 +41,11 @@ def level_digests(r):
     return d
 
 
-def chain(mesh, targets, feats=None):
+def chain(mesh, targets, feats=None, placement="average"):
     levels, cur, f = [], mesh, feats
     for tgt in targets:
         t = time.time()
-        r = mf.decimate_parallel(cur, mf.DecimationConfig(target_vertices=tgt))
+        r = mf.decimate_parallel(cur, mf.DecimationConfig(target_vertices=tgt, placement=placement))
         d = level_digests(r)
         d["target"] = tgt
         d["ref_seconds"] = round(time.time() - t, 2)
@@ -69,7 +69,7 @@ def halving(n, k=4):
 
 
 def main():
-    which = sys.argv[1:] or ["cfg3", "cfg4", "cfg5"]
+    which = sys.argv[1:] or ["cfg3", "cfg4", "cfg5", "cfg3_inverse", "cfg4_inverse"]
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
     data.update({"einsum_order": einsum_order(), "numpy": np.__version__, "reference": "meshforge 0.1.0"})
     if "cfg3" in which:
@@ -86,6 +86,16 @@ def main():
         print("cfg5", flush=True)
         mesh = msyn.perturbed_grid(3163, None, 0.02, 0)
         data["cfg5"] = {"input": input_digest(mesh), "levels": chain(mesh, halving(mesh.n_vertices))}
+    # placement='inverse' at full size (the solve is restated in numpy.linalg.solve's order)
+    if "cfg3_inverse" in which:
+        print("cfg3_inverse", flush=True)
+        mesh = msyn.delaunay_terrain(500_000, 0.02, 3)
+        data["cfg3_inverse"] = {"input": input_digest(mesh),
+                                "levels": chain(mesh, [125_000, 62_500, 31_250, 15_625], placement="inverse")}
+    if "cfg4_inverse" in which:
+        print("cfg4_inverse", flush=True)
+        batch = mf.concat_batch([msyn.delaunay_terrain(2500, 0.02, b) for b in range(256)])
+        data["cfg4_inverse"] = {"input": input_digest(batch), "levels": chain(batch, [1250], placement="inverse")}
     with open(OUT, "w") as fh:
         json.dump(data, fh, indent=1)
     print("wrote", OUT)

@@ -62,8 +62,15 @@ def halving(n, k=4):
     return out
 
 
+def placement_of(cfg):
+    return "inverse" if cfg.endswith("_inverse") else "average"
+
+
 @functools.lru_cache(maxsize=None)
 def workload(cfg):
+    if cfg.endswith("_inverse"):  # the same meshes and levels under placement='inverse', no pooling
+        mesh, levels, _ = workload(cfg[: -len("_inverse")])
+        return mesh, levels, None
     if cfg == "cfg3":
         mesh = S.delaunay_terrain(500_000, 0.02, 3)
         feats = np.random.default_rng(0).standard_normal((mesh.n_vertices, 64)).astype(np.float32)
@@ -93,7 +100,8 @@ def gpu_chain(cfg, order):
     out, cur, f = [], mesh, feats
     with forced_order(order):
         for tgt in levels:
-            res = mfg.decimate_parallel(cur, mfg.DecimationConfig(target_vertices=tgt), device=0)
+            res = mfg.decimate_parallel(cur, mfg.DecimationConfig(target_vertices=tgt, placement=placement_of(cfg)),
+                                        device=0)
             a = {k: np.array(v) for k, v in _arrays(res).items()}
             if f is not None:
                 a["pool_max"] = mfg.pool(f, res, mode="max")
@@ -114,7 +122,7 @@ def oracle_chain(oracle, cfg, order):
               threads=os.cpu_count() or 1) if batched else {}
     out, f = [], feats
     for tgt in levels:
-        o = oracle.decimate(P, F, X, target=tgt, order=order, **kw)
+        o = oracle.decimate(P, F, X, target=tgt, order=order, placement=placement_of(cfg), **kw)
         if f is not None:
             o["pool_max"] = oracle.pool(f, o["replace"], len(o["positions"]), "max")
             o["pool_average"] = oracle.pool(f, o["replace"], len(o["positions"]), "average")
@@ -159,13 +167,14 @@ def _check_oracle(oracle, cfg):
                 f"level {i}: {k} differs from the oracle"
 
 
-@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5", "cfg3_inverse", "cfg4_inverse"])
 def test_full_size_matches_reference(cfg):
-    """configs[2..4] at full size, digest-equal to meshforge's own outputs."""
+    """configs[2..4] at full size, digest-equal to meshforge's own outputs (cfg3 / cfg4 also
+    under placement='inverse': its solve follows numpy.linalg.solve's operation order)."""
     _check_reference(cfg)
 
 
-@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5", "cfg3_inverse"])
 def test_full_size_matches_oracle(oracle, cfg):
     """configs[2..4] at full size, byte-equal to the C oracle on this host."""
     _check_oracle(oracle, cfg)

@@ -165,7 +165,7 @@ FULL_PATH = os.path.join(HERE, "golden", "full.json")
 FULL = json.load(open(FULL_PATH)) if os.path.exists(FULL_PATH) else {}
 
 
-@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5", "cfg3_inverse", "cfg4_inverse"])
 def test_oracle_matches_reference_at_full_size(oracle, cfg):
     """The C oracle at BASELINE.json's full sizes (cfg5: 10M vertices, 4 levels) against the
     real reference's digests (tests/golden/make_golden_full.py) -- pins the checker the GPU
