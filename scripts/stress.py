@@ -26,16 +26,22 @@ ap.add_argument("--iters", type=int, default=500)
 args = ap.parse_args()
 wl = bench.workload(args.config, 0)
 mesh, levels = wl["mesh"], wl["levels"]
-V0 = torch.from_numpy(mesh.positions).cuda()
-F0 = torch.from_numpy(mesh.facets).cuda()
+batched = hasattr(mesh, "vertex_offsets")
+base = mesh.mesh if batched else mesh
+nv0 = np.diff(mesh.vertex_offsets) if batched else None
+nf0 = np.diff(mesh.facet_offsets) if batched else None
+V0 = torch.from_numpy(base.positions).cuda()
+F0 = torch.from_numpy(base.facets).cuda()
 ref = None
 t0 = time.time()
 for it in range(args.iters):
     faulthandler.dump_traceback_later(30, exit=True)  # a stuck call prints its Python frame and exits
-    V, F = V0, F0
+    V, F, nv, nf = V0, F0, nv0, nf0
     for t in levels:
-        dd = T.decimate(V, F, target=t)
+        dd = T.decimate(V, F, nv, nf, target=t)
         V, F = dd.vertices, dd.faces
+        if batched:
+            nv, nf = dd.nv.numpy(), dd.mf.numpy()
     digest = (int(dd.replace.sum()), int(dd.faces.sum()), float(dd.vertices.sum()))
     if ref is None:
         ref = digest
@@ -47,7 +53,8 @@ for it in range(args.iters):
         for t in levels:
             res = mfg.decimate_parallel(cur, mfg.DecimationConfig(target_vertices=t))
             cur = res.mesh
-        if (int(res.replace.sum()), int(res.mesh.facets.sum())) != ref[:2]:
+        out = res.mesh.mesh if batched else res.mesh
+        if (int(res.replace.sum()), int(out.facets.sum())) != ref[:2]:
             print(f"iter {it}: numpy-API result differs", flush=True)
             sys.exit(3)
     if it % 50 == 0:
