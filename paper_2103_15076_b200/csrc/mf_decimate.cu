@@ -399,6 +399,16 @@ static int suitor_bpsm() {
     return v;
 }
 
+// k_select's first radix pass without the prefix test (MF_SEL_FIRST=0: with it, A/B)
+static int sel_first() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MF_SEL_FIRST");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v;
+}
+
 // k_vertex_tiers blocks per SM (MF_TIERS_PER_SM, A/B)
 static int tiers_per_sm() {
     static int v = -1;
@@ -1041,7 +1051,7 @@ static void record(const Context* ctx, const Plan& p, WS& W, cudaStream_t stream
         auto select = [&](const int* seg_cnt, const int* removed_in) {
             SelectArgs sa{W.chi, W.clo, seg_cnt, voff_r, B, act, budget, removed_in, W.ksel, W.mode, W.p_hi, W.p_lo,
                           d_abort, W.selstate, W.selstate + B, 0, W.ghist, select_cap(), 0,
-                          B == 1 ? kSelChiCap : 0, sel_bulk()};
+                          B == 1 ? kSelChiCap : 0, sel_bulk(), sel_first()};
             if (big) {
                 const int hist_grid = std::min(grid_for(ctx, N / 2, 512), ctx->sm_count * 2);
                 if (cc.on() && cc.depth < 2) {  // passes until decided / handed over (WHILE node)
@@ -1188,7 +1198,7 @@ static std::vector<int64_t> graph_key(const Plan& p) {
     std::vector<int64_t> k = {p.n, p.m, p.C, p.alias, p.fdtype, p.B, p.R, p.seeded, p.order, p.first_err,
                               (int64_t)p.pcg[0], (int64_t)p.pcg[1], (int64_t)p.pcg[2], (int64_t)p.pcg[3],
                               g_prof_mode, p.ld_min, p.ld1_min, p.ld_mid, p.ld_big, p.placement, fuse_plane(), vertex_scan(), edges_rank(),
-                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(), tiers_per_sm(), sel_bulk(), suitor_bpsm(),
+                              vt16(1), vt16(1 << 21), two_pass_min(), recompute_min(), scan_ticketless(), tiers_per_sm(), sel_bulk(), sel_first(), suitor_bpsm(),
                               p.big_sel_min, p.scan4_min, p.wide_min};
     k.insert(k.end(), p.h_N.begin(), p.h_N.end());
     for (char ch : g_prof_only) k.push_back(ch);

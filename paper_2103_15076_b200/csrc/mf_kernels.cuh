@@ -2194,6 +2194,7 @@ struct SelectArgs {
     cudaGraphConditionalHandle cond;  // device-driven multi-block passes (WHILE node), 0 = fixed passes
     int chicap;         // k_select: primary keys the stage holds for the two-phase path (0 = off)
     int bulk;           // k_select: two-phase keys staged by the bulk-copy engine
+    int first_all;      // k_select: its first radix pass skips the prefix test (all keys in the bucket)
 };
 
 // Multi-block pass scratch (ints): histogram | OR (2 u64), AND (2 u64) | stop |
@@ -2220,7 +2221,11 @@ constexpr int kSelPassesMax = 12;                          // loop cap (128-bit 
 // `scratch` (cap values): once a bucket fits, it is copied there and later passes walk
 // only the bucket instead of every value.
 MF_DEV bool radix_kth_u64(const uint64_t* vals, int n, int& kr, uint64_t& p, int& top, int* hist, int* s_scan,
-                          int* s_sel, unsigned long long* s_oa, uint64_t* scratch, int cap) {
+                          int* s_sel, unsigned long long* s_oa, uint64_t* scratch, int cap,
+                          bool all_in = false) {
+    // all_in: every value already shares the prefix above `top` (the caller skipped the bits
+    // the whole input shares) -- the first pass then needs neither the prefix test nor the
+    // OR / AND of its bucket (which is the whole input, already reflected in `top`)
     bool compacted = false;
     if (n <= 32 && top >= 64) {  // tiny input (typically the ties of phase two): one warp sorts it
         if (threadIdx.x < 32) {
@@ -2255,12 +2260,19 @@ MF_DEV bool radix_kth_u64(const uint64_t* vals, int n, int& kr, uint64_t& p, int
         if (threadIdx.x < 2) s_oa[threadIdx.x] = threadIdx.x ? ~0ull : 0ull;
         __syncthreads();
         uint64_t o = 0, an = ~0ull;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint64_t x = vals[i];
-            if (top >= 64 || (x >> top) == (p >> top)) {
-                hist_add(hist, (int)((x >> shift) & ((1u << width) - 1u)));
-                o |= x;
-                an &= x;
+        if (all_in) {
+            const unsigned dmask = (1u << width) - 1u;
+#pragma unroll 4
+            for (int i = threadIdx.x; i < n; i += blockDim.x) hist_add(hist, (int)((vals[i] >> shift) & dmask));
+            all_in = false;
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint64_t x = vals[i];
+                if (top >= 64 || (x >> top) == (p >> top)) {
+                    hist_add(hist, (int)((x >> shift) & ((1u << width) - 1u)));
+                    o |= x;
+                    an &= x;
+                }
             }
         }
 #pragma unroll
@@ -2481,7 +2493,8 @@ __global__ void __launch_bounds__(NT) k_select(SelectArgs a) {
                 }
             }
             __syncthreads();
-            const bool whole = radix_kth_u64(sv, cnt, kr, t, topc, hist, s_scan, s_sel, s_oa, s_bucket, kSelBucket);
+            const bool whole =
+                radix_kth_u64(sv, cnt, kr, t, topc, hist, s_scan, s_sel, s_oa, s_bucket, kSelBucket, a.first_all);
             if (whole) {
                 t |= (topc >= 64) ? ~0ull : ((1ull << topc) - 1ull);
                 q = ~0ull;

@@ -75,6 +75,7 @@ VARIANTS = [
     {"MF_RECOMPUTE_MIN": "0"},
     {"MF_SCAN_TICKET": "1"},
     {"MF_SEL_BULK": "0"},
+    {"MF_SEL_FIRST": "0"},
     {"MF_RECOMPUTE_MIN": "0", "MF_VT16": "1", "MF_TWO_PASS_MIN": "0"},
     {"MF_EDGES_RANK": "1"},
     {"MF_EDGES_RANK": "1", "MF_LD_MIN": "1"},
