@@ -54,3 +54,18 @@ def test_documented_binding_raises_reference_errors(binding):
     with pytest.raises(mfg.InfeasibleTargetError) as err:
         binding["decimate_parallel_gpu"](mesh, mfg.DecimationConfig(target_vertices=10, rounds=1))
     assert err.value.achievable_vertices > 10
+
+
+def test_documented_binding_from_a_thread_pool(binding):
+    """meshforge decimates batch entries on a thread pool (decimate.py:356-358): the binding's
+    per-thread contexts give every concurrent call the same bytes as a sequential one."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    meshes = [S.delaunay_terrain(2000 + 500 * i, noise=0.02, seed=40 + i) for i in range(8)]
+    cfg = lambda m: mfg.DecimationConfig(target_vertices=m.n_vertices // 3)  # noqa: E731
+    seq = [binding["decimate_parallel_gpu"](m, cfg(m)) for m in meshes]
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        par = list(ex.map(lambda m: binding["decimate_parallel_gpu"](m, cfg(m)), meshes))
+    for a, b in zip(seq, par):
+        for x, y in zip(a, b):
+            assert np.array_equal(np.ascontiguousarray(x).view(np.uint8), np.ascontiguousarray(y).view(np.uint8))
