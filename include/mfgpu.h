@@ -93,6 +93,10 @@ typedef struct mf_decimate_config {
     uint64_t pcg_state[4]; /* default_rng(seed).bit_generator.state: state_hi, state_lo, inc_hi, inc_lo */
 } mf_decimate_config;
 
+/* A context owns a device workspace, streams and the captured CUDA graphs of its calls: use one
+ * context per calling thread (calls on distinct contexts may run concurrently; calls on the
+ * same context must not overlap).  The graph cache is per thread as well, so a context should
+ * stay with the thread that created it. */
 int mf_context_create(int device, mf_context **out);
 void mf_context_destroy(mf_context *ctx);
 
